@@ -1,0 +1,524 @@
+/*
+ * SMP-PCA CPU ORACLE — TEST INFRASTRUCTURE ONLY.
+ *
+ * This file is the plain, slow, obviously-correct fp64 reference for the hot
+ * path of SMP-PCA (arXiv 1610.06656).  Only tests/, __graft_entry__.smoke()
+ * and bench.py's cpu_baseline / --impl reference legs may load it.  It shares
+ * NO code with the CUDA path (paper_1610_06656_b200/csrc): the hash, the
+ * Gaussian generator, the sampling arithmetic and WAltMin are re-implemented
+ * here from the written definitions in DESIGN.md §3.
+ *
+ * Citation convention: "P:L" = /root/reference/PAPER.md line L.
+ *
+ *   Alg. 1 line 2  -> or_sketch_rows        (Step 1)
+ *   Eq. 1         -> or_qhat / or_sample   (Step 2, Alg.1 l.3)
+ *   Eq. 2         -> or_estimate           (Step 2, Alg.1 l.4)
+ *   Alg. 2       -> or_waltmin            (Step 3, Eq. 3)
+ *
+ * Every floating-point quantity is fp64 unless the definition
+ * fixes fp32 (the Gaussian generator G, which must produce identical bf16
+ * bits on both sides).  Compile with -ffp-contract=off so that no FMA is
+ * introduced where the definition does not name one.
+ *
+ * Parity status of each function is listed in DESIGN.md §4 ("pins").
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+/* ------------------------------------------------------------------------ */
+/* H: Philox4x32-10 (Salmon et al., SC'11).  DESIGN.md §3.1.                  */
+/* ------------------------------------------------------------------------ */
+void or_philox4x32_10(const uint32_t ctr_in[4], const uint32_t key_in[2], uint32_t out[4])
+{
+    uint32_t c0 = ctr_in[0], c1 = ctr_in[1], c2 = ctr_in[2], c3 = ctr_in[3];
+    uint32_t k0 = key_in[0], k1 = key_in[1];
+    for (int round = 0; round < 10; ++round) {
+        if (round > 0) {
+            k0 += 0x9E3779B9u;
+            k1 += 0xBB67AE85u;
+        }
+        uint64_t p0 = (uint64_t)0xD2511F53u * (uint64_t)c0;
+        uint64_t p1 = (uint64_t)0xCD9E8D57u * (uint64_t)c2;
+        uint32_t hi0 = (uint32_t)(p0 >> 32), lo0 = (uint32_t)p0;
+        uint32_t hi1 = (uint32_t)(p1 >> 32), lo1 = (uint32_t)p1;
+        uint32_t n0 = hi1 ^ c1 ^ k0;
+        uint32_t n1 = lo1;
+        uint32_t n2 = hi0 ^ c3 ^ k1;
+        uint32_t n3 = lo0;
+        c0 = n0; c1 = n1; c2 = n2; c3 = n3;
+    }
+    out[0] = c0; out[1] = c1; out[2] = c2; out[3] = c3;
+}
+
+static void philox_seed(uint64_t seed, uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3,
+                        uint32_t out[4])
+{
+    uint32_t ctr[4] = {c0, c1, c2, c3};
+    uint32_t key[2] = {(uint32_t)(seed & 0xffffffffu), (uint32_t)(seed >> 32)};
+    or_philox4x32_10(ctr, key, out);
+}
+
+/* ------------------------------------------------------------------------ */
+/* Π entries (Alg. 1 line 2; "any oblivious subspace embedding"). */
+/* Values are UNSCALED (±1, or a bf16-valued Gaussian); the 1/sqrt(k) factor  */
+/* of N(0,1/k) is applied to the sketch at finalize (R1).           */
+/* ------------------------------------------------------------------------ */
+enum { OR_PI_RADEMACHER = 0, OR_PI_GAUSSIAN = 1, OR_PI_HADAMARD = 2 };
+
+double or_pi_rademacher(uint64_t seed, int64_t kappa, int64_t t)
+{
+    uint32_t w[4];
+    philox_seed(seed, (uint32_t)((uint64_t)t >> 7), (uint32_t)kappa,
+                (uint32_t)((uint64_t)t >> 39), 1u, w);
+    unsigned b = (unsigned)(t & 127);
+    unsigned bit = (w[b >> 5] >> (b & 31)) & 1u;
+    return bit ? -1.0 : 1.0;
+}
+
+static float u32_as_f32(uint32_t u) { float f; memcpy(&f, &u, 4); return f; }
+static uint32_t f32_as_u32(float f) { uint32_t u; memcpy(&u, &f, 4); return u; }
+
+/* Round fp32 to the nearest bf16 (ties to even); returned as the fp32 value. */
+static float bf16_rne(float x)
+{
+    uint32_t u = f32_as_u32(x);
+    uint32_t lsb = (u >> 16) & 1u;
+    u = (u + 0x7FFFu + lsb) & 0xFFFF0000u;
+    return u32_as_f32(u);
+}
+
+/* G: stated fp32 Box–Muller.  Only IEEE correctly-rounded  */
+/* fp32 operations (+, *, fmaf, sqrtf, exact int<->float) are used, each in   */
+/* the order written, so that the CUDA side produces identical bits.          */
+static void gauss_pair(uint32_t wa, uint32_t wb, float *z0, float *z1)
+{
+    /* ln(1+y) = y * P(y), P of degree 9, coefficients fp32. */
+    static const float L[10] = {
+        0x1.000000p+0f, -0x1.000000p-1f, 0x1.5555c6p-2f, -0x1.00003ep-2f, 0x1.996178p-3f,
+        -0x1.54e596p-3f, 0x1.28ce66p-3f, -0x1.0e2b8ep-3f, 0x1.ac49bap-4f, -0x1.6e4bbap-5f};
+    const float LN2 = 0x1.62e430p-1f;
+    /* sin(pi x/2) = x*(S1 + x2*(S3 + ...)), cos(pi x/2) = 1 + x2*(C2 + ...) */
+    const float S1 = 0x1.921fb6p+0f, S3 = -0x1.4abbcep-1f, S5 = 0x1.466bc6p-4f,
+                S7 = -0x1.32d2ccp-8f, S9 = 0x1.507834p-13f;
+    const float C2 = -0x1.3bd3ccp+0f, C4 = 0x1.03c1f0p-2f, C6 = -0x1.55d3c8p-6f,
+                C8 = 0x1.e1f506p-11f, C10 = -0x1.a6d1f2p-16f;
+
+    /* u1 in (0,1] */
+    uint32_t v1 = (wa >> 8) + 1u;
+    float u1 = (float)v1 * 0x1p-24f;           /* exact */
+    uint32_t bits = f32_as_u32(u1);
+    int e = (int)(bits >> 23) - 127;
+    uint32_t mant = bits & 0x7FFFFFu;
+    float f;
+    if (mant >= 0x400000u) {                   /* f >= 1.5: use f/2 in [0.75,1) */
+        f = u32_as_f32(mant | 0x3F000000u);
+        e += 1;
+    } else {
+        f = u32_as_f32(mant | 0x3F800000u);
+    }
+    float y = f - 1.0f;                        /* exact (Sterbenz) */
+    float p = L[9];
+    for (int i = 8; i >= 0; --i) p = fmaf(p, y, L[i]);
+    float lnf = y * p;
+    float lnu = fmaf((float)e, LN2, lnf);
+    float r2 = -2.0f * lnu;                    /* exact */
+    float rho = sqrtf(r2);
+
+    /* angle 2*pi*u2, u2 = v2 * 2^-24 in [0,1) */
+    uint32_t v2 = wb >> 8;
+    uint32_t qn = (v2 + 0x200000u) >> 22;      /* nearest quadrant, 0..4 */
+    int32_t xi = (int32_t)v2 - (int32_t)(qn << 22);
+    float x = (float)xi * 0x1p-22f;            /* exact, in [-0.5,0.5) */
+    float x2 = x * x;
+    float sp = fmaf(fmaf(fmaf(fmaf(S9, x2, S7), x2, S5), x2, S3), x2, S1);
+    float sn = x * sp;
+    float cs = fmaf(fmaf(fmaf(fmaf(fmaf(C10, x2, C8), x2, C6), x2, C4), x2, C2), x2, 1.0f);
+    float c, s;
+    switch (qn & 3u) {
+    case 0: c = cs; s = sn; break;
+    case 1: c = -sn; s = cs; break;
+    case 2: c = -cs; s = -sn; break;
+    default: c = sn; s = -cs; break;
+    }
+    *z0 = bf16_rne(rho * c);
+    *z1 = bf16_rne(rho * s);
+}
+
+double or_pi_gaussian(uint64_t seed, int64_t kappa, int64_t t)
+{
+    uint32_t w[4];
+    philox_seed(seed, (uint32_t)((uint64_t)t >> 2), (uint32_t)kappa,
+                (uint32_t)((uint64_t)t >> 34), 2u, w);
+    unsigned sel = (unsigned)(t & 3);
+    float z0, z1;
+    if (sel < 2) gauss_pair(w[0], w[1], &z0, &z1);
+    else gauss_pair(w[2], w[3], &z0, &z1);
+    return (double)((sel & 1u) ? z1 : z0);
+}
+
+static int popcount64(uint64_t x)
+{
+    int c = 0;
+    while (x) { c += (int)(x & 1u); x >>= 1; }
+    return c;
+}
+
+double or_pi_hadamard(int64_t kappa, int64_t t)
+{
+    return (popcount64((uint64_t)kappa & (uint64_t)t) & 1) ? -1.0 : 1.0;
+}
+
+double or_pi_entry(int kind, uint64_t seed, int64_t kappa, int64_t t)
+{
+    if (kind == OR_PI_RADEMACHER) return or_pi_rademacher(seed, kappa, t);
+    if (kind == OR_PI_GAUSSIAN) return or_pi_gaussian(seed, kappa, t);
+    return or_pi_hadamard(kappa, t);
+}
+
+/* ------------------------------------------------------------------------ */
+/* Step 1: one pass over rows of X (Alg. 1 line 2).           */
+/*   sk[c*k + kappa] += Π(kappa, t) * X[t, c]     (unscaled, fp64)           */
+/*   norm2[c]        += X[t, c]^2                 (fp64)                     */
+/* X is row-major with leading dimension ldx; dtype 0 = fp64, 1 = fp32,      */
+/* 2 = bf16 (raw uint16).  Global row of local row r is row0 + r.            */
+/* ------------------------------------------------------------------------ */
+static double load_elem(const void *X, int dtype, int64_t idx)
+{
+    if (dtype == 0) return ((const double *)X)[idx];
+    if (dtype == 1) return (double)((const float *)X)[idx];
+    uint32_t u = (uint32_t)((const uint16_t *)X)[idx] << 16;
+    return (double)u32_as_f32(u);
+}
+
+void or_sketch_rows(int kind, uint64_t seed, int k, int64_t row0, int64_t rows, int64_t n,
+                    const void *X, int dtype, int64_t ldx, double *sk, double *norm2)
+{
+    const int64_t RB = 256;                    /* Π materialised per 256-row block */
+    double *pi = (double *)malloc(sizeof(double) * (size_t)RB * (size_t)k);
+    for (int64_t r0 = 0; r0 < rows; r0 += RB) {
+        int64_t rb = rows - r0 < RB ? rows - r0 : RB;
+        for (int64_t r = 0; r < rb; ++r)
+            for (int kp = 0; kp < k; ++kp)
+                pi[r * k + kp] = or_pi_entry(kind, seed, kp, row0 + r0 + r);
+        #pragma omp parallel for schedule(static)
+        for (int64_t c = 0; c < n; ++c) {
+            double *skc = sk + c * (int64_t)k;
+            for (int64_t r = 0; r < rb; ++r) {
+                double x = load_elem(X, dtype, (r0 + r) * ldx + c);
+                norm2[c] += x * x;
+                const double *pr = pi + r * k;
+                for (int kp = 0; kp < k; ++kp) skc[kp] += pr[kp] * x;
+            }
+        }
+    }
+    free(pi);
+}
+
+/* Sketch of a single column subset (sampled parity at full size): columns    */
+/* cols[0..nc) of X over rows [0, rows), same accumulation order as above.    */
+void or_sketch_cols(int kind, uint64_t seed, int k, int64_t row0, int64_t rows,
+                    int64_t nc, const int64_t *cols, const void *X, int dtype, int64_t ldx,
+                    double *sk, double *norm2)
+{
+    #pragma omp parallel for schedule(dynamic, 1)
+    for (int64_t ci = 0; ci < nc; ++ci) {
+        double *skc = sk + ci * (int64_t)k;
+        int64_t c = cols[ci];
+        for (int64_t r = 0; r < rows; ++r) {
+            double x = load_elem(X, dtype, r * ldx + c);
+            norm2[ci] += x * x;
+            if (x != 0.0)
+                for (int kp = 0; kp < k; ++kp)
+                    skc[kp] += or_pi_entry(kind, seed, kp, row0 + r) * x;
+        }
+    }
+}
+
+/* CSR rows (bag-of-words input, P:9): row t has entries             */
+/* (col[p], val[p]) for p in [rowptr[t], rowptr[t+1]).                       */
+void or_sketch_csr(int kind, uint64_t seed, int k, int64_t row0, int64_t rows, int64_t n,
+                   const int64_t *rowptr, const int32_t *col, const float *val,
+                   double *sk, double *norm2)
+{
+    double *pi = (double *)malloc(sizeof(double) * (size_t)k);
+    (void)n;
+    for (int64_t r = 0; r < rows; ++r) {
+        for (int kp = 0; kp < k; ++kp) pi[kp] = or_pi_entry(kind, seed, kp, row0 + r);
+        for (int64_t p = rowptr[r]; p < rowptr[r + 1]; ++p) {
+            int64_t c = col[p];
+            double x = (double)val[p];
+            norm2[c] += x * x;
+            double *skc = sk + c * (int64_t)k;
+            for (int kp = 0; kp < k; ++kp) skc[kp] += pi[kp] * x;
+        }
+    }
+    free(pi);
+}
+
+/* ------------------------------------------------------------------------ */
+/* Finalize (D_A/D_B definition).                                */
+/* ------------------------------------------------------------------------ */
+/* R5: Frobenius^2 by a fixed pairwise tree over the column norms^2:        */
+/* pad to a power of two with zeros, sum adjacent pairs level by level.      */
+double or_pairwise_sum(const double *x, int64_t n)
+{
+    if (n <= 0) return 0.0;
+    int64_t p = 1;
+    while (p < n) p <<= 1;
+    double *buf = (double *)calloc((size_t)p, sizeof(double));
+    memcpy(buf, x, sizeof(double) * (size_t)n);
+    while (p > 1) {
+        p >>= 1;
+        for (int64_t i = 0; i < p; ++i) buf[i] = buf[2 * i] + buf[2 * i + 1];
+    }
+    double s = buf[0];
+    free(buf);
+    return s;
+}
+
+/* Scales the unscaled sketch sk (n x k) by 1/sqrt(k) into out (n x k),      */
+/* and computes sknorm[c] = ||Ã_c|| and D[c] = ||X_c|| / ||Ã_c|| (0 if 0).  */
+void or_finalize(int k, int64_t n, const double *sk, const double *norm2,
+                 double *out, double *sknorm, double *D)
+{
+    double scale = 1.0 / sqrt((double)k);
+    for (int64_t c = 0; c < n; ++c) {
+        double s2 = 0.0;
+        for (int kp = 0; kp < k; ++kp) {
+            double v = sk[c * k + kp] * scale;
+            out[c * k + kp] = v;
+            s2 += v * v;
+        }
+        sknorm[c] = sqrt(s2);
+        D[c] = sknorm[c] > 0.0 ? sqrt(norm2[c]) / sknorm[c] : 0.0;
+    }
+}
+
+/* ------------------------------------------------------------------------ */
+/* Eq. 1 with q̂ = min(1, q) (Alg. 1 line 3).                */
+/* R6: alpha_i = a2_i / ((2 n2) FA), beta_j = b2_j / ((2 n1) FB),            */
+/*     q = m * (alpha_i + beta_j), no FMA.                                   */
+/* ------------------------------------------------------------------------ */
+void or_alpha_beta(int64_t n1, int64_t n2, const double *a2, const double *b2,
+                   double FA, double FB, double *alpha, double *beta)
+{
+    double da = (2.0 * (double)n2) * FA;
+    double db = (2.0 * (double)n1) * FB;
+    for (int64_t i = 0; i < n1; ++i) alpha[i] = a2[i] / da;
+    for (int64_t j = 0; j < n2; ++j) beta[j] = b2[j] / db;
+}
+
+double or_qhat(double m, double alpha_i, double beta_j)
+{
+    double q = m * (alpha_i + beta_j);
+    return q < 1.0 ? q : 1.0;
+}
+
+/* Bernoulli draw for pair (i,j): U53 from Philox(ctr=(i,j,0,3), key=seed).  */
+int or_draw(uint64_t seed, int64_t i, int64_t j, double qhat)
+{
+    uint32_t w[4];
+    philox_seed(seed, (uint32_t)i, (uint32_t)j, 0u, 3u, w);
+    uint64_t u53 = (((uint64_t)w[1] << 32) | (uint64_t)w[0]) >> 11;
+    double u = (double)u53 * 0x1p-53;          /* exact */
+    return u < qhat;
+}
+
+/* Ω in (i,j) order.  Returns the count; writes at most cap entries.        */
+int64_t or_sample(uint64_t seed, double m, int64_t n1, int64_t n2,
+                  const double *alpha, const double *beta, int64_t cap,
+                  int32_t *I, int32_t *J, double *qhat)
+{
+    int64_t cnt = 0;
+    for (int64_t i = 0; i < n1; ++i)
+        for (int64_t j = 0; j < n2; ++j) {
+            double q = or_qhat(m, alpha[i], beta[j]);
+            if (or_draw(seed, i, j, q)) {
+                if (cnt < cap) { I[cnt] = (int32_t)i; J[cnt] = (int32_t)j; qhat[cnt] = q; }
+                ++cnt;
+            }
+        }
+    return cnt;
+}
+
+/* Eq. 2: M̃_ij = ||A_i|| ||B_j|| <Ã_i,B̃_j> / (||Ã_i|| ||B̃_j||)    */
+/*              = D_A[i] * D_B[j] * <Ã_i, B̃_j>.                  */
+/* plain != 0 gives the JL estimator <Ã_i, B̃_j>.                     */
+void or_estimate(int k, int64_t cnt, const int32_t *I, const int32_t *J,
+                 const double *Ask, const double *Bsk, const double *DA, const double *DB,
+                 int plain, double *out)
+{
+    for (int64_t s = 0; s < cnt; ++s) {
+        const double *a = Ask + (int64_t)I[s] * k;
+        const double *b = Bsk + (int64_t)J[s] * k;
+        double dot = 0.0;
+        for (int kp = 0; kp < k; ++kp) dot += a[kp] * b[kp];
+        out[s] = plain ? dot : DA[I[s]] * DB[J[s]] * dot;
+    }
+}
+
+/* ------------------------------------------------------------------------ */
+/* WAltMin (Alg. 2).                                              */
+/* ------------------------------------------------------------------------ */
+/* Thin Householder QR of Z (n x r, row-major), Z <- Q (n x r).  Columns with */
+/* no remaining energy become zero (rank-deficient input, R12).    */
+static void householder_q(int64_t n, int r, double *Z)
+{
+    double *V = (double *)calloc((size_t)n * (size_t)r, sizeof(double));
+    double *beta = (double *)calloc((size_t)r, sizeof(double));
+    int *dead = (int *)calloc((size_t)r, sizeof(int));
+    double *A = (double *)malloc(sizeof(double) * (size_t)n * (size_t)r);
+    memcpy(A, Z, sizeof(double) * (size_t)n * (size_t)r);
+    double fro = 0.0;
+    for (int64_t i = 0; i < n * r; ++i) fro += A[i] * A[i];
+    fro = sqrt(fro);
+    for (int j = 0; j < r && j < n; ++j) {
+        double nrm = 0.0;
+        for (int64_t i = j; i < n; ++i) nrm += A[i * r + j] * A[i * r + j];
+        nrm = sqrt(nrm);
+        if (nrm <= 1e-14 * (fro > 0 ? fro : 1.0)) { dead[j] = 1; beta[j] = 0.0; continue; }
+        double a0 = A[(int64_t)j * r + j];
+        double alpha = a0 >= 0 ? -nrm : nrm;
+        for (int64_t i = 0; i < n; ++i) V[i * r + j] = 0.0;
+        V[(int64_t)j * r + j] = a0 - alpha;
+        for (int64_t i = j + 1; i < n; ++i) V[i * r + j] = A[i * r + j];
+        double vv = 0.0;
+        for (int64_t i = j; i < n; ++i) vv += V[i * r + j] * V[i * r + j];
+        beta[j] = vv > 0 ? 2.0 / vv : 0.0;
+        for (int c = j; c < r; ++c) {
+            double s = 0.0;
+            for (int64_t i = j; i < n; ++i) s += V[i * r + j] * A[i * r + c];
+            s *= beta[j];
+            for (int64_t i = j; i < n; ++i) A[i * r + c] -= s * V[i * r + j];
+        }
+    }
+    /* Q = H_0 H_1 ... H_{r-1} [I_r; 0] */
+    for (int64_t i = 0; i < n * r; ++i) Z[i] = 0.0;
+    for (int j = 0; j < r && j < n; ++j) Z[(int64_t)j * r + j] = dead[j] ? 0.0 : 1.0;
+    for (int j = (r < n ? r : (int)n) - 1; j >= 0; --j) {
+        if (dead[j]) continue;
+        for (int c = 0; c < r; ++c) {
+            double s = 0.0;
+            for (int64_t i = j; i < n; ++i) s += V[i * r + j] * Z[i * r + c];
+            s *= beta[j];
+            for (int64_t i = j; i < n; ++i) Z[i * r + c] -= s * V[i * r + j];
+        }
+    }
+    free(V); free(beta); free(dead); free(A);
+}
+
+/* Solve (G + lam*tr(G)/r * I) x = h by Cholesky, fp64.  Returns 0 if the   */
+/* system is empty/singular (x = 0).                                          */
+static int ridge_cholesky_solve(int r, const double *G, const double *h, double lam, double *x)
+{
+    double tr = 0.0;
+    for (int a = 0; a < r; ++a) tr += G[a * r + a];
+    for (int a = 0; a < r; ++a) x[a] = 0.0;
+    if (!(tr > 0.0)) return 0;
+    double L[32 * 32];
+    double shift = lam * tr / (double)r;
+    for (int a = 0; a < r; ++a)
+        for (int b = 0; b < r; ++b) L[a * r + b] = G[a * r + b] + (a == b ? shift : 0.0);
+    for (int j = 0; j < r; ++j) {
+        double s = L[j * r + j];
+        for (int p = 0; p < j; ++p) s -= L[j * r + p] * L[j * r + p];
+        if (!(s > 0.0)) return 0;
+        double d = sqrt(s);
+        L[j * r + j] = d;
+        for (int i = j + 1; i < r; ++i) {
+            double t = L[i * r + j];
+            for (int p = 0; p < j; ++p) t -= L[i * r + p] * L[j * r + p];
+            L[i * r + j] = t / d;
+        }
+    }
+    double y[32];
+    for (int i = 0; i < r; ++i) {
+        double t = h[i];
+        for (int p = 0; p < i; ++p) t -= L[i * r + p] * y[p];
+        y[i] = t / L[i * r + i];
+    }
+    for (int i = r - 1; i >= 0; --i) {
+        double t = y[i];
+        for (int p = i + 1; p < r; ++p) t -= L[p * r + i] * x[p];
+        x[i] = t / L[i * r + i];
+    }
+    return 1;
+}
+
+/* One weighted least-squares half step (Alg. 2 lines 8/9; closed form       */
+/* P:596-604).  For each output row o, over the samples s with side[s] == o: */
+/*   G_o = sum w_s x_{other(s)} x_{other(s)}^T,  h_o = sum w_s M_s x_other   */
+/* and out[o] = (G_o + lam tr(G_o)/r I)^{-1} h_o.                            */
+void or_als_half(int r, int64_t n_out, int64_t cnt, const int32_t *side, const int32_t *other,
+                 const double *val, const double *w, const double *X_other, double lam,
+                 double *out)
+{
+    double *G = (double *)calloc((size_t)n_out * r * r, sizeof(double));
+    double *h = (double *)calloc((size_t)n_out * r, sizeof(double));
+    for (int64_t s = 0; s < cnt; ++s) {
+        int64_t o = side[s];
+        const double *x = X_other + (int64_t)other[s] * r;
+        for (int a = 0; a < r; ++a) {
+            h[o * r + a] += w[s] * val[s] * x[a];
+            for (int b = 0; b < r; ++b) G[(o * r + a) * r + b] += w[s] * x[a] * x[b];
+        }
+    }
+    for (int64_t o = 0; o < n_out; ++o)
+        ridge_cholesky_solve(r, G + o * r * r, h + o * r, lam, out + o * r);
+    free(G); free(h);
+}
+
+/* Full WAltMin with the REUSE_ALL partition (R11):              */
+/*   R = w .* P_Ω(M̃) (Alg. 2 lines 2, 4);                                  */
+/*   U0 = top-r left singular subspace of R by subspace iteration from a     */
+/*        Rademacher start (line 5; R12), init_iters iterations;    */
+/*   trim rows of U0 with norm > trim_c sqrt(r) ||A_i||/||A||_F (line 6,     */
+/*        P:237; R13), re-orthonormalise;                          */
+/*   T x { V = argmin (line 8); U = argmin (line 9) }; output (U, V).       */
+void or_waltmin(int64_t n1, int64_t n2, int r, int T, int init_iters, double trim_c,
+                double lam, uint64_t seed, int64_t cnt, const int32_t *I, const int32_t *J,
+                const double *val, const double *qhat, const double *a_norm, double frobA,
+                double *U, double *V)
+{
+    double *w = (double *)malloc(sizeof(double) * (size_t)(cnt > 0 ? cnt : 1));
+    for (int64_t s = 0; s < cnt; ++s) w[s] = qhat[s] > 0.0 ? 1.0 / qhat[s] : 0.0;
+    double *Y = (double *)calloc((size_t)n2 * r, sizeof(double));
+    double *Z = (double *)calloc((size_t)n1 * r, sizeof(double));
+    /* Y0[j][l] = ±1 from Philox(ctr=(j,l,0,5), key=seed), bit 0 of word 0 */
+    for (int64_t j = 0; j < n2; ++j)
+        for (int l = 0; l < r; ++l) {
+            uint32_t o[4];
+            philox_seed(seed, (uint32_t)j, (uint32_t)l, 0u, 5u, o);
+            Y[j * r + l] = (o[0] & 1u) ? -1.0 : 1.0;
+        }
+    for (int it = 0; it < init_iters; ++it) {
+        for (int64_t i = 0; i < n1 * r; ++i) Z[i] = 0.0;
+        for (int64_t s = 0; s < cnt; ++s)
+            for (int l = 0; l < r; ++l) Z[(int64_t)I[s] * r + l] += w[s] * val[s] * Y[(int64_t)J[s] * r + l];
+        householder_q(n1, r, Z);
+        for (int64_t j = 0; j < n2 * r; ++j) Y[j] = 0.0;
+        for (int64_t s = 0; s < cnt; ++s)
+            for (int l = 0; l < r; ++l) Y[(int64_t)J[s] * r + l] += w[s] * val[s] * Z[(int64_t)I[s] * r + l];
+        householder_q(n2, r, Y);
+    }
+    /* trim */
+    if (trim_c > 0.0 && frobA > 0.0) {
+        for (int64_t i = 0; i < n1; ++i) {
+            double rn = 0.0;
+            for (int l = 0; l < r; ++l) rn += Z[i * r + l] * Z[i * r + l];
+            rn = sqrt(rn);
+            double thr = trim_c * sqrt((double)r) * a_norm[i] / frobA;
+            if (rn > thr)
+                for (int l = 0; l < r; ++l) Z[i * r + l] = 0.0;
+        }
+        householder_q(n1, r, Z);
+    }
+    memcpy(U, Z, sizeof(double) * (size_t)n1 * r);
+    for (int t = 0; t < T; ++t) {
+        or_als_half(r, n2, cnt, J, I, val, w, U, lam, V);
+        or_als_half(r, n1, cnt, I, J, val, w, V, lam, U);
+    }
+    free(w); free(Y); free(Z);
+}

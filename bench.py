@@ -1,0 +1,407 @@
+#!/usr/bin/env python
+"""Benchmark of the SMP-PCA hot path on B200 (driver contract).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg1] [--impl smp|reference]
+
+One STEP = one pass of the whole hot path over the
+configuration's synthetic input resident in HBM: the one-pass sketch with
+fused norms (K1/K2), the cross-GPU combine (one NCCL all-reduce when N > 1),
+finalize (K4), Ω + M̃ (K5/K6) and WAltMin (K7-K9).
+
+  value        = BASELINE metric part 1: bytes of A and B / time of the
+                 one-pass sketch+norms stage (first row block -> finalize
+                 complete, incl. the all-reduce), GB/s, max over ranks.
+  smp_pca_sec  = BASELINE metric part 2: whole Alg. 1 time per step.
+  ms_per_step  = whole step (Alg. 1) in ms.
+  e2e          = the same GB/s through the C ABI with HOST buffers (pinned),
+                 H2D copies inside the timed region, plus the whole e2e step.
+  roofline     = the dominant kernel K1 (sketch_tc_kernel), timed with CUDA
+                 events on its launching stream (smp_set_timing).
+
+--impl reference runs the CPU oracle (oracle/) as it stands on a bounded
+sample of the same workload (rank 0 only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import synth  # noqa: E402
+
+METRIC = "A,B GB/s through one-pass sketch+norms (roofline %); end-to-end SMP-PCA sec"
+L2_BYTES = 126 * 2**20
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return dict(hbm=float(d["hbm_gbs"]), tc=float(d["bf16_tflops"]),
+                    tc_sust=float(d.get("bf16_tflops_sustained", d["bf16_tflops"])), src="measured")
+    return dict(hbm=6650.0, tc=1590.0, tc_sust=1400.0, src="fallback")
+
+
+# --------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for ln in self.proc.stdout:
+            self.lines.append(ln.strip())
+
+    def stop(self):
+        if not self.proc:
+            return None
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx.append(float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return None
+        loaded = [s for s in sm if s > 0.5 * max(sm)] or sm
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": max(mx), "samples": len(sm),
+                "reasons": sorted(reasons)}
+
+
+# --------------------------------------------------------------------- data
+def shard_rows(d, world, rank, align=synth.GEN_BLOCK):
+    """Row shard of rank: equal generator-block-aligned ranges."""
+    nblk = (d + align - 1) // align
+    b0 = nblk * rank // world
+    b1 = nblk * (rank + 1) // world
+    return min(d, b0 * align), min(d, b1 * align)
+
+
+def make_inputs(cfgname, cfg, r0, r1, device):
+    n1, n2 = cfg["n1"], cfg["n2"]
+    if cfgname == "cfg1":
+        VA = synth.lowrank_factors(n1, 20, cfg["seed"], 0, device)
+        VB = synth.lowrank_factors(n2, 20, cfg["seed"], 1, device)
+        return synth.lowrank_block(r0, r1 - r0, n1, cfg["seed"], VA, VB, device=device)
+    if cfgname == "cfg2":
+        return synth.cone_block(r0, r1 - r0, n1, cfg["seed"], 30.0, device=device)
+    if cfgname == "cfg0":
+        A, B = synth.cone_tiny(cfg["d"], n1, seed=cfg["seed"])
+        return A[r0:r1].to(device), B[r0:r1].to(device)
+    if cfgname == "cfg4":
+        W, sig, D = synth.pca_params(n1, cfg["seed"], device=device)
+        return synth.pca_block(r0, r1 - r0, n1, cfg["seed"], W, sig, D, device=device), None
+    raise ValueError(f"{cfgname}: dense bench configs are cfg0, cfg1, cfg2, cfg4")
+
+
+def dtype_name(cfg):
+    return {"bf16": "bf16", "f32": "f32", "csr": "f32"}[cfg["dtype"]]
+
+
+def pi_code(cfg):
+    return {"rademacher": 0, "gaussian": 1}[cfg["pi"]]
+
+
+# --------------------------------------------------------------------- oracle arms
+def oracle_sample_rate(cfgname, cfg, target_s, max_rows=None):
+    """Time the CPU oracle's one-pass sketch+norms on the first rows of the
+    workload (CPU-generated, same distribution); returns (GB/s, info)."""
+    import oracle
+    n1, n2, k = cfg["n1"], cfg["n2"], cfg["k"]
+    a_is_b = cfg.get("a_is_b", False)
+    es = 2 if cfg["dtype"] == "bf16" else 4
+    probe = 256
+    A, B = make_inputs(cfgname, cfg, 0, min(cfg["d"], synth.GEN_BLOCK), "cpu")
+
+    def host(X):
+        return synth.bf16_bits(X) if X.dtype == torch.bfloat16 else X.numpy()
+
+    def run(rows):
+        t0 = time.perf_counter()
+        oracle.sketch_rows(pi_code(cfg), cfg["seed"], k, host(A[:rows]))
+        if not a_is_b:
+            oracle.sketch_rows(pi_code(cfg), cfg["seed"], k, host(B[:rows]))
+        return time.perf_counter() - t0
+
+    t = run(probe)
+    rows = int(min(A.shape[0] if max_rows is None else max_rows,
+                   max(probe, probe * target_s / max(t, 1e-6))))
+    t = run(rows)
+    nbytes = rows * (n1 + (0 if a_is_b else n2)) * es
+    info = {"rows": rows, "seconds": t, "bytes": nbytes, "cores": oracle.num_threads(),
+            "sample": f"oracle one-pass sketch+norms (fp64, C/OpenMP) of the first {rows} of "
+                      f"{cfg['d']} rows of A{'' if a_is_b else ' and B'} ({n1}"
+                      f"{'' if a_is_b else '+' + str(n2)} columns, k={k})"}
+    return nbytes / t / 1e9, info
+
+
+def run_reference(args, cfgname, cfg, world, rank):
+    if rank != 0:
+        return
+    per_step = []
+    info = None
+    # size each step to ~ (3 min) / (K + W) of CPU work
+    budget = max(2.0, min(20.0, 150.0 / (args.steps + args.warmup)))
+    for s in range(args.warmup + args.steps):
+        rate, info = oracle_sample_rate(cfgname, cfg, budget)
+        if s >= args.warmup:
+            per_step.append(info["seconds"])
+    value = info["bytes"] / statistics.mean(per_step) / 1e9
+    out = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * statistics.mean(per_step), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": cfgname, "d": cfg["d"], "n1": cfg["n1"], "n2": cfg["n2"],
+                   "k": cfg["k"], "sample_rows_per_step": info["rows"]},
+        "cpu_baseline": {"value": value, "unit": "GB/s", "cores": info["cores"], "kind": "oracle",
+                         "sample": info["sample"]},
+        "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out), flush=True)
+
+
+# --------------------------------------------------------------------- main arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="cfg1")
+    ap.add_argument("--impl", default="smp", choices=["smp", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--init-iters", type=int, default=30)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 0)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    cfgname = args.config
+    cfg = synth.CONFIGS[cfgname]
+
+    if args.impl == "reference":
+        run_reference(args, cfgname, cfg, world, rank)
+        return
+
+    import torch.distributed as dist
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    from paper_1610_06656_b200 import SMPSketch, IN_DENSE_BF16, IN_DENSE_F32
+
+    d, n1, n2, k = cfg["d"], cfg["n1"], cfg["n2"], cfg["k"]
+    a_is_b = cfg.get("a_is_b", False)
+    r0, r1 = shard_rows(d, world, rank)
+    A, B = make_inputs(cfgname, cfg, r0, r1, dev)
+    inp = IN_DENSE_BF16 if A.dtype == torch.bfloat16 else IN_DENSE_F32
+    es = A.element_size()
+    total_bytes = d * (n1 + (0 if a_is_b else n2)) * es
+    m = synth.m_of(cfg)
+    r, T = cfg["r"], cfg["T"]
+    stream = torch.cuda.current_stream(dev)
+    sk = SMPSketch(d, n1, n2, k, pi=pi_code(cfg), seed=cfg["seed"], a_is_b=a_is_b, input=inp,
+                   row_begin=r0, row_end=r1, stream=stream, device=dev)
+
+    def combine():
+        if world > 1:
+            a, b = sk.partials()
+            dist.all_reduce(a)
+            dist.all_reduce(b)
+
+    def step(evs, host=None):
+        sk.reset()
+        evs[0].record(stream)
+        if host is None:
+            sk.block(r0, A, B)
+        else:
+            sk.block_host(r0, host[0], host[1])
+        combine()
+        sk.finalize()
+        evs[1].record(stream)
+        I, J, val, qh = sk.sample_estimate(m, cfg["seed"])
+        U, V = sk.waltmin(I, J, val, qh, r, T, init_iters=args.init_iters, seed=cfg["seed"])
+        if host is not None:
+            Uh, Vh = U.cpu(), V.cpu()  # D2H of the result
+        evs[2].record(stream)
+        return int(I.numel()), U, V
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local_rank])
+        torch.cuda.synchronize(dev)
+
+    # warm-up
+    for _ in range(args.warmup):
+        step([torch.cuda.Event(enable_timing=True) for _ in range(3)])
+    # timed region (inputs 4.3+ GB >> 126 MB L2: no flush needed)
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    sk.set_timing(True)
+    sk.kernel_timing()
+    launches0 = sk.kernel_launches
+    barrier()
+    nomega = 0
+    for s in range(args.steps):
+        nomega, _, _ = step(evs[s])
+    barrier()
+    launches = sk.kernel_launches - launches0
+    k1_ms, k1_n = sk.kernel_timing()
+    sk.set_timing(False)
+    clk = clocks.stop()
+    t_sketch = sum(e[0].elapsed_time(e[1]) for e in evs) / args.steps
+    t_step = sum(e[0].elapsed_time(e[2]) for e in evs) / args.steps
+    if world > 1:
+        t = torch.tensor([t_sketch, t_step, k1_ms / max(k1_n, 1)], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_sketch, t_step, k1_avg = t.tolist()
+    else:
+        k1_avg = k1_ms / max(k1_n, 1)
+
+    value = total_bytes / (t_sketch * 1e-3) / 1e9
+
+    # roofline of K1 (per launch = one matrix over this rank's rows)
+    pk = peaks()
+    rows = r1 - r0
+    planes = 3 if inp == IN_DENSE_F32 else 1
+    launches_per_step = max(k1_n // max(args.steps, 1), 1)
+    ncols_total = (n1 + (0 if a_is_b else n2))
+    flops_launch = 2.0 * k * rows * ncols_total * planes / launches_per_step
+    bytes_launch = rows * ncols_total * 2 * planes / launches_per_step
+    t_hbm = bytes_launch / (pk["hbm"] * 1e9)
+    t_tc = flops_launch / (pk["tc"] * 1e12)
+    traffic = None
+    tfile = os.path.join(ROOT, "profiles", "k1_traffic.json")
+    if os.path.exists(tfile):
+        traffic = json.load(open(tfile)).get(cfgname)
+    if t_tc >= t_hbm:
+        ach = flops_launch / (k1_avg * 1e-3) / 1e12
+        roof = {"bound": "tensor", "achieved": ach, "peak": pk["tc"], "unit": "TFLOP/s",
+                "frac": ach / pk["tc"], "traffic": traffic, "kernel": "sketch_tc_kernel",
+                "peak_source": pk["src"] + " burst bf16 dense (MEASURED_PEAKS.json)"}
+        alt_ach = bytes_launch / (k1_avg * 1e-3) / 1e9
+        roof["hbm_view"] = {"achieved": alt_ach, "peak": pk["hbm"], "unit": "GB/s",
+                            "frac": alt_ach / pk["hbm"]}
+    else:
+        ach = bytes_launch / (k1_avg * 1e-3) / 1e9
+        roof = {"bound": "hbm", "achieved": ach, "peak": pk["hbm"], "unit": "GB/s",
+                "frac": ach / pk["hbm"], "traffic": traffic, "kernel": "sketch_tc_kernel",
+                "peak_source": pk["src"] + " HBM copy bandwidth (MEASURED_PEAKS.json)"}
+        alt = flops_launch / (k1_avg * 1e-3) / 1e12
+        roof["tensor_view"] = {"achieved": alt, "peak": pk["tc"], "unit": "TFLOP/s",
+                               "frac": alt / pk["tc"]}
+    roof["k1_ms_per_launch"] = k1_avg
+    roof["algorithmic_per_launch"] = {"flops": flops_launch, "bytes": bytes_launch}
+    roofline_time = max(total_bytes / (pk["hbm"] * 1e9),
+                        2.0 * k * d * ncols_total * planes / (pk["tc"] * 1e12))
+
+    # e2e through the C ABI with pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        Ah = torch.empty(A.shape, dtype=A.dtype, pin_memory=True)
+        Ah.copy_(A)
+        Bh = None
+        if B is not None:
+            Bh = torch.empty(B.shape, dtype=B.dtype, pin_memory=True)
+            Bh.copy_(B)
+        step([torch.cuda.Event(enable_timing=True) for _ in range(3)], host=(Ah, Bh))
+        ee = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.e2e_steps)]
+        barrier()
+        for s in range(args.e2e_steps):
+            step(ee[s], host=(Ah, Bh))
+        barrier()
+        te_sk = sum(e[0].elapsed_time(e[1]) for e in ee) / args.e2e_steps
+        te_all = sum(e[0].elapsed_time(e[2]) for e in ee) / args.e2e_steps
+        if world > 1:
+            t = torch.tensor([te_sk, te_all], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            te_sk, te_all = t.tolist()
+        e2e = {"value": total_bytes / (te_sk * 1e-3) / 1e9, "unit": "GB/s",
+               "h2d_bytes_per_step": int(A.numel() * es + (0 if B is None else B.numel() * es)),
+               "d2h_bytes_per_step": int((n1 + n2) * r * 4),
+               "smp_pca_sec": te_all * 1e-3, "steps": args.e2e_steps,
+               "path": "smp_sketch_block_host (library-staged pinned H2D, double-buffered) + finalize + sample_estimate + waltmin + D2H(U,V)"}
+        del Ah, Bh
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        rate, info = oracle_sample_rate(cfgname, cfg, 15.0)
+        cpu = {"value": rate, "unit": "GB/s", "cores": info["cores"], "kind": "oracle",
+               "sample": info["sample"] + f"; {info['seconds']:.1f} s"}
+
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_step,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": dtype_name(cfg), "data": "synthetic",
+            "config": {"workload": cfgname, "d": d, "n1": n1, "n2": n2, "k": k,
+                       "pi": cfg["pi"], "r": r, "T": T, "m": m, "omega": nomega,
+                       "init_iters": args.init_iters, "a_is_b": a_is_b,
+                       "parallelism": f"row-shard x{world} + NCCL all-reduce" if world > 1 else "1 GPU",
+                       "l2": "inputs (%.1f GB) larger than the 126 MB L2; no flush" % (total_bytes / 1e9),
+                       "value_scope": "A+B bytes / (sketch_block .. finalize) time; ms_per_step = whole Alg. 1"},
+            "smp_pca_sec": t_step * 1e-3,
+            "sketch_ms": t_sketch,
+            "roofline_pct_of_stage": 100.0 * roofline_time / (t_sketch * 1e-3),
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": int(launches),
+            "clocks": clk,
+        }
+        print(json.dumps(out), flush=True)
+    sk.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -274,3 +274,10 @@ def smp_pca(A, B, k, r, m, T, pi_kind=PI_RADEMACHER, seed=0, omega_seed=None,
                    init_iters=init_iters, trim_c=trim_c, lam=lam, seed=wm_seed)
     return dict(Ask=Ask, Bsk=Bsk, a2=a2, b2=b2, FA=FA, FB=FB, As=As, Bs=Bs, DA=DA, DB=DB,
                 alpha=al, beta=be, I=I, J=J, qhat=q, Mt=Mt, U=U, V=V)
+
+
+def num_threads() -> int:
+    """OpenMP threads used by the oracle (the CPU baseline's core count)."""
+    lib = _get()
+    lib.or_num_threads.restype = ctypes.c_int
+    return int(lib.or_num_threads())

@@ -72,8 +72,13 @@ double or_pi_rademacher(uint64_t seed, int64_t kappa, int64_t t)
     uint32_t w[4];
     philox_seed(seed, (uint32_t)((uint64_t)t >> 7), (uint32_t)kappa,
                 (uint32_t)((uint64_t)t >> 39), 1u, w);
+    /* row offset b = t & 127 lives in word b >> 5; inside the word, element
+       e = b & 31 sits at bit (e >> 1) + 16 (e & 1): even rows use bits 0..15,
+       odd rows bits 16..31. */
     unsigned b = (unsigned)(t & 127);
-    unsigned bit = (w[b >> 5] >> (b & 31)) & 1u;
+    unsigned e = b & 31u;
+    unsigned pos = (e >> 1) + ((e & 1u) << 4);
+    unsigned bit = (w[b >> 5] >> pos) & 1u;
     return bit ? -1.0 : 1.0;
 }
 
@@ -522,3 +527,11 @@ void or_waltmin(int64_t n1, int64_t n2, int r, int T, int init_iters, double tri
     }
     free(w); free(Y); free(Z);
 }
+
+/* Threads the oracle's OpenMP loops use (reported as the CPU baseline's cores). */
+#ifdef _OPENMP
+#include <omp.h>
+int or_num_threads(void) { return omp_get_max_threads(); }
+#else
+int or_num_threads(void) { return 1; }
+#endif

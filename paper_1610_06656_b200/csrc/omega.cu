@@ -1,0 +1,219 @@
+// K5: biased Bernoulli sample Ω (Alg. 1 line 3; Eq. 1,
+// P:70-73) and K6: rescaled-JL estimates on Ω (Alg. 1 line 4; Eq. 2,
+// P:80-83).
+//
+//   alpha_i = a2_i / ((2 n2) FA),  beta_j = b2_j / ((2 n1) FB)       (R6)
+//   q̂_ij   = min(1, m (alpha_i + beta_j))                            (Eq. 1)
+//   (i,j) ∈ Ω  iff  U53(Philox(ctr=(i,j,0,3), key=seed)) 2^-53 < q̂_ij   (§3.4)
+//   M̃_ij   = D_A[i] D_B[j] <Ã_i, B̃_j>                               (Eq. 2)
+//
+// fp64 arithmetic uses explicitly rounded intrinsics (no FMA contraction) so
+// q̂ — and therefore Ω — is bit-identical to the written definition.
+// Ω is produced in (i,j) order by a count pass, an exclusive scan of block
+// counts and a write pass that recomputes the same draws.
+#include "smp_device.cuh"
+#include "smp_kernels.h"
+
+namespace smp {
+
+constexpr int OM_THREADS = 256;
+constexpr int OM_PER_THREAD = 16;
+constexpr int64_t OM_PER_BLOCK = (int64_t)OM_THREADS * OM_PER_THREAD;
+
+__global__ void alpha_beta_kernel(const double* __restrict__ a2, int64_t n1,
+                                  const double* __restrict__ b2, int64_t n2,
+                                  const double* __restrict__ FAFB, double* __restrict__ alpha,
+                                  double* __restrict__ beta) {
+  const double da = __dmul_rn(__dmul_rn(2.0, (double)n2), FAFB[0]);
+  const double db = __dmul_rn(__dmul_rn(2.0, (double)n1), FAFB[1]);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n1 + n2;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    if (i < n1) alpha[i] = __ddiv_rn(a2[i], da);
+    else beta[i - n1] = __ddiv_rn(b2[i - n1], db);
+  }
+}
+
+cudaError_t launch_alpha_beta(const double* a2, int64_t n1, const double* b2, int64_t n2,
+                              const double* FAFB, double* alpha, double* beta, cudaStream_t st) {
+  int blocks = (int)std::min<int64_t>((n1 + n2 + 255) / 256, 1024);
+  alpha_beta_kernel<<<blocks, 256, 0, st>>>(a2, n1, b2, n2, FAFB, alpha, beta);
+  return cudaGetLastError();
+}
+
+__device__ __forceinline__ double qhat_of(double m, double al, double be) {
+  const double q = __dmul_rn(m, __dadd_rn(al, be));
+  return q < 1.0 ? q : 1.0;
+}
+
+__device__ __forceinline__ bool draw(uint32_t k0, uint32_t k1, uint32_t i, uint32_t j, double qh) {
+  const u32x4 w = philox4x32_10(i, j, 0u, TAG_OMEGA, k0, k1);
+  const uint64_t u53 = (((uint64_t)w.y << 32) | (uint64_t)w.x) >> 11;
+  const double u = __dmul_rn(__ull2double_rn(u53), 0x1p-53);
+  return u < qh;
+}
+
+// per-thread bitmask of hits among its 16 consecutive pairs
+__device__ __forceinline__ uint32_t thread_hits(const double* __restrict__ alpha,
+                                                const double* __restrict__ beta, int64_t n2,
+                                                int64_t N, double m, uint32_t k0, uint32_t k1,
+                                                int64_t P0) {
+  uint32_t mask = 0;
+  if (P0 >= N) return 0;
+  int64_t i = P0 / n2, j = P0 - i * n2;
+  double al = alpha[i];
+#pragma unroll 4
+  for (int e = 0; e < OM_PER_THREAD; ++e) {
+    if (P0 + e < N) {
+      const double qh = qhat_of(m, al, beta[j]);
+      if (draw(k0, k1, (uint32_t)i, (uint32_t)j, qh)) mask |= 1u << e;
+      if (++j == n2) { j = 0; ++i; if (i * n2 < N) al = alpha[i]; }
+    }
+  }
+  return mask;
+}
+
+// block-wide exclusive scan of one int per thread; returns the block total
+__device__ __forceinline__ int block_excl_scan(int v, int& excl) {
+  __shared__ int wsum[OM_THREADS / 32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) wsum[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    int s = lane < OM_THREADS / 32 ? wsum[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int y = __shfl_up_sync(0xffffffffu, s, o);
+      if (lane >= o) s += y;
+    }
+    if (lane < OM_THREADS / 32) wsum[lane] = s;
+  }
+  __syncthreads();
+  const int wprefix = wid > 0 ? wsum[wid - 1] : 0;
+  excl = wprefix + x - v;
+  const int total = wsum[OM_THREADS / 32 - 1];
+  __syncthreads();
+  return total;
+}
+
+__global__ void __launch_bounds__(OM_THREADS)
+omega_count_kernel(const double* __restrict__ alpha, const double* __restrict__ beta, int64_t n1,
+                   int64_t n2, double m, uint64_t seed, int64_t* __restrict__ blk_counts) {
+  const int64_t N = n1 * n2;
+  const int64_t P0 = blockIdx.x * OM_PER_BLOCK + (int64_t)threadIdx.x * OM_PER_THREAD;
+  const uint32_t mask = thread_hits(alpha, beta, n2, N, m, (uint32_t)seed, (uint32_t)(seed >> 32), P0);
+  int excl;
+  const int tot = block_excl_scan(__popc(mask), excl);
+  if (threadIdx.x == 0) blk_counts[blockIdx.x] = tot;
+}
+
+int64_t omega_num_blocks(int64_t n1, int64_t n2) { return (n1 * n2 + OM_PER_BLOCK - 1) / OM_PER_BLOCK; }
+
+cudaError_t launch_omega_count(const double* alpha, const double* beta, int64_t n1, int64_t n2,
+                               double m, uint64_t seed, int64_t* blk_counts, cudaStream_t st) {
+  const int64_t nb = omega_num_blocks(n1, n2);
+  if (nb == 0) return cudaSuccess;
+  omega_count_kernel<<<(unsigned)nb, OM_THREADS, 0, st>>>(alpha, beta, n1, n2, m, seed, blk_counts);
+  return cudaGetLastError();
+}
+
+// single-block exclusive scan of the block counts (in place); *total = sum
+__global__ void scan_counts_kernel(int64_t* __restrict__ c, int64_t nblk, int64_t* __restrict__ total) {
+  __shared__ int64_t part[1024];
+  const int tid = threadIdx.x;
+  const int64_t per = (nblk + 1023) / 1024;
+  const int64_t b0 = tid * per, b1 = min(nblk, b0 + per);
+  int64_t s = 0;
+  for (int64_t b = b0; b < b1; ++b) s += c[b];
+  part[tid] = s;
+  __syncthreads();
+  if (tid == 0) {
+    int64_t run = 0;
+    for (int q = 0; q < 1024; ++q) { int64_t v = part[q]; part[q] = run; run += v; }
+    *total = run;
+  }
+  __syncthreads();
+  int64_t run = part[tid];
+  for (int64_t b = b0; b < b1; ++b) { int64_t v = c[b]; c[b] = run; run += v; }
+}
+
+cudaError_t launch_scan_counts(int64_t* blk_counts, int64_t nblk, int64_t* total, cudaStream_t st) {
+  scan_counts_kernel<<<1, 1024, 0, st>>>(blk_counts, nblk, total);
+  return cudaGetLastError();
+}
+
+__global__ void __launch_bounds__(OM_THREADS)
+omega_write_kernel(const double* __restrict__ alpha, const double* __restrict__ beta, int64_t n1,
+                   int64_t n2, double m, uint64_t seed, const int64_t* __restrict__ blk_offsets,
+                   const int64_t* __restrict__ total, int64_t cap, int32_t* __restrict__ I,
+                   int32_t* __restrict__ J, double* __restrict__ qhat) {
+  if (*total > cap) return;  // caller re-calls with a larger buffer
+  const int64_t N = n1 * n2;
+  const int64_t P0 = blockIdx.x * OM_PER_BLOCK + (int64_t)threadIdx.x * OM_PER_THREAD;
+  const uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
+  const uint32_t mask = thread_hits(alpha, beta, n2, N, m, k0, k1, P0);
+  int excl;
+  block_excl_scan(__popc(mask), excl);
+  int64_t pos = blk_offsets[blockIdx.x] + excl;
+  uint32_t mm = mask;
+  while (mm) {
+    const int e = __ffs(mm) - 1;
+    mm &= mm - 1;
+    const int64_t P = P0 + e;
+    const int64_t i = P / n2, j = P - i * n2;
+    I[pos] = (int32_t)i;
+    J[pos] = (int32_t)j;
+    qhat[pos] = qhat_of(m, alpha[i], beta[j]);
+    ++pos;
+  }
+}
+
+cudaError_t launch_omega_write(const double* alpha, const double* beta, int64_t n1, int64_t n2,
+                               double m, uint64_t seed, const int64_t* blk_offsets,
+                               const int64_t* total, int64_t cap, int32_t* I, int32_t* J,
+                               double* qhat, cudaStream_t st) {
+  const int64_t nb = omega_num_blocks(n1, n2);
+  if (nb == 0) return cudaSuccess;
+  omega_write_kernel<<<(unsigned)nb, OM_THREADS, 0, st>>>(alpha, beta, n1, n2, m, seed, blk_offsets,
+                                                          total, cap, I, J, qhat);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- K6 SDDMM
+// one warp per sample; Ω is sorted by i so consecutive warps reuse Ã_i.
+__global__ void sddmm_kernel(const float* __restrict__ Ask, const float* __restrict__ Bsk,
+                             const double* __restrict__ DA, const double* __restrict__ DB, int k,
+                             const int32_t* __restrict__ I, const int32_t* __restrict__ J,
+                             const int64_t* __restrict__ total, int64_t cap, int plain,
+                             float* __restrict__ val) {
+  if (*total > cap) return;  // Ω not written (capacity); nothing to estimate
+  const int64_t cnt = *total;
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t s = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); s < cnt; s += nw) {
+    const int64_t i = I[s], j = J[s];
+    const float* a = Ask + i * k;
+    const float* b = Bsk + j * k;
+    double dot = 0.0;
+    for (int kp = lane; kp < k; kp += 32) dot = fma((double)__ldg(a + kp), (double)__ldg(b + kp), dot);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+    if (lane == 0) val[s] = plain ? (float)dot : (float)(__dmul_rn(__dmul_rn(DA[i], DB[j]), dot));
+  }
+}
+
+cudaError_t launch_sddmm(const float* Ask, const float* Bsk, const double* DA, const double* DB,
+                         int k, const int32_t* I, const int32_t* J, const int64_t* total,
+                         int64_t cap, int plain, float* val, cudaStream_t st) {
+  int blocks = (int)std::min<int64_t>((cap + 7) / 8, 148 * 16);
+  if (blocks < 1) blocks = 1;
+  sddmm_kernel<<<blocks, 256, 0, st>>>(Ask, Bsk, DA, DB, k, I, J, total, cap, plain, val);
+  return cudaGetLastError();
+}
+
+}  // namespace smp

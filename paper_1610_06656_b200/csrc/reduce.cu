@@ -1,0 +1,178 @@
+// K2 (partial combine), fp32 split planes, K4 (finalize, P:82,
+// P:313) and the R5 pairwise Frobenius tree.  All reductions use a fixed
+// order so that results are bit-reproducible run to run.
+#include "smp_device.cuh"
+#include "smp_kernels.h"
+
+namespace smp {
+
+// ---------------------------------------------------------------- K2
+template <int VEC>
+__global__ void reduce_sketch_kernel(const float* __restrict__ part, int splits, int planes,
+                                     int64_t n, int k, float* __restrict__ acc) {
+  const int64_t total = n * (int64_t)k / VEC;
+  const int64_t part_stride = (int64_t)planes * n * k;  // floats per split
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < total;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = v * VEC;  // element index c*k + κ
+    float s[VEC];
+#pragma unroll
+    for (int q = 0; q < VEC; ++q) s[q] = 0.f;
+    for (int sp = 0; sp < splits; ++sp) {
+      for (int pl = 0; pl < planes; ++pl) {
+        const float* src = part + sp * part_stride + (int64_t)pl * n * k + e;
+        if constexpr (VEC == 4) {
+          const float4 x = __ldg(reinterpret_cast<const float4*>(src));
+          s[0] += x.x; s[1] += x.y; s[2] += x.z; s[3] += x.w;
+        } else {
+          s[0] += __ldg(src);
+        }
+      }
+    }
+    if constexpr (VEC == 4) {
+      float4* dst = reinterpret_cast<float4*>(acc + e);
+      float4 a = *dst;
+      a.x += s[0]; a.y += s[1]; a.z += s[2]; a.w += s[3];
+      *dst = a;
+    } else {
+      acc[e] += s[0];
+    }
+  }
+}
+
+cudaError_t launch_reduce_sketch(const float* part, int splits, int planes, int64_t n, int k,
+                                 float* acc, cudaStream_t st) {
+  const int threads = 256;
+  if (k % 4 == 0) {
+    int64_t tot = n * k / 4;
+    int blocks = (int)std::min<int64_t>((tot + threads - 1) / threads, 148 * 16);
+    reduce_sketch_kernel<4><<<blocks, threads, 0, st>>>(part, splits, planes, n, k, acc);
+  } else {
+    int64_t tot = n * k;
+    int blocks = (int)std::min<int64_t>((tot + threads - 1) / threads, 148 * 16);
+    reduce_sketch_kernel<1><<<blocks, threads, 0, st>>>(part, splits, planes, n, k, acc);
+  }
+  return cudaGetLastError();
+}
+
+__global__ void reduce_norms_kernel(const double* __restrict__ pnorm, int slots, int64_t n,
+                                    double* __restrict__ nacc) {
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < n;
+       c += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int q = 0; q < slots; ++q) s += pnorm[(int64_t)q * n + c];
+    nacc[c] += s;
+  }
+}
+
+cudaError_t launch_reduce_norms(const double* pnorm, int slots, int64_t n, double* nacc,
+                                cudaStream_t st) {
+  int blocks = (int)std::min<int64_t>((n + 255) / 256, 1024);
+  reduce_norms_kernel<<<blocks, 256, 0, st>>>(pnorm, slots, n, nacc);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- fp32 split
+// x = hi + mid + lo exactly (three bf16 terms, 8+8+8 significant bits),
+// so Π·X = Π·hi + Π·mid + Π·lo with every tensor-core product exact.
+__device__ __forceinline__ uint16_t bf16_bits_rne(float x) { return bf16_rne_bits(x); }
+
+__global__ void split_f32_kernel(const float* __restrict__ X, int64_t ldx, int64_t rows, int64_t n,
+                                 uint16_t* __restrict__ planes, int64_t ldp,
+                                 double* __restrict__ pnorm, int seg_rows) {
+  const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t seg = blockIdx.y;
+  if (c >= n) return;
+  const int64_t r0 = seg * seg_rows;
+  const int64_t r1 = min(rows, r0 + seg_rows);
+  double s2 = 0.0;
+  for (int64_t t = r0; t < r1; ++t) {
+    const float x = X[t * ldx + c];
+    const uint16_t h = bf16_bits_rne(x);
+    const float r_1 = __fsub_rn(x, bf16_bits_to_float(h));
+    const uint16_t m = bf16_bits_rne(r_1);
+    const float r_2 = __fsub_rn(r_1, bf16_bits_to_float(m));
+    const uint16_t l = bf16_bits_rne(r_2);
+    uint16_t* row = planes + t * ldp;
+    row[c] = h;
+    row[n + c] = m;
+    row[2 * n + c] = l;
+    const double xd = (double)x;
+    s2 = fma(xd, xd, s2);
+  }
+  pnorm[seg * n + c] = s2;
+}
+
+cudaError_t launch_split_f32(const float* X, int64_t ldx, int64_t rows, int64_t n, uint16_t* planes,
+                             int64_t ldp, double* pnorm, int seg_rows, cudaStream_t st) {
+  dim3 grid((unsigned)((n + 127) / 128), (unsigned)((rows + seg_rows - 1) / seg_rows));
+  split_f32_kernel<<<grid, 128, 0, st>>>(X, ldx, rows, n, planes, ldp, pnorm, seg_rows);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- K4
+// One warp per column: Ã_c = acc_c * fp32(1/sqrt(k)); ||Ã_c|| in fp64;
+// D_c = ||X_c|| / ||Ã_c|| (0 if ||Ã_c|| = 0).
+__global__ void finalize_kernel(const float* __restrict__ acc, const double* __restrict__ nacc,
+                                int64_t n, int k, float scale, float* __restrict__ out,
+                                double* __restrict__ sknorm, double* __restrict__ D,
+                                int* __restrict__ status) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t c = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); c < n;
+       c += warps) {
+    double s2 = 0.0;
+    for (int kp = lane; kp < k; kp += 32) {
+      const float v = __fmul_rn(acc[c * k + kp], scale);
+      out[c * k + kp] = v;
+      s2 = fma((double)v, (double)v, s2);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+    if (lane == 0) {
+      const double sn = sqrt(s2);
+      const double a2 = nacc[c];
+      sknorm[c] = sn;
+      D[c] = sn > 0.0 ? sqrt(a2) / sn : 0.0;
+      if (!(a2 == a2) || !(sn == sn) || isinf(a2)) atomicOr(status, 1);
+    }
+  }
+}
+
+cudaError_t launch_finalize(const float* acc, const double* nacc, int64_t n, int k, float scale,
+                            float* out, double* sknorm, double* D, int* status, cudaStream_t st) {
+  int blocks = (int)std::min<int64_t>((n + 7) / 8, 148 * 8);
+  if (blocks < 1) blocks = 1;
+  finalize_kernel<<<blocks, 256, 0, st>>>(acc, nacc, n, k, scale, out, sknorm, D, status);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- R5 tree
+// pad to a power of two with zeros, sum adjacent pairs level by level
+// (ping-pong buffers; identical tree to the written definition).
+__global__ void pairwise_sum_kernel(const double* __restrict__ x, int64_t n, int64_t p,
+                                    double* __restrict__ buf, double* __restrict__ out) {
+  double* a = buf;
+  double* b = buf + p;
+  for (int64_t i = threadIdx.x; i < p; i += blockDim.x) a[i] = i < n ? x[i] : 0.0;
+  __syncthreads();
+  int64_t len = p;
+  while (len > 1) {
+    len >>= 1;
+    for (int64_t i = threadIdx.x; i < len; i += blockDim.x) b[i] = a[2 * i] + a[2 * i + 1];
+    __syncthreads();
+    double* t = a; a = b; b = t;
+  }
+  if (threadIdx.x == 0) *out = p > 0 ? a[0] : 0.0;
+}
+
+cudaError_t launch_pairwise_sum(const double* x, int64_t n, double* scratch, double* out,
+                                cudaStream_t st) {
+  int64_t p = 1;
+  while (p < n) p <<= 1;
+  if (n <= 0) p = 0;
+  pairwise_sum_kernel<<<1, 1024, 0, st>>>(x, n, p, scratch, out);
+  return cudaGetLastError();
+}
+
+}  // namespace smp

@@ -1,0 +1,331 @@
+// K1: dense one-pass sketch with fused exact column norms (Alg. 1 line 2,
+// PAPER.md P:54; Step 1), on the sm_100a tensor cores.
+//
+//   part[split][c][κ] = Σ_{t in split's rows} Π(κ, t) · X[t, c]   (fp32, TMEM)
+//   pnorm[slot][c]    = Σ_{t in split's rows} X[t, c]^2          (fp64, SIMT)
+//
+// GEMM view: D (κ × c) += Π (κ × t) · X (t × c), M = κ, N = c, K = t.
+//   * X tile (64 rows × 256 cols bf16) arrives by TMA, 128B-swizzled, as
+//     four 64×64 boxes: the B operand, MN-major.
+//   * Π tile (256 κ × 64 t bf16) is never read from memory: 4 generator
+//     warps regenerate it from the Philox hash straight into a K-major
+//     128B-swizzled SMEM tile (the A operand).  Π is stored nowhere else.
+//   * one elected thread issues tcgen05.mma (M=128, N=256, K=16) for the two
+//     κ halves into a 512-column TMEM accumulator.
+//   * 4 norm warps read the same X stage from SMEM and accumulate x² in fp64
+//     (exact squares of bf16 values), so A and B are read from HBM once.
+//   * the same 4 warps drain TMEM (tcgen05.ld) into the split's partial slot.
+// Pipelines: full[s] (TMA tx + 4 generator-warp arrivals) -> MMA;
+//            empty[s] (tcgen05.commit + 4 norm-warp arrivals) -> TMA/gen.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include "smp_device.cuh"
+#include "smp_kernels.h"
+
+namespace smp {
+
+constexpr int TC_BM = 256;                        // κ rows per CTA tile
+constexpr int TC_BN = 256;                        // X columns per CTA tile
+constexpr int TC_BK = 64;                         // X rows per K-block
+constexpr int TC_STAGES = 3;
+constexpr int PI_STAGE = TC_BM * TC_BK * 2;       // 32 KB
+constexpr int X_STAGE = TC_BK * TC_BN * 2;        // 32 KB
+constexpr int NORM_RED = 4 * TC_BN * 8;           // 8 KB
+constexpr int TC_SMEM = TC_STAGES * (PI_STAGE + X_STAGE) + NORM_RED + 256 + 1024;
+constexpr int TC_THREADS = 384;
+
+struct RadCache {
+  uint64_t g;
+  uint32_t w0, w1, w2, w3;
+};
+
+// Word W (global index over 32-row words) of the Rademacher bit string of
+// row κ: group W>>2 = Philox(ctr=(g, κ, g>>32, 1)).
+__device__ __forceinline__ uint32_t rad_word(RadCache& c, uint64_t W, uint32_t kappa,
+                                             uint32_t k0, uint32_t k1) {
+  uint64_t g = W >> 2;
+  if (g != c.g) {
+    u32x4 w = philox4x32_10((uint32_t)g, kappa, (uint32_t)(g >> 32), TAG_RADEMACHER, k0, k1);
+    c.g = g; c.w0 = w.x; c.w1 = w.y; c.w2 = w.z; c.w3 = w.w;
+  }
+  uint32_t i = (uint32_t)(W & 3);
+  return i == 0 ? c.w0 : i == 1 ? c.w1 : i == 2 ? c.w2 : c.w3;
+}
+
+// Bit position of element e (0..31) inside its 32-row word: even rows use
+// bits 0..15, odd rows bits 16..31, so that a bf16 pair
+// (rows 2p, 2p+1) is built with one shift and one LOP3.
+__device__ __forceinline__ uint32_t rad_pos(uint32_t e) { return (e >> 1) | ((e & 1u) << 4); }
+
+// Generate one κ row of the Π tile (64 bf16 = 32 packed words) into regs.
+__device__ __forceinline__ void gen_pi_row(int kind, uint64_t seed, uint32_t kappa, bool valid,
+                                           uint64_t t0, RadCache& rc, uint32_t (&o)[32]) {
+  const uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
+  if (!valid) {
+#pragma unroll
+    for (int i = 0; i < 32; ++i) o[i] = 0u;
+    return;
+  }
+  if (kind == PI_RADEMACHER && (t0 & 31) == 0) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      uint32_t w = rad_word(rc, (t0 >> 5) + h, kappa, k0, k1);
+#pragma unroll
+      for (int p = 0; p < 16; ++p) o[16 * h + p] = 0x3F803F80u | ((w << (15 - p)) & 0x80008000u);
+    }
+  } else if (kind == PI_GAUSSIAN && (t0 & 3) == 0) {
+#pragma unroll 2
+    for (int q = 0; q < 16; ++q) {
+      uint64_t tq = (t0 >> 2) + q;
+      u32x4 w = philox4x32_10((uint32_t)tq, kappa, (uint32_t)(tq >> 32), TAG_GAUSSIAN, k0, k1);
+      uint16_t a, b, c, d;
+      gauss_pair(w.x, w.y, a, b);
+      gauss_pair(w.z, w.w, c, d);
+      o[2 * q] = (uint32_t)a | ((uint32_t)b << 16);
+      o[2 * q + 1] = (uint32_t)c | ((uint32_t)d << 16);
+    }
+  } else {
+    // generic (unaligned block start, Hadamard test mode): element by element
+#pragma unroll 1
+    for (int p = 0; p < 32; ++p) {
+      uint32_t lohi[2];
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        uint64_t t = t0 + 2 * p + e;
+        if (kind == PI_RADEMACHER) {
+          uint32_t w = rad_word(rc, t >> 5, kappa, k0, k1);
+          lohi[e] = ((w >> rad_pos((uint32_t)(t & 31))) & 1u) ? 0xBF80u : 0x3F80u;
+        } else {
+          lohi[e] = pi_bits(kind, seed, kappa, t);
+        }
+      }
+      o[p] = lohi[0] | (lohi[1] << 16);
+    }
+  }
+}
+
+// fp64 value of |bf16| from the 15 magnitude bits placed at [0,15) of v:
+// exponent field e != 0 -> hi word ((v << 13) + (896 << 20)); zero -> 0.
+// bf16 subnormals (e == 0, m != 0) are flushed (R25).
+__device__ __forceinline__ double bf16mag_to_f64(uint32_t v) {
+  uint32_t hi = (v & 0x7F80u) ? (v << 13) + 0x38000000u : 0u;
+  return __hiloint2double((int)hi, 0);
+}
+
+__global__ void __launch_bounds__(TC_THREADS, 1)
+sketch_tc_kernel(const __grid_constant__ CUtensorMap tmap, SketchTCParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw_addr = smem_u32(smem_raw);
+  uint8_t* smem = smem_raw + (((raw_addr + 1023u) & ~1023u) - raw_addr);
+  uint8_t* pi_s = smem;                                        // [stages][256][128 B]
+  uint8_t* x_s = smem + TC_STAGES * PI_STAGE;                  // [stages][4][64][128 B]
+  double* red = reinterpret_cast<double*>(x_s + TC_STAGES * X_STAGE);  // [4][256]
+  uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(red) + NORM_RED);
+  uint64_t* empty = full + TC_STAGES;
+  uint64_t* tmem_full = empty + TC_STAGES;
+  uint32_t* tmem_base_s = reinterpret_cast<uint32_t*>(tmem_full + 1);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  // tile decomposition: kt innermost so CTAs sharing an X tile run together
+  int bid = blockIdx.x;
+  const int kt = bid % p.k_tiles; bid /= p.k_tiles;
+  const int nt = bid % p.n_tiles; bid /= p.n_tiles;
+  const int split = bid;
+  const int kb_begin = (int)(((int64_t)split * p.kb_total) / p.splits);
+  const int kb_end = (int)(((int64_t)(split + 1) * p.kb_total) / p.splits);
+  const int nkb = kb_end - kb_begin;
+  const int n0 = nt * TC_BN, kappa0 = kt * TC_BM;
+  const int nh = (p.k - kappa0 > 128) ? 2 : 1;
+
+  if (tid == 0) {
+    for (int s = 0; s < TC_STAGES; ++s) { mbar_init(&full[s], 1 + 4); mbar_init(&empty[s], 1 + 4); }
+    mbar_init(tmem_full, 1);
+    fence_mbar_init();
+  }
+  if (warp == 0 && lane == 0) tma_prefetch_desc(&tmap);
+  if (warp == 1) tmem_alloc(tmem_base_s, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *tmem_base_s;
+
+  if (warp == 0) {
+    // ---------------- TMA producer
+    if (lane == 0) {
+      for (int it = 0; it < nkb; ++it) {
+        const int s = it % TC_STAGES;
+        const uint32_t ph = (uint32_t)(it / TC_STAGES) & 1u;
+        mbar_wait(&empty[s], ph ^ 1u);
+        mbar_arrive_expect_tx(&full[s], X_STAGE);
+        const int row = (kb_begin + it) * TC_BK;
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          tma_load_2d(x_s + s * X_STAGE + j * 8192, &tmap, &full[s], n0 + 64 * j, row);
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer (one thread)
+    if (lane == 0) {
+      const uint32_t idesc = make_idesc_bf16(128, 256, 0, 1);
+      const uint32_t pi_addr = smem_u32(pi_s), x_addr = smem_u32(x_s);
+      for (int it = 0; it < nkb; ++it) {
+        const int s = it % TC_STAGES;
+        const uint32_t ph = (uint32_t)(it / TC_STAGES) & 1u;
+        mbar_wait(&full[s], ph);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < TC_BK / 16; ++kk) {
+          const uint64_t bdesc = make_sdesc_sw128(x_addr + s * X_STAGE + kk * 2048, 8192, 1024);
+          for (int h = 0; h < nh; ++h) {
+            const uint64_t adesc =
+                make_sdesc_sw128(pi_addr + s * PI_STAGE + h * 16384 + kk * 32, 16, 1024);
+            tc_mma_f16(tbase + h * 256, adesc, bdesc, idesc, (it | kk) != 0 ? 1u : 0u);
+          }
+        }
+        tc_commit(&empty[s]);
+      }
+      tc_commit(tmem_full);
+    }
+  } else if (warp >= 4 && warp < 8) {
+    // ---------------- Π generators: thread g owns κ rows g and g+128
+    const int g = tid - 128;
+    RadCache rc0{~0ull, 0, 0, 0, 0}, rc1{~0ull, 0, 0, 0, 0};
+    for (int it = 0; it < nkb; ++it) {
+      const int s = it % TC_STAGES;
+      const uint32_t ph = (uint32_t)(it / TC_STAGES) & 1u;
+      const uint64_t t0 = (uint64_t)p.row0 + (uint64_t)(kb_begin + it) * TC_BK;
+      mbar_wait(&empty[s], ph ^ 1u);
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        const int kl = g + 128 * r;
+        if (r == 1 && nh == 1) break;
+        const int kappa = kappa0 + kl;
+        uint32_t o[32];
+        gen_pi_row(p.kind, p.seed, (uint32_t)kappa, kappa < p.k, t0, r == 0 ? rc0 : rc1, o);
+        uint8_t* rowp = pi_s + s * PI_STAGE + kl * 128;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          uint4 v = make_uint4(o[4 * c], o[4 * c + 1], o[4 * c + 2], o[4 * c + 3]);
+          *reinterpret_cast<uint4*>(rowp + ((c ^ (kl & 7)) << 4)) = v;
+        }
+      }
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&full[s]);
+    }
+  } else if (warp >= 8) {
+    // ---------------- norm warps (fp64 Σx²), then TMEM epilogue
+    const int g = tid - 256;
+    const int q = g & 31, rg = g >> 5;
+    const int box = q >> 3, chunk = q & 7;
+    double acc[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc[e] = 0.0;
+    for (int it = 0; it < nkb; ++it) {
+      const int s = it % TC_STAGES;
+      const uint32_t ph = (uint32_t)(it / TC_STAGES) & 1u;
+      mbar_wait(&full[s], ph);
+      const bool duty = p.do_norms && (((kb_begin + it) % p.k_tiles) == kt);
+      if (duty) {
+        const uint8_t* base = x_s + s * X_STAGE + box * 8192;
+#pragma unroll 4
+        for (int rr = 0; rr < 16; ++rr) {
+          const int r = rg + 4 * rr;
+          const uint4 v = *reinterpret_cast<const uint4*>(base + r * 128 + ((chunk ^ (r & 7)) << 4));
+          const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const double lo = bf16mag_to_f64(w[e] & 0x7FFFu);
+            const double hi = bf16mag_to_f64((w[e] >> 16) & 0x7FFFu);
+            acc[2 * e] = fma(lo, lo, acc[2 * e]);
+            acc[2 * e + 1] = fma(hi, hi, acc[2 * e + 1]);
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+    }
+    // norm partials: reduce the 4 row groups in a fixed order
+#pragma unroll
+    for (int e = 0; e < 8; ++e) red[rg * TC_BN + box * 64 + chunk * 8 + e] = acc[e];
+    named_bar_sync(1, 128);
+    const int slot = split * p.k_tiles + kt;
+    for (int col = g; col < TC_BN; col += 128) {
+      const double v = ((red[col] + red[TC_BN + col]) + red[2 * TC_BN + col]) + red[3 * TC_BN + col];
+      if (n0 + col < p.n) p.pnorm[(int64_t)slot * p.n + n0 + col] = v;
+    }
+    // TMEM -> partial slot
+    const int quad = warp & 3;
+    if (nkb > 0) {
+      mbar_wait(tmem_full, 0);
+      tc_fence_after();
+    }
+    for (int h = 0; h < nh; ++h) {
+      const int kappa = kappa0 + h * 128 + 32 * quad + lane;
+      for (int cc = 0; cc < TC_BN / 32; ++cc) {
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(tbase + ((uint32_t)(32 * quad) << 16) + h * 256 + cc * 32, r);
+        tc_wait_ld();
+        if (nkb == 0) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) r[j] = 0u;
+        }
+        if (kappa < p.k) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const int col = n0 + cc * 32 + j;
+            if (col < p.n) p.part[((int64_t)split * p.n + col) * p.k + kappa] = __uint_as_float(r[j]);
+          }
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tbase, 512);
+  }
+}
+
+// ---------------------------------------------------------------- host side
+static PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* ptr = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+  }
+  return fn;
+}
+
+int sketch_tc_smem_bytes() { return TC_SMEM; }
+
+cudaError_t launch_sketch_tc(const void* X, int64_t ldx, SketchTCParams p, cudaStream_t st) {
+  auto enc = get_encode_fn();
+  if (!enc) return cudaErrorNotSupported;
+  CUtensorMap tmap;
+  cuuint64_t dims[2] = {(cuuint64_t)p.n, (cuuint64_t)p.rows};
+  cuuint64_t strides[1] = {(cuuint64_t)ldx * 2};
+  cuuint32_t box[2] = {64, 64};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(&tmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(X), dims, strides,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(sketch_tc_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  const int grid = p.n_tiles * p.k_tiles * p.splits;
+  sketch_tc_kernel<<<grid, TC_THREADS, TC_SMEM, st>>>(tmap, p);
+  return cudaGetLastError();
+}
+
+}  // namespace smp

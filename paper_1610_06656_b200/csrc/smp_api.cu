@@ -1,0 +1,555 @@
+// libsmp.so: C-ABI implementation (include/smp.h).  Owns the handle, the
+// workspace and the launch sequence of the SMP-PCA hot path:
+//   sketch_block -> K1 (tcgen05 sketch + fused norms) -> K2 (split-K reduce)
+//   finalize     -> K4 + R5 pairwise Frobenius tree
+//   sample_est.  -> alpha/beta, K5 count, scan, K5 write, K6 SDDMM
+//   waltmin      -> K7-K9
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/smp.h"
+#include "smp_device.cuh"
+#include "smp_kernels.h"
+
+cudaError_t smp_convert_f64_f32(const double* x, int64_t n, float* y, cudaStream_t st);
+
+namespace smp {
+cudaError_t launch_sketch_csr(int kind, uint64_t seed, int k, int64_t row0, int64_t rows,
+                              const int64_t* a_rowptr, const int32_t* a_col, const float* a_val,
+                              int64_t a_n, float* a_acc, double* a_nrm, const int64_t* b_rowptr,
+                              const int32_t* b_col, const float* b_val, int64_t b_n, float* b_acc,
+                              double* b_nrm, cudaStream_t st);
+}
+
+struct smp_handle {
+  smp_sketch_desc d;
+  cudaStream_t st = nullptr;
+  int dev = 0;
+  int64_t n1 = 0, n2 = 0, ntot = 0;
+  int k = 0;
+  float* acc_sk = nullptr;     // [ntot][k] unscaled sums
+  double* acc_nrm = nullptr;   // [ntot]
+  float* part = nullptr;
+  int64_t part_cap = 0;
+  double* pnorm = nullptr;
+  int64_t pnorm_cap = 0;
+  uint16_t* planes = nullptr;
+  int64_t planes_cap = 0;
+  // finalized state
+  float* fin_sk = nullptr;     // [ntot][k]
+  double* fin_sknorm = nullptr;
+  double* fin_D = nullptr;
+  double* FAFB = nullptr;      // [2]
+  int* status = nullptr;
+  double* pw_scratch = nullptr;
+  int64_t pw_cap = 0;
+  bool finalized = false;
+  // sampling scratch
+  double* alpha = nullptr;     // [n1 + n2] (alpha then beta)
+  int64_t* blk = nullptr;
+  int64_t blk_cap = 0;
+  int64_t* d_total = nullptr;
+  int64_t* h_total = nullptr;  // pinned
+  int* h_status = nullptr;     // pinned
+  double* h_fafb = nullptr;    // pinned
+  // host staging
+  void* stage[2] = {nullptr, nullptr};
+  int64_t stage_bytes = 0;
+  cudaStream_t copy_st = nullptr;
+  cudaEvent_t ev_copied[2] = {nullptr, nullptr};
+  cudaEvent_t ev_used[2] = {nullptr, nullptr};
+  int64_t launches = 0;
+  // K1 timing instrumentation
+  bool timing = false;
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_used_n = 0;
+  std::string err;
+};
+
+namespace {
+
+smp_status fail(smp_handle* h, smp_status s, const char* fmt, ...) {
+  if (h) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    h->err = buf;
+  }
+  return s;
+}
+
+smp_status cuda_fail(smp_handle* h, cudaError_t e, const char* where) {
+  return fail(h, SMP_ECUDA, "%s: %s", where, cudaGetErrorString(e));
+}
+
+#define CK(h, x, where)                                 \
+  do {                                                  \
+    cudaError_t e_ = (x);                               \
+    if (e_ != cudaSuccess) return cuda_fail(h, e_, where); \
+  } while (0)
+
+template <class T>
+cudaError_t ensure(T*& p, int64_t& cap, int64_t need) {
+  if (need <= cap) return cudaSuccess;
+  if (p) cudaFree(p);
+  p = nullptr;
+  cap = 0;
+  cudaError_t e = cudaMalloc(&p, (size_t)need * sizeof(T));
+  if (e == cudaSuccess) cap = need;
+  return e;
+}
+
+bool is_pow2(int64_t x) { return x > 0 && (x & (x - 1)) == 0; }
+
+// split-K factor for the tcgen05 sketch: fill the 148 SMs with >= 95% of the
+// last wave, fewest splits first.
+int choose_splits(int tiles, int kb_total) {
+  const int sms = 148;
+  int best_s = 1;
+  double best_eff = -1.0;
+  const int smax = std::max(1, std::min(kb_total, 64));
+  for (int s = 1; s <= smax; ++s) {
+    const int64_t ctas = (int64_t)tiles * s;
+    const int64_t waves = (ctas + sms - 1) / sms;
+    const double eff = (double)ctas / (double)(waves * sms);
+    if (eff >= 0.95 && ctas >= sms) return s;
+    if (eff > best_eff + 1e-9) { best_eff = eff; best_s = s; }
+  }
+  return best_s;
+}
+
+// One matrix, one dense bf16 block through K1 + K2.
+smp_status sketch_dense_bf16(smp_handle* h, int64_t row0, int64_t rows, const void* X, int64_t ldx,
+                             int64_t ncols, int planes, int64_t col_off, bool do_norms) {
+  using namespace smp;
+  const int k = h->k;
+  SketchTCParams p{};
+  p.rows = rows;
+  p.row0 = row0;
+  p.n = (int32_t)ncols;
+  p.k = k;
+  p.n_tiles = (int32_t)((ncols + 255) / 256);
+  p.k_tiles = (k + 255) / 256;
+  p.kb_total = (int32_t)((rows + 63) / 64);
+  p.splits = choose_splits(p.n_tiles * p.k_tiles, p.kb_total);
+  p.kind = h->d.pi_kind;
+  p.do_norms = do_norms ? 1 : 0;
+  p.seed = h->d.seed;
+  CK(h, ensure(h->part, h->part_cap, (int64_t)p.splits * ncols * k), "alloc partials");
+  CK(h, ensure(h->pnorm, h->pnorm_cap, (int64_t)p.splits * p.k_tiles * ncols), "alloc pnorm");
+  p.part = h->part;
+  p.pnorm = h->pnorm;
+  if (h->timing) {
+    while (h->ev_pool.size() < h->ev_used_n + 2) {
+      cudaEvent_t e;
+      CK(h, cudaEventCreate(&e), "event");
+      h->ev_pool.push_back(e);
+    }
+    CK(h, cudaEventRecord(h->ev_pool[h->ev_used_n], h->st), "event");
+  }
+  CK(h, launch_sketch_tc(X, ldx, p, h->st), "sketch_tc");
+  if (h->timing) {
+    CK(h, cudaEventRecord(h->ev_pool[h->ev_used_n + 1], h->st), "event");
+    h->ev_used_n += 2;
+  }
+  const int64_t n = ncols / planes;
+  CK(h, launch_reduce_sketch(h->part, p.splits, planes, n, k, h->acc_sk + col_off * k, h->st),
+     "reduce_sketch");
+  h->launches += 2;
+  if (do_norms) {
+    CK(h, launch_reduce_norms(h->pnorm, p.splits * p.k_tiles, n, h->acc_nrm + col_off, h->st),
+       "reduce_norms");
+    h->launches += 1;
+  }
+  return SMP_OK;
+}
+
+// One matrix, one fp32 block: split into 3 exact bf16 planes per row chunk,
+// norms from the fp32 values, then K1 over the 3n-wide plane matrix.
+smp_status sketch_dense_f32(smp_handle* h, int64_t row0, int64_t rows, const float* X, int64_t ldx,
+                            int64_t n, int64_t col_off) {
+  using namespace smp;
+  const int64_t ldp = ((3 * n + 7) / 8) * 8;
+  const int64_t chunk = std::max<int64_t>(64, std::min<int64_t>(rows, (int64_t)(512ll << 20) / (ldp * 2)));
+  const int seg_rows = 256;
+  CK(h, ensure(h->planes, h->planes_cap, ((chunk + 63) / 64) * 64 * ldp), "alloc planes");
+  for (int64_t r0 = 0; r0 < rows; r0 += chunk) {
+    const int64_t rc = std::min(chunk, rows - r0);
+    const int64_t segs = (rc + seg_rows - 1) / seg_rows;
+    CK(h, ensure(h->pnorm, h->pnorm_cap, segs * n), "alloc pnorm");
+    CK(h, launch_split_f32(X + r0 * ldx, ldx, rc, n, h->planes, ldp, h->pnorm, seg_rows, h->st),
+       "split_f32");
+    CK(h, launch_reduce_norms(h->pnorm, (int)segs, n, h->acc_nrm + col_off, h->st), "reduce_norms");
+    h->launches += 2;
+    smp_status s = sketch_dense_bf16(h, row0 + r0, rc, h->planes, ldp, 3 * n, 3, col_off, false);
+    if (s != SMP_OK) return s;
+  }
+  return SMP_OK;
+}
+
+// TMA needs a 16-byte aligned base and row pitch: repack unaligned bf16
+// blocks through the handle's staging buffer (device to device, chunked).
+smp_status sketch_dense_bf16_repack(smp_handle* h, int64_t row0, int64_t rows, const void* X,
+                                    int64_t ldx, int64_t n, int64_t col_off) {
+  const int64_t ldp = ((n + 7) / 8) * 8;
+  const int64_t chunk = std::max<int64_t>(64, std::min<int64_t>(rows, (int64_t)(256ll << 20) / (ldp * 2)));
+  CK(h, ensure(h->planes, h->planes_cap, chunk * ldp), "alloc repack");
+  for (int64_t r0 = 0; r0 < rows; r0 += chunk) {
+    const int64_t rc = std::min(chunk, rows - r0);
+    CK(h, cudaMemcpy2DAsync(h->planes, ldp * 2, static_cast<const uint16_t*>(X) + r0 * ldx, ldx * 2,
+                            n * 2, rc, cudaMemcpyDeviceToDevice, h->st), "repack");
+    smp_status s = sketch_dense_bf16(h, row0 + r0, rc, h->planes, ldp, n, 1, col_off, true);
+    if (s != SMP_OK) return s;
+  }
+  return SMP_OK;
+}
+
+smp_status check_rows(smp_handle* h, int64_t row0, int64_t rows) {
+  if (rows < 0 || row0 < h->d.row_begin || row0 + rows > h->d.row_end)
+    return fail(h, SMP_EINVAL, "rows [%lld, %lld) outside the handle's range [%lld, %lld)",
+                (long long)row0, (long long)(row0 + rows), (long long)h->d.row_begin,
+                (long long)h->d.row_end);
+  return SMP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* smp_status_str(smp_status s) {
+  switch (s) {
+    case SMP_OK: return "SMP_OK";
+    case SMP_EIO: return "SMP_EIO";
+    case SMP_EINVAL: return "SMP_EINVAL";
+    case SMP_ENUMERIC: return "SMP_ENUMERIC";
+    case SMP_ECUDA: return "SMP_ECUDA";
+    case SMP_ECAPACITY: return "SMP_ECAPACITY";
+    case SMP_ENOMEM: return "SMP_ENOMEM";
+  }
+  return "SMP_UNKNOWN";
+}
+
+const char* smp_last_error(const smp_handle* h) { return h ? h->err.c_str() : "null handle"; }
+
+int64_t smp_kernel_launches(const smp_handle* h) { return h ? h->launches : 0; }
+
+smp_status smp_sketch_init(smp_handle** out, const smp_sketch_desc* d, void* stream) {
+  if (!out || !d) return SMP_EINVAL;
+  *out = nullptr;
+  if (d->k < 1 || d->k > 4096 || d->n1 < 1 || (!d->a_is_b && d->n2 < 1) || d->d_total < 1 ||
+      d->row_begin < 0 || d->row_end > d->d_total || d->row_begin > d->row_end)
+    return SMP_EINVAL;
+  if (d->pi_kind < 0 || d->pi_kind > 2 || d->input < 0 || d->input > 2) return SMP_EINVAL;
+  if (d->pi_kind == SMP_PI_HADAMARD_TEST && (d->k != d->d_total || !is_pow2(d->d_total)))
+    return SMP_EINVAL;
+  if (d->n1 > (1ll << 31) - 1 || d->n2 > (1ll << 31) - 1) return SMP_EINVAL;
+  smp_handle* h = new smp_handle();
+  h->d = *d;
+  h->st = reinterpret_cast<cudaStream_t>(stream);
+  cudaGetDevice(&h->dev);
+  h->n1 = d->n1;
+  h->n2 = d->a_is_b ? d->n1 : d->n2;
+  h->ntot = d->a_is_b ? d->n1 : d->n1 + d->n2;
+  h->k = d->k;
+  const int64_t nk = h->ntot * (int64_t)h->k;
+  cudaError_t e = cudaSuccess;
+  e = cudaMalloc(&h->acc_sk, nk * 4);
+  if (e == cudaSuccess) e = cudaMalloc(&h->acc_nrm, h->ntot * 8);
+  if (e == cudaSuccess) e = cudaMalloc(&h->fin_sk, nk * 4);
+  if (e == cudaSuccess) e = cudaMalloc(&h->fin_sknorm, h->ntot * 8);
+  if (e == cudaSuccess) e = cudaMalloc(&h->fin_D, h->ntot * 8);
+  if (e == cudaSuccess) e = cudaMalloc(&h->FAFB, 2 * 8);
+  if (e == cudaSuccess) e = cudaMalloc(&h->status, sizeof(int));
+  if (e == cudaSuccess) e = cudaMalloc(&h->alpha, (h->n1 + h->n2) * 8);
+  if (e == cudaSuccess) e = cudaMalloc(&h->d_total, 8);
+  if (e == cudaSuccess) e = cudaMallocHost(&h->h_total, 8);
+  if (e == cudaSuccess) e = cudaMallocHost(&h->h_status, sizeof(int));
+  if (e == cudaSuccess) e = cudaMallocHost(&h->h_fafb, 16);
+  if (e != cudaSuccess) {
+    smp_destroy(h);
+    return e == cudaErrorMemoryAllocation ? SMP_ENOMEM : SMP_ECUDA;
+  }
+  *out = h;
+  return smp_sketch_reset(h);
+}
+
+smp_status smp_sketch_reset(smp_handle* h) {
+  if (!h) return SMP_EINVAL;
+  CK(h, cudaMemsetAsync(h->acc_sk, 0, h->ntot * (int64_t)h->k * 4, h->st), "memset");
+  CK(h, cudaMemsetAsync(h->acc_nrm, 0, h->ntot * 8, h->st), "memset");
+  CK(h, cudaMemsetAsync(h->status, 0, sizeof(int), h->st), "memset");
+  h->finalized = false;
+  return SMP_OK;
+}
+
+void smp_destroy(smp_handle* h) {
+  if (!h) return;
+  if (h->st) cudaStreamSynchronize(h->st);
+  cudaFree(h->acc_sk); cudaFree(h->acc_nrm); cudaFree(h->part); cudaFree(h->pnorm);
+  cudaFree(h->planes); cudaFree(h->fin_sk); cudaFree(h->fin_sknorm); cudaFree(h->fin_D);
+  cudaFree(h->FAFB); cudaFree(h->status); cudaFree(h->pw_scratch); cudaFree(h->alpha);
+  cudaFree(h->blk); cudaFree(h->d_total);
+  if (h->h_total) cudaFreeHost(h->h_total);
+  if (h->h_status) cudaFreeHost(h->h_status);
+  if (h->h_fafb) cudaFreeHost(h->h_fafb);
+  for (int i = 0; i < 2; ++i) {
+    if (h->stage[i]) cudaFree(h->stage[i]);
+    if (h->ev_copied[i]) cudaEventDestroy(h->ev_copied[i]);
+    if (h->ev_used[i]) cudaEventDestroy(h->ev_used[i]);
+  }
+  if (h->copy_st) cudaStreamDestroy(h->copy_st);
+  for (auto e : h->ev_pool) cudaEventDestroy(e);
+  delete h;
+}
+
+smp_status smp_sketch_block(smp_handle* h, int64_t row0, int64_t rows, const void* A, int64_t lda,
+                            const void* B, int64_t ldb) {
+  if (!h) return SMP_EINVAL;
+  smp_status s = check_rows(h, row0, rows);
+  if (s != SMP_OK) return s;
+  if (h->d.input == SMP_IN_CSR_F32)
+    return fail(h, SMP_EINVAL, "CSR handle: use smp_sketch_block_csr");
+  if (rows == 0) return SMP_OK;
+  const bool two = !h->d.a_is_b;
+  if (!A || lda < h->n1 || (two && (!B || ldb < h->n2)))
+    return fail(h, SMP_EINVAL, "null pointer or leading dimension smaller than n");
+  if (rows >= (1ll << 31)) return fail(h, SMP_EINVAL, "block of >= 2^31 rows");
+  h->finalized = false;
+  if (h->d.input == SMP_IN_DENSE_BF16) {
+    auto aligned = [](const void* p, int64_t ld) {
+      return (reinterpret_cast<uintptr_t>(p) % 16 == 0) && (ld % 8 == 0);
+    };
+    if ((reinterpret_cast<uintptr_t>(A) & 1) || (two && (reinterpret_cast<uintptr_t>(B) & 1)))
+      return fail(h, SMP_EINVAL, "bf16 input must be 2-byte aligned");
+    s = aligned(A, lda) ? sketch_dense_bf16(h, row0, rows, A, lda, h->n1, 1, 0, true)
+                        : sketch_dense_bf16_repack(h, row0, rows, A, lda, h->n1, 0);
+    if (s != SMP_OK || !two) return s;
+    return aligned(B, ldb) ? sketch_dense_bf16(h, row0, rows, B, ldb, h->n2, 1, h->n1, true)
+                           : sketch_dense_bf16_repack(h, row0, rows, B, ldb, h->n2, h->n1);
+  }
+  // fp32
+  if (reinterpret_cast<uintptr_t>(A) % 4 != 0 || (two && reinterpret_cast<uintptr_t>(B) % 4 != 0))
+    return fail(h, SMP_EINVAL, "fp32 input must be 4-byte aligned");
+  s = sketch_dense_f32(h, row0, rows, static_cast<const float*>(A), lda, h->n1, 0);
+  if (s != SMP_OK || !two) return s;
+  return sketch_dense_f32(h, row0, rows, static_cast<const float*>(B), ldb, h->n2, h->n1);
+}
+
+smp_status smp_sketch_block_host(smp_handle* h, int64_t row0, int64_t rows, const void* A,
+                                 int64_t lda, const void* B, int64_t ldb, int64_t chunk_rows) {
+  if (!h) return SMP_EINVAL;
+  smp_status s = check_rows(h, row0, rows);
+  if (s != SMP_OK) return s;
+  if (h->d.input == SMP_IN_CSR_F32) return fail(h, SMP_EINVAL, "CSR handle: host path is dense only");
+  const bool two = !h->d.a_is_b;
+  if (!A || lda < h->n1 || (two && (!B || ldb < h->n2)))
+    return fail(h, SMP_EINVAL, "null pointer or leading dimension smaller than n");
+  const int64_t es = h->d.input == SMP_IN_DENSE_BF16 ? 2 : 4;
+  // device copies are packed with ld rounded up to a multiple of 8 elements
+  const int64_t lda_d = ((h->n1 + 7) / 8) * 8, ldb_d = two ? ((h->n2 + 7) / 8) * 8 : 0;
+  const int64_t row_bytes = (lda_d + ldb_d) * es;
+  if (chunk_rows <= 0) chunk_rows = std::max<int64_t>(64, ((256ll << 20) / row_bytes) / 64 * 64);
+  const int64_t need = chunk_rows * row_bytes;
+  if (need > h->stage_bytes) {
+    for (int i = 0; i < 2; ++i) {
+      if (h->stage[i]) cudaFree(h->stage[i]);
+      h->stage[i] = nullptr;
+      CK(h, cudaMalloc(&h->stage[i], need), "alloc staging");
+    }
+    h->stage_bytes = need;
+  }
+  if (!h->copy_st) {
+    CK(h, cudaStreamCreateWithFlags(&h->copy_st, cudaStreamNonBlocking), "stream");
+    for (int i = 0; i < 2; ++i) {
+      CK(h, cudaEventCreateWithFlags(&h->ev_copied[i], cudaEventDisableTiming), "event");
+      CK(h, cudaEventCreateWithFlags(&h->ev_used[i], cudaEventDisableTiming), "event");
+      CK(h, cudaEventRecord(h->ev_used[i], h->st), "event");
+    }
+  }
+  int buf = 0;
+  for (int64_t r0 = 0; r0 < rows; r0 += chunk_rows, buf ^= 1) {
+    const int64_t rc = std::min(chunk_rows, rows - r0);
+    uint8_t* dA = static_cast<uint8_t*>(h->stage[buf]);
+    uint8_t* dB = dA + rc * lda_d * es;
+    CK(h, cudaStreamWaitEvent(h->copy_st, h->ev_used[buf], 0), "wait");
+    CK(h, cudaMemcpy2DAsync(dA, lda_d * es, static_cast<const uint8_t*>(A) + r0 * lda * es, lda * es,
+                            h->n1 * es, rc, cudaMemcpyHostToDevice, h->copy_st), "H2D A");
+    if (two)
+      CK(h, cudaMemcpy2DAsync(dB, ldb_d * es, static_cast<const uint8_t*>(B) + r0 * ldb * es,
+                              ldb * es, h->n2 * es, rc, cudaMemcpyHostToDevice, h->copy_st), "H2D B");
+    CK(h, cudaEventRecord(h->ev_copied[buf], h->copy_st), "event");
+    CK(h, cudaStreamWaitEvent(h->st, h->ev_copied[buf], 0), "wait");
+    s = smp_sketch_block(h, row0 + r0, rc, dA, lda_d, two ? dB : nullptr, ldb_d);
+    if (s != SMP_OK) return s;
+    CK(h, cudaEventRecord(h->ev_used[buf], h->st), "event");
+  }
+  CK(h, cudaStreamSynchronize(h->st), "sync");
+  return SMP_OK;
+}
+
+smp_status smp_sketch_block_csr(smp_handle* h, int64_t row0, int64_t rows, const int64_t* a_rowptr,
+                                const int32_t* a_col, const float* a_val, int64_t a_nnz,
+                                const int64_t* b_rowptr, const int32_t* b_col, const float* b_val,
+                                int64_t b_nnz) {
+  if (!h) return SMP_EINVAL;
+  smp_status s = check_rows(h, row0, rows);
+  if (s != SMP_OK) return s;
+  if (h->d.input != SMP_IN_CSR_F32) return fail(h, SMP_EINVAL, "handle is not a CSR handle");
+  if (rows == 0) return SMP_OK;
+  const bool two = !h->d.a_is_b;
+  if (!a_rowptr || (a_nnz > 0 && (!a_col || !a_val)) ||
+      (two && (!b_rowptr || (b_nnz > 0 && (!b_col || !b_val)))))
+    return fail(h, SMP_EINVAL, "null CSR array");
+  (void)a_nnz; (void)b_nnz;
+  h->finalized = false;
+  CK(h, smp::launch_sketch_csr(h->d.pi_kind, h->d.seed, h->k, row0, rows, a_rowptr, a_col, a_val,
+                               h->n1, h->acc_sk, h->acc_nrm, two ? b_rowptr : nullptr,
+                               two ? b_col : nullptr, two ? b_val : nullptr, h->n2,
+                               h->acc_sk + h->n1 * (int64_t)h->k, h->acc_nrm + h->n1, h->st),
+     "sketch_csr");
+  h->launches += 1;
+  return SMP_OK;
+}
+
+smp_status smp_set_timing(smp_handle* h, int32_t enable) {
+  if (!h) return SMP_EINVAL;
+  h->timing = enable != 0;
+  return SMP_OK;
+}
+
+smp_status smp_kernel_timing(smp_handle* h, double* ms_total, int64_t* launches) {
+  if (!h) return SMP_EINVAL;
+  CK(h, cudaStreamSynchronize(h->st), "sync");
+  double tot = 0.0;
+  for (size_t i = 0; i + 1 < h->ev_used_n; i += 2) {
+    float ms = 0.f;
+    CK(h, cudaEventElapsedTime(&ms, h->ev_pool[i], h->ev_pool[i + 1]), "elapsed");
+    tot += ms;
+  }
+  if (ms_total) *ms_total = tot;
+  if (launches) *launches = (int64_t)(h->ev_used_n / 2);
+  h->ev_used_n = 0;
+  return SMP_OK;
+}
+
+smp_status smp_sketch_partials(smp_handle* h, float** sk, int64_t* sk_count, double** nrm,
+                               int64_t* nrm_count) {
+  if (!h) return SMP_EINVAL;
+  if (sk) *sk = h->acc_sk;
+  if (sk_count) *sk_count = h->ntot * (int64_t)h->k;
+  if (nrm) *nrm = h->acc_nrm;
+  if (nrm_count) *nrm_count = h->ntot;
+  return SMP_OK;
+}
+
+smp_status smp_finalize_norms(smp_handle* h, float* A_sk, float* B_sk, double* a_norm2,
+                              double* b_norm2, double* frob2, float* a_sknorm, float* b_sknorm) {
+  using namespace smp;
+  if (!h) return SMP_EINVAL;
+  const int k = h->k;
+  const float scale = (float)(1.0 / std::sqrt((double)k));
+  CK(h, cudaMemsetAsync(h->status, 0, sizeof(int), h->st), "memset");
+  CK(h, launch_finalize(h->acc_sk, h->acc_nrm, h->ntot, k, scale, h->fin_sk, h->fin_sknorm,
+                        h->fin_D, h->status, h->st), "finalize");
+  int64_t p2 = 1;
+  while (p2 < std::max(h->n1, h->n2)) p2 <<= 1;
+  CK(h, ensure(h->pw_scratch, h->pw_cap, 2 * p2), "alloc");
+  CK(h, launch_pairwise_sum(h->acc_nrm, h->n1, h->pw_scratch, h->FAFB, h->st), "pairwise");
+  CK(h, launch_pairwise_sum(h->acc_nrm + (h->d.a_is_b ? 0 : h->n1), h->n2, h->pw_scratch,
+                            h->FAFB + 1, h->st), "pairwise");
+  h->launches += 3;
+  const int64_t boff = h->d.a_is_b ? 0 : h->n1;
+  if (A_sk) CK(h, cudaMemcpyAsync(A_sk, h->fin_sk, h->n1 * k * 4, cudaMemcpyDeviceToDevice, h->st), "copy");
+  if (B_sk) CK(h, cudaMemcpyAsync(B_sk, h->fin_sk + boff * k, h->n2 * k * 4, cudaMemcpyDeviceToDevice, h->st), "copy");
+  if (a_norm2) CK(h, cudaMemcpyAsync(a_norm2, h->acc_nrm, h->n1 * 8, cudaMemcpyDeviceToDevice, h->st), "copy");
+  if (b_norm2) CK(h, cudaMemcpyAsync(b_norm2, h->acc_nrm + boff, h->n2 * 8, cudaMemcpyDeviceToDevice, h->st), "copy");
+  if (frob2) CK(h, cudaMemcpyAsync(frob2, h->FAFB, 16, cudaMemcpyDeviceToDevice, h->st), "copy");
+  if (a_sknorm || b_sknorm) {
+    // fp64 -> fp32 conversion of ||Ã_i||
+    if (a_sknorm) CK(h, smp_convert_f64_f32(h->fin_sknorm, h->n1, a_sknorm, h->st), "convert");
+    if (b_sknorm) CK(h, smp_convert_f64_f32(h->fin_sknorm + boff, h->n2, b_sknorm, h->st), "convert");
+  }
+  CK(h, cudaMemcpyAsync(h->h_status, h->status, sizeof(int), cudaMemcpyDeviceToHost, h->st), "copy");
+  CK(h, cudaMemcpyAsync(h->h_fafb, h->FAFB, 16, cudaMemcpyDeviceToHost, h->st), "copy");
+  CK(h, cudaStreamSynchronize(h->st), "sync");
+  h->finalized = true;
+  if (*h->h_status) return fail(h, SMP_ENUMERIC, "NaN/Inf in the column norms or sketch");
+  if (!(h->h_fafb[0] > 0.0) || !(h->h_fafb[1] > 0.0))
+    return fail(h, SMP_ENUMERIC, "||A||_F = 0 or ||B||_F = 0");
+  return SMP_OK;
+}
+
+smp_status smp_sample_estimate(smp_handle* h, double m, uint64_t seed, int32_t est, int64_t cap,
+                               int32_t* I, int32_t* J, float* val, double* qhat, int64_t* count) {
+  using namespace smp;
+  if (!h) return SMP_EINVAL;
+  if (!(m > 0.0)) return fail(h, SMP_EINVAL, "m must be > 0");
+  if (!h->finalized) return fail(h, SMP_EINVAL, "call smp_finalize_norms first");
+  if (cap < 0 || (cap > 0 && (!I || !J || !val || !qhat))) return fail(h, SMP_EINVAL, "bad output");
+  const int64_t n1 = h->n1, n2 = h->n2;
+  if (n1 * n2 > (1ll << 40)) return fail(h, SMP_EINVAL, "n1*n2 too large for the Bernoulli sweep");
+  const int64_t boff = h->d.a_is_b ? 0 : n1;
+  double* beta = h->alpha + n1;
+  CK(h, launch_alpha_beta(h->acc_nrm, n1, h->acc_nrm + boff, n2, h->FAFB, h->alpha, beta, h->st), "alpha_beta");
+  const int64_t nb = omega_num_blocks(n1, n2);
+  CK(h, ensure(h->blk, h->blk_cap, std::max<int64_t>(nb, 1)), "alloc");
+  CK(h, launch_omega_count(h->alpha, beta, n1, n2, m, seed, h->blk, h->st), "omega_count");
+  CK(h, launch_scan_counts(h->blk, nb, h->d_total, h->st), "scan");
+  CK(h, launch_omega_write(h->alpha, beta, n1, n2, m, seed, h->blk, h->d_total, cap, I, J, qhat, h->st), "omega_write");
+  if (cap > 0)
+    CK(h, launch_sddmm(h->fin_sk, h->fin_sk + boff * h->k, h->fin_D, h->fin_D + boff, h->k, I, J,
+                       h->d_total, cap, est == SMP_EST_PLAIN, val, h->st), "sddmm");
+  h->launches += 5;
+  CK(h, cudaMemcpyAsync(h->h_total, h->d_total, 8, cudaMemcpyDeviceToHost, h->st), "copy");
+  CK(h, cudaStreamSynchronize(h->st), "sync");
+  if (count) *count = *h->h_total;
+  if (*h->h_total > cap)
+    return fail(h, SMP_ECAPACITY, "|Omega| = %lld > cap = %lld", (long long)*h->h_total, (long long)cap);
+  return SMP_OK;
+}
+
+smp_status smp_waltmin(smp_handle* h, const int32_t* I, const int32_t* J, const float* val,
+                       const double* qhat, int64_t count, const smp_waltmin_desc* w, float* U,
+                       float* V) {
+  if (!h || !w) return SMP_EINVAL;
+  if (!h->finalized) return fail(h, SMP_EINVAL, "call smp_finalize_norms first");
+  if (w->r < 1 || w->r > 16 || w->r > h->n1 || w->r > h->n2)
+    return fail(h, SMP_EINVAL, "r must satisfy 1 <= r <= min(16, n1, n2)");
+  if (w->T < 1) return fail(h, SMP_EINVAL, "T must be >= 1");
+  if (w->init_iters < 1) return fail(h, SMP_EINVAL, "init_iters must be >= 1");
+  if (w->partition != SMP_PART_REUSE_ALL) return fail(h, SMP_EINVAL, "unsupported partition");
+  if (count < 0 || count > (1ll << 31) - 1 || (count > 0 && (!I || !J || !val || !qhat)) || !U || !V)
+    return fail(h, SMP_EINVAL, "bad sample arrays");
+  smp::WaltminArgs a{};
+  a.n1 = h->n1; a.n2 = h->n2; a.count = count;
+  a.r = w->r; a.T = w->T; a.init_iters = w->init_iters;
+  a.trim_c = w->trim_c; a.lam = w->ridge; a.seed = w->seed;
+  a.I = I; a.J = J; a.val = val; a.qhat = qhat;
+  a.a_norm2 = h->acc_nrm; a.FA = h->FAFB;
+  a.U = U; a.V = V;
+  CK(h, smp::run_waltmin(a, h->st), "waltmin");
+  h->launches += 8 + (int64_t)w->init_iters * 14 + (w->trim_c > 0 ? 7 : 0) + 2 * w->T + 2;
+  CK(h, cudaStreamSynchronize(h->st), "sync");
+  return SMP_OK;
+}
+
+}  // extern "C"
+
+// small helper kernel (fp64 -> fp32)
+__global__ void smp_f64_to_f32_kernel(const double* __restrict__ x, int64_t n, float* __restrict__ y) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = (float)x[i];
+}
+cudaError_t smp_convert_f64_f32(const double* x, int64_t n, float* y, cudaStream_t st) {
+  int blocks = (int)std::min<int64_t>((n + 255) / 256, 1024);
+  if (blocks < 1) blocks = 1;
+  smp_f64_to_f32_kernel<<<blocks, 256, 0, st>>>(x, n, y);
+  return cudaGetLastError();
+}

@@ -1,0 +1,78 @@
+// Internal launcher declarations for the SMP-PCA sm_100a kernels (not part
+// of the public C ABI; see include/smp.h for that).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace smp {
+
+// ---- K1 dense sketch (sketch_tc.cu)
+struct SketchTCParams {
+  int64_t rows;      // local rows of this block (TMA tensor height)
+  int64_t row0;      // global row index of local row 0
+  int32_t n;         // columns (TMA tensor width)
+  int32_t k;         // sketch size
+  int32_t n_tiles, k_tiles, splits;
+  int32_t kb_total;  // ceil(rows / 64)
+  int32_t kind;      // PI_*
+  int32_t do_norms;
+  uint64_t seed;
+  float* part;       // [splits][n][k]
+  double* pnorm;     // [splits * k_tiles][n]
+};
+cudaError_t launch_sketch_tc(const void* X, int64_t ldx, SketchTCParams p, cudaStream_t st);
+int sketch_tc_smem_bytes();
+
+// ---- K2 partial reduce, fp32 split, K4 finalize (reduce.cu)
+// acc[c][κ] += Σ_s Σ_pl part[s][pl*n + c][κ]   (planes pl = 0..planes-1)
+cudaError_t launch_reduce_sketch(const float* part, int splits, int planes, int64_t n, int k,
+                                 float* acc, cudaStream_t st);
+// nacc[c] += Σ_slot pnorm[slot][c]
+cudaError_t launch_reduce_norms(const double* pnorm, int slots, int64_t n, double* nacc,
+                                cudaStream_t st);
+// fp32 rows -> 3 bf16 planes (hi, mid, lo; exact sum) laid out as a
+// rows x (3n) matrix with leading dimension ldp, and fp64 Σx² per row segment.
+cudaError_t launch_split_f32(const float* X, int64_t ldx, int64_t rows, int64_t n, uint16_t* planes,
+                             int64_t ldp, double* pnorm, int seg_rows, cudaStream_t st);
+// finalize one matrix: out = acc * scale (fp32), sknorm (fp64), D (fp64)
+cudaError_t launch_finalize(const float* acc, const double* nacc, int64_t n, int k, float scale,
+                            float* out, double* sknorm, double* D, int* status, cudaStream_t st);
+// fixed pairwise tree sum (R5) of x[0..n) into *out (single block)
+cudaError_t launch_pairwise_sum(const double* x, int64_t n, double* scratch, double* out,
+                                cudaStream_t st);
+
+// ---- K5/K6 sampling and estimation (omega.cu)
+cudaError_t launch_alpha_beta(const double* a2, int64_t n1, const double* b2, int64_t n2,
+                              const double* FAFB, double* alpha, double* beta, cudaStream_t st);
+int64_t omega_num_blocks(int64_t n1, int64_t n2);
+cudaError_t launch_omega_count(const double* alpha, const double* beta, int64_t n1, int64_t n2,
+                               double m, uint64_t seed, int64_t* blk_counts, cudaStream_t st);
+cudaError_t launch_scan_counts(int64_t* blk_counts, int64_t nblk, int64_t* total, cudaStream_t st);
+cudaError_t launch_omega_write(const double* alpha, const double* beta, int64_t n1, int64_t n2,
+                               double m, uint64_t seed, const int64_t* blk_offsets,
+                               const int64_t* total, int64_t cap, int32_t* I, int32_t* J,
+                               double* qhat, cudaStream_t st);
+cudaError_t launch_sddmm(const float* Ask, const float* Bsk, const double* DA, const double* DB,
+                         int k, const int32_t* I, const int32_t* J, const int64_t* total,
+                         int64_t cap, int plain, float* val, cudaStream_t st);
+
+// ---- K7-K9 WAltMin (waltmin.cu)
+struct WaltminArgs {
+  int64_t n1, n2, count;
+  int r, T, init_iters;
+  double trim_c, lam;
+  uint64_t seed;
+  const int32_t* I;
+  const int32_t* J;
+  const float* val;
+  const double* qhat;
+  const double* a_norm2;  // n1, device
+  const double* FA;       // device scalar
+  float* U;
+  float* V;
+};
+// returns a cudaError_t; workspace is allocated internally from the stream's
+// pool (cudaMallocAsync) and freed before return.
+cudaError_t run_waltmin(const WaltminArgs& a, cudaStream_t st);
+
+}  // namespace smp

@@ -1,0 +1,231 @@
+"""GPU parity: the CUDA path through the C ABI vs the CPU oracle, element by
+element, on seeded inputs (DESIGN.md §4 lists the tolerances and why).
+
+  sketch Ã, B̃      ||Ã_i^gpu - Ã_i^or|| / ||Ã_i^or|| <= 1e-5 per column (north star)
+  norms ||A_i||²   relative 1e-12 (both fp64; summation order differs)
+  Ω, indices        bit-exact;  q̂ relative 1e-12
+  M̃                |M̃^gpu - M̃^or| <= 1e-4 ||A_i|| ||B_j||   (R22, Lemma JL scale P:318)
+  factors           ||UVᵀ_gpu - UVᵀ_or||_2 / ||AᵀB||_2 <= 1e-3
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+PI = {"rademacher": 0, "gaussian": 1, "hadamard": 2}
+
+
+def _smp():
+    import paper_1610_06656_b200 as smp
+    return smp
+
+
+def _to_np(X):
+    if X.dtype == torch.bfloat16:
+        return synth.bf16_bits(X)
+    return X.detach().cpu().numpy()
+
+
+def gpu_sketch(A, B, k, pi, seed=0, row0=0, d_total=None, blocks=None, a_is_b=False):
+    smp = _smp()
+    inp = smp.IN_DENSE_BF16 if A.dtype == torch.bfloat16 else smp.IN_DENSE_F32
+    d = A.shape[0] + row0 if d_total is None else d_total
+    sk = smp.SMPSketch(d, A.shape[1], A.shape[1] if a_is_b else B.shape[1], k, pi=pi, seed=seed,
+                       a_is_b=a_is_b, input=inp)
+    Ad = A.cuda()
+    Bd = None if a_is_b else B.cuda()
+    if blocks is None:
+        sk.block(row0, Ad, Bd)
+    else:
+        for (r0, r1) in blocks:
+            sk.block(row0 + r0, Ad[r0:r1], None if a_is_b else Bd[r0:r1])
+    fin = sk.finalize()
+    return sk, fin
+
+
+def oracle_sketch(A, B, k, pi, seed=0, row0=0, a_is_b=False):
+    skA, a2 = oracle.sketch_rows(pi, seed, k, _to_np(A), row0=row0)
+    if a_is_b:
+        skB, b2 = skA, a2
+    else:
+        skB, b2 = oracle.sketch_rows(pi, seed, k, _to_np(B), row0=row0)
+    As, asn, DA = oracle.finalize(k, skA, a2)
+    Bs, bsn, DB = oracle.finalize(k, skB, b2)
+    return dict(As=As, Bs=Bs, a2=a2, b2=b2, DA=DA, DB=DB, asn=asn, bsn=bsn,
+                FA=oracle.pairwise_sum(a2), FB=oracle.pairwise_sum(b2))
+
+
+def col_rel_err(gpu, ref):
+    g = gpu.detach().cpu().double().numpy()
+    num = np.linalg.norm(g - ref, axis=1)
+    den = np.linalg.norm(ref, axis=1)
+    return np.where(den > 0, num / np.where(den > 0, den, 1), num)
+
+
+def check_sketch(fin, orc, tol=1e-5):
+    ea = col_rel_err(fin["A_sk"], orc["As"])
+    eb = col_rel_err(fin["B_sk"], orc["Bs"])
+    assert ea.max() <= tol, f"A sketch max col rel err {ea.max():.3e}"
+    assert eb.max() <= tol, f"B sketch max col rel err {eb.max():.3e}"
+    a2 = fin["a_norm2"].cpu().numpy()
+    b2 = fin["b_norm2"].cpu().numpy()
+    np.testing.assert_allclose(a2, orc["a2"], rtol=1e-12, atol=0)
+    np.testing.assert_allclose(b2, orc["b2"], rtol=1e-12, atol=0)
+    fr = fin["frob2"].cpu().numpy()
+    np.testing.assert_allclose(fr, [orc["FA"], orc["FB"]], rtol=1e-12)
+
+
+# ------------------------------------------------------------------ Step 1
+@pytest.mark.parametrize("d,n1,n2,k,pi", [
+    (2000, 100, 100, 64, "rademacher"),     # cfg0 shape
+    (4096, 300, 520, 256, "rademacher"),    # several n-tiles, ragged n
+    (3001, 257, 33, 130, "rademacher"),     # ragged d, k not a multiple of 128
+    (2500, 64, 96, 384, "gaussian"),        # two κ tiles
+    (1000, 40, 40, 512, "gaussian"),
+])
+def test_sketch_bf16_parity(d, n1, n2, k, pi):
+    A = synth.gaussian_small(d, n1, seed=1, scale_cols=True).to(torch.bfloat16)
+    B = synth.gaussian_small(d, n2, seed=2).to(torch.bfloat16)
+    _, fin = gpu_sketch(A, B, k, PI[pi], seed=7)
+    orc = oracle_sketch(A, B, k, PI[pi], seed=7)
+    check_sketch(fin, orc)
+
+
+@pytest.mark.parametrize("d,n,k,pi", [(2000, 100, 64, "rademacher"), (1500, 70, 256, "gaussian")])
+def test_sketch_f32_parity(d, n, k, pi):
+    """fp32 inputs go through the exact 3-term bf16 split."""
+    A, B = synth.cone_tiny(d, n, seed=0)
+    _, fin = gpu_sketch(A, B, k, PI[pi], seed=0)
+    orc = oracle_sketch(A, B, k, PI[pi], seed=0)
+    check_sketch(fin, orc)
+
+
+def test_sketch_unaligned_row0_and_blocks():
+    """Global row offsets not multiple of 32/64 exercise the generic Π path;
+    blocks in arbitrary order sum to the whole."""
+    d, n, k = 1900, 150, 128
+    A = synth.gaussian_small(d, n, seed=3).to(torch.bfloat16)
+    B = synth.gaussian_small(d, n, seed=4).to(torch.bfloat16)
+    row0 = 77
+    blocks = [(1200, 1900), (0, 333), (333, 1200)]
+    _, fin = gpu_sketch(A, B, k, 0, seed=5, row0=row0, d_total=row0 + d, blocks=blocks)
+    orc = oracle_sketch(A, B, k, 0, seed=5, row0=row0)
+    check_sketch(fin, orc)
+
+
+def test_sketch_a_equals_b():
+    d, n, k = 1024, 96, 64
+    A = synth.gaussian_small(d, n, seed=9).to(torch.bfloat16)
+    _, fin = gpu_sketch(A, None, k, 1, seed=2, a_is_b=True)
+    orc = oracle_sketch(A, A, k, 1, seed=2, a_is_b=True)
+    check_sketch(fin, orc)
+
+
+def test_hadamard_k_equals_d_exact_product():
+    """North star (a): Hadamard Π with k = d gives M̃ = AᵀB (fully sampled)."""
+    smp = _smp()
+    d, n = 256, 24
+    A = synth.gaussian_small(d, n, seed=11).to(torch.bfloat16)
+    B = synth.gaussian_small(d, n, seed=12).to(torch.bfloat16)
+    sk, fin = gpu_sketch(A, B, d, smp.PI_HADAMARD_TEST, seed=0)
+    I, J, val, qh = sk.sample_estimate(1e12, 0)
+    assert I.numel() == n * n
+    M = (A.double().T @ B.double()).numpy()
+    got = np.zeros((n, n))
+    got[I.cpu().numpy(), J.cpu().numpy()] = val.cpu().numpy()
+    scale = np.outer(np.linalg.norm(A.double().numpy(), axis=0), np.linalg.norm(B.double().numpy(), axis=0))
+    assert np.max(np.abs(got - M) / scale) < 1e-5
+
+
+# ------------------------------------------------------------------ Step 2
+@pytest.mark.parametrize("n1,n2,m_coef", [(100, 100, 0.3), (600, 450, 4.0), (300, 257, 50.0)])
+def test_omega_bit_exact_and_mtilde(n1, n2, m_coef):
+    d, k = 3000, 128
+    A = synth.gaussian_small(d, n1, seed=21, scale_cols=True).to(torch.bfloat16)
+    B = synth.gaussian_small(d, n2, seed=22, scale_cols=True).to(torch.bfloat16)
+    sk, fin = gpu_sketch(A, B, k, 0, seed=3)
+    orc = oracle_sketch(A, B, k, 0, seed=3)
+    m = m_coef * max(n1, n2) * 5 * math.log(max(n1, n2))
+    I, J, val, qh = sk.sample_estimate(m, 99)
+    al, be = oracle.alpha_beta(orc["a2"], orc["b2"], orc["FA"], orc["FB"])
+    Io, Jo, qo = oracle.sample(99, m, al, be)
+    assert np.array_equal(I.cpu().numpy(), Io) and np.array_equal(J.cpu().numpy(), Jo)
+    np.testing.assert_allclose(qh.cpu().numpy(), qo, rtol=1e-12)
+    Mo = oracle.estimate(k, Io, Jo, orc["As"], orc["Bs"], orc["DA"], orc["DB"])
+    scale = np.sqrt(orc["a2"][Io] * orc["b2"][Jo])
+    err = np.abs(val.cpu().double().numpy() - Mo) / scale
+    assert err.max() <= 1e-4, err.max()
+    # plain JL estimator as well
+    I2, J2, v2, _ = sk.sample_estimate(m, 99, plain=True)
+    Mp = oracle.estimate(k, Io, Jo, orc["As"], orc["Bs"], orc["DA"], orc["DB"], plain=True)
+    assert np.max(np.abs(v2.cpu().double().numpy() - Mp) / scale) <= 1e-4
+
+
+def test_omega_capacity_and_empty():
+    smp = _smp()
+    d, n, k = 512, 50, 64
+    A = synth.gaussian_small(d, n, seed=31).to(torch.bfloat16)
+    B = synth.gaussian_small(d, n, seed=32).to(torch.bfloat16)
+    sk, _ = gpu_sketch(A, B, k, 0)
+    I, J, v, q = sk.sample_estimate(200.0, 1, cap=5)  # grows internally
+    assert I.numel() > 5
+    I2, J2, v2, q2 = sk.sample_estimate(1e-9, 1)
+    assert I2.numel() == 0
+
+
+# ------------------------------------------------------------------ Step 3
+def _uvt_err(U1, V1, U2, V2, M):
+    P1 = U1 @ V1.T
+    P2 = U2 @ V2.T
+    return np.linalg.norm(P1 - P2, 2) / np.linalg.norm(M, 2)
+
+
+@pytest.mark.parametrize("n1,n2,r,m_coef", [(120, 100, 5, 4.0), (300, 200, 10, 6.0)])
+def test_waltmin_parity_identical_inputs(n1, n2, r, m_coef):
+    """WAltMin (Alg. 2) on the ORACLE's Ω, M̃ (rounded to fp32) and q̂ —
+    identical inputs on both sides — agrees to 1e-3 of ||AᵀB||."""
+    d, k = 2000, 256
+    Z = synth.gaussian_small(d, r, seed=41).double()
+    A = (Z @ synth.gaussian_small(r, n1, seed=42).double() + 0.1 * synth.gaussian_small(d, n1, seed=43).double()).to(torch.bfloat16)
+    B = (Z @ synth.gaussian_small(r, n2, seed=44).double() + 0.1 * synth.gaussian_small(d, n2, seed=45).double()).to(torch.bfloat16)
+    sk, fin = gpu_sketch(A, B, k, 0, seed=1)
+    orc = oracle_sketch(A, B, k, 0, seed=1)
+    m = m_coef * max(n1, n2) * r * math.log(max(n1, n2))
+    al, be = oracle.alpha_beta(orc["a2"], orc["b2"], orc["FA"], orc["FB"])
+    Io, Jo, qo = oracle.sample(5, m, al, be)
+    Mo = oracle.estimate(k, Io, Jo, orc["As"], orc["Bs"], orc["DA"], orc["DB"]).astype(np.float32)
+    Uo, Vo = oracle.waltmin(n1, n2, r, 10, Io, Jo, Mo.astype(np.float64), qo, np.sqrt(orc["a2"]),
+                            math.sqrt(orc["FA"]), init_iters=30, seed=9)
+    dev = torch.device("cuda")
+    Ug, Vg = sk.waltmin(torch.tensor(Io, device=dev), torch.tensor(Jo, device=dev),
+                        torch.tensor(Mo, device=dev), torch.tensor(qo, device=dev), r, 10,
+                        init_iters=30, seed=9)
+    M = (A.double().T @ B.double()).numpy()
+    err = _uvt_err(Ug.cpu().double().numpy(), Vg.cpu().double().numpy(), Uo, Vo, M)
+    assert err <= 1e-3, err
+
+
+def test_pipeline_end_to_end_vs_oracle():
+    """Alg. 1 end to end from the same A, B on both sides (cfg1-like regime,
+    m = 4 n r ln n): factors within 1e-3 of ||AᵀB||_2."""
+    smp = _smp()
+    d, n, r, k = 8192, 256, 5, 256
+    VA = synth.lowrank_factors(n, 20, 1, 0, "cpu")
+    VB = synth.lowrank_factors(n, 20, 1, 1, "cpu")
+    A, B = synth.lowrank_block(0, d, n, 1, VA, VB, device="cpu")
+    m = 4 * n * r * math.log(n)
+    res = smp.smp_pca(A.cuda(), B.cuda(), k=k, r=r, m=m, T=10, seed=1, init_iters=30)
+    orc = oracle.smp_pca(synth.bf16_bits(A), synth.bf16_bits(B), k=k, r=r, m=m, T=10, seed=1,
+                         init_iters=30)
+    assert np.array_equal(res["I"].cpu().numpy(), orc["I"])
+    assert np.array_equal(res["J"].cpu().numpy(), orc["J"])
+    M = (A.double().T @ B.double()).numpy()
+    err = _uvt_err(res["U"].cpu().double().numpy(), res["V"].cpu().double().numpy(),
+                   orc["U"], orc["V"], M)
+    assert err <= 1e-3, err

@@ -67,13 +67,15 @@ def test_rademacher_values_and_balance():
 
 
 def test_rademacher_counter_layout():
-    """bit (t & 127) of Philox(ctr=(t>>7, κ, t>>39, 1)) is the sign."""
+    """row t's sign is bit (e>>1) + 16(e&1), e = t & 31, of word
+    (t & 127) >> 5 of Philox(ctr=(t>>7, κ, t>>39, 1))."""
     seed = 0x1234_5678_9ABC
     key = [seed & 0xFFFFFFFF, seed >> 32]
     for kappa, t in [(0, 0), (3, 127), (200, 128), (17, 1000003), (5, 2**33 + 77)]:
         w = oracle.philox4x32_10([(t >> 7) & 0xFFFFFFFF, kappa, (t >> 39) & 0xFFFFFFFF, 1], key)
         b = t & 127
-        bit = (int(w[b >> 5]) >> (b & 31)) & 1
+        e = b & 31
+        bit = (int(w[b >> 5]) >> ((e >> 1) + 16 * (e & 1))) & 1
         assert oracle.pi_entry(oracle.PI_RADEMACHER, seed, kappa, t) == (-1.0 if bit else 1.0)
 
 

@@ -113,7 +113,7 @@ cudaError_t launch_split_f32(const float* X, int64_t ldx, int64_t rows, int64_t 
 // ---------------------------------------------------------------- K4
 // One warp per column: Ã_c = acc_c * fp32(1/sqrt(k)); ||Ã_c|| in fp64;
 // D_c = ||X_c|| / ||Ã_c|| (0 if ||Ã_c|| = 0).
-__global__ void finalize_kernel(const float* __restrict__ acc, const double* __restrict__ nacc,
+__global__ void finalize_kernel(const float* __restrict__ acc, double* __restrict__ nacc,
                                 int64_t n, int k, float scale, float* __restrict__ out,
                                 double* __restrict__ sknorm, double* __restrict__ D,
                                 int* __restrict__ status) {
@@ -131,7 +131,10 @@ __global__ void finalize_kernel(const float* __restrict__ acc, const double* __r
     for (int o = 16; o > 0; o >>= 1) s2 += __shfl_xor_sync(0xffffffffu, s2, o);
     if (lane == 0) {
       const double sn = sqrt(s2);
-      const double a2 = nacc[c];
+      double a2 = nacc[c];
+      // R25: norms² below 2^-200 are the exact-zero column (the bf16 norm
+      // path maps a zero to 2^-127, whose square is absorbed otherwise)
+      if (a2 < 0x1p-200) { a2 = 0.0; nacc[c] = 0.0; }
       sknorm[c] = sn;
       D[c] = sn > 0.0 ? sqrt(a2) / sn : 0.0;
       if (!(a2 == a2) || !(sn == sn) || isinf(a2)) atomicOr(status, 1);
@@ -139,7 +142,7 @@ __global__ void finalize_kernel(const float* __restrict__ acc, const double* __r
   }
 }
 
-cudaError_t launch_finalize(const float* acc, const double* nacc, int64_t n, int k, float scale,
+cudaError_t launch_finalize(const float* acc, double* nacc, int64_t n, int k, float scale,
                             float* out, double* sknorm, double* D, int* status, cudaStream_t st) {
   int blocks = (int)std::min<int64_t>((n + 7) / 8, 148 * 8);
   if (blocks < 1) blocks = 1;

@@ -30,9 +30,12 @@ constexpr int TC_BK = 64;                         // X rows per K-block
 constexpr int TC_STAGES = 3;
 constexpr int PI_STAGE = TC_BM * TC_BK * 2;       // 32 KB
 constexpr int X_STAGE = TC_BK * TC_BN * 2;        // 32 KB
-constexpr int NORM_RED = 4 * TC_BN * 8;           // 8 KB
+constexpr int NUM_GEN_WARPS = 4;                  // warps 4..7
+constexpr int NUM_NORM_WARPS = 8;                 // warps 8..15 (2 per SMSP)
+constexpr int NORM_ROWS = TC_BK / NUM_NORM_WARPS; // rows of a stage per norm thread
+constexpr int NORM_RED = NUM_NORM_WARPS * TC_BN * 8;  // 16 KB
 constexpr int TC_SMEM = TC_STAGES * (PI_STAGE + X_STAGE) + NORM_RED + 256 + 1024;
-constexpr int TC_THREADS = 384;
+constexpr int TC_THREADS = 32 * (8 + NUM_NORM_WARPS);
 
 struct RadCache {
   uint64_t g;
@@ -57,32 +60,39 @@ __device__ __forceinline__ uint32_t rad_word(RadCache& c, uint64_t W, uint32_t k
 // (rows 2p, 2p+1) is built with one shift and one LOP3.
 __device__ __forceinline__ uint32_t rad_pos(uint32_t e) { return (e >> 1) | ((e & 1u) << 4); }
 
-// Generate one κ row of the Π tile (64 bf16 = 32 packed words) into regs.
+// Generate one κ row of the Π tile (64 bf16 = 32 packed words) straight into
+// its K-major SWIZZLE_128B SMEM row: 16-byte chunk c of row kl lives at
+// chunk position c ^ (kl & 7).
 __device__ __forceinline__ void gen_pi_row(int kind, uint64_t seed, uint32_t kappa, bool valid,
-                                           uint64_t t0, RadCache& rc, uint32_t (&o)[32]) {
+                                           uint64_t t0, RadCache& rc, uint8_t* rowp, int sw) {
   const uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
   if (!valid) {
 #pragma unroll
-    for (int i = 0; i < 32; ++i) o[i] = 0u;
+    for (int c = 0; c < 8; ++c) *reinterpret_cast<uint4*>(rowp + ((c ^ sw) << 4)) = make_uint4(0, 0, 0, 0);
     return;
   }
   if (kind == PI_RADEMACHER && (t0 & 31) == 0) {
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-      uint32_t w = rad_word(rc, (t0 >> 5) + h, kappa, k0, k1);
+      const uint32_t w = rad_word(rc, (t0 >> 5) + h, kappa, k0, k1);
+      uint32_t o[16];
 #pragma unroll
-      for (int p = 0; p < 16; ++p) o[16 * h + p] = 0x3F803F80u | ((w << (15 - p)) & 0x80008000u);
+      for (int p = 0; p < 16; ++p) o[p] = 0x3F803F80u | ((w << (15 - p)) & 0x80008000u);
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        *reinterpret_cast<uint4*>(rowp + (((4 * h + c) ^ sw) << 4)) =
+            make_uint4(o[4 * c], o[4 * c + 1], o[4 * c + 2], o[4 * c + 3]);
     }
   } else if (kind == PI_GAUSSIAN && (t0 & 3) == 0) {
 #pragma unroll 2
     for (int q = 0; q < 16; ++q) {
-      uint64_t tq = (t0 >> 2) + q;
-      u32x4 w = philox4x32_10((uint32_t)tq, kappa, (uint32_t)(tq >> 32), TAG_GAUSSIAN, k0, k1);
+      const uint64_t tq = (t0 >> 2) + q;
+      const u32x4 w = philox4x32_10((uint32_t)tq, kappa, (uint32_t)(tq >> 32), TAG_GAUSSIAN, k0, k1);
       uint16_t a, b, c, d;
       gauss_pair(w.x, w.y, a, b);
       gauss_pair(w.z, w.w, c, d);
-      o[2 * q] = (uint32_t)a | ((uint32_t)b << 16);
-      o[2 * q + 1] = (uint32_t)c | ((uint32_t)d << 16);
+      *reinterpret_cast<uint2*>(rowp + (((q >> 1) ^ sw) << 4) + ((q & 1) << 3)) =
+          make_uint2((uint32_t)a | ((uint32_t)b << 16), (uint32_t)c | ((uint32_t)d << 16));
     }
   } else {
     // generic (unaligned block start, Hadamard test mode): element by element
@@ -91,25 +101,32 @@ __device__ __forceinline__ void gen_pi_row(int kind, uint64_t seed, uint32_t kap
       uint32_t lohi[2];
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
-        uint64_t t = t0 + 2 * p + e;
+        const uint64_t t = t0 + 2 * p + e;
         if (kind == PI_RADEMACHER) {
-          uint32_t w = rad_word(rc, t >> 5, kappa, k0, k1);
+          const uint32_t w = rad_word(rc, t >> 5, kappa, k0, k1);
           lohi[e] = ((w >> rad_pos((uint32_t)(t & 31))) & 1u) ? 0xBF80u : 0x3F80u;
         } else {
           lohi[e] = pi_bits(kind, seed, kappa, t);
         }
       }
-      o[p] = lohi[0] | (lohi[1] << 16);
+      *reinterpret_cast<uint32_t*>(rowp + (((p >> 2) ^ sw) << 4) + ((p & 3) << 2)) =
+          lohi[0] | (lohi[1] << 16);
     }
   }
 }
 
-// fp64 value of |bf16| from the 15 magnitude bits placed at [0,15) of v:
-// exponent field e != 0 -> hi word ((v << 13) + (896 << 20)); zero -> 0.
-// bf16 subnormals (e == 0, m != 0) are flushed (R25).
-__device__ __forceinline__ double bf16mag_to_f64(uint32_t v) {
-  uint32_t hi = (v & 0x7F80u) ? (v << 13) + 0x38000000u : 0u;
-  return __hiloint2double((int)hi, 0);
+// Exact fp64 |x| of the two bf16 halves of a packed word w, two integer ops
+// each: the fp64 high word is (magnitude bits << 13) + (896 << 20) (bf16 and
+// fp64 share the sign/exponent layout up to the bias 1023 - 127 = 896), the
+// low word is 0 (bf16 has only 7 stored mantissa bits).  A zero (or bf16
+// subnormal) maps to 2^-127·(1+m/128) instead of 0; its square ≤ 2^-252 is
+// absorbed exactly by any partial sum ≥ 2^-200, and finalize flushes
+// column norms² < 2^-200 to 0 (R25).
+__device__ __forceinline__ double bf16lo_mag_f64(uint32_t w) {
+  return __hiloint2double((int)((w & 0x7FFFu) * 8192u + 0x38000000u), 0);
+}
+__device__ __forceinline__ double bf16hi_mag_f64(uint32_t w) {
+  return __hiloint2double((int)(__umulhi(w & 0x7FFF0000u, 0x20000000u) + 0x38000000u), 0);
 }
 
 __global__ void __launch_bounds__(TC_THREADS, 1)
@@ -138,7 +155,10 @@ sketch_tc_kernel(const __grid_constant__ CUtensorMap tmap, SketchTCParams p) {
   const int nh = (p.k - kappa0 > 128) ? 2 : 1;
 
   if (tid == 0) {
-    for (int s = 0; s < TC_STAGES; ++s) { mbar_init(&full[s], 1 + 4); mbar_init(&empty[s], 1 + 4); }
+    for (int s = 0; s < TC_STAGES; ++s) {
+      mbar_init(&full[s], 1 + NUM_GEN_WARPS);
+      mbar_init(&empty[s], 1 + NUM_NORM_WARPS);
+    }
     mbar_init(tmem_full, 1);
     fence_mbar_init();
   }
@@ -200,14 +220,9 @@ sketch_tc_kernel(const __grid_constant__ CUtensorMap tmap, SketchTCParams p) {
         const int kl = g + 128 * r;
         if (r == 1 && nh == 1) break;
         const int kappa = kappa0 + kl;
-        uint32_t o[32];
-        gen_pi_row(p.kind, p.seed, (uint32_t)kappa, kappa < p.k, t0, r == 0 ? rc0 : rc1, o);
         uint8_t* rowp = pi_s + s * PI_STAGE + kl * 128;
-#pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          uint4 v = make_uint4(o[4 * c], o[4 * c + 1], o[4 * c + 2], o[4 * c + 3]);
-          *reinterpret_cast<uint4*>(rowp + ((c ^ (kl & 7)) << 4)) = v;
-        }
+        if (r == 0) gen_pi_row(p.kind, p.seed, (uint32_t)kappa, kappa < p.k, t0, rc0, rowp, kl & 7);
+        else gen_pi_row(p.kind, p.seed, (uint32_t)kappa, kappa < p.k, t0, rc1, rowp, kl & 7);
       }
       fence_proxy_async_smem();
       __syncwarp();
@@ -215,6 +230,7 @@ sketch_tc_kernel(const __grid_constant__ CUtensorMap tmap, SketchTCParams p) {
     }
   } else if (warp >= 8) {
     // ---------------- norm warps (fp64 Σx²), then TMEM epilogue
+    // thread (rg, q): 16-byte chunk q of every row r ≡ rg (mod 8) of a stage
     const int g = tid - 256;
     const int q = g & 31, rg = g >> 5;
     const int box = q >> 3, chunk = q & 7;
@@ -228,15 +244,19 @@ sketch_tc_kernel(const __grid_constant__ CUtensorMap tmap, SketchTCParams p) {
       const bool duty = p.do_norms && (((kb_begin + it) % p.k_tiles) == kt);
       if (duty) {
         const uint8_t* base = x_s + s * X_STAGE + box * 8192;
-#pragma unroll 4
-        for (int rr = 0; rr < 16; ++rr) {
-          const int r = rg + 4 * rr;
-          const uint4 v = *reinterpret_cast<const uint4*>(base + r * 128 + ((chunk ^ (r & 7)) << 4));
-          const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+        uint4 v[NORM_ROWS];
+#pragma unroll
+        for (int rr = 0; rr < NORM_ROWS; ++rr) {
+          const int r = rg + NUM_NORM_WARPS * rr;
+          v[rr] = *reinterpret_cast<const uint4*>(base + r * 128 + ((chunk ^ (r & 7)) << 4));
+        }
+#pragma unroll
+        for (int rr = 0; rr < NORM_ROWS; ++rr) {
+          const uint32_t w[4] = {v[rr].x, v[rr].y, v[rr].z, v[rr].w};
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
-            const double lo = bf16mag_to_f64(w[e] & 0x7FFFu);
-            const double hi = bf16mag_to_f64((w[e] >> 16) & 0x7FFFu);
+            const double lo = bf16lo_mag_f64(w[e]);
+            const double hi = bf16hi_mag_f64(w[e]);
             acc[2 * e] = fma(lo, lo, acc[2 * e]);
             acc[2 * e + 1] = fma(hi, hi, acc[2 * e + 1]);
           }
@@ -245,24 +265,28 @@ sketch_tc_kernel(const __grid_constant__ CUtensorMap tmap, SketchTCParams p) {
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
     }
-    // norm partials: reduce the 4 row groups in a fixed order
+    // norm partials: reduce the row groups in a fixed order
 #pragma unroll
     for (int e = 0; e < 8; ++e) red[rg * TC_BN + box * 64 + chunk * 8 + e] = acc[e];
-    named_bar_sync(1, 128);
+    named_bar_sync(1, 32 * NUM_NORM_WARPS);
     const int slot = split * p.k_tiles + kt;
-    for (int col = g; col < TC_BN; col += 128) {
-      const double v = ((red[col] + red[TC_BN + col]) + red[2 * TC_BN + col]) + red[3 * TC_BN + col];
+    for (int col = g; col < TC_BN; col += 32 * NUM_NORM_WARPS) {
+      double v = red[col];
+#pragma unroll
+      for (int w = 1; w < NUM_NORM_WARPS; ++w) v += red[w * TC_BN + col];
       if (n0 + col < p.n) p.pnorm[(int64_t)slot * p.n + n0 + col] = v;
     }
-    // TMEM -> partial slot
+    // TMEM -> partial slot: warp quad owns lanes 32*quad..; the two warps of
+    // a quad split the 256 columns
     const int quad = warp & 3;
+    const int chalf = (warp - 8) >> 2;
     if (nkb > 0) {
       mbar_wait(tmem_full, 0);
       tc_fence_after();
     }
     for (int h = 0; h < nh; ++h) {
       const int kappa = kappa0 + h * 128 + 32 * quad + lane;
-      for (int cc = 0; cc < TC_BN / 32; ++cc) {
+      for (int cc = chalf * 4; cc < chalf * 4 + 4; ++cc) {
         uint32_t r[32];
         tmem_ld_32x32b_x32(tbase + ((uint32_t)(32 * quad) << 16) + h * 256 + cc * 32, r);
         tc_wait_ld();

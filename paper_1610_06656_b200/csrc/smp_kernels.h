@@ -35,7 +35,7 @@ cudaError_t launch_reduce_norms(const double* pnorm, int slots, int64_t n, doubl
 cudaError_t launch_split_f32(const float* X, int64_t ldx, int64_t rows, int64_t n, uint16_t* planes,
                              int64_t ldp, double* pnorm, int seg_rows, cudaStream_t st);
 // finalize one matrix: out = acc * scale (fp32), sknorm (fp64), D (fp64)
-cudaError_t launch_finalize(const float* acc, const double* nacc, int64_t n, int k, float scale,
+cudaError_t launch_finalize(const float* acc, double* nacc, int64_t n, int k, float scale,
                             float* out, double* sknorm, double* D, int* status, cudaStream_t st);
 // fixed pairwise tree sum (R5) of x[0..n) into *out (single block)
 cudaError_t launch_pairwise_sum(const double* x, int64_t n, double* scratch, double* out,

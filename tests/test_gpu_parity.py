@@ -127,6 +127,28 @@ def test_sketch_a_equals_b():
     check_sketch(fin, orc)
 
 
+def test_zero_and_sparse_columns():
+    """Degenerate columns: an all-zero column (norm 0, D = 0, never sampled
+    beyond the B-side term) and a column with a single nonzero entry."""
+    d, n, k = 777, 40, 64
+    A = synth.gaussian_small(d, n, seed=13)
+    A[:, 3] = 0.0
+    A[:, 5] = 0.0
+    A[100, 5] = 2.5
+    A = A.to(torch.bfloat16)
+    B = synth.gaussian_small(d, n, seed=14).to(torch.bfloat16)
+    sk, fin = gpu_sketch(A, B, k, 0, seed=1)
+    orc = oracle_sketch(A, B, k, 0, seed=1)
+    check_sketch(fin, orc)
+    assert float(fin["a_norm2"][3]) == 0.0 and float(fin["a_norm2"][5]) == 6.25
+    I, J, val, qh = sk.sample_estimate(500.0, 4)
+    al, be = oracle.alpha_beta(orc["a2"], orc["b2"], orc["FA"], orc["FB"])
+    Io, Jo, qo = oracle.sample(4, 500.0, al, be)
+    assert np.array_equal(I.cpu().numpy(), Io) and np.array_equal(J.cpu().numpy(), Jo)
+    v = val.cpu().numpy()
+    assert np.all(v[I.cpu().numpy() == 3] == 0.0)  # D_A = 0 for the zero column
+
+
 def test_hadamard_k_equals_d_exact_product():
     """North star (a): Hadamard Π with k = d gives M̃ = AᵀB (fully sampled)."""
     smp = _smp()

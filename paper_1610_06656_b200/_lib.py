@@ -52,11 +52,14 @@ class SmpError(RuntimeError):
 _lib = None
 
 
-def load(path: str = LIB_PATH):
-    """Load libsmp.so and declare signatures (no CUDA work happens here)."""
+def load(path: str = None):
+    """Load libsmp.so and declare signatures (no CUDA work happens here).
+    SMP_LIB may name an alternative in-tree build (tuning experiments)."""
     global _lib
     if _lib is not None:
         return _lib
+    if path is None:
+        path = os.environ.get("SMP_LIB", LIB_PATH)
     if not os.path.exists(path):
         raise FileNotFoundError(
             f"{path} missing: build it with `python -m paper_1610_06656_b200.build` "

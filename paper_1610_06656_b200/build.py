@@ -36,31 +36,42 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, defines=(), out: str = None) -> str:
+    """Compile csrc/*.cu (in parallel) and link libsmp.so.  `defines` and
+    `out` produce tuning variants (e.g. libsmp_x4p3.so) next to the default."""
+    out = out or LIB
+    if not force and out == LIB and not _stale():
         return LIB
     nvcc = os.environ.get("NVCC", "nvcc")
-    objdir = os.path.join(PKG, "build")
+    tag = os.path.basename(out).replace(".so", "")
+    objdir = os.path.join(PKG, "build", tag)
     os.makedirs(objdir, exist_ok=True)
-    objs = []
+    dflags = [f"-D{d}" for d in defines]
+    procs = []
     for src in sources():
         obj = os.path.join(objdir, os.path.basename(src).replace(".cu", ".o"))
-        cmd = [nvcc, *NVCC_FLAGS, "-dc" if False else "-c", src, "-o", obj,
-               "-I", os.path.join(ROOT, "include")]
-        r = subprocess.run(cmd, capture_output=True, text=True)
-        if r.returncode != 0:
-            sys.stderr.write(r.stdout + r.stderr)
+        cmd = [nvcc, *NVCC_FLAGS, *dflags, "-c", src, "-o", obj, "-I", os.path.join(ROOT, "include")]
+        procs.append((src, obj, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE,
+                                                 text=True)))
+    objs = []
+    for src, obj, pr in procs:
+        so, se = pr.communicate()
+        if pr.returncode != 0:
+            sys.stderr.write(so + se)
             raise RuntimeError(f"nvcc failed on {src}")
         if verbose:
-            sys.stderr.write(r.stderr)
+            sys.stderr.write(se)
         objs.append(obj)
-    cmd = [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", LIB + ".tmp", *objs,
+    cmd = [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", out + ".tmp", *objs,
            "-Xcompiler", "-fPIC"]
     subprocess.check_call(cmd)
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    os.replace(out + ".tmp", out)
+    return out
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose=True)
-    print(LIB)
+    args = [a for a in sys.argv[1:] if not a.startswith("--")]
+    defs = [a[2:] for a in args if a.startswith("-D")]
+    outs = [a for a in sys.argv[1:] if a.startswith("--out=")]
+    print(build(force="--force" in sys.argv or bool(defs), verbose="--quiet" not in sys.argv,
+                defines=defs, out=os.path.join(PKG, outs[0][6:]) if outs else None))

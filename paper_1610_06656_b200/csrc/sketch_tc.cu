@@ -27,14 +27,24 @@ namespace smp {
 constexpr int TC_BM = 256;                        // κ rows per CTA tile
 constexpr int TC_BN = 256;                        // X columns per CTA tile
 constexpr int TC_BK = 64;                         // X rows per K-block
-constexpr int TC_STAGES = 3;
+#ifndef SMP_X_STAGES
+#define SMP_X_STAGES 5
+#endif
+#ifndef SMP_PI_STAGES
+#define SMP_PI_STAGES 2
+#endif
+constexpr int X_STAGES = SMP_X_STAGES;            // X ring: HBM latency hiding
+constexpr int PI_STAGES = SMP_PI_STAGES;          // Π ring: on-chip generation
 constexpr int PI_STAGE = TC_BM * TC_BK * 2;       // 32 KB
 constexpr int X_STAGE = TC_BK * TC_BN * 2;        // 32 KB
 constexpr int NUM_GEN_WARPS = 4;                  // warps 4..7
 constexpr int NUM_NORM_WARPS = 8;                 // warps 8..15 (2 per SMSP)
 constexpr int NORM_ROWS = TC_BK / NUM_NORM_WARPS; // rows of a stage per norm thread
-constexpr int NORM_RED = NUM_NORM_WARPS * TC_BN * 8;  // 16 KB
-constexpr int TC_SMEM = TC_STAGES * (PI_STAGE + X_STAGE) + NORM_RED + 256 + 1024;
+constexpr int NORM_RED = NUM_NORM_WARPS * TC_BN * 8;  // 16 KB, aliases the Π ring at the end
+static_assert(NORM_RED <= PI_STAGES * PI_STAGE, "norm reduction buffer must fit the Π ring");
+constexpr int TC_BARS = 2 * X_STAGES + 2 * PI_STAGES + 1;
+constexpr int TC_SMEM = X_STAGES * X_STAGE + PI_STAGES * PI_STAGE + TC_BARS * 8 + 16 + 1024;
+static_assert(TC_SMEM <= 227 * 1024, "K1 exceeds the 227 KB SMEM budget");
 constexpr int TC_THREADS = 32 * (8 + NUM_NORM_WARPS);
 
 struct RadCache {
@@ -134,12 +144,14 @@ sketch_tc_kernel(const __grid_constant__ CUtensorMap tmap, SketchTCParams p) {
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_addr = smem_u32(smem_raw);
   uint8_t* smem = smem_raw + (((raw_addr + 1023u) & ~1023u) - raw_addr);
-  uint8_t* pi_s = smem;                                        // [stages][256][128 B]
-  uint8_t* x_s = smem + TC_STAGES * PI_STAGE;                  // [stages][4][64][128 B]
-  double* red = reinterpret_cast<double*>(x_s + TC_STAGES * X_STAGE);  // [4][256]
-  uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(red) + NORM_RED);
-  uint64_t* empty = full + TC_STAGES;
-  uint64_t* tmem_full = empty + TC_STAGES;
+  uint8_t* x_s = smem;                                   // [X_STAGES][4 boxes][64 rows][128 B]
+  uint8_t* pi_s = smem + X_STAGES * X_STAGE;             // [PI_STAGES][256 κ][128 B]
+  double* red = reinterpret_cast<double*>(pi_s);         // [8][256], after the last MMA
+  uint64_t* xfull = reinterpret_cast<uint64_t*>(pi_s + PI_STAGES * PI_STAGE);
+  uint64_t* xempty = xfull + X_STAGES;
+  uint64_t* pfull = xempty + X_STAGES;
+  uint64_t* pempty = pfull + PI_STAGES;
+  uint64_t* tmem_full = pempty + PI_STAGES;
   uint32_t* tmem_base_s = reinterpret_cast<uint32_t*>(tmem_full + 1);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -155,9 +167,13 @@ sketch_tc_kernel(const __grid_constant__ CUtensorMap tmap, SketchTCParams p) {
   const int nh = (p.k - kappa0 > 128) ? 2 : 1;
 
   if (tid == 0) {
-    for (int s = 0; s < TC_STAGES; ++s) {
-      mbar_init(&full[s], 1 + NUM_GEN_WARPS);
-      mbar_init(&empty[s], 1 + NUM_NORM_WARPS);
+    for (int s = 0; s < X_STAGES; ++s) {
+      mbar_init(&xfull[s], 1);                       // TMA expect_tx
+      mbar_init(&xempty[s], 1 + NUM_NORM_WARPS);     // MMA commit + norm warps
+    }
+    for (int s = 0; s < PI_STAGES; ++s) {
+      mbar_init(&pfull[s], NUM_GEN_WARPS);           // generator warps
+      mbar_init(&pempty[s], 1);                      // MMA commit
     }
     mbar_init(tmem_full, 1);
     fence_mbar_init();
@@ -170,17 +186,17 @@ sketch_tc_kernel(const __grid_constant__ CUtensorMap tmap, SketchTCParams p) {
   const uint32_t tbase = *tmem_base_s;
 
   if (warp == 0) {
-    // ---------------- TMA producer
+    // ---------------- TMA producer: X ring
     if (lane == 0) {
       for (int it = 0; it < nkb; ++it) {
-        const int s = it % TC_STAGES;
-        const uint32_t ph = (uint32_t)(it / TC_STAGES) & 1u;
-        mbar_wait(&empty[s], ph ^ 1u);
-        mbar_arrive_expect_tx(&full[s], X_STAGE);
+        const int s = it % X_STAGES;
+        const uint32_t ph = (uint32_t)(it / X_STAGES) & 1u;
+        mbar_wait(&xempty[s], ph ^ 1u);
+        mbar_arrive_expect_tx(&xfull[s], X_STAGE);
         const int row = (kb_begin + it) * TC_BK;
 #pragma unroll
         for (int j = 0; j < 4; ++j)
-          tma_load_2d(x_s + s * X_STAGE + j * 8192, &tmap, &full[s], n0 + 64 * j, row);
+          tma_load_2d(x_s + s * X_STAGE + j * 8192, &tmap, &xfull[s], n0 + 64 * j, row);
       }
     }
   } else if (warp == 1) {
@@ -189,20 +205,22 @@ sketch_tc_kernel(const __grid_constant__ CUtensorMap tmap, SketchTCParams p) {
       const uint32_t idesc = make_idesc_bf16(128, 256, 0, 1);
       const uint32_t pi_addr = smem_u32(pi_s), x_addr = smem_u32(x_s);
       for (int it = 0; it < nkb; ++it) {
-        const int s = it % TC_STAGES;
-        const uint32_t ph = (uint32_t)(it / TC_STAGES) & 1u;
-        mbar_wait(&full[s], ph);
+        const int s = it % X_STAGES, ps = it % PI_STAGES;
+        mbar_wait(&xfull[s], (uint32_t)(it / X_STAGES) & 1u);
+        mbar_wait(&pfull[ps], (uint32_t)(it / PI_STAGES) & 1u);
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < TC_BK / 16; ++kk) {
+          if (p.debug & 4) break;
           const uint64_t bdesc = make_sdesc_sw128(x_addr + s * X_STAGE + kk * 2048, 8192, 1024);
           for (int h = 0; h < nh; ++h) {
             const uint64_t adesc =
-                make_sdesc_sw128(pi_addr + s * PI_STAGE + h * 16384 + kk * 32, 16, 1024);
+                make_sdesc_sw128(pi_addr + ps * PI_STAGE + h * 16384 + kk * 32, 16, 1024);
             tc_mma_f16(tbase + h * 256, adesc, bdesc, idesc, (it | kk) != 0 ? 1u : 0u);
           }
         }
-        tc_commit(&empty[s]);
+        tc_commit(&xempty[s]);
+        tc_commit(&pempty[ps]);
       }
       tc_commit(tmem_full);
     }
@@ -211,22 +229,21 @@ sketch_tc_kernel(const __grid_constant__ CUtensorMap tmap, SketchTCParams p) {
     const int g = tid - 128;
     RadCache rc0{~0ull, 0, 0, 0, 0}, rc1{~0ull, 0, 0, 0, 0};
     for (int it = 0; it < nkb; ++it) {
-      const int s = it % TC_STAGES;
-      const uint32_t ph = (uint32_t)(it / TC_STAGES) & 1u;
+      const int ps = it % PI_STAGES;
       const uint64_t t0 = (uint64_t)p.row0 + (uint64_t)(kb_begin + it) * TC_BK;
-      mbar_wait(&empty[s], ph ^ 1u);
+      mbar_wait(&pempty[ps], ((uint32_t)(it / PI_STAGES) & 1u) ^ 1u);
 #pragma unroll
       for (int r = 0; r < 2; ++r) {
         const int kl = g + 128 * r;
-        if (r == 1 && nh == 1) break;
+        if ((r == 1 && nh == 1) || (p.debug & 2)) break;
         const int kappa = kappa0 + kl;
-        uint8_t* rowp = pi_s + s * PI_STAGE + kl * 128;
+        uint8_t* rowp = pi_s + ps * PI_STAGE + kl * 128;
         if (r == 0) gen_pi_row(p.kind, p.seed, (uint32_t)kappa, kappa < p.k, t0, rc0, rowp, kl & 7);
         else gen_pi_row(p.kind, p.seed, (uint32_t)kappa, kappa < p.k, t0, rc1, rowp, kl & 7);
       }
       fence_proxy_async_smem();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&full[s]);
+      if (lane == 0) mbar_arrive(&pfull[ps]);
     }
   } else if (warp >= 8) {
     // ---------------- norm warps (fp64 Σx²), then TMEM epilogue
@@ -238,10 +255,9 @@ sketch_tc_kernel(const __grid_constant__ CUtensorMap tmap, SketchTCParams p) {
 #pragma unroll
     for (int e = 0; e < 8; ++e) acc[e] = 0.0;
     for (int it = 0; it < nkb; ++it) {
-      const int s = it % TC_STAGES;
-      const uint32_t ph = (uint32_t)(it / TC_STAGES) & 1u;
-      mbar_wait(&full[s], ph);
-      const bool duty = p.do_norms && (((kb_begin + it) % p.k_tiles) == kt);
+      const int s = it % X_STAGES;
+      mbar_wait(&xfull[s], (uint32_t)(it / X_STAGES) & 1u);
+      const bool duty = p.do_norms && !(p.debug & 1) && (((kb_begin + it) % p.k_tiles) == kt);
       if (duty) {
         const uint8_t* base = x_s + s * X_STAGE + box * 8192;
         uint4 v[NORM_ROWS];
@@ -263,9 +279,13 @@ sketch_tc_kernel(const __grid_constant__ CUtensorMap tmap, SketchTCParams p) {
         }
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);
+      if (lane == 0) mbar_arrive(&xempty[s]);
     }
-    // norm partials: reduce the row groups in a fixed order
+    // all MMAs done -> the Π ring is free: reuse it for the norm reduction
+    if (nkb > 0) {
+      mbar_wait(tmem_full, 0);
+      tc_fence_after();
+    }
 #pragma unroll
     for (int e = 0; e < 8; ++e) red[rg * TC_BN + box * 64 + chunk * 8 + e] = acc[e];
     named_bar_sync(1, 32 * NUM_NORM_WARPS);
@@ -280,10 +300,6 @@ sketch_tc_kernel(const __grid_constant__ CUtensorMap tmap, SketchTCParams p) {
     // a quad split the 256 columns
     const int quad = warp & 3;
     const int chalf = (warp - 8) >> 2;
-    if (nkb > 0) {
-      mbar_wait(tmem_full, 0);
-      tc_fence_after();
-    }
     for (int h = 0; h < nh; ++h) {
       const int kappa = kappa0 + h * 128 + 32 * quad + lane;
       for (int cc = chalf * 4; cc < chalf * 4 + 4; ++cc) {

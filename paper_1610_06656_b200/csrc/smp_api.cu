@@ -140,6 +140,7 @@ smp_status sketch_dense_bf16(smp_handle* h, int64_t row0, int64_t rows, const vo
   p.splits = choose_splits(p.n_tiles * p.k_tiles, p.kb_total);
   p.kind = h->d.pi_kind;
   p.do_norms = do_norms ? 1 : 0;
+  { const char* dbg = getenv("SMP_K1_DEBUG"); p.debug = dbg ? atoi(dbg) : 0; }
   p.seed = h->d.seed;
   CK(h, ensure(h->part, h->part_cap, (int64_t)p.splits * ncols * k), "alloc partials");
   CK(h, ensure(h->pnorm, h->pnorm_cap, (int64_t)p.splits * p.k_tiles * ncols), "alloc pnorm");

@@ -1,0 +1,48 @@
+"""Row sharding across GPUs and the single combine step.
+
+ΠA = Σ_g Π[:, rows_g] A[rows_g, :] and ||A_i||² = Σ_g ||A_i^(g)||² are sums
+over row blocks (the Spark treeAggregate of P:145), so each rank sketches its
+own rows and the packed partials are combined by ONE all-reduce (NCCL over
+NVLink on B200; gloo works for the CPU tests).  Everything after the combine
+(finalize, Ω, M̃, WAltMin) is replicated: the hashes make Ω identical on every
+rank without further communication.
+"""
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+GEN_BLOCK = 65536
+
+
+def shard_rows(d: int, world: int, rank: int, align: int = GEN_BLOCK):
+    """[r0, r1) of rank: equal, `align`-aligned row ranges (the input
+    generators are keyed by 65,536-row blocks, so shards see identical data)."""
+    if world < 1 or not (0 <= rank < world):
+        raise ValueError("bad world/rank")
+    nblk = (d + align - 1) // align
+    b0 = nblk * rank // world
+    b1 = nblk * (rank + 1) // world
+    return min(d, b0 * align), min(d, b1 * align)
+
+
+def allreduce_partials(tensors, group=None):
+    """Sum the partial sketch (fp32) and norm (fp64) buffers across ranks in
+    place, as one coalesced collective."""
+    if not dist.is_available() or not dist.is_initialized() or dist.get_world_size(group) == 1:
+        return tensors
+    if dist.get_backend(group) == "nccl":
+        with dist._coalescing_manager(group=group, async_ops=False):
+            for t in tensors:
+                dist.all_reduce(t, group=group)
+    else:  # gloo coalesces only same-dtype tensors
+        for t in tensors:
+            dist.all_reduce(t, group=group)
+    return tensors
+
+
+def combine(sketch, group=None):
+    """All-reduce an SMPSketch's packed partials in place (before finalize)."""
+    sk, nrm = sketch.partials()
+    allreduce_partials([sk, nrm], group=group)
+    return sk, nrm

@@ -29,7 +29,12 @@ def main():
     for _ in range(reps):
         sk.reset()
         sk.block(0, A, B)
-        sk.finalize()
+        try:
+            sk.finalize()
+        except Exception as e:  # debug variants produce invalid sketches
+            if not os.environ.get("SMP_K1_DEBUG"):
+                raise
+            _ = e
     ms, n = sk.kernel_timing()
     print(f"{name}: K1 {ms / max(n, 1):.4f} ms/launch over {n} launches")
     sk.close()

@@ -5,18 +5,29 @@
 //   pnorm[slot][c]    = Σ_{t in split's rows} X[t, c]^2          (fp64, SIMT)
 //
 // GEMM view: D (κ × c) += Π (κ × t) · X (t × c), M = κ, N = c, K = t.
-//   * X tile (64 rows × 256 cols bf16) arrives by TMA, 128B-swizzled, as
-//     four 64×64 boxes: the B operand, MN-major.
-//   * Π tile (256 κ × 64 t bf16) is never read from memory: 4 generator
-//     warps regenerate it from the Philox hash straight into a K-major
-//     128B-swizzled SMEM tile (the A operand).  Π is stored nowhere else.
-//   * one elected thread issues tcgen05.mma (M=128, N=256, K=16) for the two
-//     κ halves into a 512-column TMEM accumulator.
-//   * 4 norm warps read the same X stage from SMEM and accumulate x² in fp64
-//     (exact squares of bf16 values), so A and B are read from HBM once.
-//   * the same 4 warps drain TMEM (tcgen05.ld) into the split's partial slot.
-// Pipelines: full[s] (TMA tx + 4 generator-warp arrivals) -> MMA;
-//            empty[s] (tcgen05.commit + 4 norm-warp arrivals) -> TMA/gen.
+// A CTA PAIR (cluster of 2, tcgen05 cta_group::2) owns a 256 κ × 256 column
+// tile: each SM holds 128 κ rows of Π (its half of A) and 128 columns of X
+// (its half of B); one thread of the leader issues M=256, N=256, K=16 MMAs
+// that run on both SMs.  Per SM:
+//   * X half tile (64 rows × 128 cols bf16) arrives by TMA as two 64×64
+//     128B-swizzled boxes: the B operand, MN-major (8-stage SMEM ring).
+//   * Π half tile (128 κ × 64 t) is regenerated from the Philox hash by 4
+//     generator warps and written straight into TMEM with tcgen05.st: the A
+//     operand lives in TMEM (4-stage ring of 32 columns), so Π costs no SMEM
+//     bandwidth and is stored nowhere else.
+//   * 8 norm warps read the X stage once from SMEM and accumulate exact x²
+//     in fp64 (two integer ops + one DFMA per element): A and B are read from
+//     HBM exactly once.
+//   * the same 8 warps drain the 128 × 256 fp32 accumulator (tcgen05.ld)
+//     into the split's partial slot.
+// Per-SM SMEM traffic per 64-row K-block: 16 KB TMA write + 16 KB MMA B read
+// + 16 KB norm read = 48 KB per 512 tensor cycles (vs 96 B/cycle for the
+// MMA operands alone in the one-SM SMEM-SMEM form).
+// Synchronisation (per CTA): xfull (TMA tx) / xempty (MMA commit + norm
+// warps); pfull (generator warps) / pempty (MMA commit); a relay thread in
+// each CTA forwards "X and Π of stage s ready" to the leader's ready[s]
+// (count 2, remote mbarrier arrive for the peer); MMA commits are multicast
+// to both CTAs.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include "smp_device.cuh"
@@ -24,26 +35,30 @@
 
 namespace smp {
 
-constexpr int TC_BM = 256;                        // κ rows per CTA tile
-constexpr int TC_BN = 256;                        // X columns per CTA tile
+constexpr int TC_BM = 256;                        // κ rows per CTA pair (128 per SM)
+constexpr int TC_BN = 256;                        // X columns per CTA pair (128 per SM)
+constexpr int HALF_N = TC_BN / 2;
 constexpr int TC_BK = 64;                         // X rows per K-block
 #ifndef SMP_X_STAGES
-#define SMP_X_STAGES 5
+#define SMP_X_STAGES 8
 #endif
+constexpr int X_STAGES = SMP_X_STAGES;            // SMEM ring (HBM latency hiding)
 #ifndef SMP_PI_STAGES
-#define SMP_PI_STAGES 2
+#define SMP_PI_STAGES 4
 #endif
-constexpr int X_STAGES = SMP_X_STAGES;            // X ring: HBM latency hiding
-constexpr int PI_STAGES = SMP_PI_STAGES;          // Π ring: on-chip generation
-constexpr int PI_STAGE = TC_BM * TC_BK * 2;       // 32 KB
-constexpr int X_STAGE = TC_BK * TC_BN * 2;        // 32 KB
-constexpr int NUM_GEN_WARPS = 4;                  // warps 4..7
-constexpr int NUM_NORM_WARPS = 8;                 // warps 8..15 (2 per SMSP)
-constexpr int NORM_ROWS = TC_BK / NUM_NORM_WARPS; // rows of a stage per norm thread
-constexpr int NORM_RED = NUM_NORM_WARPS * TC_BN * 8;  // 16 KB, aliases the Π ring at the end
-static_assert(NORM_RED <= PI_STAGES * PI_STAGE, "norm reduction buffer must fit the Π ring");
-constexpr int TC_BARS = 2 * X_STAGES + 2 * PI_STAGES + 1;
-constexpr int TC_SMEM = X_STAGES * X_STAGE + PI_STAGES * PI_STAGE + TC_BARS * 8 + 16 + 1024;
+constexpr int PI_STAGES = SMP_PI_STAGES;          // TMEM ring for Π (A operand)
+constexpr int X_STAGE = TC_BK * HALF_N * 2;       // 16 KB
+constexpr int ACC_COLS = TC_BN;                   // fp32 accumulator columns
+constexpr int PI_COLS = TC_BK / 2;                // 64 bf16 per lane = 32 columns
+constexpr int TMEM_COLS = 512;
+static_assert(ACC_COLS + PI_STAGES * PI_COLS <= TMEM_COLS, "TMEM budget");
+constexpr int NUM_GEN_WARPS = 4;                  // warps 4..7 (one per TMEM lane quadrant)
+constexpr int NUM_NORM_WARPS = 8;                 // warps 8..15
+constexpr int NORM_RG = (32 * NUM_NORM_WARPS) / 16;   // row groups (16 chunks per row)
+constexpr int NORM_ROWS = TC_BK / NORM_RG;        // rows per norm thread per stage
+constexpr int NORM_RED = NORM_RG * HALF_N * 8;    // 16 KB
+constexpr int TC_BARS = 3 * X_STAGES + 2 * PI_STAGES + 1;
+constexpr int TC_SMEM = X_STAGES * X_STAGE + NORM_RED + TC_BARS * 8 + 16 + 1024;
 static_assert(TC_SMEM <= 227 * 1024, "K1 exceeds the 227 KB SMEM budget");
 constexpr int TC_THREADS = 32 * (8 + NUM_NORM_WARPS);
 
@@ -70,43 +85,37 @@ __device__ __forceinline__ uint32_t rad_word(RadCache& c, uint64_t W, uint32_t k
 // (rows 2p, 2p+1) is built with one shift and one LOP3.
 __device__ __forceinline__ uint32_t rad_pos(uint32_t e) { return (e >> 1) | ((e & 1u) << 4); }
 
-// Generate one κ row of the Π tile (64 bf16 = 32 packed words) straight into
-// its K-major SWIZZLE_128B SMEM row: 16-byte chunk c of row kl lives at
-// chunk position c ^ (kl & 7).
+// One κ row of the Π tile for rows t0..t0+63: 64 bf16 packed in 32 words
+// (word p = rows 2p (low half) and 2p+1 (high half)), the TMEM A layout.
 __device__ __forceinline__ void gen_pi_row(int kind, uint64_t seed, uint32_t kappa, bool valid,
-                                           uint64_t t0, RadCache& rc, uint8_t* rowp, int sw) {
+                                           uint64_t t0, RadCache& rc, uint32_t (&o)[32]) {
   const uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
   if (!valid) {
 #pragma unroll
-    for (int c = 0; c < 8; ++c) *reinterpret_cast<uint4*>(rowp + ((c ^ sw) << 4)) = make_uint4(0, 0, 0, 0);
+    for (int i = 0; i < 32; ++i) o[i] = 0u;
     return;
   }
   if (kind == PI_RADEMACHER && (t0 & 31) == 0) {
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const uint32_t w = rad_word(rc, (t0 >> 5) + h, kappa, k0, k1);
-      uint32_t o[16];
 #pragma unroll
-      for (int p = 0; p < 16; ++p) o[p] = 0x3F803F80u | ((w << (15 - p)) & 0x80008000u);
-#pragma unroll
-      for (int c = 0; c < 4; ++c)
-        *reinterpret_cast<uint4*>(rowp + (((4 * h + c) ^ sw) << 4)) =
-            make_uint4(o[4 * c], o[4 * c + 1], o[4 * c + 2], o[4 * c + 3]);
+      for (int p = 0; p < 16; ++p) o[16 * h + p] = 0x3F803F80u | ((w << (15 - p)) & 0x80008000u);
     }
   } else if (kind == PI_GAUSSIAN && (t0 & 3) == 0) {
-#pragma unroll 2
+#pragma unroll
     for (int q = 0; q < 16; ++q) {
       const uint64_t tq = (t0 >> 2) + q;
       const u32x4 w = philox4x32_10((uint32_t)tq, kappa, (uint32_t)(tq >> 32), TAG_GAUSSIAN, k0, k1);
       uint16_t a, b, c, d;
       gauss_pair(w.x, w.y, a, b);
       gauss_pair(w.z, w.w, c, d);
-      *reinterpret_cast<uint2*>(rowp + (((q >> 1) ^ sw) << 4) + ((q & 1) << 3)) =
-          make_uint2((uint32_t)a | ((uint32_t)b << 16), (uint32_t)c | ((uint32_t)d << 16));
+      o[2 * q] = (uint32_t)a | ((uint32_t)b << 16);
+      o[2 * q + 1] = (uint32_t)c | ((uint32_t)d << 16);
     }
   } else {
     // generic (unaligned block start, Hadamard test mode): element by element
-#pragma unroll 1
+#pragma unroll
     for (int p = 0; p < 32; ++p) {
       uint32_t lohi[2];
 #pragma unroll
@@ -119,8 +128,7 @@ __device__ __forceinline__ void gen_pi_row(int kind, uint64_t seed, uint32_t kap
           lohi[e] = pi_bits(kind, seed, kappa, t);
         }
       }
-      *reinterpret_cast<uint32_t*>(rowp + (((p >> 2) ^ sw) << 4) + ((p & 3) << 2)) =
-          lohi[0] | (lohi[1] << 16);
+      o[p] = lohi[0] | (lohi[1] << 16);
     }
   }
 }
@@ -144,112 +152,123 @@ sketch_tc_kernel(const __grid_constant__ CUtensorMap tmap, SketchTCParams p) {
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_addr = smem_u32(smem_raw);
   uint8_t* smem = smem_raw + (((raw_addr + 1023u) & ~1023u) - raw_addr);
-  uint8_t* x_s = smem;                                   // [X_STAGES][4 boxes][64 rows][128 B]
-  uint8_t* pi_s = smem + X_STAGES * X_STAGE;             // [PI_STAGES][256 κ][128 B]
-  double* red = reinterpret_cast<double*>(pi_s);         // [8][256], after the last MMA
-  uint64_t* xfull = reinterpret_cast<uint64_t*>(pi_s + PI_STAGES * PI_STAGE);
+  uint8_t* x_s = smem;                                              // [X_STAGES][2][64][128 B]
+  double* red = reinterpret_cast<double*>(smem + X_STAGES * X_STAGE);  // [NORM_RG][128]
+  uint64_t* xfull = reinterpret_cast<uint64_t*>(smem + X_STAGES * X_STAGE + NORM_RED);
   uint64_t* xempty = xfull + X_STAGES;
-  uint64_t* pfull = xempty + X_STAGES;
+  uint64_t* ready = xempty + X_STAGES;    // leader only: X and Π of both CTAs ready
+  uint64_t* pfull = ready + X_STAGES;
   uint64_t* pempty = pfull + PI_STAGES;
   uint64_t* tmem_full = pempty + PI_STAGES;
   uint32_t* tmem_base_s = reinterpret_cast<uint32_t*>(tmem_full + 1);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  // tile decomposition: kt innermost so CTAs sharing an X tile run together
-  int bid = blockIdx.x;
+  const uint32_t rank = cluster_ctarank();
+  // pair decomposition: kt innermost so pairs sharing an X tile run together
+  int bid = blockIdx.x >> 1;
   const int kt = bid % p.k_tiles; bid /= p.k_tiles;
   const int nt = bid % p.n_tiles; bid /= p.n_tiles;
   const int split = bid;
   const int kb_begin = (int)(((int64_t)split * p.kb_total) / p.splits);
   const int kb_end = (int)(((int64_t)(split + 1) * p.kb_total) / p.splits);
   const int nkb = kb_end - kb_begin;
-  const int n0 = nt * TC_BN, kappa0 = kt * TC_BM;
-  const int nh = (p.k - kappa0 > 128) ? 2 : 1;
+  const int n0 = nt * TC_BN + (int)rank * HALF_N;                // this SM's columns
+  const int kappa0 = kt * TC_BM + (int)rank * 128;               // this SM's κ rows
 
   if (tid == 0) {
     for (int s = 0; s < X_STAGES; ++s) {
-      mbar_init(&xfull[s], 1);                       // TMA expect_tx
-      mbar_init(&xempty[s], 1 + NUM_NORM_WARPS);     // MMA commit + norm warps
+      mbar_init(&xfull[s], 1);
+      mbar_init(&xempty[s], 1 + NUM_NORM_WARPS);
+      mbar_init(&ready[s], 2);
     }
     for (int s = 0; s < PI_STAGES; ++s) {
-      mbar_init(&pfull[s], NUM_GEN_WARPS);           // generator warps
-      mbar_init(&pempty[s], 1);                      // MMA commit
+      mbar_init(&pfull[s], NUM_GEN_WARPS);
+      mbar_init(&pempty[s], 1);
     }
     mbar_init(tmem_full, 1);
     fence_mbar_init();
   }
   if (warp == 0 && lane == 0) tma_prefetch_desc(&tmap);
-  if (warp == 1) tmem_alloc(tmem_base_s, 512);
+  if (warp == 1) tmem_alloc2(tmem_base_s, TMEM_COLS);
   tc_fence_before();
-  __syncthreads();
+  cluster_sync();
   tc_fence_after();
   const uint32_t tbase = *tmem_base_s;
 
   if (warp == 0) {
-    // ---------------- TMA producer: X ring
+    // ---------------- TMA producer: this SM's half of the X tile
     if (lane == 0) {
       for (int it = 0; it < nkb; ++it) {
         const int s = it % X_STAGES;
-        const uint32_t ph = (uint32_t)(it / X_STAGES) & 1u;
-        mbar_wait(&xempty[s], ph ^ 1u);
+        mbar_wait(&xempty[s], ((uint32_t)(it / X_STAGES) & 1u) ^ 1u);
         mbar_arrive_expect_tx(&xfull[s], X_STAGE);
         const int row = (kb_begin + it) * TC_BK;
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-          tma_load_2d(x_s + s * X_STAGE + j * 8192, &tmap, &xfull[s], n0 + 64 * j, row);
+        tma_load_2d(x_s + s * X_STAGE, &tmap, &xfull[s], n0, row);
+        tma_load_2d(x_s + s * X_STAGE + 8192, &tmap, &xfull[s], n0 + 64, row);
       }
     }
   } else if (warp == 1) {
-    // ---------------- MMA issuer (one thread)
+    // ---------------- MMA issuer (leader CTA, one thread)
+    if (rank == 0 && lane == 0) {
+      const uint32_t idesc = make_idesc_bf16(256, 256, 0, 1);
+      const uint32_t x_addr = smem_u32(x_s);
+      for (int it = 0; it < nkb; ++it) {
+        const int s = it % X_STAGES, ps = it % PI_STAGES;
+        mbar_wait(&ready[s], (uint32_t)(it / X_STAGES) & 1u);
+        tc_fence_after();
+        if (!(p.debug & 4)) {
+#pragma unroll
+          for (int kk = 0; kk < TC_BK / 16; ++kk) {
+            const uint64_t bdesc = make_sdesc_sw128(x_addr + s * X_STAGE + kk * 2048, 8192, 1024);
+            tc_mma2_ts(tbase, tbase + ACC_COLS + ps * PI_COLS + kk * 8, bdesc, idesc,
+                       (it | kk) != 0 ? 1u : 0u);
+          }
+        }
+        tc_commit2(&xempty[s], 0x3);
+        tc_commit2(&pempty[ps], 0x3);
+      }
+      tc_commit2(tmem_full, 0x3);
+    }
+  } else if (warp == 2) {
+    // ---------------- relay: this CTA's X and Π of stage s are ready
     if (lane == 0) {
-      const uint32_t idesc = make_idesc_bf16(128, 256, 0, 1);
-      const uint32_t pi_addr = smem_u32(pi_s), x_addr = smem_u32(x_s);
+      const uint32_t leader_ready = mapa_shared(smem_u32(ready), 0);
       for (int it = 0; it < nkb; ++it) {
         const int s = it % X_STAGES, ps = it % PI_STAGES;
         mbar_wait(&xfull[s], (uint32_t)(it / X_STAGES) & 1u);
         mbar_wait(&pfull[ps], (uint32_t)(it / PI_STAGES) & 1u);
-        tc_fence_after();
-#pragma unroll
-        for (int kk = 0; kk < TC_BK / 16; ++kk) {
-          if (p.debug & 4) break;
-          const uint64_t bdesc = make_sdesc_sw128(x_addr + s * X_STAGE + kk * 2048, 8192, 1024);
-          for (int h = 0; h < nh; ++h) {
-            const uint64_t adesc =
-                make_sdesc_sw128(pi_addr + ps * PI_STAGE + h * 16384 + kk * 32, 16, 1024);
-            tc_mma_f16(tbase + h * 256, adesc, bdesc, idesc, (it | kk) != 0 ? 1u : 0u);
-          }
-        }
-        tc_commit(&xempty[s]);
-        tc_commit(&pempty[ps]);
+        mbar_arrive_cluster(leader_ready + 8u * (uint32_t)s);
       }
-      tc_commit(tmem_full);
     }
   } else if (warp >= 4 && warp < 8) {
-    // ---------------- Π generators: thread g owns κ rows g and g+128
-    const int g = tid - 128;
-    RadCache rc0{~0ull, 0, 0, 0, 0}, rc1{~0ull, 0, 0, 0, 0};
+    // ---------------- Π generators: thread owns TMEM lane 32*quad + lane
+    const int quad = warp & 3;
+    const int kl = 32 * quad + lane;
+    const int kappa = kappa0 + kl;
+    RadCache rc{~0ull, 0, 0, 0, 0};
     for (int it = 0; it < nkb; ++it) {
       const int ps = it % PI_STAGES;
       const uint64_t t0 = (uint64_t)p.row0 + (uint64_t)(kb_begin + it) * TC_BK;
-      mbar_wait(&pempty[ps], ((uint32_t)(it / PI_STAGES) & 1u) ^ 1u);
+      uint32_t o[32];
+      if (p.debug & 2) {
 #pragma unroll
-      for (int r = 0; r < 2; ++r) {
-        const int kl = g + 128 * r;
-        if ((r == 1 && nh == 1) || (p.debug & 2)) break;
-        const int kappa = kappa0 + kl;
-        uint8_t* rowp = pi_s + ps * PI_STAGE + kl * 128;
-        if (r == 0) gen_pi_row(p.kind, p.seed, (uint32_t)kappa, kappa < p.k, t0, rc0, rowp, kl & 7);
-        else gen_pi_row(p.kind, p.seed, (uint32_t)kappa, kappa < p.k, t0, rc1, rowp, kl & 7);
+        for (int i = 0; i < 32; ++i) o[i] = 0x3F803F80u;
+      } else {
+        gen_pi_row(p.kind, p.seed, (uint32_t)kappa, kappa < p.k, t0, rc, o);
       }
-      fence_proxy_async_smem();
+      mbar_wait(&pempty[ps], ((uint32_t)(it / PI_STAGES) & 1u) ^ 1u);
+      tc_fence_after();
+      tmem_st_32x32b_x32(tbase + ((uint32_t)(32 * quad) << 16) + ACC_COLS + ps * PI_COLS, o);
+      tc_wait_st();
+      tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&pfull[ps]);
     }
   } else if (warp >= 8) {
     // ---------------- norm warps (fp64 Σx²), then TMEM epilogue
-    // thread (rg, q): 16-byte chunk q of every row r ≡ rg (mod 8) of a stage
+    // thread (rg, q): 16-byte chunk q (box q>>3, chunk q&7) of rows r ≡ rg (mod 16)
     const int g = tid - 256;
-    const int q = g & 31, rg = g >> 5;
+    const int q = g & 15, rg = g >> 4;
     const int box = q >> 3, chunk = q & 7;
     double acc[8];
 #pragma unroll
@@ -263,7 +282,7 @@ sketch_tc_kernel(const __grid_constant__ CUtensorMap tmap, SketchTCParams p) {
         uint4 v[NORM_ROWS];
 #pragma unroll
         for (int rr = 0; rr < NORM_ROWS; ++rr) {
-          const int r = rg + NUM_NORM_WARPS * rr;
+          const int r = rg + NORM_RG * rr;
           v[rr] = *reinterpret_cast<const uint4*>(base + r * 128 + ((chunk ^ (r & 7)) << 4));
         }
 #pragma unroll
@@ -281,50 +300,50 @@ sketch_tc_kernel(const __grid_constant__ CUtensorMap tmap, SketchTCParams p) {
       __syncwarp();
       if (lane == 0) mbar_arrive(&xempty[s]);
     }
-    // all MMAs done -> the Π ring is free: reuse it for the norm reduction
+    // norm partials: reduce the row groups in a fixed order
+#pragma unroll
+    for (int e = 0; e < 8; ++e) red[rg * HALF_N + box * 64 + chunk * 8 + e] = acc[e];
+    named_bar_sync(1, 32 * NUM_NORM_WARPS);
+    const int slot = split * p.k_tiles + kt;
+    if (g < HALF_N) {
+      double v = red[g];
+#pragma unroll
+      for (int w = 1; w < NORM_RG; ++w) v += red[w * HALF_N + g];
+      if (n0 + g < p.n) p.pnorm[(int64_t)slot * p.n + n0 + g] = v;
+    }
+    // TMEM -> partial slot: warp quad owns lanes 32*quad..; the two warps of
+    // a quad split the 256 accumulator columns
+    const int quad = warp & 3;
+    const int chalf = (warp - 8) >> 2;
     if (nkb > 0) {
       mbar_wait(tmem_full, 0);
       tc_fence_after();
     }
+    const int kappa = kappa0 + 32 * quad + lane;
+    const int ncol0 = nt * TC_BN;
+    for (int cc = chalf * 4; cc < chalf * 4 + 4; ++cc) {
+      uint32_t r[32];
+      tmem_ld_32x32b_x32(tbase + ((uint32_t)(32 * quad) << 16) + cc * 32, r);
+      tc_wait_ld();
+      if (nkb == 0) {
 #pragma unroll
-    for (int e = 0; e < 8; ++e) red[rg * TC_BN + box * 64 + chunk * 8 + e] = acc[e];
-    named_bar_sync(1, 32 * NUM_NORM_WARPS);
-    const int slot = split * p.k_tiles + kt;
-    for (int col = g; col < TC_BN; col += 32 * NUM_NORM_WARPS) {
-      double v = red[col];
+        for (int j = 0; j < 32; ++j) r[j] = 0u;
+      }
+      if (kappa < p.k) {
 #pragma unroll
-      for (int w = 1; w < NUM_NORM_WARPS; ++w) v += red[w * TC_BN + col];
-      if (n0 + col < p.n) p.pnorm[(int64_t)slot * p.n + n0 + col] = v;
-    }
-    // TMEM -> partial slot: warp quad owns lanes 32*quad..; the two warps of
-    // a quad split the 256 columns
-    const int quad = warp & 3;
-    const int chalf = (warp - 8) >> 2;
-    for (int h = 0; h < nh; ++h) {
-      const int kappa = kappa0 + h * 128 + 32 * quad + lane;
-      for (int cc = chalf * 4; cc < chalf * 4 + 4; ++cc) {
-        uint32_t r[32];
-        tmem_ld_32x32b_x32(tbase + ((uint32_t)(32 * quad) << 16) + h * 256 + cc * 32, r);
-        tc_wait_ld();
-        if (nkb == 0) {
-#pragma unroll
-          for (int j = 0; j < 32; ++j) r[j] = 0u;
-        }
-        if (kappa < p.k) {
-#pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const int col = n0 + cc * 32 + j;
-            if (col < p.n) p.part[((int64_t)split * p.n + col) * p.k + kappa] = __uint_as_float(r[j]);
-          }
+        for (int j = 0; j < 32; ++j) {
+          const int col = ncol0 + cc * 32 + j;
+          if (col < p.n) p.part[((int64_t)split * p.n + col) * p.k + kappa] = __uint_as_float(r[j]);
         }
       }
     }
   }
   tc_fence_before();
   __syncthreads();
+  cluster_sync();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc(tbase, 512);
+    tmem_dealloc2(tbase, TMEM_COLS);
   }
 }
 
@@ -343,6 +362,7 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
 }
 
 int sketch_tc_smem_bytes() { return TC_SMEM; }
+int sketch_tc_ctas_per_tile() { return 2; }
 
 cudaError_t launch_sketch_tc(const void* X, int64_t ldx, SketchTCParams p, cudaStream_t st) {
   auto enc = get_encode_fn();
@@ -363,9 +383,19 @@ cudaError_t launch_sketch_tc(const void* X, int64_t ldx, SketchTCParams p, cudaS
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  const int grid = p.n_tiles * p.k_tiles * p.splits;
-  sketch_tc_kernel<<<grid, TC_THREADS, TC_SMEM, st>>>(tmap, p);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(2u * (unsigned)(p.n_tiles * p.k_tiles * p.splits));
+  cfg.blockDim = dim3(TC_THREADS);
+  cfg.dynamicSmemBytes = TC_SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, sketch_tc_kernel, tmap, p);
 }
 
 }  // namespace smp

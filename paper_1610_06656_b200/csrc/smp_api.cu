@@ -118,7 +118,7 @@ int choose_splits(int tiles, int kb_total) {
     const int64_t ctas = (int64_t)tiles * s;
     const int64_t waves = (ctas + sms - 1) / sms;
     const double eff = (double)ctas / (double)(waves * sms);
-    if (eff >= 0.95 && ctas >= sms) return s;
+    if (eff >= 0.95) return s;
     if (eff > best_eff + 1e-9) { best_eff = eff; best_s = s; }
   }
   return best_s;
@@ -137,7 +137,7 @@ smp_status sketch_dense_bf16(smp_handle* h, int64_t row0, int64_t rows, const vo
   p.n_tiles = (int32_t)((ncols + 255) / 256);
   p.k_tiles = (k + 255) / 256;
   p.kb_total = (int32_t)((rows + 63) / 64);
-  p.splits = choose_splits(p.n_tiles * p.k_tiles, p.kb_total);
+  p.splits = choose_splits(2 * p.n_tiles * p.k_tiles, p.kb_total);  // CTA pairs
   p.kind = h->d.pi_kind;
   p.do_norms = do_norms ? 1 : 0;
   { const char* dbg = getenv("SMP_K1_DEBUG"); p.debug = dbg ? atoi(dbg) : 0; }

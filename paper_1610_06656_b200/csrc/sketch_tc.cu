@@ -52,7 +52,10 @@ constexpr int ACC_COLS = TC_BN;                   // fp32 accumulator columns
 constexpr int PI_COLS = TC_BK / 2;                // 64 bf16 per lane = 32 columns
 constexpr int TMEM_COLS = 512;
 static_assert(ACC_COLS + PI_STAGES * PI_COLS <= TMEM_COLS, "TMEM budget");
-constexpr int NUM_GEN_WARPS = 4;                  // warps 4..7 (one per TMEM lane quadrant)
+// Warp roles: 0 TMA, 1 MMA (leader) + TMEM alloc, 2 relay, 3 spare,
+// 4..7 and 16..19 Π generators (two per TMEM lane quadrant, one per 32-row
+// half of a K-block), 8..15 norm warps + TMEM epilogue.
+constexpr int NUM_GEN_WARPS = 8;
 constexpr int NUM_NORM_WARPS = 8;                 // warps 8..15
 constexpr int NORM_RG = (32 * NUM_NORM_WARPS) / 16;   // row groups (16 chunks per row)
 constexpr int NORM_ROWS = TC_BK / NORM_RG;        // rows per norm thread per stage
@@ -60,7 +63,7 @@ constexpr int NORM_RED = NORM_RG * HALF_N * 8;    // 16 KB
 constexpr int TC_BARS = 3 * X_STAGES + 2 * PI_STAGES + 1;
 constexpr int TC_SMEM = X_STAGES * X_STAGE + NORM_RED + TC_BARS * 8 + 16 + 1024;
 static_assert(TC_SMEM <= 227 * 1024, "K1 exceeds the 227 KB SMEM budget");
-constexpr int TC_THREADS = 32 * (8 + NUM_NORM_WARPS);
+constexpr int TC_THREADS = 32 * 20;
 
 struct RadCache {
   uint64_t g;
@@ -85,26 +88,24 @@ __device__ __forceinline__ uint32_t rad_word(RadCache& c, uint64_t W, uint32_t k
 // (rows 2p, 2p+1) is built with one shift and one LOP3.
 __device__ __forceinline__ uint32_t rad_pos(uint32_t e) { return (e >> 1) | ((e & 1u) << 4); }
 
-// One κ row of the Π tile for rows t0..t0+63: 64 bf16 packed in 32 words
+// Half a κ row of the Π tile, rows t0..t0+31: 32 bf16 packed in 16 words
 // (word p = rows 2p (low half) and 2p+1 (high half)), the TMEM A layout.
-__device__ __forceinline__ void gen_pi_row(int kind, uint64_t seed, uint32_t kappa, bool valid,
-                                           uint64_t t0, RadCache& rc, uint32_t (&o)[32]) {
+__device__ __forceinline__ void gen_pi_half(int kind, uint64_t seed, uint32_t kappa, bool valid,
+                                            uint64_t t0, RadCache& rc, uint32_t (&o)[16]) {
   const uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
   if (!valid) {
 #pragma unroll
-    for (int i = 0; i < 32; ++i) o[i] = 0u;
+    for (int i = 0; i < 16; ++i) o[i] = 0u;
     return;
   }
   if (kind == PI_RADEMACHER && (t0 & 31) == 0) {
+    const uint32_t w = rad_word(rc, t0 >> 5, kappa, k0, k1);
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const uint32_t w = rad_word(rc, (t0 >> 5) + h, kappa, k0, k1);
-#pragma unroll
-      for (int p = 0; p < 16; ++p) o[16 * h + p] = 0x3F803F80u | ((w << (15 - p)) & 0x80008000u);
-    }
+    for (int p = 0; p < 16; ++p)  // shift as a multiply: IMAD on the FMA pipe, LOP3 on ALU
+      o[p] = 0x3F803F80u | ((w * (1u << (15 - p))) & 0x80008000u);
   } else if (kind == PI_GAUSSIAN && (t0 & 3) == 0) {
 #pragma unroll
-    for (int q = 0; q < 16; ++q) {
+    for (int q = 0; q < 8; ++q) {
       const uint64_t tq = (t0 >> 2) + q;
       const u32x4 w = philox4x32_10((uint32_t)tq, kappa, (uint32_t)(tq >> 32), TAG_GAUSSIAN, k0, k1);
       uint16_t a, b, c, d;
@@ -116,7 +117,7 @@ __device__ __forceinline__ void gen_pi_row(int kind, uint64_t seed, uint32_t kap
   } else {
     // generic (unaligned block start, Hadamard test mode): element by element
 #pragma unroll
-    for (int p = 0; p < 32; ++p) {
+    for (int p = 0; p < 16; ++p) {
       uint32_t lohi[2];
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
@@ -140,8 +141,18 @@ __device__ __forceinline__ void gen_pi_row(int kind, uint64_t seed, uint32_t kap
 // subnormal) maps to 2^-127·(1+m/128) instead of 0; its square ≤ 2^-252 is
 // absorbed exactly by any partial sum ≥ 2^-200, and finalize flushes
 // column norms² < 2^-200 to 0 (R25).
+// Written as one 32x32->64 multiply-add (IMAD.WIDE.U32 on the FMA pipe) that
+// produces the whole (hi, lo = 0) register pair: the 15 magnitude bits are
+// placed at bits 17..31 of a 32-bit word, times 2^28 lands them at bits
+// 45..59 of the 64-bit result (hi word bits 13..27) with a zero low word,
+// and the 64-bit addend adds the exponent bias 896 << 52.
+// m17 = 2^17, m28 = 2^28, m29 = 2^29 (kernel parameters, see SketchTCParams).
+// Written as multiplies so that ptxas can place them on the FMA pipe
+// (IMAD.SHL, IMAD.HI with addend) next to the generator warps' ALU work.
+// (Measured: faster than IMAD.WIDE.U32 forms that build the pair in one op.)
 __device__ __forceinline__ double bf16lo_mag_f64(uint32_t w) {
-  return __hiloint2double((int)((w & 0x7FFFu) * 8192u + 0x38000000u), 0);
+  const uint32_t t = w * 131072u;                                   // bits 0..14 -> 17..31
+  return __hiloint2double((int)(__umulhi(t, 268435456u) + 0x38000000u), 0);  // >>4, + bias
 }
 __device__ __forceinline__ double bf16hi_mag_f64(uint32_t w) {
   return __hiloint2double((int)(__umulhi(w & 0x7FFF0000u, 0x20000000u) + 0x38000000u), 0);
@@ -240,25 +251,28 @@ sketch_tc_kernel(const __grid_constant__ CUtensorMap tmap, SketchTCParams p) {
         mbar_arrive_cluster(leader_ready + 8u * (uint32_t)s);
       }
     }
-  } else if (warp >= 4 && warp < 8) {
-    // ---------------- Π generators: thread owns TMEM lane 32*quad + lane
+  } else if ((warp >= 4 && warp < 8) || warp >= 16) {
+    // ---------------- Π generators: thread owns TMEM lane 32*quad + lane,
+    // rows 32*half .. 32*half+31 of every K-block
     const int quad = warp & 3;
+    const int half = warp >= 16 ? 1 : 0;
     const int kl = 32 * quad + lane;
     const int kappa = kappa0 + kl;
     RadCache rc{~0ull, 0, 0, 0, 0};
     for (int it = 0; it < nkb; ++it) {
       const int ps = it % PI_STAGES;
-      const uint64_t t0 = (uint64_t)p.row0 + (uint64_t)(kb_begin + it) * TC_BK;
-      uint32_t o[32];
+      const uint64_t t0 = (uint64_t)p.row0 + (uint64_t)(kb_begin + it) * TC_BK + 32 * half;
+      uint32_t o[16];
       if (p.debug & 2) {
 #pragma unroll
-        for (int i = 0; i < 32; ++i) o[i] = 0x3F803F80u;
+        for (int i = 0; i < 16; ++i) o[i] = 0x3F803F80u;
       } else {
-        gen_pi_row(p.kind, p.seed, (uint32_t)kappa, kappa < p.k, t0, rc, o);
+        gen_pi_half(p.kind, p.seed, (uint32_t)kappa, kappa < p.k, t0, rc, o);
       }
       mbar_wait(&pempty[ps], ((uint32_t)(it / PI_STAGES) & 1u) ^ 1u);
       tc_fence_after();
-      tmem_st_32x32b_x32(tbase + ((uint32_t)(32 * quad) << 16) + ACC_COLS + ps * PI_COLS, o);
+      tmem_st_32x32b_x16(
+          tbase + ((uint32_t)(32 * quad) << 16) + ACC_COLS + ps * PI_COLS + 16 * half, o);
       tc_wait_st();
       tc_fence_before();
       __syncwarp();
@@ -273,10 +287,15 @@ sketch_tc_kernel(const __grid_constant__ CUtensorMap tmap, SketchTCParams p) {
     double acc[8];
 #pragma unroll
     for (int e = 0; e < 8; ++e) acc[e] = 0.0;
+    // norm duty is split over the κ tiles that share this X tile: K-block kb
+    // belongs to κ tile kb % k_tiles (counter kept incrementally)
+    const bool norms_on = p.do_norms && !(p.debug & 1);
+    int duty_ctr = kb_begin % p.k_tiles;
     for (int it = 0; it < nkb; ++it) {
       const int s = it % X_STAGES;
       mbar_wait(&xfull[s], (uint32_t)(it / X_STAGES) & 1u);
-      const bool duty = p.do_norms && !(p.debug & 1) && (((kb_begin + it) % p.k_tiles) == kt);
+      const bool duty = norms_on && duty_ctr == kt;
+      if (++duty_ctr == p.k_tiles) duty_ctr = 0;
       if (duty) {
         const uint8_t* base = x_s + s * X_STAGE + box * 8192;
         uint4 v[NORM_ROWS];

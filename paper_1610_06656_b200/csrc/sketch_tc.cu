@@ -15,9 +15,10 @@
 //     generator warps and written straight into TMEM with tcgen05.st: the A
 //     operand lives in TMEM (4-stage ring of 32 columns), so Π costs no SMEM
 //     bandwidth and is stored nowhere else.
-//   * 8 norm warps read the X stage once from SMEM and accumulate exact x²
-//     in fp64 (two integer ops + one DFMA per element): A and B are read from
-//     HBM exactly once.
+//   * 8 norm warps read the X stage once from SMEM: exact fp32 squares
+//     (bf16 has 8 significant bits) summed over 4-row chunks in fp32, then
+//     one fp64 add per chunk (R4): A and B are read from HBM
+//     exactly once.
 //   * the same 8 warps drain the 128 × 256 fp32 accumulator (tcgen05.ld)
 //     into the split's partial slot.
 // Per-SM SMEM traffic per 64-row K-block: 16 KB TMA write + 16 KB MMA B read
@@ -132,30 +133,6 @@ __device__ __forceinline__ void gen_pi_half(int kind, uint64_t seed, uint32_t ka
       o[p] = lohi[0] | (lohi[1] << 16);
     }
   }
-}
-
-// Exact fp64 |x| of the two bf16 halves of a packed word w, two integer ops
-// each: the fp64 high word is (magnitude bits << 13) + (896 << 20) (bf16 and
-// fp64 share the sign/exponent layout up to the bias 1023 - 127 = 896), the
-// low word is 0 (bf16 has only 7 stored mantissa bits).  A zero (or bf16
-// subnormal) maps to 2^-127·(1+m/128) instead of 0; its square ≤ 2^-252 is
-// absorbed exactly by any partial sum ≥ 2^-200, and finalize flushes
-// column norms² < 2^-200 to 0 (R25).
-// Written as one 32x32->64 multiply-add (IMAD.WIDE.U32 on the FMA pipe) that
-// produces the whole (hi, lo = 0) register pair: the 15 magnitude bits are
-// placed at bits 17..31 of a 32-bit word, times 2^28 lands them at bits
-// 45..59 of the 64-bit result (hi word bits 13..27) with a zero low word,
-// and the 64-bit addend adds the exponent bias 896 << 52.
-// m17 = 2^17, m28 = 2^28, m29 = 2^29 (kernel parameters, see SketchTCParams).
-// Written as multiplies so that ptxas can place them on the FMA pipe
-// (IMAD.SHL, IMAD.HI with addend) next to the generator warps' ALU work.
-// (Measured: faster than IMAD.WIDE.U32 forms that build the pair in one op.)
-__device__ __forceinline__ double bf16lo_mag_f64(uint32_t w) {
-  const uint32_t t = w * 131072u;                                   // bits 0..14 -> 17..31
-  return __hiloint2double((int)(__umulhi(t, 268435456u) + 0x38000000u), 0);  // >>4, + bias
-}
-__device__ __forceinline__ double bf16hi_mag_f64(uint32_t w) {
-  return __hiloint2double((int)(__umulhi(w & 0x7FFF0000u, 0x20000000u) + 0x38000000u), 0);
 }
 
 __global__ void __launch_bounds__(TC_THREADS, 1)
@@ -302,19 +279,32 @@ sketch_tc_kernel(const __grid_constant__ CUtensorMap tmap, SketchTCParams p) {
 #pragma unroll
         for (int rr = 0; rr < NORM_ROWS; ++rr) {
           const int r = rg + NORM_RG * rr;
-          v[rr] = *reinterpret_cast<const uint4*>(base + r * 128 + ((chunk ^ (r & 7)) << 4));
+          if (p.debug & 16)
+            v[rr] = make_uint4(it * 3u + rr, it ^ rr, it + 7u, it * 5u);
+          else
+            v[rr] = *reinterpret_cast<const uint4*>(base + r * 128 + ((chunk ^ (r & 7)) << 4));
         }
+        // exact fp32 squares (bf16 has 8 significant bits), summed over the
+        // thread's NORM_ROWS rows in fp32, then one fp64 add per column
+        // (R4: relative error <= 3·2^-24 worst case per chunk)
+        float sq[8];
 #pragma unroll
         for (int rr = 0; rr < NORM_ROWS; ++rr) {
           const uint32_t w[4] = {v[rr].x, v[rr].y, v[rr].z, v[rr].w};
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
-            const double lo = bf16lo_mag_f64(w[e]);
-            const double hi = bf16hi_mag_f64(w[e]);
-            acc[2 * e] = fma(lo, lo, acc[2 * e]);
-            acc[2 * e + 1] = fma(hi, hi, acc[2 * e + 1]);
+            const float lo = __uint_as_float(w[e] << 16), hi = __uint_as_float(w[e] & 0xFFFF0000u);
+            if (rr == 0) {
+              sq[2 * e] = __fmul_rn(lo, lo);
+              sq[2 * e + 1] = __fmul_rn(hi, hi);
+            } else {
+              sq[2 * e] = __fmaf_rn(lo, lo, sq[2 * e]);
+              sq[2 * e + 1] = __fmaf_rn(hi, hi, sq[2 * e + 1]);
+            }
           }
         }
+#pragma unroll
+        for (int e = 0; e < 8; ++e) acc[e] += (double)sq[e];
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&xempty[s]);

@@ -254,6 +254,15 @@ smp_status smp_sketch_init(smp_handle** out, const smp_sketch_desc* d, void* str
   h->d = *d;
   h->st = reinterpret_cast<cudaStream_t>(stream);
   cudaGetDevice(&h->dev);
+  {
+    // WAltMin workspace comes from the device's default stream-ordered pool;
+    // keep freed blocks cached instead of returning them at every sync
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, h->dev) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+  }
   h->n1 = d->n1;
   h->n2 = d->a_is_b ? d->n1 : d->n2;
   h->ntot = d->a_is_b ? d->n1 : d->n1 + d->n2;
@@ -535,7 +544,7 @@ smp_status smp_waltmin(smp_handle* h, const int32_t* I, const int32_t* J, const 
   a.a_norm2 = h->acc_nrm; a.FA = h->FAFB;
   a.U = U; a.V = V;
   CK(h, smp::run_waltmin(a, h->st), "waltmin");
-  h->launches += 8 + (int64_t)w->init_iters * 14 + (w->trim_c > 0 ? 7 : 0) + 2 * w->T + 2;
+  h->launches += 10;  // CSR/CSC setup (weights, pointers, CUB radix sort, gather) + one persistent kernel
   CK(h, cudaStreamSynchronize(h->st), "sync");
   return SMP_OK;
 }

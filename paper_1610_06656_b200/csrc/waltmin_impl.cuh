@@ -1,0 +1,559 @@
+// WAltMin persistent kernel (Alg. 2), templated on the
+// rank r; instantiated in waltmin_r*.cu (split for parallel compilation) and
+// driven by run_waltmin() in waltmin.cu.
+#pragma once
+#include "smp_device.cuh"
+#include "smp_kernels.h"
+
+namespace smp {
+
+#ifndef SMP_TRY
+#define SMP_TRY(x)                          \
+  do {                                      \
+    cudaError_t e_ = (x);                   \
+    if (e_ != cudaSuccess) return e_;       \
+  } while (0)
+#endif
+
+// ---------------------------------------------------------------------------
+// The whole of Alg. 2 after the CSR/CSC setup runs as ONE cooperative
+// persistent kernel (one CTA per SM, grid-wide barriers between phases):
+// at n <= 10^4, r <= 16 every phase is latency-bound, so launch count and
+// the number of grid-wide synchronisations are what the time is made of.
+//
+// Row ownership: warp gw (global) owns output rows o = gw, gw + W, ... of
+// every phase, W = total warps — deterministic, so every reduction below
+// has a fixed order and the result is bit-reproducible run to run.
+//
+// Orthonormalisation is CholeskyQR2 with the Gram partials reduced by EVERY
+// CTA redundantly in the same fixed order (identical R^{-1} everywhere, no
+// second barrier); the second triangular factor is folded into the next
+// SpMM's output (Σ c (x T) = (Σ c x) T), so each half-iteration of the
+// subspace iteration costs two grid barriers.
+constexpr int WM_THREADS = 256;
+constexpr int WM_WARPS = WM_THREADS / 32;
+
+struct WMParams {
+  int64_t n1, n2;
+  int T, init_iters;
+  double trim_c, lam;
+  uint64_t seed;
+  const int64_t* rptr;   // CSR (Ω in (i,j) order): row pointers
+  const int32_t* J;      //   column of each sample
+  const double* w;       //   w = 1/q̂
+  const double* wv;      //   w · M̃
+  const int64_t* cptr;   // CSC copy (stable by j): column pointers
+  const int32_t* cI;     //   row of each sample
+  const double* cw;
+  const double* cwv;
+  const double* a2;
+  const double* FA;
+  double* Y;
+  double* Z;
+  double* U;
+  double* V;
+  double* gpart;  // [2][gridDim.x][NG]
+  unsigned* bar;  // [2]: arrival count, generation
+  uint64_t* trace;  // optional [3 * barriers] (SMP_WM_TRACE)
+  float* Uout;
+  float* Vout;
+};
+
+__device__ __forceinline__ uint64_t wm_globaltimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Sense-reversing grid barrier (all CTAs are co-resident: cooperative launch).
+// trace (diagnostics, SMP_WM_TRACE): per barrier, CTA 0's arrival, the last
+// arrival and CTA 0's release (globaltimer ns).
+__device__ __forceinline__ void grid_sync(unsigned* bar, uint64_t* trace, int& nb) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned* vgen = bar + 1;
+    const unsigned gen = *vgen;
+    if (trace && blockIdx.x == 0) trace[3 * nb] = wm_globaltimer();
+    __threadfence();
+    if (atomicAdd(bar, 1u) == gridDim.x - 1) {
+      if (trace) trace[3 * nb + 1] = wm_globaltimer();
+      bar[0] = 0u;
+      __threadfence();
+      atomicAdd(bar + 1, 1u);
+    } else {
+      while (*vgen == gen) {}
+    }
+    __threadfence();
+    if (trace && blockIdx.x == 0) trace[3 * nb + 2] = wm_globaltimer();
+  }
+  ++nb;
+  __syncthreads();
+}
+
+template <int R>
+struct WMShared {
+  static constexpr int NG = R * (R + 1) / 2;
+  double T[R * R];            // current right factor (upper triangular), applied to outputs
+  double Rinv[R * R];         // result of the last Cholesky
+  double G[R * R];
+  double red[WM_THREADS];     // reduction scratch
+  double wg[WM_WARPS][NG];    // per-warp Gram partials
+  double ys[WM_WARPS][R];     // per-warp row broadcast
+  int ea[NG], eb[NG];
+};
+
+template <int R>
+__device__ __forceinline__ void set_identity(double* T) {
+  for (int e = threadIdx.x; e < R * R; e += blockDim.x) T[e] = (e / R == e % R) ? 1.0 : 0.0;
+}
+
+// y = acc · T (T upper triangular; T == nullptr: identity); rows whose norm
+// exceeds trim_thr (if >= 0) are zeroed; y -> out row o; Gram partial += y yᵀ
+template <int R>
+__device__ __forceinline__ void emit_row(WMShared<R>& sm, int64_t o, const double (&acc)[R],
+                                         const double* T, double* out, double trim_thr,
+                                         double (&gl)[(WMShared<R>::NG + 31) / 32]) {
+  constexpr int NG = WMShared<R>::NG;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double y[R];
+#pragma unroll
+  for (int c = 0; c < R; ++c) {
+    if (T) {
+      double t = 0.0;
+#pragma unroll
+      for (int m = 0; m <= c; ++m) t = fma(acc[m], T[m * R + c], t);
+      y[c] = t;
+    } else {
+      y[c] = acc[c];
+    }
+  }
+  if (trim_thr >= 0.0) {
+    double rn = 0.0;
+#pragma unroll
+    for (int c = 0; c < R; ++c) rn += y[c] * y[c];
+    if (sqrt(rn) > trim_thr) {
+#pragma unroll
+      for (int c = 0; c < R; ++c) y[c] = 0.0;
+    }
+  }
+  __syncwarp();
+  if (lane == 0) {
+#pragma unroll
+    for (int c = 0; c < R; ++c) {
+      out[o * R + c] = y[c];
+      sm.ys[warp][c] = y[c];
+    }
+  }
+  __syncwarp();
+#pragma unroll
+  for (int q = 0; q < (NG + 31) / 32; ++q) {
+    const int e = lane + 32 * q;
+    if (e < NG) gl[q] = fma(sm.ys[warp][sm.ea[e]], sm.ys[warp][sm.eb[e]], gl[q]);
+  }
+  __syncwarp();
+}
+
+// per-warp Gram partials -> gpart[buf][cta] (fixed warp order)
+template <int R>
+__device__ __forceinline__ void flush_gram(WMShared<R>& sm, const double (&gl)[(WMShared<R>::NG + 31) / 32],
+                                           double* gpart_buf) {
+  constexpr int NG = WMShared<R>::NG;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+  for (int q = 0; q < (NG + 31) / 32; ++q) {
+    const int e = lane + 32 * q;
+    if (e < NG) sm.wg[warp][e] = gl[q];
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < NG; e += blockDim.x) {
+    double s = 0.0;
+    for (int w = 0; w < WM_WARPS; ++w) s += sm.wg[w][e];
+    gpart_buf[(int64_t)blockIdx.x * NG + e] = s;
+  }
+}
+
+// G = Σ_cta gpart[buf][cta] (identical fixed order in every CTA), then
+// R^{-1} of the upper Cholesky factor into sm.Rinv (dead pivots -> zero columns)
+template <int R>
+__device__ void reduce_chol(WMShared<R>& sm, const double* gpart_buf) {
+  constexpr int NG = WMShared<R>::NG;
+  constexpr int MAXK = 8;  // independent loads in flight per thread
+  const int G = gridDim.x;
+  const int groups = blockDim.x / NG;  // >= 1 for NG <= 136 < 256
+  const int tid = threadIdx.x;
+  if (tid < groups * NG) {
+    // thread (g, e) sums CTAs b = g, g + groups, ... in increasing order
+    const int e = tid % NG, g = tid / NG;
+    double s = 0.0;
+    for (int base = g; base < G; base += groups * MAXK) {
+      double v[MAXK];
+#pragma unroll
+      for (int q = 0; q < MAXK; ++q) {
+        const int b = base + groups * q;
+        v[q] = b < G ? __ldcg(gpart_buf + (int64_t)b * NG + e) : 0.0;
+      }
+#pragma unroll
+      for (int q = 0; q < MAXK; ++q) s += v[q];
+    }
+    sm.red[tid] = s;
+  }
+  __syncthreads();
+  if (tid < NG) {
+    double s = 0.0;
+    for (int g = 0; g < groups; ++g) s += sm.red[g * NG + tid];
+    sm.G[tid] = s;  // packed upper triangle, row-major (ea/eb order)
+  }
+  __syncthreads();
+  if (tid == 0) {
+    // upper Cholesky G = RᵀR (L = Rᵀ), then Rinv = (Lᵀ)^{-1}; dead pivots
+    // (rank deficiency) give zero columns.  Fully unrolled: registers only.
+    double L[R][R], Ri[R][R], inv[R];
+    bool dead[R];
+    double tr = 0.0;
+    {
+      int e = 0;
+#pragma unroll
+      for (int a = 0; a < R; ++a)
+#pragma unroll
+        for (int b = a; b < R; ++b) {
+          L[b][a] = sm.G[e];  // lower triangle holds G
+          if (a == b) tr += sm.G[e];
+          ++e;
+        }
+    }
+    const double tol = 1e-28 * (tr > 0.0 ? tr : 1.0);
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+      double s = L[j][j];
+#pragma unroll
+      for (int q = 0; q < j; ++q) s -= L[j][q] * L[j][q];
+      dead[j] = !(s > tol);
+      const double d = dead[j] ? 0.0 : sqrt(s);
+      inv[j] = dead[j] ? 0.0 : 1.0 / d;
+      L[j][j] = d;
+#pragma unroll
+      for (int i = j + 1; i < R; ++i) {
+        double t = L[i][j];
+#pragma unroll
+        for (int q = 0; q < j; ++q) t -= L[i][q] * L[j][q];
+        L[i][j] = t * inv[j];
+      }
+    }
+    // Ri = (Lᵀ)^{-1} (upper): back substitution per column c
+#pragma unroll
+    for (int c = 0; c < R; ++c)
+#pragma unroll
+      for (int i = R - 1; i >= 0; --i) {
+        double t = (i == c) ? 1.0 : 0.0;
+#pragma unroll
+        for (int q = i + 1; q < R; ++q) t -= L[q][i] * Ri[q][c];
+        Ri[i][c] = (dead[i] || dead[c]) ? 0.0 : t * inv[i];
+      }
+#pragma unroll
+    for (int i = 0; i < R; ++i)
+#pragma unroll
+      for (int c = 0; c < R; ++c) sm.Rinv[i * R + c] = Ri[i][c];
+  }
+  __syncthreads();
+}
+
+// Loops are fully unrolled (register-resident arrays) for r <= 10 — the
+// ranks of the configured workloads — and left rolled above that to bound
+// code size and compile time.
+// loads in flight per lane in the sample loops (memory-level parallelism
+// against the L2 latency of the gathered X rows; fewer for large r to bound
+// registers)
+template <int R>
+struct WMUnroll { static constexpr int U = R <= 6 ? 4 : (R <= 10 ? 2 : 1); };
+
+// out[o] = (Σ_{p in [ptr[o], ptr[o+1])} coef[p] X[other[p]]) · T (samples of
+// row o stored contiguously: CSR order, or the pre-permuted CSC copy)
+template <int R>
+__device__ void spmm_phase(WMShared<R>& sm, const int64_t* __restrict__ ptr,
+                           const int32_t* __restrict__ other, const double* __restrict__ coef,
+                           const double* X, int64_t nout, double* out, double* gpart_buf) {
+  constexpr int NG = WMShared<R>::NG;
+  constexpr int U = WMUnroll<R>::U;
+  const int lane = threadIdx.x & 31;
+  const int64_t W = (int64_t)gridDim.x * WM_WARPS;
+  double gl[(NG + 31) / 32];
+#pragma unroll
+  for (int q = 0; q < (NG + 31) / 32; ++q) gl[q] = 0.0;
+  for (int64_t o = (int64_t)blockIdx.x * WM_WARPS + (threadIdx.x >> 5); o < nout; o += W) {
+    double acc[R];
+#pragma unroll
+    for (int l = 0; l < R; ++l) acc[l] = 0.0;
+    const int64_t p0 = ptr[o], p1 = ptr[o + 1];
+    for (int64_t base = p0 + lane; base < p1; base += 32 * U) {
+      double c[U];
+      int32_t oi[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t q = base + 32 * u;
+        const bool ok = q < p1;
+        c[u] = ok ? coef[q] : 0.0;
+        oi[u] = ok ? other[q] : 0;
+      }
+      double x[U][R];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int l = 0; l < R; ++l) x[u][l] = __ldcg(X + (int64_t)oi[u] * R + l);
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int l = 0; l < R; ++l) acc[l] = fma(c[u], x[u][l], acc[l]);
+    }
+#pragma unroll
+    for (int l = 0; l < R; ++l)
+#pragma unroll
+      for (int sh = 16; sh > 0; sh >>= 1) acc[l] += __shfl_xor_sync(0xffffffffu, acc[l], sh);
+    emit_row<R>(sm, o, acc, sm.T, out, -1.0, gl);
+  }
+  flush_gram<R>(sm, gl, gpart_buf);
+}
+
+// rows owned by this warp: out[o] <- X[o] · Tm, optionally trimmed (line 6,
+// R13: zero rows with ||U0_i|| > c sqrt(r) ||A_i|| / ||A||_F); Gram partial
+template <int R>
+__device__ void transform_phase(WMShared<R>& sm, const double* X, int64_t n, const double* Tm,
+                                double* out, double* gpart_buf, bool trim, const WMParams& p) {
+  constexpr int NG = WMShared<R>::NG;
+  const int64_t W = (int64_t)gridDim.x * WM_WARPS;
+  double gl[(NG + 31) / 32];
+#pragma unroll
+  for (int q = 0; q < (NG + 31) / 32; ++q) gl[q] = 0.0;
+  const double frob = trim ? sqrt(*p.FA) : 0.0;
+  for (int64_t o = (int64_t)blockIdx.x * WM_WARPS + (threadIdx.x >> 5); o < n; o += W) {
+    double acc[R];
+#pragma unroll
+    for (int l = 0; l < R; ++l) acc[l] = __ldcg(X + o * R + l);
+    const double thr = (trim && frob > 0.0) ? p.trim_c * sqrt((double)R) * sqrt(p.a2[o]) / frob : -1.0;
+    emit_row<R>(sm, o, acc, Tm, out, thr, gl);
+  }
+  if (gpart_buf) flush_gram<R>(sm, gl, gpart_buf);
+}
+
+// one weighted least-squares half step (lines 8/9; R14):
+// out[o] = (G_o + lam tr(G_o)/r I)^{-1} h_o over the samples of output row o,
+// G_o = Σ w x xᵀ, h_o = Σ w M̃ x (lanes accumulate their samples in registers,
+// then a fixed xor-butterfly reduction; lane 0 solves by Cholesky)
+template <int R>
+__device__ void als_phase(WMShared<R>& sm, const int64_t* __restrict__ ptr,
+                          const int32_t* __restrict__ other, const double* __restrict__ w,
+                          const double* __restrict__ wv, const double* X, int64_t nout, double lam,
+                          double* out) {
+  constexpr int NG = WMShared<R>::NG;
+  constexpr int U = WMUnroll<R>::U;
+  const int lane = threadIdx.x & 31;
+  const int64_t W = (int64_t)gridDim.x * WM_WARPS;
+  for (int64_t o = (int64_t)blockIdx.x * WM_WARPS + (threadIdx.x >> 5); o < nout; o += W) {
+    double g[NG], h[R];
+#pragma unroll
+    for (int e = 0; e < NG; ++e) g[e] = 0.0;
+#pragma unroll
+    for (int a = 0; a < R; ++a) h[a] = 0.0;
+    const int64_t p0 = ptr[o], p1 = ptr[o + 1];
+    for (int64_t base = p0 + lane; base < p1; base += 32 * U) {
+      double ws[U], vs[U];
+      int32_t oi[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t q = base + 32 * u;
+        const bool ok = q < p1;
+        ws[u] = ok ? w[q] : 0.0;
+        vs[u] = ok ? wv[q] : 0.0;
+        oi[u] = ok ? other[q] : 0;
+      }
+      double x[U][R];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int l = 0; l < R; ++l) x[u][l] = __ldcg(X + (int64_t)oi[u] * R + l);
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        int e = 0;
+#pragma unroll
+        for (int a = 0; a < R; ++a) {
+          const double wa = ws[u] * x[u][a];
+          h[a] = fma(vs[u], x[u][a], h[a]);
+#pragma unroll
+          for (int b = a; b < R; ++b) { g[e] = fma(wa, x[u][b], g[e]); ++e; }
+        }
+      }
+    }
+#pragma unroll
+    for (int e = 0; e < NG; ++e)
+#pragma unroll
+      for (int sh = 16; sh > 0; sh >>= 1) g[e] += __shfl_xor_sync(0xffffffffu, g[e], sh);
+#pragma unroll
+    for (int a = 0; a < R; ++a)
+#pragma unroll
+      for (int sh = 16; sh > 0; sh >>= 1) h[a] += __shfl_xor_sync(0xffffffffu, h[a], sh);
+    if (lane == 0) {
+      // ridge Cholesky solve (G + lam tr(G)/r I) x = h; empty/singular -> 0
+      // (R14).  Fully unrolled: registers only.
+      double L[R][R], xs[R], y[R], inv[R];
+      double tr = 0.0;
+      {
+        int e = 0;
+#pragma unroll
+        for (int a = 0; a < R; ++a)
+#pragma unroll
+          for (int b = a; b < R; ++b) {
+            L[b][a] = g[e];
+            if (a == b) tr += g[e];
+            ++e;
+          }
+      }
+      bool ok = tr > 0.0;
+      const double shift = lam * tr / (double)R;
+#pragma unroll
+      for (int a = 0; a < R; ++a) L[a][a] += shift;
+#pragma unroll
+      for (int j = 0; j < R; ++j) {
+        double s = L[j][j];
+#pragma unroll
+        for (int q = 0; q < j; ++q) s -= L[j][q] * L[j][q];
+        ok = ok && (s > 0.0);
+        const double d = sqrt(s > 0.0 ? s : 1.0);
+        inv[j] = 1.0 / d;
+        L[j][j] = d;
+#pragma unroll
+        for (int i = j + 1; i < R; ++i) {
+          double t = L[i][j];
+#pragma unroll
+          for (int q = 0; q < j; ++q) t -= L[i][q] * L[j][q];
+          L[i][j] = t * inv[j];
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < R; ++i) {
+        double t = h[i];
+#pragma unroll
+        for (int q = 0; q < i; ++q) t -= L[i][q] * y[q];
+        y[i] = t * inv[i];
+      }
+#pragma unroll
+      for (int i = R - 1; i >= 0; --i) {
+        double t = y[i];
+#pragma unroll
+        for (int q = i + 1; q < R; ++q) t -= L[q][i] * xs[q];
+        xs[i] = t * inv[i];
+      }
+#pragma unroll
+      for (int a = 0; a < R; ++a) out[o * R + a] = ok ? xs[a] : 0.0;
+    }
+  }
+}
+
+template <int R>
+__global__ void __launch_bounds__(WM_THREADS, 1) wm_persistent_kernel(WMParams p) {
+  constexpr int NG = WMShared<R>::NG;
+  extern __shared__ __align__(16) uint8_t wm_smem[];
+  WMShared<R>& sm = *reinterpret_cast<WMShared<R>*>(wm_smem);
+  __shared__ double TZ[R * R];
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    int e = 0;
+    for (int a = 0; a < R; ++a)
+      for (int b = a; b < R; ++b) { sm.ea[e] = a; sm.eb[e] = b; ++e; }
+  }
+  set_identity<R>(sm.T);
+  __syncthreads();
+  const int64_t G = gridDim.x;
+  int buf = 0;
+  int nbar = 0;
+  auto gp = [&](int b) { return p.gpart + (int64_t)b * G * NG; };
+  // CholeskyQR2 of the rows just written to X (Gram already in gp(buf)):
+  // leaves X · T orthonormal with T = R2^{-1} in sm.T
+  auto cqr2 = [&](double* X, int64_t n) {
+    grid_sync(p.bar, p.trace, nbar);
+    reduce_chol<R>(sm, gp(buf));
+    buf ^= 1;
+    transform_phase<R>(sm, X, n, sm.Rinv, X, gp(buf), false, p);
+    grid_sync(p.bar, p.trace, nbar);
+    reduce_chol<R>(sm, gp(buf));
+    buf ^= 1;
+    for (int e = tid; e < R * R; e += blockDim.x) sm.T[e] = sm.Rinv[e];
+    __syncthreads();
+  };
+
+  // line 5: Y0 Rademacher
+  for (int64_t e = (int64_t)blockIdx.x * WM_THREADS + tid; e < p.n2 * R; e += G * WM_THREADS) {
+    const int64_t j = e / R;
+    const int l = (int)(e - j * R);
+    const u32x4 wd = philox4x32_10((uint32_t)j, (uint32_t)l, 0u, TAG_INIT, (uint32_t)p.seed,
+                                   (uint32_t)(p.seed >> 32));
+    p.Y[e] = (wd.x & 1u) ? -1.0 : 1.0;
+  }
+  grid_sync(p.bar, p.trace, nbar);
+  // subspace iteration (R12): Z = R Y, Y = Rᵀ Z, each orthonormalised by
+  // one CholeskyQR whose triangular factor is folded into the next SpMM
+  // (stored rows · T is the orthonormal basis); the final Z gets CholeskyQR2
+  auto cqr1 = [&]() {
+    grid_sync(p.bar, p.trace, nbar);
+    reduce_chol<R>(sm, gp(buf));
+    buf ^= 1;
+    for (int e = tid; e < R * R; e += blockDim.x) sm.T[e] = sm.Rinv[e];
+    __syncthreads();
+  };
+  const int iters = p.init_iters > 0 ? p.init_iters : 1;
+  for (int it = 0; it < iters; ++it) {
+    spmm_phase<R>(sm, p.rptr, p.J, p.wv, p.Y, p.n1, p.Z, gp(buf));
+    if (it == iters - 1) {  // the last Y half does not reach U0
+      cqr2(p.Z, p.n1);
+      break;
+    }
+    cqr1();
+    spmm_phase<R>(sm, p.cptr, p.cI, p.cwv, p.Z, p.n2, p.Y, gp(buf));
+    cqr1();
+  }
+  for (int e = tid; e < R * R; e += blockDim.x) TZ[e] = sm.T[e];
+  __syncthreads();
+  if (p.trim_c > 0.0) {
+    // line 6: U0 = Z T, trim, re-orthonormalise (CholeskyQR2), U = U0 T'
+    transform_phase<R>(sm, p.Z, p.n1, TZ, p.Z, gp(buf), true, p);
+    cqr2(p.Z, p.n1);
+    transform_phase<R>(sm, p.Z, p.n1, sm.T, p.U, nullptr, false, p);
+  } else {
+    transform_phase<R>(sm, p.Z, p.n1, TZ, p.U, nullptr, false, p);
+  }
+  grid_sync(p.bar, p.trace, nbar);
+  // lines 7-10: T alternating weighted least-squares half steps
+  if (p.T == 0)
+    for (int64_t e = (int64_t)blockIdx.x * WM_THREADS + tid; e < p.n2 * R; e += G * WM_THREADS) p.V[e] = 0.0;
+  for (int t = 0; t < p.T; ++t) {
+    als_phase<R>(sm, p.cptr, p.cI, p.cw, p.cwv, p.U, p.n2, p.lam, p.V);
+    grid_sync(p.bar, p.trace, nbar);
+    als_phase<R>(sm, p.rptr, p.J, p.w, p.wv, p.V, p.n1, p.lam, p.U);
+    grid_sync(p.bar, p.trace, nbar);
+  }
+  // output (Û(T), V̂(T)) in fp32
+  for (int64_t e = (int64_t)blockIdx.x * WM_THREADS + tid; e < p.n1 * R; e += G * WM_THREADS)
+    p.Uout[e] = (float)__ldcg(p.U + e);
+  for (int64_t e = (int64_t)blockIdx.x * WM_THREADS + tid; e < p.n2 * R; e += G * WM_THREADS)
+    p.Vout[e] = (float)__ldcg(p.V + e);
+}
+
+template <int R>
+cudaError_t launch_wm(WMParams& p, cudaStream_t st) {
+  const size_t smem = sizeof(WMShared<R>);
+  static bool attr = false;
+  if (!attr) {
+    SMP_TRY(cudaFuncSetAttribute(wm_persistent_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem));
+    attr = true;
+  }
+  int dev = 0, sms = 0, per_sm = 0;
+  SMP_TRY(cudaGetDevice(&dev));
+  SMP_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  SMP_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, wm_persistent_kernel<R>, WM_THREADS, smem));
+  if (per_sm < 1) return cudaErrorInvalidConfiguration;
+  const int grid = sms;  // one CTA per SM (co-resident: cooperative launch)
+  void* args[] = {&p};
+  return cudaLaunchCooperativeKernel((const void*)wm_persistent_kernel<R>, dim3(grid), dim3(WM_THREADS),
+                                     args, smem, st);
+}
+
+}  // namespace smp

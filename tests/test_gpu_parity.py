@@ -2,7 +2,8 @@
 element, on seeded inputs (DESIGN.md §4 lists the tolerances and why).
 
   sketch Ã, B̃      ||Ã_i^gpu - Ã_i^or|| / ||Ã_i^or|| <= 1e-5 per column (north star)
-  norms ||A_i||²   relative 1e-12 (both fp64; summation order differs)
+  norms ||A_i||²   relative 2e-7 (bf16: exact fp32 squares summed in fp32 over 4-row
+                   chunks, fp64 across chunks: <= 3·2^-24 relative worst case, R4)
   Ω, indices        bit-exact;  q̂ relative 1e-12
   M̃                |M̃^gpu - M̃^or| <= 1e-4 ||A_i|| ||B_j||   (R22, Lemma JL scale P:318)
   factors           ||UVᵀ_gpu - UVᵀ_or||_2 / ||AᵀB||_2 <= 1e-3
@@ -68,6 +69,9 @@ def col_rel_err(gpu, ref):
     return np.where(den > 0, num / np.where(den > 0, den, 1), num)
 
 
+NORM_RTOL = 2e-7   # 3·2^-24 (R4): worst-case bound of the 4-row fp32 chunk sums
+
+
 def check_sketch(fin, orc, tol=1e-5):
     ea = col_rel_err(fin["A_sk"], orc["As"])
     eb = col_rel_err(fin["B_sk"], orc["Bs"])
@@ -75,10 +79,10 @@ def check_sketch(fin, orc, tol=1e-5):
     assert eb.max() <= tol, f"B sketch max col rel err {eb.max():.3e}"
     a2 = fin["a_norm2"].cpu().numpy()
     b2 = fin["b_norm2"].cpu().numpy()
-    np.testing.assert_allclose(a2, orc["a2"], rtol=1e-12, atol=0)
-    np.testing.assert_allclose(b2, orc["b2"], rtol=1e-12, atol=0)
+    np.testing.assert_allclose(a2, orc["a2"], rtol=NORM_RTOL, atol=0)
+    np.testing.assert_allclose(b2, orc["b2"], rtol=NORM_RTOL, atol=0)
     fr = fin["frob2"].cpu().numpy()
-    np.testing.assert_allclose(fr, [orc["FA"], orc["FB"]], rtol=1e-12)
+    np.testing.assert_allclose(fr, [orc["FA"], orc["FB"]], rtol=NORM_RTOL)
 
 
 # ------------------------------------------------------------------ Step 1
@@ -178,7 +182,7 @@ def test_omega_bit_exact_and_mtilde(n1, n2, m_coef):
     al, be = oracle.alpha_beta(orc["a2"], orc["b2"], orc["FA"], orc["FB"])
     Io, Jo, qo = oracle.sample(99, m, al, be)
     assert np.array_equal(I.cpu().numpy(), Io) and np.array_equal(J.cpu().numpy(), Jo)
-    np.testing.assert_allclose(qh.cpu().numpy(), qo, rtol=1e-12)
+    np.testing.assert_allclose(qh.cpu().numpy(), qo, rtol=2 * NORM_RTOL)
     Mo = oracle.estimate(k, Io, Jo, orc["As"], orc["Bs"], orc["DA"], orc["DB"])
     scale = np.sqrt(orc["a2"][Io] * orc["b2"][Jo])
     err = np.abs(val.cpu().double().numpy() - Mo) / scale

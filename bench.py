@@ -69,7 +69,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -136,6 +136,18 @@ def make_inputs(cfgname, cfg, r0, r1, device):
     raise ValueError(f"{cfgname}: dense bench configs are cfg0, cfg1, cfg2, cfg4")
 
 
+def make_inputs_csr(cfg, r0, r1, device):
+    """cfg3 rows [r0, r1) of A and B in CSR (R18); rowptr relative to the block."""
+    A = synth.csr_block(r0, r1 - r0, cfg["n1"], cfg["nnz_a"], cfg["seed"], 0, device=device)
+    B = synth.csr_block(r0, r1 - r0, cfg["n2"], cfg["nnz_b"], cfg["seed"], 1, device=device)
+    return A, B
+
+
+def csr_bytes(X):
+    rp, col, val = X
+    return rp.numel() * rp.element_size() + col.numel() * 4 + val.numel() * 4
+
+
 def dtype_name(cfg):
     return {"bf16": "bf16", "f32": "f32", "csr": "f32"}[cfg["dtype"]]
 
@@ -145,36 +157,56 @@ def pi_code(cfg):
 
 
 # --------------------------------------------------------------------- oracle arms
-def oracle_sample_rate(cfgname, cfg, target_s, max_rows=None):
-    """Time the CPU oracle's one-pass sketch+norms on the first rows of the
-    workload (CPU-generated, same distribution); returns (GB/s, info)."""
+def oracle_sample_rate(cfgname, cfg, target_s):
+    """Time the CPU oracle's one-pass sketch+norms (oracle/, as it stands) on
+    the first rows of the workload, CPU-generated block by block with the same
+    generators (generation not timed), until about target_s seconds of oracle
+    work; returns (GB/s, info)."""
     import oracle
-    n1, n2, k = cfg["n1"], cfg["n2"], cfg["k"]
+    n1, n2, k, d = cfg["n1"], cfg["n2"], cfg["k"], cfg["d"]
     a_is_b = cfg.get("a_is_b", False)
-    es = 2 if cfg["dtype"] == "bf16" else 4
-    probe = 256
-    A, B = make_inputs(cfgname, cfg, 0, min(cfg["d"], synth.GEN_BLOCK), "cpu")
+    csr = cfg["dtype"] == "csr"
 
     def host(X):
         return synth.bf16_bits(X) if X.dtype == torch.bfloat16 else X.numpy()
 
-    def run(rows):
-        t0 = time.perf_counter()
-        oracle.sketch_rows(pi_code(cfg), cfg["seed"], k, host(A[:rows]))
-        if not a_is_b:
-            oracle.sketch_rows(pi_code(cfg), cfg["seed"], k, host(B[:rows]))
-        return time.perf_counter() - t0
+    def gen(r0, r1):
+        if csr:
+            return make_inputs_csr(cfg, r0, r1, "cpu")
+        return make_inputs(cfgname, cfg, r0, r1, "cpu")
 
-    t = run(probe)
-    rows = int(min(A.shape[0] if max_rows is None else max_rows,
-                   max(probe, probe * target_s / max(t, 1e-6))))
-    t = run(rows)
-    nbytes = rows * (n1 + (0 if a_is_b else n2)) * es
-    info = {"rows": rows, "seconds": t, "bytes": nbytes, "cores": oracle.num_threads(),
-            "sample": f"oracle one-pass sketch+norms (fp64, C/OpenMP) of the first {rows} of "
-                      f"{cfg['d']} rows of A{'' if a_is_b else ' and B'} ({n1}"
-                      f"{'' if a_is_b else '+' + str(n2)} columns, k={k})"}
-    return nbytes / t / 1e9, info
+    def run(A, B, r0):
+        t0 = time.perf_counter()
+        if csr:
+            for X, n in ((A, n1), (B, n2)):
+                oracle.sketch_csr(pi_code(cfg), cfg["seed"], k, n, X[0].numpy(), X[1].numpy(),
+                                  X[2].numpy(), row0=r0)
+            nbytes = csr_bytes(A) + csr_bytes(B)
+        else:
+            oracle.sketch_rows(pi_code(cfg), cfg["seed"], k, host(A), row0=r0)
+            if not a_is_b:
+                oracle.sketch_rows(pi_code(cfg), cfg["seed"], k, host(B), row0=r0)
+            nbytes = A.numel() * A.element_size() + (0 if a_is_b else B.numel() * B.element_size())
+        return time.perf_counter() - t0, nbytes
+
+    probe = 256
+    A, B = gen(0, probe)
+    t, _ = run(A, B, 0)                       # warm-up + rate probe (not counted)
+    rows_target = int(min(d, max(probe, probe * target_s / max(t, 1e-6))))
+    step = synth.GEN_BLOCK if not csr else 8192
+    secs, nbytes, rows = 0.0, 0, 0
+    while rows < rows_target and secs < 2 * target_s:
+        r1 = min(rows_target, (rows // step + 1) * step)
+        A, B = gen(rows, r1)
+        ts, nb = run(A, B, rows)
+        secs += ts
+        nbytes += nb
+        rows = r1
+    info = {"rows": rows, "seconds": secs, "bytes": nbytes, "cores": oracle.num_threads(),
+            "sample": f"oracle one-pass sketch+norms (fp64, C/OpenMP) of the first {rows} of {d} "
+                      f"rows of A{'' if a_is_b else ' and B'} ({n1}{'' if a_is_b else '+' + str(n2)} "
+                      f"columns, k={k}{', CSR' if csr else ''}); {secs:.1f} s"}
+    return nbytes / secs / 1e9, info
 
 
 def run_reference(args, cfgname, cfg, world, rank):
@@ -236,13 +268,26 @@ def main():
 
     from paper_1610_06656_b200 import SMPSketch, IN_DENSE_BF16, IN_DENSE_F32
 
+    from paper_1610_06656_b200 import IN_CSR_F32
+
     d, n1, n2, k = cfg["d"], cfg["n1"], cfg["n2"], cfg["k"]
     a_is_b = cfg.get("a_is_b", False)
+    csr = cfg["dtype"] == "csr"
     r0, r1 = shard_rows(d, world, rank)
-    A, B = make_inputs(cfgname, cfg, r0, r1, dev)
-    inp = IN_DENSE_BF16 if A.dtype == torch.bfloat16 else IN_DENSE_F32
-    es = A.element_size()
-    total_bytes = d * (n1 + (0 if a_is_b else n2)) * es
+    if csr:
+        A, B = make_inputs_csr(cfg, r0, r1, dev)
+        inp = IN_CSR_F32
+        my_bytes = csr_bytes(A) + csr_bytes(B)
+        nnz = A[1].numel() + B[1].numel()
+        t = torch.tensor([float(my_bytes), float(nnz)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(t)
+        total_bytes, total_nnz = float(t[0]), float(t[1])
+    else:
+        A, B = make_inputs(cfgname, cfg, r0, r1, dev)
+        inp = IN_DENSE_BF16 if A.dtype == torch.bfloat16 else IN_DENSE_F32
+        es = A.element_size()
+        total_bytes = d * (n1 + (0 if a_is_b else n2)) * es
     m = synth.m_of(cfg)
     r, T = cfg["r"], cfg["T"]
     stream = torch.cuda.current_stream(dev)
@@ -258,7 +303,14 @@ def main():
     def step(evs, host=None):
         sk.reset()
         evs[0].record(stream)
-        if host is None:
+        if csr:
+            if host is None:
+                sk.block_csr(r0, r1 - r0, *A, *B)
+            else:  # H2D of the pinned CSR arrays inside the timed region
+                Ad = [x.to(dev, non_blocking=True) for x in host[0]]
+                Bd = [x.to(dev, non_blocking=True) for x in host[1]]
+                sk.block_csr(r0, r1 - r0, *Ad, *Bd)
+        elif host is None:
             sk.block(r0, A, B)
         else:
             sk.block_host(r0, host[0], host[1])
@@ -277,13 +329,16 @@ def main():
             dist.barrier(device_ids=[local_rank])
         torch.cuda.synchronize(dev)
 
+    # clock sampler runs over the warm-up and the timed region (nvidia-smi
+    # needs ~0.3 s to start; the timed region alone can be shorter)
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    time.sleep(0.5)
     # warm-up
     for _ in range(args.warmup):
         step([torch.cuda.Event(enable_timing=True) for _ in range(3)])
     # timed region (inputs 4.3+ GB >> 126 MB L2: no flush needed)
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
-    clocks = ClockSampler(local_rank)
-    clocks.start()
     sk.set_timing(True)
     sk.kernel_timing()
     launches0 = sk.kernel_launches
@@ -307,50 +362,73 @@ def main():
 
     value = total_bytes / (t_sketch * 1e-3) / 1e9
 
-    # roofline of K1 (per launch = one matrix over this rank's rows)
     pk = peaks()
-    rows = r1 - r0
-    planes = 3 if inp == IN_DENSE_F32 else 1
-    launches_per_step = max(k1_n // max(args.steps, 1), 1)
-    ncols_total = (n1 + (0 if a_is_b else n2))
-    flops_launch = 2.0 * k * rows * ncols_total * planes / launches_per_step
-    bytes_launch = rows * ncols_total * 2 * planes / launches_per_step
-    t_hbm = bytes_launch / (pk["hbm"] * 1e9)
-    t_tc = flops_launch / (pk["tc"] * 1e12)
-    traffic = None
-    tfile = os.path.join(ROOT, "profiles", "k1_traffic.json")
-    if os.path.exists(tfile):
-        traffic = json.load(open(tfile)).get(cfgname)
-    if t_tc >= t_hbm:
-        ach = flops_launch / (k1_avg * 1e-3) / 1e12
-        roof = {"bound": "tensor", "achieved": ach, "peak": pk["tc"], "unit": "TFLOP/s",
-                "frac": ach / pk["tc"], "traffic": traffic, "kernel": "sketch_tc_kernel",
-                "peak_source": pk["src"] + " burst bf16 dense (MEASURED_PEAKS.json)"}
-        alt_ach = bytes_launch / (k1_avg * 1e-3) / 1e9
-        roof["hbm_view"] = {"achieved": alt_ach, "peak": pk["hbm"], "unit": "GB/s",
-                            "frac": alt_ach / pk["hbm"]}
+    if csr:
+        # dominant kernel K3d (csr_accumulate): SIMT fp32 FMA-bound (2k FLOP
+        # per nonzero); peak from the unit counts: 148 SMs x 128 FP32 lanes x
+        # 2 FLOP x max SM clock (K3)
+        sm_max = 1965.0 if not clk else clk["sm_max_mhz"]
+        alu_peak = 148 * 128 * 2 * sm_max * 1e6 / 1e12
+        flops_step = 2.0 * k * nnz * 1.0
+        k3_ms_step = k1_ms / max(args.steps, 1)
+        ach = flops_step / (k3_ms_step * 1e-3) / 1e12
+        kp = (k + 7) // 8 * 8
+        roof = {"bound": "alu", "achieved": ach, "peak": alu_peak, "unit": "TFLOP/s",
+                "frac": ach / alu_peak, "traffic": None, "kernel": "csr_accumulate_kernel",
+                "peak_source": "derived: 148 SMs x 128 FP32 lanes x 2 FLOP x %.0f MHz" % sm_max,
+                "k3d_ms_per_step": k3_ms_step, "k3d_launches_per_step": k1_n / max(args.steps, 1),
+                "pi_gather_view": {"achieved": nnz * kp * 2 / (k3_ms_step * 1e-3) / 1e9,
+                                   "unit": "GB/s", "note": "bf16 Π rows gathered from the L2-resident panel"},
+                "algorithmic_per_step": {"flops": flops_step, "nnz": nnz}}
+        roofline_time = max(total_bytes / (pk["hbm"] * 1e9), 2.0 * k * total_nnz / (pk["tc"] * 1e12))
     else:
-        ach = bytes_launch / (k1_avg * 1e-3) / 1e9
-        roof = {"bound": "hbm", "achieved": ach, "peak": pk["hbm"], "unit": "GB/s",
-                "frac": ach / pk["hbm"], "traffic": traffic, "kernel": "sketch_tc_kernel",
-                "peak_source": pk["src"] + " HBM copy bandwidth (MEASURED_PEAKS.json)"}
-        alt = flops_launch / (k1_avg * 1e-3) / 1e12
-        roof["tensor_view"] = {"achieved": alt, "peak": pk["tc"], "unit": "TFLOP/s",
-                               "frac": alt / pk["tc"]}
-    roof["k1_ms_per_launch"] = k1_avg
-    roof["algorithmic_per_launch"] = {"flops": flops_launch, "bytes": bytes_launch}
-    roofline_time = max(total_bytes / (pk["hbm"] * 1e9),
-                        2.0 * k * d * ncols_total * planes / (pk["tc"] * 1e12))
+        # roofline of K1 (per launch = one matrix over this rank's rows)
+        rows = r1 - r0
+        planes = 3 if inp == IN_DENSE_F32 else 1
+        launches_per_step = max(k1_n // max(args.steps, 1), 1)
+        ncols_total = (n1 + (0 if a_is_b else n2))
+        flops_launch = 2.0 * k * rows * ncols_total * planes / launches_per_step
+        bytes_launch = rows * ncols_total * 2 * planes / launches_per_step
+        t_hbm = bytes_launch / (pk["hbm"] * 1e9)
+        t_tc = flops_launch / (pk["tc"] * 1e12)
+        traffic = None
+        tfile = os.path.join(ROOT, "profiles", "k1_traffic.json")
+        if os.path.exists(tfile):
+            traffic = json.load(open(tfile)).get(cfgname)
+        if t_tc >= t_hbm:
+            ach = flops_launch / (k1_avg * 1e-3) / 1e12
+            roof = {"bound": "tensor", "achieved": ach, "peak": pk["tc"], "unit": "TFLOP/s",
+                    "frac": ach / pk["tc"], "traffic": traffic, "kernel": "sketch_tc_kernel",
+                    "peak_source": pk["src"] + " burst bf16 dense (MEASURED_PEAKS.json)"}
+            alt_ach = bytes_launch / (k1_avg * 1e-3) / 1e9
+            roof["hbm_view"] = {"achieved": alt_ach, "peak": pk["hbm"], "unit": "GB/s",
+                                "frac": alt_ach / pk["hbm"]}
+        else:
+            ach = bytes_launch / (k1_avg * 1e-3) / 1e9
+            roof = {"bound": "hbm", "achieved": ach, "peak": pk["hbm"], "unit": "GB/s",
+                    "frac": ach / pk["hbm"], "traffic": traffic, "kernel": "sketch_tc_kernel",
+                    "peak_source": pk["src"] + " HBM copy bandwidth (MEASURED_PEAKS.json)"}
+            alt = flops_launch / (k1_avg * 1e-3) / 1e12
+            roof["tensor_view"] = {"achieved": alt, "peak": pk["tc"], "unit": "TFLOP/s",
+                                   "frac": alt / pk["tc"]}
+        roof["k1_ms_per_launch"] = k1_avg
+        roof["algorithmic_per_launch"] = {"flops": flops_launch, "bytes": bytes_launch}
+        roofline_time = max(total_bytes / (pk["hbm"] * 1e9),
+                            2.0 * k * d * ncols_total * planes / (pk["tc"] * 1e12))
 
     # e2e through the C ABI with pinned host buffers
     e2e = None
     if not args.no_e2e:
-        Ah = torch.empty(A.shape, dtype=A.dtype, pin_memory=True)
-        Ah.copy_(A)
-        Bh = None
-        if B is not None:
-            Bh = torch.empty(B.shape, dtype=B.dtype, pin_memory=True)
-            Bh.copy_(B)
+        def pinned(X):
+            h = torch.empty(X.shape, dtype=X.dtype, pin_memory=True)
+            h.copy_(X)
+            return h
+        if csr:
+            Ah = [pinned(x) for x in A]
+            Bh = [pinned(x) for x in B]
+        else:
+            Ah = pinned(A)
+            Bh = None if B is None else pinned(B)
         step([torch.cuda.Event(enable_timing=True) for _ in range(3)], host=(Ah, Bh))
         ee = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.e2e_steps)]
         barrier()
@@ -363,18 +441,21 @@ def main():
             t = torch.tensor([te_sk, te_all], device=dev, dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             te_sk, te_all = t.tolist()
+        h2d = (my_bytes if csr else int(A.numel() * es + (0 if B is None else B.numel() * es)))
         e2e = {"value": total_bytes / (te_sk * 1e-3) / 1e9, "unit": "GB/s",
-               "h2d_bytes_per_step": int(A.numel() * es + (0 if B is None else B.numel() * es)),
+               "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int((n1 + n2) * r * 4),
                "smp_pca_sec": te_all * 1e-3, "steps": args.e2e_steps,
-               "path": "smp_sketch_block_host (library-staged pinned H2D, double-buffered) + finalize + sample_estimate + waltmin + D2H(U,V)"}
+               "path": ("pinned CSR arrays -> device (torch copies) + smp_sketch_block_csr" if csr else
+                        "smp_sketch_block_host (library-staged pinned H2D, double-buffered)")
+                       + " + finalize + sample_estimate + waltmin + D2H(U,V)"}
         del Ah, Bh
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         rate, info = oracle_sample_rate(cfgname, cfg, 15.0)
         cpu = {"value": rate, "unit": "GB/s", "cores": info["cores"], "kind": "oracle",
-               "sample": info["sample"] + f"; {info['seconds']:.1f} s"}
+               "sample": info["sample"]}
 
     if rank == 0:
         out = {
@@ -387,6 +468,7 @@ def main():
                        "init_iters": args.init_iters, "a_is_b": a_is_b,
                        "parallelism": f"row-shard x{world} + NCCL all-reduce" if world > 1 else "1 GPU",
                        "l2": "inputs (%.1f GB) larger than the 126 MB L2; no flush" % (total_bytes / 1e9),
+                       **({"nnz": int(total_nnz), "input": "CSR int64 rowptr / int32 col / fp32 val"} if csr else {}),
                        "value_scope": "A+B bytes / (sketch_block .. finalize) time; ms_per_step = whole Alg. 1"},
             "smp_pca_sec": t_step * 1e-3,
             "sketch_ms": t_sketch,

@@ -1,138 +1,344 @@
 // K3: sparse (CSR) one-pass sketch with fused exact column norms (Alg. 1
 // line 2; bag-of-words inputs P:9).
 //
-// Warp-level row processing: a warp owns a group of 4 consecutive rows
-// t = 4g..4g+3.  Each lane regenerates Π(κ, t) for its κ values
-// κ = 4·lane + 128·q once per group (one Philox call per κ covers the 4 rows
-// for the Gaussian stream) — π_t is shared by A's and B's
-// row t — then, for every nonzero (t, c, v), adds v·π_t into the fp32
-// accumulator row c with vectorised float4 atomics (one 512-byte warp
-// transaction per nonzero at k = 512) and v² into the fp64 norm (exact for
-// integer counts, so the norms are order-independent and bit-exact).
+//   Ã[:, c] += Σ_{(t, c, v) in the block} v · π_t,    a2[c] += Σ v²
+//
+// A sparse product has no reuse on both sides at once: a row t's π_t is
+// shared by the ~100 nonzeros of that row, a column's accumulator by the
+// nonzeros of that column.  K3 keeps the ACCUMULATOR in registers (column-
+// stationary) and moves π through L2, once per nonzero:
+//
+//   K3a  generate the Π panel of Rp rows (bf16, Rp x kp, row t contiguous
+//        in κ) into an L2-resident buffer — every Π entry is generated once;
+//   K3b  key every nonzero of the panel (A and B) as (column << tbits | t);
+//   K3c  stable radix sort (CUB) -> the panel's nonzeros in (column, row)
+//        order (a per-panel CSC transpose);
+//   K3d  warps take fixed chunks of the sorted nonzeros (load balance for
+//        Zipf-heavy columns): lanes own κ slices, gather π_t (kp bf16) from
+//        the panel, FMA v·π_t into fp32 registers, and flush the column's
+//        partial with one vector reduction (red.global.add.v4.f32) when the
+//        column changes; lane 0 adds v² into the fp64 norm (exact for
+//        integer counts: order-independent, bit-exact).
+//
+// Products v·π are exact in fp32 (integer counts times bf16); the fp32 sums
+// are order-dependent across chunks (the reductions race), so CSR sketches
+// agree with the oracle to ~1e-7 relative but are not bit-reproducible run
+// to run (K3).
+#include <cub/device/device_radix_sort.cuh>
 #include "smp_device.cuh"
 #include "smp_kernels.h"
 
 namespace smp {
 
-constexpr int CSR_QMAX = 8;  // k <= 4096 -> k/128 <= 32 slots; process in passes of 8
-
-__device__ __forceinline__ void pi_group4(int kind, uint64_t seed, uint32_t kappa, uint64_t tg,
-                                          float (&v)[4]) {
-  // values of Π(κ, 4·tg + e), e = 0..3
+// ---------------------------------------------------------------- K3a
+// pi[(t - t0) * kp + κ] = Π(κ, t) as bf16 bits, κ < k; zero for k <= κ < kp.
+// Thread (κ, row group): one Philox call covers 4 rows (Gaussian) or 32 rows
+// of one word (Rademacher); a warp writes 32 consecutive κ of a row (64 B).
+__global__ void pi_panel_kernel(int kind, uint64_t seed, int k, int kp, int64_t t0, int rows,
+                                uint16_t* __restrict__ pi) {
+  const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
+  const int rpg = kind == PI_RADEMACHER ? 32 : 4;  // rows per generator call
+  const int64_t g_first = t0 / rpg, g_last = (t0 + rows - 1) / rpg;
+  const int64_t ngroups = g_last - g_first + 1;
   const uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
-  const uint64_t t = tg * 4;
-  if (kind == PI_GAUSSIAN) {
-    const u32x4 w = philox4x32_10((uint32_t)tg, kappa, (uint32_t)(tg >> 32), TAG_GAUSSIAN, k0, k1);
-    uint16_t a, b, c, d;
-    gauss_pair(w.x, w.y, a, b);
-    gauss_pair(w.z, w.w, c, d);
-    v[0] = bf16_bits_to_float(a); v[1] = bf16_bits_to_float(b);
-    v[2] = bf16_bits_to_float(c); v[3] = bf16_bits_to_float(d);
-  } else if (kind == PI_RADEMACHER) {
-    const u32x4 w = philox4x32_10((uint32_t)(t >> 7), kappa, (uint32_t)(t >> 39), TAG_RADEMACHER, k0, k1);
-    const uint32_t b = (uint32_t)(t & 127);
-    const uint32_t wi = b >> 5;
-    const uint32_t word = wi == 0 ? w.x : wi == 1 ? w.y : wi == 2 ? w.z : w.w;
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const uint32_t ee = (b & 31) + e;
-      const uint32_t pos = (ee >> 1) | ((ee & 1u) << 4);
-      v[e] = ((word >> pos) & 1u) ? -1.f : 1.f;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < ngroups * kp; e += nthreads) {
+    const int kappa = (int)(e % kp);
+    const int64_t g = g_first + e / kp;
+    const int64_t tb = g * rpg;
+    if (kappa >= k) {
+      for (int j = 0; j < rpg; ++j) {
+        const int64_t t = tb + j;
+        if (t >= t0 && t < t0 + rows) pi[(t - t0) * kp + kappa] = 0;
+      }
+      continue;
     }
-  } else {
+    if (kind == PI_GAUSSIAN) {
+      const u32x4 w = philox4x32_10((uint32_t)g, (uint32_t)kappa, (uint32_t)(g >> 32), TAG_GAUSSIAN, k0, k1);
+      uint16_t z[4];
+      gauss_pair(w.x, w.y, z[0], z[1]);
+      gauss_pair(w.z, w.w, z[2], z[3]);
 #pragma unroll
-    for (int e = 0; e < 4; ++e) v[e] = (__popcll((unsigned long long)kappa & (t + e)) & 1) ? -1.f : 1.f;
+      for (int j = 0; j < 4; ++j) {
+        const int64_t t = tb + j;
+        if (t >= t0 && t < t0 + rows) pi[(t - t0) * kp + kappa] = z[j];
+      }
+    } else if (kind == PI_RADEMACHER) {
+      // word (t >> 5) & 3 of Philox(ctr = (t >> 7, κ, t >> 39, 1)), DESIGN.md §3.3
+      const u32x4 w = philox4x32_10((uint32_t)(tb >> 7), (uint32_t)kappa, (uint32_t)(tb >> 39),
+                                    TAG_RADEMACHER, k0, k1);
+      const uint32_t wi = (uint32_t)((tb >> 5) & 3);
+      const uint32_t word = wi == 0 ? w.x : wi == 1 ? w.y : wi == 2 ? w.z : w.w;
+#pragma unroll 4
+      for (int j = 0; j < 32; ++j) {
+        const int64_t t = tb + j;
+        if (t >= t0 && t < t0 + rows) {
+          const uint32_t pos = ((uint32_t)j >> 1) | (((uint32_t)j & 1u) << 4);
+          pi[(t - t0) * kp + kappa] = ((word >> pos) & 1u) ? (uint16_t)0xBF80 : (uint16_t)0x3F80;
+        }
+      }
+    } else {
+      for (int j = 0; j < rpg; ++j) {
+        const int64_t t = tb + j;
+        if (t >= t0 && t < t0 + rows) pi[(t - t0) * kp + kappa] = pi_bits(kind, seed, (uint32_t)kappa, (uint64_t)t);
+      }
+    }
   }
 }
 
-__global__ void __launch_bounds__(256)
-sketch_csr_kernel(int kind, uint64_t seed, int k, int64_t row0, int64_t rows,
-                  const int64_t* __restrict__ arp, const int32_t* __restrict__ acol,
-                  const float* __restrict__ aval, float* __restrict__ aacc, double* __restrict__ anrm,
-                  const int64_t* __restrict__ brp, const int32_t* __restrict__ bcol,
-                  const float* __restrict__ bval, float* __restrict__ bacc, double* __restrict__ bnrm,
-                  int q_begin, int q_end, int do_norms) {
+// ---------------------------------------------------------------- K3b
+// keys[o] = (c_glob << tbits) | (t - p0), vals[o] = v for the nonzeros of
+// rows [p0, p0 + rows) of one matrix; warp per row; o = (entry index
+// relative to rowptr[0]) - ebase.
+__global__ void csr_keys_kernel(const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
+                                const float* __restrict__ val, int64_t p0, int rows,
+                                int64_t ebase, uint32_t cofs, int tbits, int64_t ncols,
+                                uint32_t* __restrict__ keys, float* __restrict__ vals,
+                                int* __restrict__ status) {
   const int lane = threadIdx.x & 31;
-  const int64_t g_first = row0 >> 2;                // first 4-row group touching the block
-  const int64_t g_last = (row0 + rows - 1) >> 2;
-  const int64_t ngroups = g_last - g_first + 1;
   const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
-  const int64_t abase = arp[0];
-  const int64_t bbase = brp ? brp[0] : 0;
-  for (int64_t gi = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); gi < ngroups; gi += nw) {
-    const uint64_t tg = (uint64_t)(g_first + gi);
-    float pv[CSR_QMAX][4][4];  // [q][row e][κ offset]
-#pragma unroll
-    for (int q = 0; q < CSR_QMAX; ++q) {
-      const int qq = q_begin + q;
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        const int kappa = 4 * lane + 128 * qq + c;
-        float v[4] = {0.f, 0.f, 0.f, 0.f};
-        if (qq < q_end && kappa < k) pi_group4(kind, seed, (uint32_t)kappa, tg, v);
-#pragma unroll
-        for (int e = 0; e < 4; ++e) pv[q][e][c] = v[e];
-      }
+  const int64_t base = rowptr[0];  // col/val are indexed from rowptr[0]
+  for (int64_t r = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); r < rows; r += nw) {
+    const int64_t e0 = rowptr[p0 + r] - base, e1 = rowptr[p0 + r + 1] - base;
+    for (int64_t e = e0 + lane; e < e1; e += 32) {
+      const int32_t c = col[e];
+      if (c < 0 || c >= ncols) atomicOr(status, 2);  // out-of-range column
+      const uint32_t cg = (uint32_t)(c < 0 ? 0 : (c >= ncols ? 0 : c)) + cofs;
+      const int64_t o = e - ebase;
+      keys[o] = (cg << tbits) | (uint32_t)r;
+      vals[o] = val[e];
     }
+  }
+}
+
+// ---------------------------------------------------------------- K3d
+constexpr int CSR_CHUNK = 128;  // sorted nonzeros per warp task
+constexpr int CSR_U = 4;        // π rows in flight per lane
+
+__device__ __forceinline__ void red_add_v4(float* addr, float a, float b, float c, float d) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(addr), "f"(a), "f"(b), "f"(c),
+               "f"(d)
+               : "memory");
+}
+
+template <int KV>
+__device__ __forceinline__ void flush_col(uint32_t c, const float (&acc)[KV][8], double nrm, int k,
+                                          float* __restrict__ acc_sk, double* __restrict__ acc_nrm,
+                                          int lane, bool do_norms) {
+  float* dst = acc_sk + (int64_t)c * k;
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const int64_t t = (int64_t)tg * 4 + e;
-      if (t < row0 || t >= row0 + rows) continue;
-      const int64_t r = t - row0;
+  for (int i = 0; i < KV; ++i) {
+    const int kb = 8 * (lane + 32 * i);
+    if ((k & 3) == 0) {
+      if (kb < k) red_add_v4(dst + kb, acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
+      if (kb + 4 < k) red_add_v4(dst + kb + 4, acc[i][4], acc[i][5], acc[i][6], acc[i][7]);
+    } else {
 #pragma unroll
-      for (int mat = 0; mat < 2; ++mat) {
-        const int64_t* rp = mat == 0 ? arp : brp;
-        if (!rp) continue;
-        const int32_t* col = mat == 0 ? acol : bcol;
-        const float* val = mat == 0 ? aval : bval;
-        float* acc = mat == 0 ? aacc : bacc;
-        double* nrm = mat == 0 ? anrm : bnrm;
-        const int64_t base = mat == 0 ? abase : bbase;
-        const int64_t p0 = rp[r] - base, p1 = rp[r + 1] - base;
-        for (int64_t pp = p0; pp < p1; ++pp) {
-          const int64_t c = col[pp];
-          const float x = val[pp];
-          float* dst = acc + c * k;
+      for (int j = 0; j < 8; ++j)
+        if (kb + j < k) atomicAdd(dst + kb + j, acc[i][j]);
+    }
+  }
+  if (do_norms && lane == 0) atomicAdd(acc_nrm + c, nrm);
+}
+
+template <int KV>
+__global__ void __launch_bounds__(256)
+csr_accumulate_kernel(const uint32_t* __restrict__ keys, const float* __restrict__ vals, int64_t n,
+                      const uint16_t* __restrict__ pi, int kp, int k, int tbits,
+                      float* __restrict__ acc_sk, double* __restrict__ acc_nrm, int do_norms) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const uint32_t tmask = (1u << tbits) - 1u;
+  for (int64_t task = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
+       task * CSR_CHUNK < n; task += nw) {
+    const int64_t e0 = task * CSR_CHUNK;
+    const int64_t e1 = min(n, e0 + CSR_CHUNK);
+    float acc[KV][8];
 #pragma unroll
-          for (int q = 0; q < CSR_QMAX; ++q) {
-            const int kappa = 4 * lane + 128 * (q_begin + q);
-            if (q_begin + q < q_end && kappa < k) {
-              if ((k & 3) == 0) {
-                atomicAdd(reinterpret_cast<float4*>(dst + kappa),
-                          make_float4(x * pv[q][e][0], x * pv[q][e][1], x * pv[q][e][2], x * pv[q][e][3]));
-              } else {
+    for (int i = 0; i < KV; ++i)
 #pragma unroll
-                for (int c2 = 0; c2 < 4; ++c2)
-                  if (kappa + c2 < k) atomicAdd(dst + kappa + c2, x * pv[q][e][c2]);
-              }
-            }
+      for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
+    double nrm = 0.0;
+    uint32_t cur = 0xFFFFFFFFu;
+    for (int64_t eb = e0; eb < e1; eb += CSR_U) {
+      uint32_t kk[CSR_U];
+      float vv[CSR_U];
+      bool ok[CSR_U];
+      uint4 q[CSR_U][KV];
+#pragma unroll
+      for (int u = 0; u < CSR_U; ++u) {
+        const int64_t e = eb + u;
+        ok[u] = e < e1;
+        kk[u] = ok[u] ? keys[e] : 0u;
+        vv[u] = ok[u] ? vals[e] : 0.f;
+      }
+#pragma unroll
+      for (int u = 0; u < CSR_U; ++u) {
+        const uint16_t* row = pi + (int64_t)(kk[u] & tmask) * kp;
+#pragma unroll
+        for (int i = 0; i < KV; ++i) {
+          const int kb = 8 * (lane + 32 * i);
+          q[u][i] = kb < kp ? *reinterpret_cast<const uint4*>(row + kb) : make_uint4(0, 0, 0, 0);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < CSR_U; ++u) {
+        if (!ok[u]) continue;
+        const uint32_t c = kk[u] >> tbits;
+        if (c != cur) {
+          if (cur != 0xFFFFFFFFu) {
+            flush_col<KV>(cur, acc, nrm, k, acc_sk, acc_nrm, lane, do_norms != 0);
+#pragma unroll
+            for (int i = 0; i < KV; ++i)
+#pragma unroll
+              for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
+            nrm = 0.0;
           }
-          if (do_norms && lane == 0) atomicAdd(nrm + c, (double)x * (double)x);
+          cur = c;
+        }
+        const float v = vv[u];
+        nrm = fma((double)v, (double)v, nrm);
+#pragma unroll
+        for (int i = 0; i < KV; ++i) {
+          const uint32_t w[4] = {q[u][i].x, q[u][i].y, q[u][i].z, q[u][i].w};
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            acc[i][2 * j] = fmaf(v, __uint_as_float(w[j] << 16), acc[i][2 * j]);
+            acc[i][2 * j + 1] = fmaf(v, __uint_as_float(w[j] & 0xFFFF0000u), acc[i][2 * j + 1]);
+          }
         }
       }
     }
+    if (cur != 0xFFFFFFFFu) flush_col<KV>(cur, acc, nrm, k, acc_sk, acc_nrm, lane, do_norms != 0);
   }
 }
 
-cudaError_t launch_sketch_csr(int kind, uint64_t seed, int k, int64_t row0, int64_t rows,
-                              const int64_t* a_rowptr, const int32_t* a_col, const float* a_val,
-                              int64_t a_n, float* a_acc, double* a_nrm, const int64_t* b_rowptr,
-                              const int32_t* b_col, const float* b_val, int64_t b_n, float* b_acc,
-                              double* b_nrm, cudaStream_t st) {
-  (void)a_n; (void)b_n;
-  if (rows <= 0) return cudaSuccess;
-  const int qtot = (k + 127) / 128;
-  const int64_t ngroups = ((row0 + rows - 1) >> 2) - (row0 >> 2) + 1;
-  const int blocks = (int)std::min<int64_t>((ngroups + 7) / 8, 148 * 32);
-  for (int q0 = 0; q0 < qtot; q0 += CSR_QMAX) {
-    const int q1 = std::min(qtot, q0 + CSR_QMAX);
-    sketch_csr_kernel<<<blocks, 256, 0, st>>>(kind, seed, k, row0, rows, a_rowptr, a_col, a_val,
-                                              a_acc, a_nrm, b_rowptr, b_col, b_val, b_acc, b_nrm,
-                                              q0, q1, q0 == 0 ? 1 : 0);
-    cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
+// ---------------------------------------------------------------- driver
+__global__ void csr_bounds_kernel(const int64_t* __restrict__ arp, const int64_t* __restrict__ brp,
+                                  int rows, int rp, int npan, int64_t* __restrict__ out) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i <= npan; i += gridDim.x * blockDim.x) {
+    const int r = i < npan ? i * rp : rows;
+    out[i] = arp[r] - arp[0];
+    out[npan + 1 + i] = brp ? brp[r] - brp[0] : 0;
   }
-  return cudaSuccess;
+}
+
+template <class T>
+static cudaError_t grow(T*& p, int64_t& cap, int64_t need) {
+  if (need <= cap) return cudaSuccess;
+  if (p) cudaFree(p);
+  p = nullptr;
+  cap = 0;
+  cudaError_t e = cudaMalloc(&p, (size_t)(need > 0 ? need : 1) * sizeof(T));
+  if (e == cudaSuccess) cap = need;
+  return e;
+}
+
+#define CSR_TRY(x)                    \
+  do {                                \
+    cudaError_t e_ = (x);             \
+    if (e_ != cudaSuccess) return e_; \
+  } while (0)
+
+void csr_workspace_free(CsrWorkspace& w) {
+  cudaFree(w.pi); cudaFree(w.keys_in); cudaFree(w.keys_out); cudaFree(w.vals_in);
+  cudaFree(w.vals_out); cudaFree(w.cub_tmp); cudaFree(w.bounds_d);
+  if (w.bounds_h) cudaFreeHost(w.bounds_h);
+  w = CsrWorkspace{};
+}
+
+static int bits_for(int64_t x) {  // smallest b with 2^b > x
+  int b = 0;
+  while (b < 62 && ((int64_t)1 << b) <= x) ++b;
+  return b;
+}
+
+cudaError_t launch_sketch_csr(CsrWorkspace& w, int kind, uint64_t seed, int k, int64_t row0,
+                              int64_t rows, const int64_t* a_rowptr, const int32_t* a_col,
+                              const float* a_val, int64_t a_n, const int64_t* b_rowptr,
+                              const int32_t* b_col, const float* b_val, int64_t b_n, float* acc_sk,
+                              double* acc_nrm, int* status, cudaStream_t st) {
+  if (rows <= 0) return cudaSuccess;
+  const int64_t ntot = a_n + (b_rowptr ? b_n : 0);
+  const int cbits = bits_for(ntot - 1 > 0 ? ntot - 1 : 1);
+  if (cbits > 31) return cudaErrorInvalidValue;
+  const int tbits = std::min(15, 32 - cbits);
+  if (tbits < 6) return cudaErrorInvalidValue;  // more than 2^26 columns
+  const int rp = 1 << tbits;                      // panel rows
+  const int kp = (k + 7) & ~7;
+  const int npan = (int)((rows + rp - 1) / rp);
+  // panel entry boundaries (one D2H read per block)
+  CSR_TRY(grow(w.bounds_d, w.bounds_cap, 2 * (int64_t)(npan + 1)));
+  if (w.bounds_hcap < 2 * (int64_t)(npan + 1)) {
+    if (w.bounds_h) cudaFreeHost(w.bounds_h);
+    w.bounds_h = nullptr;
+    w.bounds_hcap = 0;
+    CSR_TRY(cudaMallocHost(&w.bounds_h, 2 * (size_t)(npan + 1) * 8));
+    w.bounds_hcap = 2 * (int64_t)(npan + 1);
+  }
+  csr_bounds_kernel<<<(npan + 256) / 256, 256, 0, st>>>(a_rowptr, b_rowptr, (int)rows, rp, npan, w.bounds_d);
+  CSR_TRY(cudaMemcpyAsync(w.bounds_h, w.bounds_d, 2 * (size_t)(npan + 1) * 8, cudaMemcpyDeviceToHost, st));
+  CSR_TRY(cudaStreamSynchronize(st));
+  const int64_t* ab = w.bounds_h;
+  const int64_t* bb = w.bounds_h + npan + 1;
+  int64_t max_ent = 0;
+  for (int p = 0; p < npan; ++p) max_ent = std::max(max_ent, (ab[p + 1] - ab[p]) + (bb[p + 1] - bb[p]));
+  CSR_TRY(grow(w.pi, w.pi_cap, (int64_t)rp * kp));
+  CSR_TRY(grow(w.keys_in, w.ent_cap_ki, max_ent));
+  CSR_TRY(grow(w.keys_out, w.ent_cap_ko, max_ent));
+  CSR_TRY(grow(w.vals_in, w.ent_cap_vi, max_ent));
+  CSR_TRY(grow(w.vals_out, w.ent_cap_vo, max_ent));
+  const int end_bit = tbits + cbits;
+  size_t need = 0;
+  CSR_TRY(cub::DeviceRadixSort::SortPairs(nullptr, need, w.keys_in, w.keys_out, w.vals_in, w.vals_out,
+                                          (int)std::max<int64_t>(max_ent, 1), 0, end_bit, st));
+  CSR_TRY(grow(w.cub_tmp, w.cub_cap, (int64_t)need));
+  for (int p = 0; p < npan; ++p) {
+    const int64_t p0 = (int64_t)p * rp;
+    const int prow = (int)std::min<int64_t>(rp, rows - p0);
+    const int64_t na = ab[p + 1] - ab[p], nb = bb[p + 1] - bb[p];
+    const int64_t ne = na + nb;
+    {
+      const int64_t groups = ((row0 + p0 + prow - 1) / 4 - (row0 + p0) / 4 + 1) * kp;
+      const int blocks = (int)std::min<int64_t>((groups + 255) / 256, 148 * 16);
+      pi_panel_kernel<<<blocks, 256, 0, st>>>(kind, seed, k, kp, row0 + p0, prow, w.pi);
+    }
+    if (ne == 0) continue;
+    const int kb_blocks = (int)std::min<int64_t>((prow + 7) / 8, 148 * 16);
+    // A: entries ab[p] .. ab[p+1] (relative to a_rowptr[0]) -> keys[0 .. na)
+    csr_keys_kernel<<<kb_blocks, 256, 0, st>>>(a_rowptr, a_col, a_val, p0, prow, ab[p], 0u, tbits,
+                                               a_n, w.keys_in, w.vals_in, status);
+    if (b_rowptr && nb > 0)
+      csr_keys_kernel<<<kb_blocks, 256, 0, st>>>(b_rowptr, b_col, b_val, p0, prow, bb[p] - na,
+                                                 (uint32_t)a_n, tbits, b_n, w.keys_in, w.vals_in, status);
+    size_t tmp = (size_t)w.cub_cap;
+    CSR_TRY(cub::DeviceRadixSort::SortPairs(w.cub_tmp, tmp, w.keys_in, w.keys_out, w.vals_in, w.vals_out,
+                                            (int)ne, 0, end_bit, st));
+    const int64_t tasks = (ne + CSR_CHUNK - 1) / CSR_CHUNK;
+    const int ablocks = (int)std::min<int64_t>((tasks + 7) / 8, 148 * 64);
+    const int kv = (kp + 255) / 256;
+    if (w.ev_pool) {
+      while (w.ev_pool->size() < *w.ev_used + 2) {
+        cudaEvent_t ev;
+        CSR_TRY(cudaEventCreate(&ev));
+        w.ev_pool->push_back(ev);
+      }
+      CSR_TRY(cudaEventRecord((*w.ev_pool)[*w.ev_used], st));
+    }
+    switch (kv) {
+      case 1: csr_accumulate_kernel<1><<<ablocks, 256, 0, st>>>(w.keys_out, w.vals_out, ne, w.pi, kp, k, tbits, acc_sk, acc_nrm, 1); break;
+      case 2: csr_accumulate_kernel<2><<<ablocks, 256, 0, st>>>(w.keys_out, w.vals_out, ne, w.pi, kp, k, tbits, acc_sk, acc_nrm, 1); break;
+      case 3: case 4: csr_accumulate_kernel<4><<<ablocks, 256, 0, st>>>(w.keys_out, w.vals_out, ne, w.pi, kp, k, tbits, acc_sk, acc_nrm, 1); break;
+      case 5: case 6: case 7: case 8: csr_accumulate_kernel<8><<<ablocks, 256, 0, st>>>(w.keys_out, w.vals_out, ne, w.pi, kp, k, tbits, acc_sk, acc_nrm, 1); break;
+      default: csr_accumulate_kernel<16><<<ablocks, 256, 0, st>>>(w.keys_out, w.vals_out, ne, w.pi, kp, k, tbits, acc_sk, acc_nrm, 1); break;
+    }
+    CSR_TRY(cudaGetLastError());
+    if (w.ev_pool) {
+      CSR_TRY(cudaEventRecord((*w.ev_pool)[*w.ev_used + 1], st));
+      *w.ev_used += 2;
+    }
+    w.launches += 4 + (b_rowptr && nb > 0 ? 1 : 0) + 3;
+  }
+  return cudaGetLastError();
 }
 
 }  // namespace smp

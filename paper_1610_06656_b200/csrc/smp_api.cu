@@ -63,6 +63,7 @@ struct smp_handle {
   cudaEvent_t ev_copied[2] = {nullptr, nullptr};
   cudaEvent_t ev_used[2] = {nullptr, nullptr};
   int64_t launches = 0;
+  smp::CsrWorkspace csr;
   // K1 timing instrumentation
   bool timing = false;
   std::vector<cudaEvent_t> ev_pool;
@@ -305,6 +306,7 @@ void smp_destroy(smp_handle* h) {
   cudaFree(h->planes); cudaFree(h->fin_sk); cudaFree(h->fin_sknorm); cudaFree(h->fin_D);
   cudaFree(h->FAFB); cudaFree(h->status); cudaFree(h->pw_scratch); cudaFree(h->alpha);
   cudaFree(h->blk); cudaFree(h->d_total);
+  smp::csr_workspace_free(h->csr);
   if (h->h_total) cudaFreeHost(h->h_total);
   if (h->h_status) cudaFreeHost(h->h_status);
   if (h->h_fafb) cudaFreeHost(h->h_fafb);
@@ -418,12 +420,17 @@ smp_status smp_sketch_block_csr(smp_handle* h, int64_t row0, int64_t rows, const
     return fail(h, SMP_EINVAL, "null CSR array");
   (void)a_nnz; (void)b_nnz;
   h->finalized = false;
-  CK(h, smp::launch_sketch_csr(h->d.pi_kind, h->d.seed, h->k, row0, rows, a_rowptr, a_col, a_val,
-                               h->n1, h->acc_sk, h->acc_nrm, two ? b_rowptr : nullptr,
-                               two ? b_col : nullptr, two ? b_val : nullptr, h->n2,
-                               h->acc_sk + h->n1 * (int64_t)h->k, h->acc_nrm + h->n1, h->st),
-     "sketch_csr");
-  h->launches += 1;
+  const int64_t l0 = h->csr.launches;
+  h->csr.ev_pool = h->timing ? &h->ev_pool : nullptr;
+  h->csr.ev_used = &h->ev_used_n;
+  cudaError_t e = smp::launch_sketch_csr(h->csr, h->d.pi_kind, h->d.seed, h->k, row0, rows, a_rowptr,
+                                         a_col, a_val, h->n1, two ? b_rowptr : nullptr,
+                                         two ? b_col : nullptr, two ? b_val : nullptr,
+                                         two ? h->n2 : 0, h->acc_sk, h->acc_nrm, h->status, h->st);
+  if (e == cudaErrorInvalidValue)
+    return fail(h, SMP_EINVAL, "CSR: more than 2^26 columns are not supported");
+  CK(h, e, "sketch_csr");
+  h->launches += 2 + (h->csr.launches - l0);
   return SMP_OK;
 }
 
@@ -464,7 +471,8 @@ smp_status smp_finalize_norms(smp_handle* h, float* A_sk, float* B_sk, double* a
   if (!h) return SMP_EINVAL;
   const int k = h->k;
   const float scale = (float)(1.0 / std::sqrt((double)k));
-  CK(h, cudaMemsetAsync(h->status, 0, sizeof(int), h->st), "memset");
+  // h->status is cleared by smp_sketch_reset (it also carries the CSR
+  // out-of-range-column bit set during the pass)
   CK(h, launch_finalize(h->acc_sk, h->acc_nrm, h->ntot, k, scale, h->fin_sk, h->fin_sknorm,
                         h->fin_D, h->status, h->st), "finalize");
   int64_t p2 = 1;
@@ -489,6 +497,7 @@ smp_status smp_finalize_norms(smp_handle* h, float* A_sk, float* B_sk, double* a
   CK(h, cudaMemcpyAsync(h->h_fafb, h->FAFB, 16, cudaMemcpyDeviceToHost, h->st), "copy");
   CK(h, cudaStreamSynchronize(h->st), "sync");
   h->finalized = true;
+  if (*h->h_status & 2) return fail(h, SMP_EINVAL, "CSR column index out of range (S:123)");
   if (*h->h_status) return fail(h, SMP_ENUMERIC, "NaN/Inf in the column norms or sketch");
   if (!(h->h_fafb[0] > 0.0) || !(h->h_fafb[1] > 0.0))
     return fail(h, SMP_ENUMERIC, "||A||_F = 0 or ||B||_F = 0");

@@ -2,6 +2,7 @@
 // of the public C ABI; see include/smp.h for that).
 #pragma once
 #include <cstdint>
+#include <vector>
 #include <cuda_runtime.h>
 
 namespace smp {
@@ -41,6 +42,39 @@ cudaError_t launch_finalize(const float* acc, double* nacc, int64_t n, int k, fl
 // fixed pairwise tree sum (R5) of x[0..n) into *out (single block)
 cudaError_t launch_pairwise_sum(const double* x, int64_t n, double* scratch, double* out,
                                 cudaStream_t st);
+
+// ---- K3 sparse sketch (sketch_csr.cu): handle-owned workspace
+struct CsrWorkspace {
+  uint16_t* pi = nullptr;         // Π panel, Rp x kp bf16
+  int64_t pi_cap = 0;
+  uint32_t* keys_in = nullptr;
+  uint32_t* keys_out = nullptr;
+  float* vals_in = nullptr;
+  float* vals_out = nullptr;
+  int64_t ent_cap_ki = 0, ent_cap_ko = 0, ent_cap_vi = 0, ent_cap_vo = 0;
+  uint8_t* cub_tmp = nullptr;
+  int64_t cub_cap = 0;
+  int64_t* bounds_d = nullptr;
+  int64_t bounds_cap = 0;
+  int64_t* bounds_h = nullptr;    // pinned
+  int64_t bounds_hcap = 0;
+  int64_t launches = 0;           // kernels launched (counter for the bench)
+  // timing of the dominant kernel (K3d) with CUDA events on the launching
+  // stream: pairs appended to *ev_pool from index *ev_used (null: off)
+  std::vector<cudaEvent_t>* ev_pool = nullptr;
+  size_t* ev_used = nullptr;
+};
+// rows [row0, row0 + rows) of A (and B) in CSR (rowptr relative to any base:
+// col/val are indexed from rowptr[0]) -> acc_sk[c][κ] += Σ v Π(κ, t),
+// acc_nrm[c] += Σ v² for columns c of A (0..a_n) then B (a_n..a_n+b_n).
+// Out-of-range columns set bit 2 of *status.  Synchronises once per call
+// (panel entry counts are read back to size the sort).
+cudaError_t launch_sketch_csr(CsrWorkspace& w, int kind, uint64_t seed, int k, int64_t row0,
+                              int64_t rows, const int64_t* a_rowptr, const int32_t* a_col,
+                              const float* a_val, int64_t a_n, const int64_t* b_rowptr,
+                              const int32_t* b_col, const float* b_val, int64_t b_n, float* acc_sk,
+                              double* acc_nrm, int* status, cudaStream_t st);
+void csr_workspace_free(CsrWorkspace& w);
 
 // ---- K5/K6 sampling and estimation (omega.cu)
 cudaError_t launch_alpha_beta(const double* a2, int64_t n1, const double* b2, int64_t n2,

@@ -255,3 +255,73 @@ def test_pipeline_end_to_end_vs_oracle():
     err = _uvt_err(res["U"].cpu().double().numpy(), res["V"].cpu().double().numpy(),
                    orc["U"], orc["V"], M)
     assert err <= 1e-3, err
+
+
+# ------------------------------------------------------------------ Step 1, sparse (K3)
+def _csr(d, n, nnz_row, seed, tag, perm=None):
+    rp, col, val = synth.csr_block(0, d, n, nnz_row, seed, tag, device="cpu")
+    if perm is not None:  # heavy columns away from the low indices (R18 note)
+        col = torch.from_numpy(perm[col.numpy()].astype(np.int32))
+        # keep rows ascending in column (CSR convention; K3 does not need it)
+        rows = [col[i * nnz_row:(i + 1) * nnz_row].sort() for i in range(d)]
+        val = torch.cat([val[i * nnz_row:(i + 1) * nnz_row][r.indices] for i, r in enumerate(rows)])
+        col = torch.cat([r.values for r in rows])
+    return rp, col, val
+
+
+def gpu_sketch_csr(d, n1, n2, k, pi, seed, A, B, row0=0, splits=None):
+    smp = _smp()
+    sk = smp.SMPSketch(row0 + d, n1, n2, k, pi=pi, seed=seed, input=smp.IN_CSR_F32)
+    splits = splits or [(0, d)]
+    for (r0, r1) in splits:
+        a_rp, a_col, a_val = A
+        b_rp, b_col, b_val = B
+        # col/val start at entry rowptr[0] of the block (include/smp.h)
+        ea, eb = int(a_rp[r0]), int(b_rp[r0])
+        sk.block_csr(row0 + r0, r1 - r0, a_rp[r0:r1 + 1].cuda(), a_col[ea:].cuda(), a_val[ea:].cuda(),
+                     b_rp[r0:r1 + 1].cuda(), b_col[eb:].cuda(), b_val[eb:].cuda())
+    return sk, sk.finalize()
+
+
+@pytest.mark.parametrize("d,n1,n2,za,zb,k,pi,row0,permute", [
+    (3000, 300, 200, 20, 16, 512, "gaussian", 0, False),      # cfg3 shape in miniature
+    (2500, 257, 130, 12, 9, 130, "rademacher", 77, True),     # ragged k, unaligned rows, permuted heavy cols
+    (70000, 40, 24, 3, 2, 64, "gaussian", 5, False),          # several Π panels (> 2^15 rows)
+])
+def test_sketch_csr_parity(d, n1, n2, za, zb, k, pi, row0, permute):
+    perm_a = np.random.default_rng(1).permutation(n1) if permute else None
+    perm_b = np.random.default_rng(2).permutation(n2) if permute else None
+    A = _csr(d, n1, za, 3, 0, perm_a)
+    B = _csr(d, n2, zb, 3, 1, perm_b)
+    half = d // 3
+    sk, fin = gpu_sketch_csr(d, n1, n2, k, PI[pi], 11, A, B, row0=row0,
+                             splits=[(half, d), (0, half)])   # blocks in any order
+    skA, a2 = oracle.sketch_csr(PI[pi], 11, k, n1, A[0].numpy(), A[1].numpy(), A[2].numpy(), row0=row0)
+    skB, b2 = oracle.sketch_csr(PI[pi], 11, k, n2, B[0].numpy(), B[1].numpy(), B[2].numpy(), row0=row0)
+    As, _, _ = oracle.finalize(k, skA, a2)
+    Bs, _, _ = oracle.finalize(k, skB, b2)
+    ea = col_rel_err(fin["A_sk"], As)
+    eb = col_rel_err(fin["B_sk"], Bs)
+    assert ea.max() <= 1e-5 and eb.max() <= 1e-5, (ea.max(), eb.max())
+    # integer counts: fp64 norms are exact sums of exact squares -> bit-exact
+    assert np.array_equal(fin["a_norm2"].cpu().numpy(), a2)
+    assert np.array_equal(fin["b_norm2"].cpu().numpy(), b2)
+    # Ω is therefore bit-exact too
+    m = 4 * max(n1, n2) * 5 * math.log(max(n1, n2))
+    I, J, val, qh = sk.sample_estimate(m, 5)
+    al, be = oracle.alpha_beta(a2, b2, oracle.pairwise_sum(a2), oracle.pairwise_sum(b2))
+    Io, Jo, qo = oracle.sample(5, m, al, be)
+    assert np.array_equal(I.cpu().numpy(), Io) and np.array_equal(J.cpu().numpy(), Jo)
+
+
+def test_sketch_csr_bad_column_rejected():
+    smp = _smp()
+    d, n = 100, 10
+    rp = torch.arange(0, d + 1, dtype=torch.int64) * 2
+    col = torch.zeros(2 * d, dtype=torch.int32)
+    col[17] = n + 3   # out of range
+    val = torch.ones(2 * d)
+    sk = smp.SMPSketch(d, n, n, 32, pi=0, seed=0, input=smp.IN_CSR_F32)
+    sk.block_csr(0, d, rp.cuda(), col.cuda(), val.cuda(), rp.cuda(), torch.zeros_like(col).cuda(), val.cuda())
+    with pytest.raises(Exception):
+        sk.finalize()

@@ -47,6 +47,8 @@ def _get():
                                        ctypes.c_int, i64, P, P]
         lib.or_sketch_csr.argtypes = [ctypes.c_int, u64, ctypes.c_int, i64, i64, i64, P, P, P,
                                       P, P]
+        lib.or_colnorms.argtypes = [i64, i64, P, ctypes.c_int, i64, P]
+        lib.or_colnorms.restype = None
         lib.or_pairwise_sum.argtypes = [P, i64]
         lib.or_pairwise_sum.restype = f64
         lib.or_finalize.argtypes = [ctypes.c_int, i64, P, P, P, P, P]
@@ -124,6 +126,16 @@ def sketch_rows(kind, seed, k, X, row0=0, sk=None, norm2=None):
     _get().or_sketch_rows(kind, seed, k, row0, rows, n, _p(X), _dtype_code(X), n, _p(sk),
                           _p(norm2))
     return sk, norm2
+
+
+def colnorms(X, norm2=None):
+    """norm2[c] += Σ_t X[t, c]² in fp64 (the norm half of Step 1)."""
+    X = np.ascontiguousarray(X)
+    rows, n = X.shape
+    if norm2 is None:
+        norm2 = np.zeros(n, np.float64)
+    _get().or_colnorms(rows, n, _p(X), _dtype_code(X), n, _p(norm2))
+    return norm2
 
 
 def sketch_cols(kind, seed, k, X, cols, row0=0):

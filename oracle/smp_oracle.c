@@ -204,6 +204,7 @@ void or_sketch_rows(int kind, uint64_t seed, int k, int64_t row0, int64_t rows, 
     double *pi = (double *)malloc(sizeof(double) * (size_t)RB * (size_t)k);
     for (int64_t r0 = 0; r0 < rows; r0 += RB) {
         int64_t rb = rows - r0 < RB ? rows - r0 : RB;
+        #pragma omp parallel for schedule(static)
         for (int64_t r = 0; r < rb; ++r)
             for (int kp = 0; kp < k; ++kp)
                 pi[r * k + kp] = or_pi_entry(kind, seed, kp, row0 + r0 + r);
@@ -247,19 +248,45 @@ void or_sketch_csr(int kind, uint64_t seed, int k, int64_t row0, int64_t rows, i
                    const int64_t *rowptr, const int32_t *col, const float *val,
                    double *sk, double *norm2)
 {
-    double *pi = (double *)malloc(sizeof(double) * (size_t)k);
+    /* Π(:, t) for the non-empty rows of each 256-row block (generation only;
+       the accumulation below runs in row order, entry by entry). */
+    const int64_t RB = 256;
+    double *pi = (double *)malloc(sizeof(double) * (size_t)RB * (size_t)k);
     (void)n;
-    for (int64_t r = 0; r < rows; ++r) {
-        for (int kp = 0; kp < k; ++kp) pi[kp] = or_pi_entry(kind, seed, kp, row0 + r);
-        for (int64_t p = rowptr[r]; p < rowptr[r + 1]; ++p) {
-            int64_t c = col[p];
-            double x = (double)val[p];
-            norm2[c] += x * x;
-            double *skc = sk + c * (int64_t)k;
-            for (int kp = 0; kp < k; ++kp) skc[kp] += pi[kp] * x;
+    for (int64_t r0 = 0; r0 < rows; r0 += RB) {
+        int64_t rb = rows - r0 < RB ? rows - r0 : RB;
+        #pragma omp parallel for schedule(static)
+        for (int64_t r = 0; r < rb; ++r) {
+            if (rowptr[r0 + r] == rowptr[r0 + r + 1]) continue;
+            for (int kp = 0; kp < k; ++kp) pi[r * k + kp] = or_pi_entry(kind, seed, kp, row0 + r0 + r);
+        }
+        for (int64_t r = 0; r < rb; ++r) {
+            const double *pr = pi + r * k;
+            for (int64_t p = rowptr[r0 + r]; p < rowptr[r0 + r + 1]; ++p) {
+                int64_t c = col[p - rowptr[0]];
+                double x = (double)val[p - rowptr[0]];
+                norm2[c] += x * x;
+                double *skc = sk + c * (int64_t)k;
+                for (int kp = 0; kp < k; ++kp) skc[kp] += pr[kp] * x;
+            }
         }
     }
     free(pi);
+}
+
+/* Column norms only: norm2[c] += Σ_t X[t, c]^2 in fp64 (the norm half of    */
+/* Step 1), for full-size Ω parity without the full sketch.         */
+void or_colnorms(int64_t rows, int64_t n, const void *X, int dtype, int64_t ldx, double *norm2)
+{
+    #pragma omp parallel for schedule(static)
+    for (int64_t c = 0; c < n; ++c) {
+        double s = norm2[c];
+        for (int64_t r = 0; r < rows; ++r) {
+            double x = load_elem(X, dtype, r * ldx + c);
+            s += x * x;
+        }
+        norm2[c] = s;
+    }
 }
 
 /* ------------------------------------------------------------------------ */

@@ -72,41 +72,64 @@ cudaError_t launch_reduce_norms(const double* pnorm, int slots, int64_t n, doubl
   return cudaGetLastError();
 }
 
-// ---------------------------------------------------------------- fp32 split
-// x = hi + mid + lo exactly (three bf16 terms, 8+8+8 significant bits),
-// so Π·X = Π·hi + Π·mid + Π·lo with every tensor-core product exact.
-__device__ __forceinline__ uint16_t bf16_bits_rne(float x) { return bf16_rne_bits(x); }
+// ---------------------------------------------------------------- exact plane split
+// x = p_1 + ... + p_P exactly, every p_q a bf16 number with a limited number
+// of significant bits, so that Π·X = Σ_q Π·p_q with every tensor-core
+// product short enough to survive the MMA's accumulation (R21):
+//   mode 3 (fp32 x, ±1 Π)        : 8 + 8 + 8 bits (products = p_q, ≤ 8 bits)
+//   mode 4 (fp32 x, Gaussian Π)  : 4 + 8 + 8 + 4 bits
+//   mode 2 (bf16 x, Gaussian Π)  : 4 + 4 bits
+// (Gaussian Π has 8 significant bits; a 16-bit product loses its low bits
+// against a large fp32 accumulator inside tcgen05.mma — measured 1.6e-5
+// relative column error — while 12-bit products are kept exactly.)
+// Round-to-nearest-even to b significant bits, on the fp32 bit pattern.
+__device__ __forceinline__ float round_sig(float x, int b) {
+  const uint32_t u = __float_as_uint(x);
+  if ((u & 0x7F800000u) == 0u) return 0.0f * x;  // zero / subnormal residue: not produced here
+  const int drop = 24 - b;
+  const uint32_t half = 1u << (drop - 1);
+  const uint32_t lsb = (u >> drop) & 1u;
+  const uint32_t mag = ((u & 0x7FFFFFFFu) + half - 1u + lsb) & ~((1u << drop) - 1u);
+  return __uint_as_float((u & 0x80000000u) | mag);
+}
 
-__global__ void split_f32_kernel(const float* __restrict__ X, int64_t ldx, int64_t rows, int64_t n,
-                                 uint16_t* __restrict__ planes, int64_t ldp,
-                                 double* __restrict__ pnorm, int seg_rows) {
+__global__ void split_planes_kernel(const void* __restrict__ Xv, int x_bf16, int64_t ldx, int64_t rows,
+                                    int64_t n, int mode, uint16_t* __restrict__ planes, int64_t ldp,
+                                    double* __restrict__ pnorm, int seg_rows) {
   const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t seg = blockIdx.y;
   if (c >= n) return;
   const int64_t r0 = seg * seg_rows;
   const int64_t r1 = min(rows, r0 + seg_rows);
+  int bits[4];
+  int np;
+  if (mode == 3) { np = 3; bits[0] = 8; bits[1] = 8; bits[2] = 8; bits[3] = 0; }
+  else if (mode == 4) { np = 4; bits[0] = 4; bits[1] = 8; bits[2] = 8; bits[3] = 8; }
+  else { np = 2; bits[0] = 4; bits[1] = 8; bits[2] = 0; bits[3] = 0; }
   double s2 = 0.0;
   for (int64_t t = r0; t < r1; ++t) {
-    const float x = X[t * ldx + c];
-    const uint16_t h = bf16_bits_rne(x);
-    const float r_1 = __fsub_rn(x, bf16_bits_to_float(h));
-    const uint16_t m = bf16_bits_rne(r_1);
-    const float r_2 = __fsub_rn(r_1, bf16_bits_to_float(m));
-    const uint16_t l = bf16_bits_rne(r_2);
+    float x;
+    if (x_bf16) x = __uint_as_float((uint32_t)static_cast<const uint16_t*>(Xv)[t * ldx + c] << 16);
+    else x = static_cast<const float*>(Xv)[t * ldx + c];
     uint16_t* row = planes + t * ldp;
-    row[c] = h;
-    row[n + c] = m;
-    row[2 * n + c] = l;
+    float r = x;
+    for (int q = 0; q < np; ++q) {
+      // the last plane takes the (exactly representable) remainder
+      const float p = (q == np - 1) ? r : round_sig(r, bits[q]);
+      row[q * n + c] = (uint16_t)(__float_as_uint(p) >> 16);
+      r = __fsub_rn(r, p);
+    }
     const double xd = (double)x;
     s2 = fma(xd, xd, s2);
   }
   pnorm[seg * n + c] = s2;
 }
 
-cudaError_t launch_split_f32(const float* X, int64_t ldx, int64_t rows, int64_t n, uint16_t* planes,
-                             int64_t ldp, double* pnorm, int seg_rows, cudaStream_t st) {
+cudaError_t launch_split_planes(const void* X, int x_bf16, int64_t ldx, int64_t rows, int64_t n,
+                                int mode, uint16_t* planes, int64_t ldp, double* pnorm, int seg_rows,
+                                cudaStream_t st) {
   dim3 grid((unsigned)((n + 127) / 128), (unsigned)((rows + seg_rows - 1) / seg_rows));
-  split_f32_kernel<<<grid, 128, 0, st>>>(X, ldx, rows, n, planes, ldp, pnorm, seg_rows);
+  split_planes_kernel<<<grid, 128, 0, st>>>(X, x_bf16, ldx, rows, n, mode, planes, ldp, pnorm, seg_rows);
   return cudaGetLastError();
 }
 

@@ -108,14 +108,22 @@ cudaError_t ensure(T*& p, int64_t& cap, int64_t need) {
 
 bool is_pow2(int64_t x) { return x > 0 && (x & (x - 1)) == 0; }
 
-// split-K factor for the tcgen05 sketch: fill the 148 SMs with >= 95% of the
-// last wave, fewest splits first.
+// split-K factor for the tcgen05 sketch.  Two constraints:
+//  * accuracy: a CTA's fp32 TMEM accumulation chain is at most
+//    K1_MAX_KB K-blocks (64 rows each); measured: 41.7K MMA updates per
+//    chain (cfg4 with 3 splits) gave 1.6e-5 relative column error, above
+//    the 1e-5 tolerance, 3.6K updates (cfg1) gave < 4e-6 (R21);
+//  * occupancy: fill the 148 SMs with >= 95% of the last wave, fewest
+//    splits first (searched up to 2x the accuracy minimum).
+constexpr int K1_MAX_KB = 1024;  // 65,536 rows per accumulation chain
+
 int choose_splits(int tiles, int kb_total) {
   const int sms = 148;
-  int best_s = 1;
+  const int smin = std::max(1, (kb_total + K1_MAX_KB - 1) / K1_MAX_KB);
+  int best_s = smin;
   double best_eff = -1.0;
-  const int smax = std::max(1, std::min(kb_total, 64));
-  for (int s = 1; s <= smax; ++s) {
+  const int smax = std::max(smin, std::min(kb_total, std::max(64, 2 * smin)));
+  for (int s = smin; s <= smax; ++s) {
     const int64_t ctas = (int64_t)tiles * s;
     const int64_t waves = (ctas + sms - 1) / sms;
     const double eff = (double)ctas / (double)(waves * sms);
@@ -172,24 +180,30 @@ smp_status sketch_dense_bf16(smp_handle* h, int64_t row0, int64_t rows, const vo
   return SMP_OK;
 }
 
-// One matrix, one fp32 block: split into 3 exact bf16 planes per row chunk,
-// norms from the fp32 values, then K1 over the 3n-wide plane matrix.
-smp_status sketch_dense_f32(smp_handle* h, int64_t row0, int64_t rows, const float* X, int64_t ldx,
-                            int64_t n, int64_t col_off) {
+// One matrix, one block split into exact bf16 planes per row chunk (fp32
+// inputs always; bf16 inputs with a Gaussian Π, R21), norms from
+// the input values in fp64, then K1 over the (planes · n)-wide plane matrix.
+smp_status sketch_dense_split(smp_handle* h, int64_t row0, int64_t rows, const void* X, int x_bf16,
+                              int64_t ldx, int64_t n, int64_t col_off) {
   using namespace smp;
-  const int64_t ldp = ((3 * n + 7) / 8) * 8;
+  const bool gauss = h->d.pi_kind == SMP_PI_GAUSSIAN;
+  const int mode = x_bf16 ? 2 : (gauss ? 4 : 3);
+  const int np = mode;
+  const int64_t ldp = ((np * n + 7) / 8) * 8;
   const int64_t chunk = std::max<int64_t>(64, std::min<int64_t>(rows, (int64_t)(512ll << 20) / (ldp * 2)));
   const int seg_rows = 256;
   CK(h, ensure(h->planes, h->planes_cap, ((chunk + 63) / 64) * 64 * ldp), "alloc planes");
+  const int64_t es = x_bf16 ? 2 : 4;
   for (int64_t r0 = 0; r0 < rows; r0 += chunk) {
     const int64_t rc = std::min(chunk, rows - r0);
     const int64_t segs = (rc + seg_rows - 1) / seg_rows;
     CK(h, ensure(h->pnorm, h->pnorm_cap, segs * n), "alloc pnorm");
-    CK(h, launch_split_f32(X + r0 * ldx, ldx, rc, n, h->planes, ldp, h->pnorm, seg_rows, h->st),
-       "split_f32");
+    CK(h, launch_split_planes(static_cast<const uint8_t*>(X) + r0 * ldx * es, x_bf16, ldx, rc, n, mode,
+                              h->planes, ldp, h->pnorm, seg_rows, h->st),
+       "split_planes");
     CK(h, launch_reduce_norms(h->pnorm, (int)segs, n, h->acc_nrm + col_off, h->st), "reduce_norms");
     h->launches += 2;
-    smp_status s = sketch_dense_bf16(h, row0 + r0, rc, h->planes, ldp, 3 * n, 3, col_off, false);
+    smp_status s = sketch_dense_bf16(h, row0 + r0, rc, h->planes, ldp, np * n, np, col_off, false);
     if (s != SMP_OK) return s;
   }
   return SMP_OK;
@@ -339,6 +353,11 @@ smp_status smp_sketch_block(smp_handle* h, int64_t row0, int64_t rows, const voi
     };
     if ((reinterpret_cast<uintptr_t>(A) & 1) || (two && (reinterpret_cast<uintptr_t>(B) & 1)))
       return fail(h, SMP_EINVAL, "bf16 input must be 2-byte aligned");
+    if (h->d.pi_kind == SMP_PI_GAUSSIAN) {
+      s = sketch_dense_split(h, row0, rows, A, 1, lda, h->n1, 0);
+      if (s != SMP_OK || !two) return s;
+      return sketch_dense_split(h, row0, rows, B, 1, ldb, h->n2, h->n1);
+    }
     s = aligned(A, lda) ? sketch_dense_bf16(h, row0, rows, A, lda, h->n1, 1, 0, true)
                         : sketch_dense_bf16_repack(h, row0, rows, A, lda, h->n1, 0);
     if (s != SMP_OK || !two) return s;
@@ -348,9 +367,9 @@ smp_status smp_sketch_block(smp_handle* h, int64_t row0, int64_t rows, const voi
   // fp32
   if (reinterpret_cast<uintptr_t>(A) % 4 != 0 || (two && reinterpret_cast<uintptr_t>(B) % 4 != 0))
     return fail(h, SMP_EINVAL, "fp32 input must be 4-byte aligned");
-  s = sketch_dense_f32(h, row0, rows, static_cast<const float*>(A), lda, h->n1, 0);
+  s = sketch_dense_split(h, row0, rows, A, 0, lda, h->n1, 0);
   if (s != SMP_OK || !two) return s;
-  return sketch_dense_f32(h, row0, rows, static_cast<const float*>(B), ldb, h->n2, h->n1);
+  return sketch_dense_split(h, row0, rows, B, 0, ldb, h->n2, h->n1);
 }
 
 smp_status smp_sketch_block_host(smp_handle* h, int64_t row0, int64_t rows, const void* A,

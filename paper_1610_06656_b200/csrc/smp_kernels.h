@@ -32,10 +32,12 @@ cudaError_t launch_reduce_sketch(const float* part, int splits, int planes, int6
 // nacc[c] += Σ_slot pnorm[slot][c]
 cudaError_t launch_reduce_norms(const double* pnorm, int slots, int64_t n, double* nacc,
                                 cudaStream_t st);
-// fp32 rows -> 3 bf16 planes (hi, mid, lo; exact sum) laid out as a
-// rows x (3n) matrix with leading dimension ldp, and fp64 Σx² per row segment.
-cudaError_t launch_split_f32(const float* X, int64_t ldx, int64_t rows, int64_t n, uint16_t* planes,
-                             int64_t ldp, double* pnorm, int seg_rows, cudaStream_t st);
+// rows of X (fp32, or bf16 if x_bf16) -> P exact bf16 planes (mode 3: fp32
+// 8+8+8 bits; mode 4: fp32 4+8+8+4; mode 2: bf16 4+4) laid out as a
+// rows x (P n) matrix with leading dimension ldp, and fp64 Σx² per row segment.
+cudaError_t launch_split_planes(const void* X, int x_bf16, int64_t ldx, int64_t rows, int64_t n,
+                                int mode, uint16_t* planes, int64_t ldp, double* pnorm, int seg_rows,
+                                cudaStream_t st);
 // finalize one matrix: out = acc * scale (fp32), sknorm (fp64), D (fp64)
 cudaError_t launch_finalize(const float* acc, double* nacc, int64_t n, int k, float scale,
                             float* out, double* sknorm, double* D, int* status, cudaStream_t st);

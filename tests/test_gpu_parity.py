@@ -325,3 +325,23 @@ def test_sketch_csr_bad_column_rejected():
     sk.block_csr(0, d, rp.cuda(), col.cuda(), val.cuda(), rp.cuda(), torch.zeros_like(col).cuda(), val.cuda())
     with pytest.raises(Exception):
         sk.finalize()
+
+
+@pytest.mark.parametrize("pi", ["gaussian", "rademacher"])
+def test_pi_bit_exact_sampled_rows(pi):
+    """Π itself, bit for bit: X has one 1 per column at a random row t_c over
+    a long row range, so Ã[:, c]·√k = Π[:, t_c] exactly (a1, R2/R3)."""
+    smp = _smp()
+    d, n, k, seed = 1 << 21, 256, 512, 4
+    rng = np.random.default_rng(7)
+    t = np.sort(rng.choice(d, n, replace=False))
+    X = torch.zeros(d, n, dtype=torch.bfloat16)
+    X[torch.as_tensor(t), torch.arange(n)] = 1.0
+    sk = smp.SMPSketch(d, n, n, k, pi=PI[pi], seed=seed, a_is_b=True, input=smp.IN_DENSE_BF16)
+    sk.block(0, X.cuda())
+    fin = sk.finalize()
+    got = fin["A_sk"].cpu().numpy()                       # fp32: Π(κ, t_c) · fp32(1/√k), RN
+    want = np.array([[oracle.pi_entry(PI[pi], seed, kap, int(tc)) for kap in range(k)] for tc in t])
+    want32 = want.astype(np.float32) * np.float32(1.0 / np.sqrt(k))
+    bad = got != want32
+    assert bad.sum() == 0, f"{bad.sum()} of {bad.size} Π entries differ, e.g. {np.argwhere(bad)[:5]}"

@@ -212,6 +212,28 @@ def test_sketch_csr_matches_dense():
     ref, rn = oracle.sketch_rows(oracle.PI_GAUSSIAN, 8, k, D, row0=10)
     np.testing.assert_allclose(sk, ref, rtol=1e-12, atol=1e-11)
     assert np.array_equal(n2, rn)  # integer counts: exact
+    # a block whose rowptr does not start at 0 (col/val indexed from rowptr[0])
+    a, b = 37, 121
+    sk2, n22 = oracle.sketch_csr(oracle.PI_GAUSSIAN, 8, k, n, rowptr[a:b + 1], col[rowptr[a]:],
+                                 val[rowptr[a]:], row0=10 + a)
+    ref2, rn2 = oracle.sketch_rows(oracle.PI_GAUSSIAN, 8, k, D[a:b], row0=10 + a)
+    np.testing.assert_allclose(sk2, ref2, rtol=1e-12, atol=1e-11)
+    assert np.array_equal(n22, rn2)
+
+
+def test_colnorms_closed_form():
+    """Σ_t X[t,c]² against its definition (numpy fp64), bf16/fp32/fp64 inputs."""
+    rng = np.random.default_rng(9)
+    X = (rng.standard_normal((513, 37)) * np.exp(rng.uniform(-5, 5, 37))).astype(np.float32)
+    np.testing.assert_allclose(oracle.colnorms(X), (X.astype(np.float64) ** 2).sum(0), rtol=1e-13)
+    Xd = X.astype(np.float64)
+    np.testing.assert_allclose(oracle.colnorms(Xd), (Xd ** 2).sum(0), rtol=1e-13)
+    bits = (X.view(np.uint32) >> 16).astype(np.uint16)
+    Xb = (bits.astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+    np.testing.assert_allclose(oracle.colnorms(bits), (Xb ** 2).sum(0), rtol=1e-13)
+    # equals the norm half of the one-pass sketch
+    _, n2 = oracle.sketch_rows(oracle.PI_RADEMACHER, 1, 8, X)
+    np.testing.assert_allclose(oracle.colnorms(X), n2, rtol=1e-13)
 
 
 def test_pairwise_sum_exact_cases():

@@ -384,7 +384,10 @@ def main():
     else:
         # roofline of K1 (per launch = one matrix over this rank's rows)
         rows = r1 - r0
-        planes = 3 if inp == IN_DENSE_F32 else 1
+        # bf16 planes per input element (R21): fp32 -> 3; bf16 with a
+        # Gaussian Π -> 2
+        gauss = cfg["pi"] == "gaussian"
+        planes = 3 if inp == IN_DENSE_F32 else (2 if gauss else 1)
         launches_per_step = max(k1_n // max(args.steps, 1), 1)
         ncols_total = (n1 + (0 if a_is_b else n2))
         flops_launch = 2.0 * k * rows * ncols_total * planes / launches_per_step
@@ -453,7 +456,7 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        rate, info = oracle_sample_rate(cfgname, cfg, 15.0)
+        rate, info = oracle_sample_rate(cfgname, cfg, 20.0)
         cpu = {"value": rate, "unit": "GB/s", "cores": info["cores"], "kind": "oracle",
                "sample": info["sample"]}
 

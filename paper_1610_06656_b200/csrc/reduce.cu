@@ -76,9 +76,10 @@ cudaError_t launch_reduce_norms(const double* pnorm, int slots, int64_t n, doubl
 // x = p_1 + ... + p_P exactly, every p_q a bf16 number with a limited number
 // of significant bits, so that Π·X = Σ_q Π·p_q with every tensor-core
 // product short enough to survive the MMA's accumulation (R21):
-//   mode 3 (fp32 x, ±1 Π)        : 8 + 8 + 8 bits (products = p_q, ≤ 8 bits)
-//   mode 4 (fp32 x, Gaussian Π)  : 4 + 8 + 8 + 4 bits
-//   mode 2 (bf16 x, Gaussian Π)  : 4 + 4 bits
+//   mode 3 (fp32 x, ±1 Π)        : 8 + 8 + 8 bits, exact (products = p_q, ≤ 8 bits)
+//   mode 4 (fp32 x, Gaussian Π)  : 4 + 8 + 8 bits, remainder (|r| <= 2^-21 |x|)
+//                                  dropped: <= 5e-7 relative per element
+//   mode 2 (bf16 x, Gaussian Π)  : 4 + 4 bits, exact
 // (Gaussian Π has 8 significant bits; a 16-bit product loses its low bits
 // against a large fp32 accumulator inside tcgen05.mma — measured 1.6e-5
 // relative column error — while 12-bit products are kept exactly.)
@@ -103,8 +104,9 @@ __global__ void split_planes_kernel(const void* __restrict__ Xv, int x_bf16, int
   const int64_t r1 = min(rows, r0 + seg_rows);
   int bits[4];
   int np;
+  bool exact = true;
   if (mode == 3) { np = 3; bits[0] = 8; bits[1] = 8; bits[2] = 8; bits[3] = 0; }
-  else if (mode == 4) { np = 4; bits[0] = 4; bits[1] = 8; bits[2] = 8; bits[3] = 8; }
+  else if (mode == 4) { np = 3; bits[0] = 4; bits[1] = 8; bits[2] = 8; bits[3] = 0; exact = false; }
   else { np = 2; bits[0] = 4; bits[1] = 8; bits[2] = 0; bits[3] = 0; }
   double s2 = 0.0;
   for (int64_t t = r0; t < r1; ++t) {
@@ -115,7 +117,7 @@ __global__ void split_planes_kernel(const void* __restrict__ Xv, int x_bf16, int
     float r = x;
     for (int q = 0; q < np; ++q) {
       // the last plane takes the (exactly representable) remainder
-      const float p = (q == np - 1) ? r : round_sig(r, bits[q]);
+      const float p = (q == np - 1 && exact) ? r : round_sig(r, bits[q]);
       row[q * n + c] = (uint16_t)(__float_as_uint(p) >> 16);
       r = __fsub_rn(r, p);
     }

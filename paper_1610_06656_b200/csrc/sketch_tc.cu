@@ -243,6 +243,22 @@ sketch_tc_kernel(const __grid_constant__ CUtensorMap tmap, SketchTCParams p) {
       if (p.debug & 2) {
 #pragma unroll
         for (int i = 0; i < 16; ++i) o[i] = 0x3F803F80u;
+      } else if (p.pi_panel) {
+        // Π generated once per block into an L2-resident κ-major panel
+        // (Gaussian: ~33 ALU ops per entry would otherwise be repeated for
+        // every column tile); 64 contiguous bytes per thread
+        if (kappa < p.k) {
+          const uint4* src = reinterpret_cast<const uint4*>(
+              p.pi_panel + (int64_t)kappa * p.pi_ld + (int64_t)(kb_begin + it) * TC_BK + 32 * half);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const uint4 v = __ldcg(src + q);
+            o[4 * q] = v.x; o[4 * q + 1] = v.y; o[4 * q + 2] = v.z; o[4 * q + 3] = v.w;
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) o[i] = 0u;
+        }
       } else {
         gen_pi_half(p.kind, p.seed, (uint32_t)kappa, kappa < p.k, t0, rc, o);
       }
@@ -354,6 +370,50 @@ sketch_tc_kernel(const __grid_constant__ CUtensorMap tmap, SketchTCParams p) {
     tc_fence_after();
     tmem_dealloc2(tbase, TMEM_COLS);
   }
+}
+
+// ---------------------------------------------------------------- Π panel
+// panel[κ * ld + (t - t0)] = Π(κ, t) (bf16 bits) for κ < k, t in [t0, t0 + rows);
+// thread per (κ, 4-row group): one Philox call for the Gaussian stream
+// (DESIGN.md §3.2-3.3), 8 contiguous bytes written.
+__global__ void pi_panel_kmajor_kernel(int kind, uint64_t seed, int k, int64_t t0, int64_t rows,
+                                       int64_t ld, uint16_t* __restrict__ panel) {
+  const int64_t ng = (rows + 3) / 4;
+  const uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < ng * k;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int kappa = (int)(e / ng);
+    const int64_t g = e - (int64_t)kappa * ng;
+    const int64_t t = t0 + 4 * g;
+    uint16_t z[4];
+    if (kind == PI_GAUSSIAN && (t & 3) == 0) {
+      const uint64_t tq = (uint64_t)t >> 2;
+      const u32x4 w = philox4x32_10((uint32_t)tq, (uint32_t)kappa, (uint32_t)(tq >> 32), TAG_GAUSSIAN, k0, k1);
+      gauss_pair(w.x, w.y, z[0], z[1]);
+      gauss_pair(w.z, w.w, z[2], z[3]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) z[j] = pi_bits(kind, seed, (uint32_t)kappa, (uint64_t)(t + j));
+    }
+    uint16_t* dst = panel + (int64_t)kappa * ld + 4 * g;
+    if ((ld & 3) == 0) {
+      uint2 v;
+      v.x = (uint32_t)z[0] | ((uint32_t)z[1] << 16);
+      v.y = (uint32_t)z[2] | ((uint32_t)z[3] << 16);
+      *reinterpret_cast<uint2*>(dst) = v;
+    } else {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) dst[j] = z[j];
+    }
+  }
+}
+
+cudaError_t launch_pi_panel_kmajor(int kind, uint64_t seed, int k, int64_t t0, int64_t rows, int64_t ld,
+                                   uint16_t* panel, cudaStream_t st) {
+  const int64_t tot = ((rows + 3) / 4) * k;
+  const int blocks = (int)std::min<int64_t>((tot + 255) / 256, 148 * 16);
+  pi_panel_kmajor_kernel<<<blocks, 256, 0, st>>>(kind, seed, k, t0, rows, ld, panel);
+  return cudaGetLastError();
 }
 
 // ---------------------------------------------------------------- host side

@@ -39,6 +39,8 @@ struct smp_handle {
   int64_t pnorm_cap = 0;
   uint16_t* planes = nullptr;
   int64_t planes_cap = 0;
+  uint16_t* pi_panel = nullptr;  // K1 Gaussian Π panel (κ-major)
+  int64_t pi_panel_cap = 0;
   // finalized state
   float* fin_sk = nullptr;     // [ntot][k]
   double* fin_sknorm = nullptr;
@@ -155,6 +157,19 @@ smp_status sketch_dense_bf16(smp_handle* h, int64_t row0, int64_t rows, const vo
   CK(h, ensure(h->pnorm, h->pnorm_cap, (int64_t)p.splits * p.k_tiles * ncols), "alloc pnorm");
   p.part = h->part;
   p.pnorm = h->pnorm;
+  p.pi_panel = nullptr;
+  p.pi_ld = 0;
+  if (p.kind == SMP_PI_GAUSSIAN) {
+    // Gaussian Π once per block into an L2-resident κ-major panel (K1 reads it
+    // instead of regenerating it for every column tile)
+    const int64_t ld = (int64_t)p.kb_total * 64;
+    const int64_t kpad = (int64_t)p.k_tiles * 256;
+    CK(h, ensure(h->pi_panel, h->pi_panel_cap, kpad * ld), "alloc pi panel");
+    CK(h, launch_pi_panel_kmajor(p.kind, p.seed, k, row0, ld, ld, h->pi_panel, h->st), "pi panel");
+    h->launches += 1;
+    p.pi_panel = h->pi_panel;
+    p.pi_ld = ld;
+  }
   if (h->timing) {
     while (h->ev_pool.size() < h->ev_used_n + 2) {
       cudaEvent_t e;
@@ -188,7 +203,7 @@ smp_status sketch_dense_split(smp_handle* h, int64_t row0, int64_t rows, const v
   using namespace smp;
   const bool gauss = h->d.pi_kind == SMP_PI_GAUSSIAN;
   const int mode = x_bf16 ? 2 : (gauss ? 4 : 3);
-  const int np = mode;
+  const int np = x_bf16 ? 2 : 3;
   const int64_t ldp = ((np * n + 7) / 8) * 8;
   const int64_t chunk = std::max<int64_t>(64, std::min<int64_t>(rows, (int64_t)(512ll << 20) / (ldp * 2)));
   const int seg_rows = 256;
@@ -317,7 +332,7 @@ void smp_destroy(smp_handle* h) {
   if (!h) return;
   if (h->st) cudaStreamSynchronize(h->st);
   cudaFree(h->acc_sk); cudaFree(h->acc_nrm); cudaFree(h->part); cudaFree(h->pnorm);
-  cudaFree(h->planes); cudaFree(h->fin_sk); cudaFree(h->fin_sknorm); cudaFree(h->fin_D);
+  cudaFree(h->planes); cudaFree(h->pi_panel); cudaFree(h->fin_sk); cudaFree(h->fin_sknorm); cudaFree(h->fin_D);
   cudaFree(h->FAFB); cudaFree(h->status); cudaFree(h->pw_scratch); cudaFree(h->alpha);
   cudaFree(h->blk); cudaFree(h->d_total);
   smp::csr_workspace_free(h->csr);

@@ -21,7 +21,12 @@ struct SketchTCParams {
   uint64_t seed;
   float* part;       // [splits][n][k]
   double* pnorm;     // [splits * k_tiles][n]
+  const uint16_t* pi_panel;  // optional κ-major Π panel [k][pi_ld] for rows row0.. (else generated in-kernel)
+  int64_t pi_ld;             // multiple of 64 rows, >= kb_total * 64
 };
+// Π(κ, t) for t in [t0, t0 + rows) into panel[κ * ld + t - t0] (bf16 bits; rows padded by the caller)
+cudaError_t launch_pi_panel_kmajor(int kind, uint64_t seed, int k, int64_t t0, int64_t rows, int64_t ld,
+                                   uint16_t* panel, cudaStream_t st);
 cudaError_t launch_sketch_tc(const void* X, int64_t ldx, SketchTCParams p, cudaStream_t st);
 int sketch_tc_smem_bytes();
 

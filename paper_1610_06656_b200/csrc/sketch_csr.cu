@@ -11,8 +11,10 @@
 //   K3a  generate the Π panel of Rp rows (bf16, Rp x kp, row t contiguous
 //        in κ) into an L2-resident buffer — every Π entry is generated once;
 //   K3b  key every nonzero of the panel (A and B) as (column << tbits | t);
-//   K3c  stable radix sort (CUB) -> the panel's nonzeros in (column, row)
-//        order (a per-panel CSC transpose);
+//   K3c  counting sort by column (SMEM histograms per CTA row range, one
+//        exclusive scan over (column, CTA), SMEM-cursor scatter) -> the
+//        panel's nonzeros grouped by column (a per-panel CSC transpose);
+//        CUB radix sort for more columns than fit a CTA's SMEM histogram;
 //   K3d  warps take fixed chunks of the sorted nonzeros (load balance for
 //        Zipf-heavy columns): lanes own κ slices, gather π_t (kp bf16) from
 //        the panel, FMA v·π_t into fp32 registers, and flush the column's
@@ -25,6 +27,9 @@
 // agree with the oracle to ~1e-7 relative but are not bit-reproducible run
 // to run (K3).
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+#include <cstdio>
+#include <cstdlib>
 #include "smp_device.cuh"
 #include "smp_kernels.h"
 
@@ -41,9 +46,10 @@ __global__ void pi_panel_kernel(int kind, uint64_t seed, int k, int kp, int64_t 
   const int64_t g_first = t0 / rpg, g_last = (t0 + rows - 1) / rpg;
   const int64_t ngroups = g_last - g_first + 1;
   const uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < ngroups * kp; e += nthreads) {
-    const int kappa = (int)(e % kp);
-    const int64_t g = g_first + e / kp;
+  const uint32_t total = (uint32_t)(ngroups * kp);  // < 2^32: rows <= 2^15 per panel
+  for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (uint32_t)nthreads) {
+    const int kappa = (int)(e % (uint32_t)kp);
+    const int64_t g = g_first + (int64_t)(e / (uint32_t)kp);
     const int64_t tb = g * rpg;
     if (kappa >= k) {
       for (int j = 0; j < rpg; ++j) {
@@ -212,6 +218,103 @@ csr_accumulate_kernel(const uint32_t* __restrict__ keys, const float* __restrict
   }
 }
 
+// ---------------------------------------------------------------- K3c counting sort
+// CTA b owns panel rows [b·rows/G, (b+1)·rows/G) of both matrices.
+__device__ __forceinline__ void cta_rows(int rows, int& r0, int& r1) {
+  r0 = (int)(((int64_t)blockIdx.x * rows) / gridDim.x);
+  r1 = (int)(((int64_t)(blockIdx.x + 1) * rows) / gridDim.x);
+}
+
+// histT[c * G + b] = nonzeros of column c in CTA b's rows (c of B offset by a_n).
+// Warp per row; each lane issues its (up to 4) column loads before the SMEM
+// atomics so a row costs one memory round trip.
+constexpr int CSR_T_THREADS = 1024;
+
+__global__ void __launch_bounds__(CSR_T_THREADS)
+csr_hist_kernel(const int64_t* __restrict__ arp, const int32_t* __restrict__ acol, int64_t a_n,
+                const int64_t* __restrict__ brp, const int32_t* __restrict__ bcol, int64_t b_n,
+                int64_t p0, int rows, int ntot, uint32_t* __restrict__ histT) {
+  extern __shared__ uint32_t hist[];
+  for (int c = threadIdx.x; c < ntot; c += blockDim.x) hist[c] = 0u;
+  __syncthreads();
+  int r0, r1;
+  cta_rows(rows, r0, r1);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int mat = 0; mat < 2; ++mat) {
+    const int64_t* rp = mat == 0 ? arp : brp;
+    if (!rp) continue;
+    const int32_t* col = mat == 0 ? acol : bcol;
+    const int64_t ncols = mat == 0 ? a_n : b_n;
+    const uint32_t cofs = mat == 0 ? 0u : (uint32_t)a_n;
+    const int64_t base = rp[0];
+    for (int r = r0 + warp; r < r1; r += nw) {
+      const int64_t e0 = rp[p0 + r] - base, e1 = rp[p0 + r + 1] - base;
+      for (int64_t eb = e0 + lane; eb < e1; eb += 128) {
+        int32_t c[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) c[u] = eb + 32 * u < e1 ? col[eb + 32 * u] : -1;
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (eb + 32 * u < e1) {
+            const uint32_t cg = (uint32_t)(c[u] < 0 || c[u] >= ncols ? 0 : c[u]) + cofs;
+            atomicAdd(&hist[cg], 1u);
+          }
+      }
+    }
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < ntot; c += blockDim.x) histT[(int64_t)c * gridDim.x + blockIdx.x] = hist[c];
+}
+
+// keys/vals at offsT[c * G + b] + (rank within the CTA's column c, SMEM atomic order)
+__global__ void __launch_bounds__(CSR_T_THREADS)
+csr_scatter_kernel(const int64_t* __restrict__ arp, const int32_t* __restrict__ acol,
+                   const float* __restrict__ aval, int64_t a_n, const int64_t* __restrict__ brp,
+                   const int32_t* __restrict__ bcol, const float* __restrict__ bval, int64_t b_n,
+                   int64_t p0, int rows, int ntot, int tbits, const uint32_t* __restrict__ offsT,
+                   uint32_t* __restrict__ keys, float* __restrict__ vals, int* __restrict__ status) {
+  extern __shared__ uint32_t cur[];
+  for (int c = threadIdx.x; c < ntot; c += blockDim.x) cur[c] = offsT[(int64_t)c * gridDim.x + blockIdx.x];
+  __syncthreads();
+  int r0, r1;
+  cta_rows(rows, r0, r1);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int mat = 0; mat < 2; ++mat) {
+    const int64_t* rp = mat == 0 ? arp : brp;
+    if (!rp) continue;
+    const int32_t* col = mat == 0 ? acol : bcol;
+    const float* val = mat == 0 ? aval : bval;
+    const int64_t ncols = mat == 0 ? a_n : b_n;
+    const uint32_t cofs = mat == 0 ? 0u : (uint32_t)a_n;
+    const int64_t base = rp[0];
+    for (int r = r0 + warp; r < r1; r += nw) {
+      const int64_t e0 = rp[p0 + r] - base, e1 = rp[p0 + r + 1] - base;
+      for (int64_t eb = e0 + lane; eb < e1; eb += 128) {
+        int32_t c[4];
+        float v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const bool ok = eb + 32 * u < e1;
+          c[u] = ok ? col[eb + 32 * u] : 0;
+          v[u] = ok ? val[eb + 32 * u] : 0.f;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (eb + 32 * u < e1) {
+            if (c[u] < 0 || c[u] >= ncols) atomicOr(status, 2);  // out-of-range column
+            const uint32_t cg = (uint32_t)(c[u] < 0 || c[u] >= ncols ? 0 : c[u]) + cofs;
+            const uint32_t pos = atomicAdd(&cur[cg], 1u);
+            keys[pos] = (cg << tbits) | (uint32_t)r;
+            vals[pos] = v[u];
+          }
+      }
+    }
+  }
+}
+
+constexpr int CSR_HIST_CTAS = 148;
+constexpr int CSR_HIST_MAX_COLS = 53248;  // 208 KB of SMEM counters
+
 // ---------------------------------------------------------------- driver
 __global__ void csr_bounds_kernel(const int64_t* __restrict__ arp, const int64_t* __restrict__ brp,
                                   int rows, int rp, int npan, int64_t* __restrict__ out) {
@@ -241,7 +344,7 @@ static cudaError_t grow(T*& p, int64_t& cap, int64_t need) {
 
 void csr_workspace_free(CsrWorkspace& w) {
   cudaFree(w.pi); cudaFree(w.keys_in); cudaFree(w.keys_out); cudaFree(w.vals_in);
-  cudaFree(w.vals_out); cudaFree(w.cub_tmp); cudaFree(w.bounds_d);
+  cudaFree(w.vals_out); cudaFree(w.cub_tmp); cudaFree(w.bounds_d); cudaFree(w.hist); cudaFree(w.offs);
   if (w.bounds_h) cudaFreeHost(w.bounds_h);
   w = CsrWorkspace{};
 }
@@ -283,17 +386,43 @@ cudaError_t launch_sketch_csr(CsrWorkspace& w, int kind, uint64_t seed, int k, i
   int64_t max_ent = 0;
   for (int p = 0; p < npan; ++p) max_ent = std::max(max_ent, (ab[p + 1] - ab[p]) + (bb[p + 1] - bb[p]));
   CSR_TRY(grow(w.pi, w.pi_cap, (int64_t)rp * kp));
-  CSR_TRY(grow(w.keys_in, w.ent_cap_ki, max_ent));
-  CSR_TRY(grow(w.keys_out, w.ent_cap_ko, max_ent));
-  CSR_TRY(grow(w.vals_in, w.ent_cap_vi, max_ent));
-  CSR_TRY(grow(w.vals_out, w.ent_cap_vo, max_ent));
   const int end_bit = tbits + cbits;
+  const bool counting = ntot <= CSR_HIST_MAX_COLS;
+  if (!counting) {
+    CSR_TRY(grow(w.keys_in, w.ent_cap_ki, max_ent));
+    CSR_TRY(grow(w.vals_in, w.ent_cap_vi, max_ent));
+  }
+  CSR_TRY(grow(w.keys_out, w.ent_cap_ko, max_ent));
+  CSR_TRY(grow(w.vals_out, w.ent_cap_vo, max_ent));
   size_t need = 0;
-  CSR_TRY(cub::DeviceRadixSort::SortPairs(nullptr, need, w.keys_in, w.keys_out, w.vals_in, w.vals_out,
-                                          (int)std::max<int64_t>(max_ent, 1), 0, end_bit, st));
+  if (counting) {
+    const int64_t nh = ntot * (int64_t)CSR_HIST_CTAS;
+    CSR_TRY(grow(w.hist, w.hist_cap, nh));
+    CSR_TRY(grow(w.offs, w.offs_cap, nh));
+    CSR_TRY(cub::DeviceScan::ExclusiveSum(nullptr, need, w.hist, w.offs, (int)nh, st));
+    static bool attr = false;
+    if (!attr) {
+      CSR_TRY(cudaFuncSetAttribute(csr_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   CSR_HIST_MAX_COLS * 4));
+      CSR_TRY(cudaFuncSetAttribute(csr_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   CSR_HIST_MAX_COLS * 4));
+      attr = true;
+    }
+  } else {
+    CSR_TRY(cub::DeviceRadixSort::SortPairs(nullptr, need, w.keys_in, w.keys_out, w.vals_in, w.vals_out,
+                                            (int)std::max<int64_t>(max_ent, 1), 0, end_bit, st));
+  }
   CSR_TRY(grow(w.cub_tmp, w.cub_cap, (int64_t)need));
+  // diagnostics (SMP_CSR_PROFILE=1): device time per K3 stage, summed over panels
+  const char* prof_env = getenv("SMP_CSR_PROFILE");
+  const bool prof = prof_env && atoi(prof_env);
+  cudaEvent_t pev[5] = {};
+  float pms[4] = {0.f, 0.f, 0.f, 0.f};
+  if (prof)
+    for (int i = 0; i < 5; ++i) CSR_TRY(cudaEventCreate(&pev[i]));
   for (int p = 0; p < npan; ++p) {
     const int64_t p0 = (int64_t)p * rp;
+    if (prof) CSR_TRY(cudaEventRecord(pev[0], st));
     const int prow = (int)std::min<int64_t>(rp, rows - p0);
     const int64_t na = ab[p + 1] - ab[p], nb = bb[p + 1] - bb[p];
     const int64_t ne = na + nb;
@@ -302,17 +431,31 @@ cudaError_t launch_sketch_csr(CsrWorkspace& w, int kind, uint64_t seed, int k, i
       const int blocks = (int)std::min<int64_t>((groups + 255) / 256, 148 * 16);
       pi_panel_kernel<<<blocks, 256, 0, st>>>(kind, seed, k, kp, row0 + p0, prow, w.pi);
     }
+    if (prof) CSR_TRY(cudaEventRecord(pev[1], st));
     if (ne == 0) continue;
-    const int kb_blocks = (int)std::min<int64_t>((prow + 7) / 8, 148 * 16);
-    // A: entries ab[p] .. ab[p+1] (relative to a_rowptr[0]) -> keys[0 .. na)
-    csr_keys_kernel<<<kb_blocks, 256, 0, st>>>(a_rowptr, a_col, a_val, p0, prow, ab[p], 0u, tbits,
-                                               a_n, w.keys_in, w.vals_in, status);
-    if (b_rowptr && nb > 0)
-      csr_keys_kernel<<<kb_blocks, 256, 0, st>>>(b_rowptr, b_col, b_val, p0, prow, bb[p] - na,
-                                                 (uint32_t)a_n, tbits, b_n, w.keys_in, w.vals_in, status);
-    size_t tmp = (size_t)w.cub_cap;
-    CSR_TRY(cub::DeviceRadixSort::SortPairs(w.cub_tmp, tmp, w.keys_in, w.keys_out, w.vals_in, w.vals_out,
-                                            (int)ne, 0, end_bit, st));
+    if (counting) {
+      const size_t sm = (size_t)ntot * 4;
+      csr_hist_kernel<<<CSR_HIST_CTAS, CSR_T_THREADS, sm, st>>>(a_rowptr, a_col, a_n, b_rowptr, b_col, b_n, p0,
+                                                     prow, (int)ntot, w.hist);
+      size_t tmp = (size_t)w.cub_cap;
+      CSR_TRY(cub::DeviceScan::ExclusiveSum(w.cub_tmp, tmp, w.hist, w.offs,
+                                            (int)(ntot * (int64_t)CSR_HIST_CTAS), st));
+      csr_scatter_kernel<<<CSR_HIST_CTAS, CSR_T_THREADS, sm, st>>>(a_rowptr, a_col, a_val, a_n, b_rowptr, b_col,
+                                                        b_val, b_n, p0, prow, (int)ntot, tbits, w.offs,
+                                                        w.keys_out, w.vals_out, status);
+    } else {
+      const int kb_blocks = (int)std::min<int64_t>((prow + 7) / 8, 148 * 16);
+      // A: entries ab[p] .. ab[p+1] (relative to a_rowptr[0]) -> keys[0 .. na)
+      csr_keys_kernel<<<kb_blocks, 256, 0, st>>>(a_rowptr, a_col, a_val, p0, prow, ab[p], 0u, tbits,
+                                                 a_n, w.keys_in, w.vals_in, status);
+      if (b_rowptr && nb > 0)
+        csr_keys_kernel<<<kb_blocks, 256, 0, st>>>(b_rowptr, b_col, b_val, p0, prow, bb[p] - na,
+                                                   (uint32_t)a_n, tbits, b_n, w.keys_in, w.vals_in, status);
+      size_t tmp = (size_t)w.cub_cap;
+      CSR_TRY(cub::DeviceRadixSort::SortPairs(w.cub_tmp, tmp, w.keys_in, w.keys_out, w.vals_in, w.vals_out,
+                                              (int)ne, 0, end_bit, st));
+    }
+    if (prof) CSR_TRY(cudaEventRecord(pev[2], st));
     const int64_t tasks = (ne + CSR_CHUNK - 1) / CSR_CHUNK;
     const int ablocks = (int)std::min<int64_t>((tasks + 7) / 8, 148 * 64);
     const int kv = (kp + 255) / 256;
@@ -337,6 +480,20 @@ cudaError_t launch_sketch_csr(CsrWorkspace& w, int kind, uint64_t seed, int k, i
       *w.ev_used += 2;
     }
     w.launches += 4 + (b_rowptr && nb > 0 ? 1 : 0) + 3;
+    if (prof) {
+      CSR_TRY(cudaEventRecord(pev[3], st));
+      CSR_TRY(cudaEventSynchronize(pev[3]));
+      for (int i = 0; i < 3; ++i) {
+        float ms = 0.f;
+        CSR_TRY(cudaEventElapsedTime(&ms, pev[i], pev[i + 1]));
+        pms[i] += ms;
+      }
+    }
+  }
+  if (prof) {
+    fprintf(stderr, "K3 stages over %d panels: pi panel %.3f ms, transpose %.3f ms, accumulate %.3f ms\n",
+            npan, pms[0], pms[1], pms[2]);
+    for (int i = 0; i < 5; ++i) cudaEventDestroy(pev[i]);
   }
   return cudaGetLastError();
 }

@@ -64,6 +64,16 @@ constexpr int NORM_RED = NORM_RG * HALF_N * 8;    // 16 KB
 constexpr int TC_BARS = 3 * X_STAGES + 2 * PI_STAGES + 1;
 constexpr int TC_SMEM = X_STAGES * X_STAGE + NORM_RED + TC_BARS * 8 + 16 + 1024;
 static_assert(TC_SMEM <= 227 * 1024, "K1 exceeds the 227 KB SMEM budget");
+// PANEL variant (Gaussian Π read from an L2-resident κ-major panel): each
+// stage holds the X half tile AND this SM's 128 κ x 64 t Π tile, both by
+// TMA (128B swizzle; the Π box is exactly the K-major SW128 layout of the
+// MMA's A operand), and the MMA reads A from SMEM.
+constexpr int P_STAGES = 6;
+constexpr int PI_TILE = 128 * TC_BK * 2;          // 16 KB
+constexpr int P_STAGE = X_STAGE + PI_TILE;        // 32 KB
+constexpr int P_BARS = 3 * P_STAGES + 2 * PI_STAGES + 1;
+constexpr int P_SMEM = P_STAGES * P_STAGE + NORM_RED + P_BARS * 8 + 16 + 1024;
+static_assert(P_SMEM <= 227 * 1024, "K1 (panel) exceeds the 227 KB SMEM budget");
 constexpr int TC_THREADS = 32 * 20;
 
 struct RadCache {
@@ -135,17 +145,21 @@ __device__ __forceinline__ void gen_pi_half(int kind, uint64_t seed, uint32_t ka
   }
 }
 
+template <bool PANEL>
 __global__ void __launch_bounds__(TC_THREADS, 1)
-sketch_tc_kernel(const __grid_constant__ CUtensorMap tmap, SketchTCParams p) {
+sketch_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap tmap_pi,
+                 SketchTCParams p) {
+  constexpr int NST = PANEL ? P_STAGES : X_STAGES;   // ring stages
+  constexpr int STG = PANEL ? P_STAGE : X_STAGE;     // bytes per stage
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_addr = smem_u32(smem_raw);
   uint8_t* smem = smem_raw + (((raw_addr + 1023u) & ~1023u) - raw_addr);
-  uint8_t* x_s = smem;                                              // [X_STAGES][2][64][128 B]
-  double* red = reinterpret_cast<double*>(smem + X_STAGES * X_STAGE);  // [NORM_RG][128]
-  uint64_t* xfull = reinterpret_cast<uint64_t*>(smem + X_STAGES * X_STAGE + NORM_RED);
-  uint64_t* xempty = xfull + X_STAGES;
-  uint64_t* ready = xempty + X_STAGES;    // leader only: X and Π of both CTAs ready
-  uint64_t* pfull = ready + X_STAGES;
+  uint8_t* x_s = smem;                                              // [NST][X 16 KB (| Π 16 KB)]
+  double* red = reinterpret_cast<double*>(smem + NST * STG);        // [NORM_RG][128]
+  uint64_t* xfull = reinterpret_cast<uint64_t*>(smem + NST * STG + NORM_RED);
+  uint64_t* xempty = xfull + NST;
+  uint64_t* ready = xempty + NST;         // leader only: X and Π of both CTAs ready
+  uint64_t* pfull = ready + NST;
   uint64_t* pempty = pfull + PI_STAGES;
   uint64_t* tmem_full = pempty + PI_STAGES;
   uint32_t* tmem_base_s = reinterpret_cast<uint32_t*>(tmem_full + 1);
@@ -164,7 +178,7 @@ sketch_tc_kernel(const __grid_constant__ CUtensorMap tmap, SketchTCParams p) {
   const int kappa0 = kt * TC_BM + (int)rank * 128;               // this SM's κ rows
 
   if (tid == 0) {
-    for (int s = 0; s < X_STAGES; ++s) {
+    for (int s = 0; s < NST; ++s) {
       mbar_init(&xfull[s], 1);
       mbar_init(&xempty[s], 1 + NUM_NORM_WARPS);
       mbar_init(&ready[s], 2);
@@ -176,7 +190,10 @@ sketch_tc_kernel(const __grid_constant__ CUtensorMap tmap, SketchTCParams p) {
     mbar_init(tmem_full, 1);
     fence_mbar_init();
   }
-  if (warp == 0 && lane == 0) tma_prefetch_desc(&tmap);
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmap);
+    if (PANEL) tma_prefetch_desc(&tmap_pi);
+  }
   if (warp == 1) tmem_alloc2(tmem_base_s, TMEM_COLS);
   tc_fence_before();
   cluster_sync();
@@ -187,12 +204,13 @@ sketch_tc_kernel(const __grid_constant__ CUtensorMap tmap, SketchTCParams p) {
     // ---------------- TMA producer: this SM's half of the X tile
     if (lane == 0) {
       for (int it = 0; it < nkb; ++it) {
-        const int s = it % X_STAGES;
-        mbar_wait(&xempty[s], ((uint32_t)(it / X_STAGES) & 1u) ^ 1u);
-        mbar_arrive_expect_tx(&xfull[s], X_STAGE);
+        const int s = it % NST;
+        mbar_wait(&xempty[s], ((uint32_t)(it / NST) & 1u) ^ 1u);
+        mbar_arrive_expect_tx(&xfull[s], STG);
         const int row = (kb_begin + it) * TC_BK;
-        tma_load_2d(x_s + s * X_STAGE, &tmap, &xfull[s], n0, row);
-        tma_load_2d(x_s + s * X_STAGE + 8192, &tmap, &xfull[s], n0 + 64, row);
+        tma_load_2d(x_s + s * STG, &tmap, &xfull[s], n0, row);
+        tma_load_2d(x_s + s * STG + 8192, &tmap, &xfull[s], n0 + 64, row);
+        if (PANEL) tma_load_2d(x_s + s * STG + X_STAGE, &tmap_pi, &xfull[s], row, kappa0);
       }
     }
   } else if (warp == 1) {
@@ -201,19 +219,25 @@ sketch_tc_kernel(const __grid_constant__ CUtensorMap tmap, SketchTCParams p) {
       const uint32_t idesc = make_idesc_bf16(256, 256, 0, 1);
       const uint32_t x_addr = smem_u32(x_s);
       for (int it = 0; it < nkb; ++it) {
-        const int s = it % X_STAGES, ps = it % PI_STAGES;
-        mbar_wait(&ready[s], (uint32_t)(it / X_STAGES) & 1u);
+        const int s = it % NST, ps = it % PI_STAGES;
+        mbar_wait(&ready[s], (uint32_t)(it / NST) & 1u);
         tc_fence_after();
         if (!(p.debug & 4)) {
 #pragma unroll
           for (int kk = 0; kk < TC_BK / 16; ++kk) {
-            const uint64_t bdesc = make_sdesc_sw128(x_addr + s * X_STAGE + kk * 2048, 8192, 1024);
-            tc_mma2_ts(tbase, tbase + ACC_COLS + ps * PI_COLS + kk * 8, bdesc, idesc,
-                       (it | kk) != 0 ? 1u : 0u);
+            const uint64_t bdesc = make_sdesc_sw128(x_addr + s * STG + kk * 2048, 8192, 1024);
+            if (PANEL) {
+              // A = Π tile, K-major SW128 (128 B rows = 64 t; 16 t = 32 B per MMA)
+              const uint64_t adesc = make_sdesc_sw128(x_addr + s * STG + X_STAGE + kk * 32, 16, 1024);
+              tc_mma2_ss(tbase, adesc, bdesc, idesc, (it | kk) != 0 ? 1u : 0u);
+            } else {
+              tc_mma2_ts(tbase, tbase + ACC_COLS + ps * PI_COLS + kk * 8, bdesc, idesc,
+                         (it | kk) != 0 ? 1u : 0u);
+            }
           }
         }
         tc_commit2(&xempty[s], 0x3);
-        tc_commit2(&pempty[ps], 0x3);
+        if (!PANEL) tc_commit2(&pempty[ps], 0x3);
       }
       tc_commit2(tmem_full, 0x3);
     }
@@ -222,15 +246,17 @@ sketch_tc_kernel(const __grid_constant__ CUtensorMap tmap, SketchTCParams p) {
     if (lane == 0) {
       const uint32_t leader_ready = mapa_shared(smem_u32(ready), 0);
       for (int it = 0; it < nkb; ++it) {
-        const int s = it % X_STAGES, ps = it % PI_STAGES;
-        mbar_wait(&xfull[s], (uint32_t)(it / X_STAGES) & 1u);
-        mbar_wait(&pfull[ps], (uint32_t)(it / PI_STAGES) & 1u);
+        const int s = it % NST, ps = it % PI_STAGES;
+        mbar_wait(&xfull[s], (uint32_t)(it / NST) & 1u);
+        if (!PANEL) mbar_wait(&pfull[ps], (uint32_t)(it / PI_STAGES) & 1u);
         mbar_arrive_cluster(leader_ready + 8u * (uint32_t)s);
       }
     }
   } else if ((warp >= 4 && warp < 8) || warp >= 16) {
     // ---------------- Π generators: thread owns TMEM lane 32*quad + lane,
-    // rows 32*half .. 32*half+31 of every K-block
+    // rows 32*half .. 32*half+31 of every K-block (idle in PANEL mode: Π
+    // arrives by TMA)
+    if (PANEL) goto role_done;
     const int quad = warp & 3;
     const int half = warp >= 16 ? 1 : 0;
     const int kl = 32 * quad + lane;
@@ -243,22 +269,6 @@ sketch_tc_kernel(const __grid_constant__ CUtensorMap tmap, SketchTCParams p) {
       if (p.debug & 2) {
 #pragma unroll
         for (int i = 0; i < 16; ++i) o[i] = 0x3F803F80u;
-      } else if (p.pi_panel) {
-        // Π generated once per block into an L2-resident κ-major panel
-        // (Gaussian: ~33 ALU ops per entry would otherwise be repeated for
-        // every column tile); 64 contiguous bytes per thread
-        if (kappa < p.k) {
-          const uint4* src = reinterpret_cast<const uint4*>(
-              p.pi_panel + (int64_t)kappa * p.pi_ld + (int64_t)(kb_begin + it) * TC_BK + 32 * half);
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const uint4 v = __ldcg(src + q);
-            o[4 * q] = v.x; o[4 * q + 1] = v.y; o[4 * q + 2] = v.z; o[4 * q + 3] = v.w;
-          }
-        } else {
-#pragma unroll
-          for (int i = 0; i < 16; ++i) o[i] = 0u;
-        }
       } else {
         gen_pi_half(p.kind, p.seed, (uint32_t)kappa, kappa < p.k, t0, rc, o);
       }
@@ -285,12 +295,12 @@ sketch_tc_kernel(const __grid_constant__ CUtensorMap tmap, SketchTCParams p) {
     const bool norms_on = p.do_norms && !(p.debug & 1);
     int duty_ctr = kb_begin % p.k_tiles;
     for (int it = 0; it < nkb; ++it) {
-      const int s = it % X_STAGES;
-      mbar_wait(&xfull[s], (uint32_t)(it / X_STAGES) & 1u);
+      const int s = it % NST;
+      mbar_wait(&xfull[s], (uint32_t)(it / NST) & 1u);
       const bool duty = norms_on && duty_ctr == kt;
       if (++duty_ctr == p.k_tiles) duty_ctr = 0;
       if (duty) {
-        const uint8_t* base = x_s + s * X_STAGE + box * 8192;
+        const uint8_t* base = x_s + s * STG + box * 8192;
         uint4 v[NORM_ROWS];
 #pragma unroll
         for (int rr = 0; rr < NORM_ROWS; ++rr) {
@@ -363,6 +373,7 @@ sketch_tc_kernel(const __grid_constant__ CUtensorMap tmap, SketchTCParams p) {
       }
     }
   }
+role_done:
   tc_fence_before();
   __syncthreads();
   cluster_sync();
@@ -376,17 +387,41 @@ sketch_tc_kernel(const __grid_constant__ CUtensorMap tmap, SketchTCParams p) {
 // panel[κ * ld + (t - t0)] = Π(κ, t) (bf16 bits) for κ < k, t in [t0, t0 + rows);
 // thread per (κ, 4-row group): one Philox call for the Gaussian stream
 // (DESIGN.md §3.2-3.3), 8 contiguous bytes written.
-__global__ void pi_panel_kmajor_kernel(int kind, uint64_t seed, int k, int64_t t0, int64_t rows,
-                                       int64_t ld, uint16_t* __restrict__ panel) {
-  const int64_t ng = (rows + 3) / 4;
+__global__ void pi_panel_kmajor_kernel(int kind, uint64_t seed, int k, int kpad, int64_t t0,
+                                       int64_t rows, int64_t ld, uint16_t* __restrict__ panel) {
+  // Rademacher: thread per (κ, 32-row word), one Philox call per 128 rows
+  // (the word of DESIGN.md §3.3), 64 bytes written; otherwise thread per
+  // (κ, 4-row group), one Philox call for the Gaussian stream, 8 bytes.
+  const int grp = (kind == PI_RADEMACHER && (t0 & 31) == 0) ? 32 : 4;
+  const int64_t ng = (rows + grp - 1) / grp;
   const uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < ng * k;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < ng * kpad;
        e += (int64_t)gridDim.x * blockDim.x) {
     const int kappa = (int)(e / ng);
     const int64_t g = e - (int64_t)kappa * ng;
-    const int64_t t = t0 + 4 * g;
+    const int64_t t = t0 + grp * g;
+    uint16_t* dst = panel + (int64_t)kappa * ld + grp * g;
+    if (grp == 32) {
+      uint32_t w32 = 0;
+      if (kappa < k) {
+        const uint64_t tg = (uint64_t)t >> 7;
+        const u32x4 w = philox4x32_10((uint32_t)tg, (uint32_t)kappa, (uint32_t)(tg >> 32), TAG_RADEMACHER, k0, k1);
+        const uint32_t wi = (uint32_t)((t >> 5) & 3);
+        w32 = wi == 0 ? w.x : wi == 1 ? w.y : wi == 2 ? w.z : w.w;
+      }
+      uint32_t o[16];
+#pragma unroll
+      for (int q = 0; q < 16; ++q)  // rows 2q (bit q), 2q+1 (bit 16+q)
+        o[q] = kappa < k ? (0x3F803F80u | ((w32 << (15 - q)) & 0x8000u) | ((w32 >> (16 + q)) << 31)) : 0u;
+      uint4* d4 = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) d4[q] = make_uint4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
+      continue;
+    }
     uint16_t z[4];
-    if (kind == PI_GAUSSIAN && (t & 3) == 0) {
+    if (kappa >= k) {
+      z[0] = z[1] = z[2] = z[3] = 0;
+    } else if (kind == PI_GAUSSIAN && (t & 3) == 0) {
       const uint64_t tq = (uint64_t)t >> 2;
       const u32x4 w = philox4x32_10((uint32_t)tq, (uint32_t)kappa, (uint32_t)(tq >> 32), TAG_GAUSSIAN, k0, k1);
       gauss_pair(w.x, w.y, z[0], z[1]);
@@ -395,7 +430,6 @@ __global__ void pi_panel_kmajor_kernel(int kind, uint64_t seed, int k, int64_t t
 #pragma unroll
       for (int j = 0; j < 4; ++j) z[j] = pi_bits(kind, seed, (uint32_t)kappa, (uint64_t)(t + j));
     }
-    uint16_t* dst = panel + (int64_t)kappa * ld + 4 * g;
     if ((ld & 3) == 0) {
       uint2 v;
       v.x = (uint32_t)z[0] | ((uint32_t)z[1] << 16);
@@ -408,11 +442,11 @@ __global__ void pi_panel_kmajor_kernel(int kind, uint64_t seed, int k, int64_t t
   }
 }
 
-cudaError_t launch_pi_panel_kmajor(int kind, uint64_t seed, int k, int64_t t0, int64_t rows, int64_t ld,
-                                   uint16_t* panel, cudaStream_t st) {
-  const int64_t tot = ((rows + 3) / 4) * k;
+cudaError_t launch_pi_panel_kmajor(int kind, uint64_t seed, int k, int kpad, int64_t t0, int64_t rows,
+                                   int64_t ld, uint16_t* panel, cudaStream_t st) {
+  const int64_t tot = ((rows + 3) / 4) * kpad;  // upper bound on threads needed
   const int blocks = (int)std::min<int64_t>((tot + 255) / 256, 148 * 16);
-  pi_panel_kmajor_kernel<<<blocks, 256, 0, st>>>(kind, seed, k, t0, rows, ld, panel);
+  pi_panel_kmajor_kernel<<<blocks, 256, 0, st>>>(kind, seed, k, kpad, t0, rows, ld, panel);
   return cudaGetLastError();
 }
 
@@ -436,26 +470,45 @@ int sketch_tc_ctas_per_tile() { return 2; }
 cudaError_t launch_sketch_tc(const void* X, int64_t ldx, SketchTCParams p, cudaStream_t st) {
   auto enc = get_encode_fn();
   if (!enc) return cudaErrorNotSupported;
-  CUtensorMap tmap;
-  cuuint64_t dims[2] = {(cuuint64_t)p.n, (cuuint64_t)p.rows};
-  cuuint64_t strides[1] = {(cuuint64_t)ldx * 2};
-  cuuint32_t box[2] = {64, 64};
-  cuuint32_t estr[2] = {1, 1};
-  CUresult r = enc(&tmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(X), dims, strides,
-                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(sketch_tc_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM);
+  CUtensorMap tmap, tmap_pi;
+  {
+    cuuint64_t dims[2] = {(cuuint64_t)p.n, (cuuint64_t)p.rows};
+    cuuint64_t strides[1] = {(cuuint64_t)ldx * 2};
+    cuuint32_t box[2] = {64, 64};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = enc(&tmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(X), dims, strides,
+                     box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
+  }
+  const bool panel = p.pi_panel != nullptr;
+  if (panel) {
+    // κ-major panel [k_tiles * 256][pi_ld]: box = 64 t (128 B, swizzled) x 128 κ
+    cuuint64_t dims[2] = {(cuuint64_t)p.pi_ld, (cuuint64_t)p.k_tiles * 256};
+    cuuint64_t strides[1] = {(cuuint64_t)p.pi_ld * 2};
+    cuuint32_t box[2] = {64, 128};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = enc(&tmap_pi, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<uint16_t*>(p.pi_panel),
+                     dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
+  } else {
+    tmap_pi = tmap;
+  }
+  static bool attr_set[2] = {false, false};
+  const int smem = panel ? P_SMEM : TC_SMEM;
+  if (!attr_set[panel]) {
+    cudaError_t e = panel ? cudaFuncSetAttribute(sketch_tc_kernel<true>,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, P_SMEM)
+                          : cudaFuncSetAttribute(sketch_tc_kernel<false>,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM);
     if (e != cudaSuccess) return e;
-    attr_set = true;
+    attr_set[panel] = true;
   }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(2u * (unsigned)(p.n_tiles * p.k_tiles * p.splits));
   cfg.blockDim = dim3(TC_THREADS);
-  cfg.dynamicSmemBytes = TC_SMEM;
+  cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -464,7 +517,8 @@ cudaError_t launch_sketch_tc(const void* X, int64_t ldx, SketchTCParams p, cudaS
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, sketch_tc_kernel, tmap, p);
+  return panel ? cudaLaunchKernelEx(&cfg, sketch_tc_kernel<true>, tmap, tmap_pi, p)
+               : cudaLaunchKernelEx(&cfg, sketch_tc_kernel<false>, tmap, tmap_pi, p);
 }
 
 }  // namespace smp

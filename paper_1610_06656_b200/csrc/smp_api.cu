@@ -41,6 +41,7 @@ struct smp_handle {
   int64_t planes_cap = 0;
   uint16_t* pi_panel = nullptr;  // K1 Gaussian Π panel (κ-major)
   int64_t pi_panel_cap = 0;
+  int64_t panel_row0 = -1, panel_ld = 0, panel_kpad = 0;  // rows the panel holds
   // finalized state
   float* fin_sk = nullptr;     // [ntot][k]
   double* fin_sknorm = nullptr;
@@ -117,11 +118,15 @@ bool is_pow2(int64_t x) { return x > 0 && (x & (x - 1)) == 0; }
 //    the 1e-5 tolerance, 3.6K updates (cfg1) gave < 4e-6 (R21);
 //  * occupancy: fill the 148 SMs with >= 95% of the last wave, fewest
 //    splits first (searched up to 2x the accuracy minimum).
-constexpr int K1_MAX_KB = 1024;  // 65,536 rows per accumulation chain
+//    With a Gaussian Π the (plane-split) products carry 12 significant bits
+//    and the chain is capped at 16,384 rows: 14.5K-row chains measured
+//    1.5e-6, 58K-row chains 4.3e-5 (cfg4, full size).
+constexpr int K1_MAX_KB = 1024;        // 65,536 rows per accumulation chain (±1 Π)
+constexpr int K1_MAX_KB_GAUSS = 256;   // 16,384 rows (Gaussian Π)
 
-int choose_splits(int tiles, int kb_total) {
+int choose_splits(int tiles, int kb_total, int max_kb) {
   const int sms = 148;
-  const int smin = std::max(1, (kb_total + K1_MAX_KB - 1) / K1_MAX_KB);
+  const int smin = std::max(1, (kb_total + max_kb - 1) / max_kb);
   int best_s = smin;
   double best_eff = -1.0;
   const int smax = std::max(smin, std::min(kb_total, std::max(64, 2 * smin)));
@@ -148,7 +153,8 @@ smp_status sketch_dense_bf16(smp_handle* h, int64_t row0, int64_t rows, const vo
   p.n_tiles = (int32_t)((ncols + 255) / 256);
   p.k_tiles = (k + 255) / 256;
   p.kb_total = (int32_t)((rows + 63) / 64);
-  p.splits = choose_splits(2 * p.n_tiles * p.k_tiles, p.kb_total);  // CTA pairs
+  p.splits = choose_splits(2 * p.n_tiles * p.k_tiles, p.kb_total,
+                           h->d.pi_kind == SMP_PI_GAUSSIAN ? K1_MAX_KB_GAUSS : K1_MAX_KB);
   p.kind = h->d.pi_kind;
   p.do_norms = do_norms ? 1 : 0;
   { const char* dbg = getenv("SMP_K1_DEBUG"); p.debug = dbg ? atoi(dbg) : 0; }
@@ -159,14 +165,27 @@ smp_status sketch_dense_bf16(smp_handle* h, int64_t row0, int64_t rows, const vo
   p.pnorm = h->pnorm;
   p.pi_panel = nullptr;
   p.pi_ld = 0;
-  if (p.kind == SMP_PI_GAUSSIAN) {
-    // Gaussian Π once per block into an L2-resident κ-major panel (K1 reads it
-    // instead of regenerating it for every column tile)
+  static const int panel_mode = [] {
+    const char* e = getenv("SMP_K1_PANEL");  // tuning switch: 1 = panel for every Π kind
+    return e ? atoi(e) : 0;
+  }();
+  if (p.kind == SMP_PI_GAUSSIAN || panel_mode == 1) {
+    // Π once per block into a κ-major panel that K1 streams by TMA (Gaussian:
+    // ~33 ALU ops per entry would otherwise be repeated for every column
+    // tile).  A and B blocks over the same rows reuse the panel.
     const int64_t ld = (int64_t)p.kb_total * 64;
     const int64_t kpad = (int64_t)p.k_tiles * 256;
-    CK(h, ensure(h->pi_panel, h->pi_panel_cap, kpad * ld), "alloc pi panel");
-    CK(h, launch_pi_panel_kmajor(p.kind, p.seed, k, row0, ld, ld, h->pi_panel, h->st), "pi panel");
-    h->launches += 1;
+    const bool cached = h->pi_panel && h->panel_row0 == row0 && h->panel_ld == ld &&
+                        h->panel_kpad == kpad;
+    if (!cached) {
+      CK(h, ensure(h->pi_panel, h->pi_panel_cap, kpad * ld), "alloc pi panel");
+      CK(h, launch_pi_panel_kmajor(p.kind, p.seed, k, (int)kpad, row0, ld, ld, h->pi_panel, h->st),
+         "pi panel");
+      h->launches += 1;
+      h->panel_row0 = row0;
+      h->panel_ld = ld;
+      h->panel_kpad = kpad;
+    }
     p.pi_panel = h->pi_panel;
     p.pi_ld = ld;
   }
@@ -205,7 +224,7 @@ smp_status sketch_dense_split(smp_handle* h, int64_t row0, int64_t rows, const v
   const int mode = x_bf16 ? 2 : (gauss ? 4 : 3);
   const int np = x_bf16 ? 2 : 3;
   const int64_t ldp = ((np * n + 7) / 8) * 8;
-  const int64_t chunk = std::max<int64_t>(64, std::min<int64_t>(rows, (int64_t)(512ll << 20) / (ldp * 2)));
+  const int64_t chunk = std::max<int64_t>(64, std::min<int64_t>(rows, (int64_t)(2048ll << 20) / (ldp * 2)));
   const int seg_rows = 256;
   CK(h, ensure(h->planes, h->planes_cap, ((chunk + 63) / 64) * 64 * ldp), "alloc planes");
   const int64_t es = x_bf16 ? 2 : 4;

@@ -261,6 +261,16 @@ __device__ __forceinline__ void tc_mma2_ts(uint32_t d_tmem, uint32_t a_tmem, uin
       "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
       "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate));
 }
+// D[tmem] (+)= A[smem] * B[smem] across the CTA pair (M = 256; each CTA
+// supplies its 128 rows of A and half of B's N columns), kind::f16
+__device__ __forceinline__ void tc_mma2_ss(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
+                                           uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
 // commit all prior MMAs of this thread; arrive on the barrier at the same
 // offset in every CTA of cta_mask
 __device__ __forceinline__ void tc_commit2(uint64_t* bar, uint16_t cta_mask) {

@@ -25,8 +25,8 @@ struct SketchTCParams {
   int64_t pi_ld;             // multiple of 64 rows, >= kb_total * 64
 };
 // Π(κ, t) for t in [t0, t0 + rows) into panel[κ * ld + t - t0] (bf16 bits; rows padded by the caller)
-cudaError_t launch_pi_panel_kmajor(int kind, uint64_t seed, int k, int64_t t0, int64_t rows, int64_t ld,
-                                   uint16_t* panel, cudaStream_t st);
+cudaError_t launch_pi_panel_kmajor(int kind, uint64_t seed, int k, int kpad, int64_t t0, int64_t rows,
+                                   int64_t ld, uint16_t* panel, cudaStream_t st);
 cudaError_t launch_sketch_tc(const void* X, int64_t ldx, SketchTCParams p, cudaStream_t st);
 int sketch_tc_smem_bytes();
 
@@ -61,6 +61,9 @@ struct CsrWorkspace {
   int64_t ent_cap_ki = 0, ent_cap_ko = 0, ent_cap_vi = 0, ent_cap_vo = 0;
   uint8_t* cub_tmp = nullptr;
   int64_t cub_cap = 0;
+  uint32_t* hist = nullptr;       // counting sort: [ntot][CTAs] counts and offsets
+  uint32_t* offs = nullptr;
+  int64_t hist_cap = 0, offs_cap = 0;
   int64_t* bounds_d = nullptr;
   int64_t bounds_cap = 0;
   int64_t* bounds_h = nullptr;    // pinned

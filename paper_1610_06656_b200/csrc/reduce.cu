@@ -9,7 +9,8 @@ namespace smp {
 // ---------------------------------------------------------------- K2
 template <int VEC>
 __global__ void reduce_sketch_kernel(const float* __restrict__ part, int splits, int planes,
-                                     int64_t n, int k, float* __restrict__ acc) {
+                                     int64_t n, int k, float* __restrict__ acc,
+                                     const int32_t* __restrict__ map) {
   const int64_t total = n * (int64_t)k / VEC;
   const int64_t part_stride = (int64_t)planes * n * k;  // floats per split
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < total;
@@ -29,46 +30,58 @@ __global__ void reduce_sketch_kernel(const float* __restrict__ part, int splits,
         }
       }
     }
+    // output column: c, or map[c] (scattered head columns of the CSR path)
+    const int64_t c = e / k;
+    const int64_t eo = map ? (int64_t)map[c] * k + (e - c * k) : e;
     if constexpr (VEC == 4) {
-      float4* dst = reinterpret_cast<float4*>(acc + e);
+      float4* dst = reinterpret_cast<float4*>(acc + eo);
       float4 a = *dst;
       a.x += s[0]; a.y += s[1]; a.z += s[2]; a.w += s[3];
       *dst = a;
     } else {
-      acc[e] += s[0];
+      acc[eo] += s[0];
     }
   }
 }
 
 cudaError_t launch_reduce_sketch(const float* part, int splits, int planes, int64_t n, int k,
-                                 float* acc, cudaStream_t st) {
+                                 float* acc, cudaStream_t st, const int32_t* map) {
   const int threads = 256;
   if (k % 4 == 0) {
     int64_t tot = n * k / 4;
     int blocks = (int)std::min<int64_t>((tot + threads - 1) / threads, 148 * 16);
-    reduce_sketch_kernel<4><<<blocks, threads, 0, st>>>(part, splits, planes, n, k, acc);
+    reduce_sketch_kernel<4><<<blocks, threads, 0, st>>>(part, splits, planes, n, k, acc, map);
   } else {
     int64_t tot = n * k;
     int blocks = (int)std::min<int64_t>((tot + threads - 1) / threads, 148 * 16);
-    reduce_sketch_kernel<1><<<blocks, threads, 0, st>>>(part, splits, planes, n, k, acc);
+    reduce_sketch_kernel<1><<<blocks, threads, 0, st>>>(part, splits, planes, n, k, acc, map);
   }
   return cudaGetLastError();
 }
 
 __global__ void reduce_norms_kernel(const double* __restrict__ pnorm, int slots, int64_t n,
-                                    double* __restrict__ nacc) {
+                                    double* __restrict__ nacc, const int32_t* __restrict__ map) {
   for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < n;
        c += (int64_t)gridDim.x * blockDim.x) {
+    // fixed (sequential) order; 8 independent loads in flight
     double s = 0.0;
-    for (int q = 0; q < slots; ++q) s += pnorm[(int64_t)q * n + c];
-    nacc[c] += s;
+    int q = 0;
+    for (; q + 8 <= slots; q += 8) {
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = pnorm[(int64_t)(q + u) * n + c];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) s += v[u];
+    }
+    for (; q < slots; ++q) s += pnorm[(int64_t)q * n + c];
+    nacc[map ? (int64_t)map[c] : c] += s;
   }
 }
 
 cudaError_t launch_reduce_norms(const double* pnorm, int slots, int64_t n, double* nacc,
-                                cudaStream_t st) {
+                                cudaStream_t st, const int32_t* map) {
   int blocks = (int)std::min<int64_t>((n + 255) / 256, 1024);
-  reduce_norms_kernel<<<blocks, 256, 0, st>>>(pnorm, slots, n, nacc);
+  reduce_norms_kernel<<<blocks, 256, 0, st>>>(pnorm, slots, n, nacc, map);
   return cudaGetLastError();
 }
 
@@ -127,11 +140,72 @@ __global__ void split_planes_kernel(const void* __restrict__ Xv, int x_bf16, int
   pnorm[seg * n + c] = s2;
 }
 
+// Vectorised variant: thread per 8 consecutive columns (two float4 or one
+// uint4 load, one 16-byte store per plane), same arithmetic per element.
+__global__ void split_planes_v8_kernel(const void* __restrict__ Xv, int x_bf16, int64_t ldx, int64_t rows,
+                                       int64_t n, int mode, uint16_t* __restrict__ planes, int64_t ldp,
+                                       double* __restrict__ pnorm, int seg_rows) {
+  const int64_t c0 = 8 * (blockIdx.x * (int64_t)blockDim.x + threadIdx.x);
+  const int64_t seg = blockIdx.y;
+  if (c0 >= n) return;
+  const int64_t r0 = seg * seg_rows;
+  const int64_t r1 = min(rows, r0 + seg_rows);
+  int bits[3];
+  int np;
+  bool exact = true;
+  if (mode == 3) { np = 3; bits[0] = 8; bits[1] = 8; bits[2] = 8; }
+  else if (mode == 4) { np = 3; bits[0] = 4; bits[1] = 8; bits[2] = 8; exact = false; }
+  else { np = 2; bits[0] = 4; bits[1] = 8; bits[2] = 0; }
+  double s2[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) s2[j] = 0.0;
+  for (int64_t t = r0; t < r1; ++t) {
+    float x[8];
+    if (x_bf16) {
+      const uint4 v = *reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(Xv) + t * ldx + c0);
+      const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) { x[2 * j] = __uint_as_float(w[j] << 16); x[2 * j + 1] = __uint_as_float(w[j] & 0xFFFF0000u); }
+    } else {
+      const float4* src = reinterpret_cast<const float4*>(static_cast<const float*>(Xv) + t * ldx + c0);
+      const float4 a = src[0], b = src[1];
+      x[0] = a.x; x[1] = a.y; x[2] = a.z; x[3] = a.w; x[4] = b.x; x[5] = b.y; x[6] = b.z; x[7] = b.w;
+    }
+    uint16_t* row = planes + t * ldp + c0;
+    float r[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) { r[j] = x[j]; s2[j] = fma((double)x[j], (double)x[j], s2[j]); }
+    for (int q = 0; q < np; ++q) {
+      uint32_t o[4];
+#pragma unroll
+      for (int j = 0; j < 8; j += 2) {
+        const float pa = (q == np - 1 && exact) ? r[j] : round_sig(r[j], bits[q]);
+        const float pb = (q == np - 1 && exact) ? r[j + 1] : round_sig(r[j + 1], bits[q]);
+        o[j / 2] = (__float_as_uint(pa) >> 16) | (__float_as_uint(pb) & 0xFFFF0000u);
+        r[j] = __fsub_rn(r[j], pa);
+        r[j + 1] = __fsub_rn(r[j + 1], pb);
+      }
+      *reinterpret_cast<uint4*>(row + q * n) = make_uint4(o[0], o[1], o[2], o[3]);
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < 8; ++j) pnorm[seg * n + c0 + j] = s2[j];
+}
+
 cudaError_t launch_split_planes(const void* X, int x_bf16, int64_t ldx, int64_t rows, int64_t n,
                                 int mode, uint16_t* planes, int64_t ldp, double* pnorm, int seg_rows,
                                 cudaStream_t st) {
-  dim3 grid((unsigned)((n + 127) / 128), (unsigned)((rows + seg_rows - 1) / seg_rows));
-  split_planes_kernel<<<grid, 128, 0, st>>>(X, x_bf16, ldx, rows, n, mode, planes, ldp, pnorm, seg_rows);
+  const int es = x_bf16 ? 2 : 4;
+  const bool vec = (n % 8 == 0) && (ldx % 8 == 0) && (ldp % 8 == 0) &&
+                   (reinterpret_cast<uintptr_t>(X) % 16 == 0);
+  (void)es;
+  if (vec) {
+    dim3 grid((unsigned)((n / 8 + 127) / 128), (unsigned)((rows + seg_rows - 1) / seg_rows));
+    split_planes_v8_kernel<<<grid, 128, 0, st>>>(X, x_bf16, ldx, rows, n, mode, planes, ldp, pnorm, seg_rows);
+  } else {
+    dim3 grid((unsigned)((n + 127) / 128), (unsigned)((rows + seg_rows - 1) / seg_rows));
+    split_planes_kernel<<<grid, 128, 0, st>>>(X, x_bf16, ldx, rows, n, mode, planes, ldp, pnorm, seg_rows);
+  }
   return cudaGetLastError();
 }
 

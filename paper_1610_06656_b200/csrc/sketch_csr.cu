@@ -150,7 +150,9 @@ template <int KV>
 __global__ void __launch_bounds__(256)
 csr_accumulate_kernel(const uint32_t* __restrict__ keys, const float* __restrict__ vals, int64_t n,
                       const uint16_t* __restrict__ pi, int kp, int k, int tbits,
-                      float* __restrict__ acc_sk, double* __restrict__ acc_nrm, int do_norms) {
+                      float* __restrict__ acc_sk, double* __restrict__ acc_nrm, int do_norms,
+                      const uint32_t* __restrict__ n_dev) {
+  if (n_dev) n = min(n, (int64_t)*n_dev);  // tail entries actually scattered
   const int lane = threadIdx.x & 31;
   const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
   const uint32_t tmask = (1u << tbits) - 1u;
@@ -218,6 +220,19 @@ csr_accumulate_kernel(const uint32_t* __restrict__ keys, const float* __restrict
   }
 }
 
+// ---------------------------------------------------------------- head/tail split
+// A nonzero goes to the tensor-core head path iff its column is a head column
+// (lut >= 0) and its value has at most 4 significant bits (small integer
+// counts): Gaussian Π (8 bits) times such a value is a 12-bit product, which
+// tcgen05 accumulates exactly (R21).  Everything else is the tail.
+__device__ __forceinline__ bool is_4bit(float v) {
+  const uint32_t u = __float_as_uint(v);
+  return ((u & 0x7F800000u) != 0x7F800000u) && ((u & 0x000FFFFFu) == 0u);
+}
+__device__ __forceinline__ bool is_head(const int32_t* __restrict__ lut, uint32_t cg, float v) {
+  return lut != nullptr && lut[cg] >= 0 && is_4bit(v);
+}
+
 // ---------------------------------------------------------------- K3c counting sort
 // CTA b owns panel rows [b·rows/G, (b+1)·rows/G) of both matrices.
 __device__ __forceinline__ void cta_rows(int rows, int& r0, int& r1) {
@@ -231,9 +246,11 @@ __device__ __forceinline__ void cta_rows(int rows, int& r0, int& r1) {
 constexpr int CSR_T_THREADS = 1024;
 
 __global__ void __launch_bounds__(CSR_T_THREADS)
-csr_hist_kernel(const int64_t* __restrict__ arp, const int32_t* __restrict__ acol, int64_t a_n,
-                const int64_t* __restrict__ brp, const int32_t* __restrict__ bcol, int64_t b_n,
-                int64_t p0, int rows, int ntot, uint32_t* __restrict__ histT) {
+csr_hist_kernel(const int64_t* __restrict__ arp, const int32_t* __restrict__ acol,
+                const float* __restrict__ aval, int64_t a_n, const int64_t* __restrict__ brp,
+                const int32_t* __restrict__ bcol, const float* __restrict__ bval, int64_t b_n,
+                int64_t p0, int rows, int ntot, const int32_t* __restrict__ lut,
+                uint32_t* __restrict__ histT) {
   extern __shared__ uint32_t hist[];
   for (int c = threadIdx.x; c < ntot; c += blockDim.x) hist[c] = 0u;
   __syncthreads();
@@ -244,6 +261,7 @@ csr_hist_kernel(const int64_t* __restrict__ arp, const int32_t* __restrict__ aco
     const int64_t* rp = mat == 0 ? arp : brp;
     if (!rp) continue;
     const int32_t* col = mat == 0 ? acol : bcol;
+    const float* val = mat == 0 ? aval : bval;
     const int64_t ncols = mat == 0 ? a_n : b_n;
     const uint32_t cofs = mat == 0 ? 0u : (uint32_t)a_n;
     const int64_t base = rp[0];
@@ -251,13 +269,17 @@ csr_hist_kernel(const int64_t* __restrict__ arp, const int32_t* __restrict__ aco
       const int64_t e0 = rp[p0 + r] - base, e1 = rp[p0 + r + 1] - base;
       for (int64_t eb = e0 + lane; eb < e1; eb += 128) {
         int32_t c[4];
+        float v[4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) c[u] = eb + 32 * u < e1 ? col[eb + 32 * u] : -1;
+        for (int u = 0; u < 4; ++u) {
+          c[u] = eb + 32 * u < e1 ? col[eb + 32 * u] : -1;
+          v[u] = (lut && eb + 32 * u < e1) ? val[eb + 32 * u] : 0.f;
+        }
 #pragma unroll
         for (int u = 0; u < 4; ++u)
           if (eb + 32 * u < e1) {
             const uint32_t cg = (uint32_t)(c[u] < 0 || c[u] >= ncols ? 0 : c[u]) + cofs;
-            atomicAdd(&hist[cg], 1u);
+            if (!is_head(lut, cg, v[u])) atomicAdd(&hist[cg], 1u);
           }
       }
     }
@@ -271,8 +293,9 @@ __global__ void __launch_bounds__(CSR_T_THREADS)
 csr_scatter_kernel(const int64_t* __restrict__ arp, const int32_t* __restrict__ acol,
                    const float* __restrict__ aval, int64_t a_n, const int64_t* __restrict__ brp,
                    const int32_t* __restrict__ bcol, const float* __restrict__ bval, int64_t b_n,
-                   int64_t p0, int rows, int ntot, int tbits, const uint32_t* __restrict__ offsT,
-                   uint32_t* __restrict__ keys, float* __restrict__ vals, int* __restrict__ status) {
+                   int64_t p0, int rows, int ntot, int tbits, const int32_t* __restrict__ lut,
+                   const uint32_t* __restrict__ offsT, uint32_t* __restrict__ keys,
+                   float* __restrict__ vals, int* __restrict__ status) {
   extern __shared__ uint32_t cur[];
   for (int c = threadIdx.x; c < ntot; c += blockDim.x) cur[c] = offsT[(int64_t)c * gridDim.x + blockIdx.x];
   __syncthreads();
@@ -303,6 +326,7 @@ csr_scatter_kernel(const int64_t* __restrict__ arp, const int32_t* __restrict__ 
           if (eb + 32 * u < e1) {
             if (c[u] < 0 || c[u] >= ncols) atomicOr(status, 2);  // out-of-range column
             const uint32_t cg = (uint32_t)(c[u] < 0 || c[u] >= ncols ? 0 : c[u]) + cofs;
+            if (is_head(lut, cg, v[u])) continue;  // densified for the tensor cores
             const uint32_t pos = atomicAdd(&cur[cg], 1u);
             keys[pos] = (cg << tbits) | (uint32_t)r;
             vals[pos] = v[u];
@@ -312,18 +336,13 @@ csr_scatter_kernel(const int64_t* __restrict__ arp, const int32_t* __restrict__ 
   }
 }
 
+__global__ void csr_total_kernel(const uint32_t* __restrict__ hist, const uint32_t* __restrict__ offs,
+                                 int64_t nh, uint32_t* __restrict__ total) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) *total = nh > 0 ? offs[nh - 1] + hist[nh - 1] : 0u;
+}
+
 constexpr int CSR_HIST_CTAS = 148;
 constexpr int CSR_HIST_MAX_COLS = 53248;  // 208 KB of SMEM counters
-
-// ---------------------------------------------------------------- driver
-__global__ void csr_bounds_kernel(const int64_t* __restrict__ arp, const int64_t* __restrict__ brp,
-                                  int rows, int rp, int npan, int64_t* __restrict__ out) {
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i <= npan; i += gridDim.x * blockDim.x) {
-    const int r = i < npan ? i * rp : rows;
-    out[i] = arp[r] - arp[0];
-    out[npan + 1 + i] = brp ? brp[r] - brp[0] : 0;
-  }
-}
 
 template <class T>
 static cudaError_t grow(T*& p, int64_t& cap, int64_t need) {
@@ -342,9 +361,156 @@ static cudaError_t grow(T*& p, int64_t& cap, int64_t need) {
     if (e_ != cudaSuccess) return e_; \
   } while (0)
 
+// ---------------------------------------------------------------- tensor-core head
+// column counts over the block (global column index: A then B)
+__global__ void __launch_bounds__(CSR_T_THREADS)
+csr_colcount_kernel(const int64_t* __restrict__ arp, const int32_t* __restrict__ acol, int64_t a_n,
+                    const int64_t* __restrict__ brp, const int32_t* __restrict__ bcol, int64_t b_n,
+                    int rows, int ntot, uint32_t* __restrict__ cnt) {
+  extern __shared__ uint32_t hist[];
+  for (int c = threadIdx.x; c < ntot; c += blockDim.x) hist[c] = 0u;
+  __syncthreads();
+  int r0, r1;
+  cta_rows(rows, r0, r1);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int mat = 0; mat < 2; ++mat) {
+    const int64_t* rp = mat == 0 ? arp : brp;
+    if (!rp) continue;
+    const int32_t* col = mat == 0 ? acol : bcol;
+    const int64_t ncols = mat == 0 ? a_n : b_n;
+    const uint32_t cofs = mat == 0 ? 0u : (uint32_t)a_n;
+    const int64_t base = rp[0];
+    for (int r = r0 + warp; r < r1; r += nw) {
+      const int64_t e0 = rp[r] - base, e1 = rp[r + 1] - base;
+      for (int64_t eb = e0 + lane; eb < e1; eb += 128) {
+        int32_t c[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) c[u] = eb + 32 * u < e1 ? col[eb + 32 * u] : -1;
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (eb + 32 * u < e1 && c[u] >= 0 && c[u] < ncols) atomicAdd(&hist[(uint32_t)c[u] + cofs], 1u);
+      }
+    }
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < ntot; c += blockDim.x)
+    if (hist[c]) atomicAdd(&cnt[c], hist[c]);
+}
+
+__global__ void csr_head_flag_kernel(const uint32_t* __restrict__ cnt, int ntot, uint32_t thr,
+                                     uint32_t* __restrict__ flag) {
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < ntot; c += gridDim.x * blockDim.x)
+    flag[c] = cnt[c] >= thr ? 1u : 0u;
+}
+
+// slot = exclusive scan of the flags (column order: deterministic)
+__global__ void csr_head_map_kernel(const uint32_t* __restrict__ flag, const uint32_t* __restrict__ scan,
+                                    int ntot, int32_t* __restrict__ lut, int32_t* __restrict__ map,
+                                    uint32_t* __restrict__ total) {
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < ntot; c += gridDim.x * blockDim.x) {
+    const int32_t slot = flag[c] ? (int32_t)scan[c] : -1;
+    lut[c] = slot;
+    if (slot >= 0) map[slot] = c;
+    if (c == ntot - 1) *total = scan[c] + flag[c];
+  }
+}
+
+// X_head[t - r0][slot] = bf16(v) for head nonzeros of rows [r0, r0 + rows)
+__global__ void __launch_bounds__(256)
+csr_densify_kernel(const int64_t* __restrict__ arp, const int32_t* __restrict__ acol,
+                   const float* __restrict__ aval, int64_t a_n, const int64_t* __restrict__ brp,
+                   const int32_t* __restrict__ bcol, const float* __restrict__ bval, int64_t b_n,
+                   int64_t r0, int rows, const int32_t* __restrict__ lut, int64_t ldh,
+                   uint16_t* __restrict__ xh) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t task = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); task < 2 * (int64_t)rows;
+       task += nw) {
+    const int mat = (int)(task & 1);
+    const int64_t r = task >> 1;
+    const int64_t* rp = mat == 0 ? arp : brp;
+    if (!rp) continue;
+    const int32_t* col = mat == 0 ? acol : bcol;
+    const float* val = mat == 0 ? aval : bval;
+    const int64_t ncols = mat == 0 ? a_n : b_n;
+    const uint32_t cofs = mat == 0 ? 0u : (uint32_t)a_n;
+    const int64_t base = rp[0];
+    const int64_t e0 = rp[r0 + r] - base, e1 = rp[r0 + r + 1] - base;
+    for (int64_t e = e0 + lane; e < e1; e += 32) {
+      const int32_t c = col[e];
+      if (c < 0 || c >= ncols) continue;
+      const float v = val[e];
+      const uint32_t cg = (uint32_t)c + cofs;
+      if (is_head(lut, cg, v)) xh[r * ldh + lut[cg]] = (uint16_t)(__float_as_uint(v) >> 16);
+    }
+  }
+}
+
+cudaError_t csr_select_head(CsrWorkspace& w, const int64_t* a_rowptr, const int32_t* a_col, int64_t a_n,
+                            const int64_t* b_rowptr, const int32_t* b_col, int64_t b_n, int64_t rows,
+                            double density, int* n_head, cudaStream_t st) {
+  *n_head = 0;
+  const int64_t ntot = a_n + (b_rowptr ? b_n : 0);
+  if (ntot > CSR_HIST_MAX_COLS || rows <= 0 || rows >= (1ll << 31)) return cudaSuccess;
+  CSR_TRY(grow(w.head_cnt, w.head_cnt_cap, ntot));
+  CSR_TRY(grow(w.head_flag, w.head_flag_cap, 2 * ntot));
+  CSR_TRY(grow(w.head_lut, w.head_lut_cap, ntot));
+  CSR_TRY(grow(w.head_map, w.head_map_cap, ntot));
+  CSR_TRY(cudaMemsetAsync(w.head_cnt, 0, ntot * 4, st));
+  static bool attr = false;
+  if (!attr) {
+    CSR_TRY(cudaFuncSetAttribute(csr_colcount_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 CSR_HIST_MAX_COLS * 4));
+    attr = true;
+  }
+  csr_colcount_kernel<<<148, CSR_T_THREADS, ntot * 4, st>>>(a_rowptr, a_col, a_n, b_rowptr, b_col, b_n,
+                                                           (int)rows, (int)ntot, w.head_cnt);
+  const uint32_t thr = (uint32_t)std::max(1.0, std::ceil(density * (double)rows));
+  const int blocks = (int)((ntot + 255) / 256);
+  csr_head_flag_kernel<<<blocks, 256, 0, st>>>(w.head_cnt, (int)ntot, thr, w.head_flag);
+  size_t need = 0;
+  CSR_TRY(cub::DeviceScan::ExclusiveSum(nullptr, need, w.head_flag, w.head_flag + ntot, (int)ntot, st));
+  CSR_TRY(grow(w.head_tmp, w.head_tmp_cap, (int64_t)need));
+  size_t tmp = (size_t)w.head_tmp_cap;
+  CSR_TRY(cub::DeviceScan::ExclusiveSum(w.head_tmp, tmp, w.head_flag, w.head_flag + ntot, (int)ntot, st));
+  CSR_TRY(grow(w.ne_dev, w.ne_cap, 2));
+  csr_head_map_kernel<<<blocks, 256, 0, st>>>(w.head_flag, w.head_flag + ntot, (int)ntot, w.head_lut,
+                                              w.head_map, w.ne_dev + 1);
+  if (!w.head_h) CSR_TRY(cudaMallocHost(&w.head_h, 8));
+  CSR_TRY(cudaMemcpyAsync(w.head_h, w.ne_dev + 1, 4, cudaMemcpyDeviceToHost, st));
+  CSR_TRY(cudaStreamSynchronize(st));
+  *n_head = (int)*reinterpret_cast<uint32_t*>(w.head_h);
+  w.launches += 5;
+  return cudaGetLastError();
+}
+
+cudaError_t csr_densify(CsrWorkspace& w, const int64_t* a_rowptr, const int32_t* a_col, const float* a_val,
+                        int64_t a_n, const int64_t* b_rowptr, const int32_t* b_col, const float* b_val,
+                        int64_t b_n, int64_t r0, int64_t rows, int64_t ldh, uint16_t* xh, cudaStream_t st) {
+  CSR_TRY(cudaMemsetAsync(xh, 0, (size_t)(((rows + 63) / 64) * 64) * ldh * 2, st));
+  const int blocks = (int)std::min<int64_t>((2 * rows + 7) / 8, 148 * 32);
+  csr_densify_kernel<<<blocks, 256, 0, st>>>(a_rowptr, a_col, a_val, a_n, b_rowptr, b_col, b_val, b_n, r0,
+                                             (int)rows, w.head_lut, ldh, xh);
+  w.launches += 1;
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- driver
+__global__ void csr_bounds_kernel(const int64_t* __restrict__ arp, const int64_t* __restrict__ brp,
+                                  int rows, int rp, int npan, int64_t* __restrict__ out) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i <= npan; i += gridDim.x * blockDim.x) {
+    const int r = i < npan ? i * rp : rows;
+    out[i] = arp[r] - arp[0];
+    out[npan + 1 + i] = brp ? brp[r] - brp[0] : 0;
+  }
+}
+
 void csr_workspace_free(CsrWorkspace& w) {
   cudaFree(w.pi); cudaFree(w.keys_in); cudaFree(w.keys_out); cudaFree(w.vals_in);
   cudaFree(w.vals_out); cudaFree(w.cub_tmp); cudaFree(w.bounds_d); cudaFree(w.hist); cudaFree(w.offs);
+  cudaFree(w.ne_dev); cudaFree(w.head_lut); cudaFree(w.head_map); cudaFree(w.head_cnt); cudaFree(w.head_flag);
+  cudaFree(w.xhead); cudaFree(w.head_tmp);
+  if (w.head_h) cudaFreeHost(w.head_h);
   if (w.bounds_h) cudaFreeHost(w.bounds_h);
   w = CsrWorkspace{};
 }
@@ -359,7 +525,7 @@ cudaError_t launch_sketch_csr(CsrWorkspace& w, int kind, uint64_t seed, int k, i
                               int64_t rows, const int64_t* a_rowptr, const int32_t* a_col,
                               const float* a_val, int64_t a_n, const int64_t* b_rowptr,
                               const int32_t* b_col, const float* b_val, int64_t b_n, float* acc_sk,
-                              double* acc_nrm, int* status, cudaStream_t st) {
+                              double* acc_nrm, int* status, cudaStream_t st, const int32_t* head_lut) {
   if (rows <= 0) return cudaSuccess;
   const int64_t ntot = a_n + (b_rowptr ? b_n : 0);
   const int cbits = bits_for(ntot - 1 > 0 ? ntot - 1 : 1);
@@ -388,6 +554,7 @@ cudaError_t launch_sketch_csr(CsrWorkspace& w, int kind, uint64_t seed, int k, i
   CSR_TRY(grow(w.pi, w.pi_cap, (int64_t)rp * kp));
   const int end_bit = tbits + cbits;
   const bool counting = ntot <= CSR_HIST_MAX_COLS;
+  if (!counting) head_lut = nullptr;  // (the caller only selects heads when counting)
   if (!counting) {
     CSR_TRY(grow(w.keys_in, w.ent_cap_ki, max_ent));
     CSR_TRY(grow(w.vals_in, w.ent_cap_vi, max_ent));
@@ -399,6 +566,7 @@ cudaError_t launch_sketch_csr(CsrWorkspace& w, int kind, uint64_t seed, int k, i
     const int64_t nh = ntot * (int64_t)CSR_HIST_CTAS;
     CSR_TRY(grow(w.hist, w.hist_cap, nh));
     CSR_TRY(grow(w.offs, w.offs_cap, nh));
+    CSR_TRY(grow(w.ne_dev, w.ne_cap, 1));
     CSR_TRY(cub::DeviceScan::ExclusiveSum(nullptr, need, w.hist, w.offs, (int)nh, st));
     static bool attr = false;
     if (!attr) {
@@ -435,14 +603,17 @@ cudaError_t launch_sketch_csr(CsrWorkspace& w, int kind, uint64_t seed, int k, i
     if (ne == 0) continue;
     if (counting) {
       const size_t sm = (size_t)ntot * 4;
-      csr_hist_kernel<<<CSR_HIST_CTAS, CSR_T_THREADS, sm, st>>>(a_rowptr, a_col, a_n, b_rowptr, b_col, b_n, p0,
-                                                     prow, (int)ntot, w.hist);
+      csr_hist_kernel<<<CSR_HIST_CTAS, CSR_T_THREADS, sm, st>>>(a_rowptr, a_col, a_val, a_n, b_rowptr,
+                                                                b_col, b_val, b_n, p0, prow, (int)ntot,
+                                                                head_lut, w.hist);
       size_t tmp = (size_t)w.cub_cap;
       CSR_TRY(cub::DeviceScan::ExclusiveSum(w.cub_tmp, tmp, w.hist, w.offs,
                                             (int)(ntot * (int64_t)CSR_HIST_CTAS), st));
-      csr_scatter_kernel<<<CSR_HIST_CTAS, CSR_T_THREADS, sm, st>>>(a_rowptr, a_col, a_val, a_n, b_rowptr, b_col,
-                                                        b_val, b_n, p0, prow, (int)ntot, tbits, w.offs,
-                                                        w.keys_out, w.vals_out, status);
+      csr_scatter_kernel<<<CSR_HIST_CTAS, CSR_T_THREADS, sm, st>>>(a_rowptr, a_col, a_val, a_n, b_rowptr,
+                                                                   b_col, b_val, b_n, p0, prow, (int)ntot,
+                                                                   tbits, head_lut, w.offs, w.keys_out,
+                                                                   w.vals_out, status);
+      csr_total_kernel<<<1, 32, 0, st>>>(w.hist, w.offs, ntot * (int64_t)CSR_HIST_CTAS, w.ne_dev);
     } else {
       const int kb_blocks = (int)std::min<int64_t>((prow + 7) / 8, 148 * 16);
       // A: entries ab[p] .. ab[p+1] (relative to a_rowptr[0]) -> keys[0 .. na)
@@ -468,11 +639,11 @@ cudaError_t launch_sketch_csr(CsrWorkspace& w, int kind, uint64_t seed, int k, i
       CSR_TRY(cudaEventRecord((*w.ev_pool)[*w.ev_used], st));
     }
     switch (kv) {
-      case 1: csr_accumulate_kernel<1><<<ablocks, 256, 0, st>>>(w.keys_out, w.vals_out, ne, w.pi, kp, k, tbits, acc_sk, acc_nrm, 1); break;
-      case 2: csr_accumulate_kernel<2><<<ablocks, 256, 0, st>>>(w.keys_out, w.vals_out, ne, w.pi, kp, k, tbits, acc_sk, acc_nrm, 1); break;
-      case 3: case 4: csr_accumulate_kernel<4><<<ablocks, 256, 0, st>>>(w.keys_out, w.vals_out, ne, w.pi, kp, k, tbits, acc_sk, acc_nrm, 1); break;
-      case 5: case 6: case 7: case 8: csr_accumulate_kernel<8><<<ablocks, 256, 0, st>>>(w.keys_out, w.vals_out, ne, w.pi, kp, k, tbits, acc_sk, acc_nrm, 1); break;
-      default: csr_accumulate_kernel<16><<<ablocks, 256, 0, st>>>(w.keys_out, w.vals_out, ne, w.pi, kp, k, tbits, acc_sk, acc_nrm, 1); break;
+      case 1: csr_accumulate_kernel<1><<<ablocks, 256, 0, st>>>(w.keys_out, w.vals_out, ne, w.pi, kp, k, tbits, acc_sk, acc_nrm, 1, counting ? w.ne_dev : nullptr); break;
+      case 2: csr_accumulate_kernel<2><<<ablocks, 256, 0, st>>>(w.keys_out, w.vals_out, ne, w.pi, kp, k, tbits, acc_sk, acc_nrm, 1, counting ? w.ne_dev : nullptr); break;
+      case 3: case 4: csr_accumulate_kernel<4><<<ablocks, 256, 0, st>>>(w.keys_out, w.vals_out, ne, w.pi, kp, k, tbits, acc_sk, acc_nrm, 1, counting ? w.ne_dev : nullptr); break;
+      case 5: case 6: case 7: case 8: csr_accumulate_kernel<8><<<ablocks, 256, 0, st>>>(w.keys_out, w.vals_out, ne, w.pi, kp, k, tbits, acc_sk, acc_nrm, 1, counting ? w.ne_dev : nullptr); break;
+      default: csr_accumulate_kernel<16><<<ablocks, 256, 0, st>>>(w.keys_out, w.vals_out, ne, w.pi, kp, k, tbits, acc_sk, acc_nrm, 1, counting ? w.ne_dev : nullptr); break;
     }
     CSR_TRY(cudaGetLastError());
     if (w.ev_pool) {

@@ -395,10 +395,12 @@ __global__ void pi_panel_kmajor_kernel(int kind, uint64_t seed, int k, int kpad,
   const int grp = (kind == PI_RADEMACHER && (t0 & 31) == 0) ? 32 : 4;
   const int64_t ng = (rows + grp - 1) / grp;
   const uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
+  // (e < 2^32 for any panel K1 uses: kpad <= 4096 and rows / grp < 2^20)
+  const uint32_t ngu = (uint32_t)ng;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < ng * kpad;
        e += (int64_t)gridDim.x * blockDim.x) {
-    const int kappa = (int)(e / ng);
-    const int64_t g = e - (int64_t)kappa * ng;
+    const int kappa = (int)((uint32_t)e / ngu);
+    const int64_t g = (int64_t)((uint32_t)e - (uint32_t)kappa * ngu);
     const int64_t t = t0 + grp * g;
     uint16_t* dst = panel + (int64_t)kappa * ld + grp * g;
     if (grp == 32) {

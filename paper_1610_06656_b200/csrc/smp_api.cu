@@ -39,6 +39,15 @@ struct smp_handle {
   int64_t pnorm_cap = 0;
   uint16_t* planes = nullptr;
   int64_t planes_cap = 0;
+  // pipelined plane split (sketch_dense_split): double buffers, aux stream
+  uint16_t* planes2[2] = {nullptr, nullptr};
+  int64_t planes2_cap[2] = {0, 0};
+  double* pnorm2[2] = {nullptr, nullptr};
+  int64_t pnorm2_cap[2] = {0, 0};
+  uint16_t* panel2[2] = {nullptr, nullptr};
+  int64_t panel2_cap[2] = {0, 0};
+  cudaEvent_t ev_prep[2] = {nullptr, nullptr}, ev_free[2] = {nullptr, nullptr}, ev_sync = nullptr;
+  cudaStream_t aux_st = nullptr;
   uint16_t* pi_panel = nullptr;  // K1 Gaussian Π panel (κ-major)
   int64_t pi_panel_cap = 0;
   int64_t panel_row0 = -1, panel_ld = 0, panel_kpad = 0;  // rows the panel holds
@@ -142,7 +151,8 @@ int choose_splits(int tiles, int kb_total, int max_kb) {
 
 // One matrix, one dense bf16 block through K1 + K2.
 smp_status sketch_dense_bf16(smp_handle* h, int64_t row0, int64_t rows, const void* X, int64_t ldx,
-                             int64_t ncols, int planes, int64_t col_off, bool do_norms) {
+                             int64_t ncols, int planes, int64_t col_off, bool do_norms,
+                             const uint16_t* ext_panel = nullptr, const int32_t* col_map = nullptr) {
   using namespace smp;
   const int k = h->k;
   SketchTCParams p{};
@@ -169,7 +179,11 @@ smp_status sketch_dense_bf16(smp_handle* h, int64_t row0, int64_t rows, const vo
     const char* e = getenv("SMP_K1_PANEL");  // tuning switch: 1 = panel for every Π kind
     return e ? atoi(e) : 0;
   }();
-  if (p.kind == SMP_PI_GAUSSIAN || panel_mode == 1) {
+  const bool panel_fits = (int64_t)p.k_tiles * 256 * (int64_t)p.kb_total * 64 <= (1ll << 30);
+  if (ext_panel) {  // generated by the caller (pipelined split path)
+    p.pi_panel = ext_panel;
+    p.pi_ld = (int64_t)p.kb_total * 64;
+  } else if ((p.kind == SMP_PI_GAUSSIAN || panel_mode == 1) && panel_fits) {
     // Π once per block into a κ-major panel that K1 streams by TMA (Gaussian:
     // ~33 ALU ops per entry would otherwise be repeated for every column
     // tile).  A and B blocks over the same rows reuse the panel.
@@ -189,7 +203,8 @@ smp_status sketch_dense_bf16(smp_handle* h, int64_t row0, int64_t rows, const vo
     p.pi_panel = h->pi_panel;
     p.pi_ld = ld;
   }
-  if (h->timing) {
+  const bool time_k1 = h->timing && h->d.input != SMP_IN_CSR_F32;  // CSR handles time K3d
+  if (time_k1) {
     while (h->ev_pool.size() < h->ev_used_n + 2) {
       cudaEvent_t e;
       CK(h, cudaEventCreate(&e), "event");
@@ -198,16 +213,18 @@ smp_status sketch_dense_bf16(smp_handle* h, int64_t row0, int64_t rows, const vo
     CK(h, cudaEventRecord(h->ev_pool[h->ev_used_n], h->st), "event");
   }
   CK(h, launch_sketch_tc(X, ldx, p, h->st), "sketch_tc");
-  if (h->timing) {
+  if (time_k1) {
     CK(h, cudaEventRecord(h->ev_pool[h->ev_used_n + 1], h->st), "event");
     h->ev_used_n += 2;
   }
   const int64_t n = ncols / planes;
-  CK(h, launch_reduce_sketch(h->part, p.splits, planes, n, k, h->acc_sk + col_off * k, h->st),
+  CK(h, launch_reduce_sketch(h->part, p.splits, planes, n, k,
+                             col_map ? h->acc_sk : h->acc_sk + col_off * k, h->st, col_map),
      "reduce_sketch");
   h->launches += 2;
   if (do_norms) {
-    CK(h, launch_reduce_norms(h->pnorm, p.splits * p.k_tiles, n, h->acc_nrm + col_off, h->st),
+    CK(h, launch_reduce_norms(h->pnorm, p.splits * p.k_tiles, n,
+                              col_map ? h->acc_nrm : h->acc_nrm + col_off, h->st, col_map),
        "reduce_norms");
     h->launches += 1;
   }
@@ -224,22 +241,63 @@ smp_status sketch_dense_split(smp_handle* h, int64_t row0, int64_t rows, const v
   const int mode = x_bf16 ? 2 : (gauss ? 4 : 3);
   const int np = x_bf16 ? 2 : 3;
   const int64_t ldp = ((np * n + 7) / 8) * 8;
-  const int64_t chunk = std::max<int64_t>(64, std::min<int64_t>(rows, (int64_t)(2048ll << 20) / (ldp * 2)));
-  const int seg_rows = 256;
-  CK(h, ensure(h->planes, h->planes_cap, ((chunk + 63) / 64) * 64 * ldp), "alloc planes");
+  const int64_t kpad = ((h->k + 255) / 256) * 256;
+  int64_t chunk = std::max<int64_t>(64, std::min<int64_t>(rows, (int64_t)(2048ll << 20) / (ldp * 2)));
+  if (gauss)  // K1's Π panel for a chunk: at most 512 MB (kpad x chunk bf16)
+    chunk = std::max<int64_t>(64, std::min<int64_t>(chunk, (512ll << 20) / (kpad * 2)));
+  const int seg_rows = 512;  // rows per split thread (and per fp64 norm partial)
+  const int64_t chunk_pad = ((chunk + 63) / 64) * 64;
+  const int64_t segs_max = (chunk + seg_rows - 1) / seg_rows;
+  // Row chunks, double-buffered: split into planes (HBM-bound) and the
+  // Gaussian Π panel (ALU-bound), then K1 (tensor-bound).
+  for (int b = 0; b < 2; ++b) {
+    CK(h, ensure(h->planes2[b], h->planes2_cap[b], chunk_pad * ldp), "alloc planes");
+    CK(h, ensure(h->pnorm2[b], h->pnorm2_cap[b], segs_max * n), "alloc pnorm");
+    if (gauss) CK(h, ensure(h->panel2[b], h->panel2_cap[b], kpad * chunk_pad), "alloc pi panel");
+    if (!h->ev_prep[b]) CK(h, cudaEventCreateWithFlags(&h->ev_prep[b], cudaEventDisableTiming), "event");
+    if (!h->ev_free[b]) CK(h, cudaEventCreateWithFlags(&h->ev_free[b], cudaEventDisableTiming), "event");
+  }
+  // SMP_SPLIT_OVERLAP=1 runs the split on a second stream, overlapped with K1
+  // (measured no faster on cfg4: the kernels share the SMs); default: one stream
+  static const bool overlap = [] {
+    const char* e = getenv("SMP_SPLIT_OVERLAP");
+    return e && atoi(e) == 1;
+  }();
+  if (overlap && !h->aux_st) CK(h, cudaStreamCreateWithFlags(&h->aux_st, cudaStreamNonBlocking), "stream");
+  cudaStream_t aux = overlap ? h->aux_st : h->st;
+  if (!h->ev_sync) CK(h, cudaEventCreateWithFlags(&h->ev_sync, cudaEventDisableTiming), "event");
+  // aux starts after everything already on the main stream (reset, earlier blocks)
+  CK(h, cudaEventRecord(h->ev_sync, h->st), "event");
+  CK(h, cudaStreamWaitEvent(aux, h->ev_sync, 0), "wait");
   const int64_t es = x_bf16 ? 2 : 4;
-  for (int64_t r0 = 0; r0 < rows; r0 += chunk) {
+  int i = 0;
+  for (int64_t r0 = 0; r0 < rows; r0 += chunk, ++i) {
+    const int b = i & 1;
     const int64_t rc = std::min(chunk, rows - r0);
     const int64_t segs = (rc + seg_rows - 1) / seg_rows;
-    CK(h, ensure(h->pnorm, h->pnorm_cap, segs * n), "alloc pnorm");
+    if (i >= 2) CK(h, cudaStreamWaitEvent(aux, h->ev_free[b], 0), "wait");
     CK(h, launch_split_planes(static_cast<const uint8_t*>(X) + r0 * ldx * es, x_bf16, ldx, rc, n, mode,
-                              h->planes, ldp, h->pnorm, seg_rows, h->st),
+                              h->planes2[b], ldp, h->pnorm2[b], seg_rows, aux),
        "split_planes");
-    CK(h, launch_reduce_norms(h->pnorm, (int)segs, n, h->acc_nrm + col_off, h->st), "reduce_norms");
+    CK(h, launch_reduce_norms(h->pnorm2[b], (int)segs, n, h->acc_nrm + col_off, aux), "reduce_norms");
     h->launches += 2;
-    smp_status s = sketch_dense_bf16(h, row0 + r0, rc, h->planes, ldp, np * n, np, col_off, false);
+    if (gauss) {
+      const int64_t ld = ((rc + 63) / 64) * 64;
+      CK(h, launch_pi_panel_kmajor(h->d.pi_kind, h->d.seed, h->k, (int)kpad, row0 + r0, ld, ld,
+                                   h->panel2[b], aux),
+         "pi panel");
+      h->launches += 1;
+    }
+    CK(h, cudaEventRecord(h->ev_prep[b], aux), "event");
+    CK(h, cudaStreamWaitEvent(h->st, h->ev_prep[b], 0), "wait");
+    smp_status s = sketch_dense_bf16(h, row0 + r0, rc, h->planes2[b], ldp, np * n, np, col_off, false,
+                                     gauss ? h->panel2[b] : nullptr);
     if (s != SMP_OK) return s;
+    CK(h, cudaEventRecord(h->ev_free[b], h->st), "event");
   }
+  // the norms (reduced on aux) are complete before anything later on main
+  CK(h, cudaEventRecord(h->ev_sync, aux), "event");
+  CK(h, cudaStreamWaitEvent(h->st, h->ev_sync, 0), "wait");
   return SMP_OK;
 }
 
@@ -364,6 +422,13 @@ void smp_destroy(smp_handle* h) {
     if (h->ev_used[i]) cudaEventDestroy(h->ev_used[i]);
   }
   if (h->copy_st) cudaStreamDestroy(h->copy_st);
+  if (h->aux_st) { cudaStreamSynchronize(h->aux_st); cudaStreamDestroy(h->aux_st); }
+  for (int b = 0; b < 2; ++b) {
+    cudaFree(h->planes2[b]); cudaFree(h->pnorm2[b]); cudaFree(h->panel2[b]);
+    if (h->ev_prep[b]) cudaEventDestroy(h->ev_prep[b]);
+    if (h->ev_free[b]) cudaEventDestroy(h->ev_free[b]);
+  }
+  if (h->ev_sync) cudaEventDestroy(h->ev_sync);
   for (auto e : h->ev_pool) cudaEventDestroy(e);
   delete h;
 }
@@ -474,12 +539,46 @@ smp_status smp_sketch_block_csr(smp_handle* h, int64_t row0, int64_t rows, const
   (void)a_nnz; (void)b_nnz;
   h->finalized = false;
   const int64_t l0 = h->csr.launches;
-  h->csr.ev_pool = h->timing ? &h->ev_pool : nullptr;
+  h->csr.ev_pool = nullptr;
   h->csr.ev_used = &h->ev_used_n;
+  // tensor-core head (K3): columns with density >= δ whose
+  // nonzeros are small integers go through K1 as a dense bf16 matrix
+  static const double head_density = [] {
+    const char* e = getenv("SMP_CSR_HEAD_DENSITY");
+    return e ? atof(e) : 0.02;
+  }();
+  const int64_t a_n = h->n1, b_n = two ? h->n2 : 0;
+  const int32_t* lut = nullptr;
+  if (head_density > 0.0) {
+    int n_head = 0;
+    CK(h, smp::csr_select_head(h->csr, a_rowptr, a_col, a_n, two ? b_rowptr : nullptr,
+                               two ? b_col : nullptr, b_n, rows, head_density, &n_head, h->st),
+       "csr head");
+    if (n_head > 0) {
+      lut = h->csr.head_lut;
+      const int64_t ldh = ((n_head + 63) / 64) * 64;
+      const int64_t kpad = ((h->k + 255) / 256) * 256;
+      int64_t chunk = std::min<int64_t>(rows, (1ll << 30) / (ldh * 2));            // 1 GB dense chunk
+      chunk = std::min<int64_t>(chunk, (512ll << 20) / (kpad * 2));                // 512 MB Π panel
+      chunk = std::max<int64_t>(64, (chunk / 64) * 64);
+      CK(h, ensure(h->csr.xhead, h->csr.xhead_cap, ((chunk + 63) / 64) * 64 * ldh), "alloc head");
+      for (int64_t r0 = 0; r0 < rows; r0 += chunk) {
+        const int64_t rc = std::min(chunk, rows - r0);
+        CK(h, smp::csr_densify(h->csr, a_rowptr, a_col, a_val, a_n, two ? b_rowptr : nullptr,
+                               two ? b_col : nullptr, two ? b_val : nullptr, b_n, r0, rc, ldh,
+                               h->csr.xhead, h->st),
+           "densify");
+        smp_status s2 = sketch_dense_bf16(h, row0 + r0, rc, h->csr.xhead, ldh, n_head, 1, 0, true,
+                                          nullptr, h->csr.head_map);
+        if (s2 != SMP_OK) return s2;
+      }
+    }
+  }
+  h->csr.ev_pool = h->timing ? &h->ev_pool : nullptr;
   cudaError_t e = smp::launch_sketch_csr(h->csr, h->d.pi_kind, h->d.seed, h->k, row0, rows, a_rowptr,
                                          a_col, a_val, h->n1, two ? b_rowptr : nullptr,
                                          two ? b_col : nullptr, two ? b_val : nullptr,
-                                         two ? h->n2 : 0, h->acc_sk, h->acc_nrm, h->status, h->st);
+                                         two ? h->n2 : 0, h->acc_sk, h->acc_nrm, h->status, h->st, lut);
   if (e == cudaErrorInvalidValue)
     return fail(h, SMP_EINVAL, "CSR: more than 2^26 columns are not supported");
   CK(h, e, "sketch_csr");

@@ -32,11 +32,13 @@ int sketch_tc_smem_bytes();
 
 // ---- K2 partial reduce, fp32 split, K4 finalize (reduce.cu)
 // acc[c][κ] += Σ_s Σ_pl part[s][pl*n + c][κ]   (planes pl = 0..planes-1)
+// map (optional): output column of input column c is map[c] (acc is then the
+// base of the whole [n_tot][k] accumulator)
 cudaError_t launch_reduce_sketch(const float* part, int splits, int planes, int64_t n, int k,
-                                 float* acc, cudaStream_t st);
+                                 float* acc, cudaStream_t st, const int32_t* map = nullptr);
 // nacc[c] += Σ_slot pnorm[slot][c]
 cudaError_t launch_reduce_norms(const double* pnorm, int slots, int64_t n, double* nacc,
-                                cudaStream_t st);
+                                cudaStream_t st, const int32_t* map = nullptr);
 // rows of X (fp32, or bf16 if x_bf16) -> P exact bf16 planes (mode 3: fp32
 // 8+8+8 bits; mode 4: fp32 4+8+8+4; mode 2: bf16 4+4) laid out as a
 // rows x (P n) matrix with leading dimension ldp, and fp64 Σx² per row segment.
@@ -64,6 +66,19 @@ struct CsrWorkspace {
   uint32_t* hist = nullptr;       // counting sort: [ntot][CTAs] counts and offsets
   uint32_t* offs = nullptr;
   int64_t hist_cap = 0, offs_cap = 0;
+  uint32_t* ne_dev = nullptr;     // [0] tail entries of the panel, [1] head columns
+  int64_t ne_cap = 0;
+  // tensor-core head (columns with density >= SMP_CSR_HEAD_DENSITY)
+  int32_t* head_lut = nullptr;    // [ntot] slot or -1
+  int32_t* head_map = nullptr;    // [slots] global column
+  uint32_t* head_cnt = nullptr;
+  uint32_t* head_flag = nullptr;  // [2 ntot]: flags, scan
+  uint8_t* head_tmp = nullptr;
+  int64_t head_lut_cap = 0, head_map_cap = 0, head_cnt_cap = 0, head_flag_cap = 0, head_tmp_cap = 0;
+  uint16_t* xhead = nullptr;      // dense head chunk (bf16)
+  int64_t xhead_cap = 0;
+  int64_t* head_h = nullptr;      // pinned
+
   int64_t* bounds_d = nullptr;
   int64_t bounds_cap = 0;
   int64_t* bounds_h = nullptr;    // pinned
@@ -83,8 +98,19 @@ cudaError_t launch_sketch_csr(CsrWorkspace& w, int kind, uint64_t seed, int k, i
                               int64_t rows, const int64_t* a_rowptr, const int32_t* a_col,
                               const float* a_val, int64_t a_n, const int64_t* b_rowptr,
                               const int32_t* b_col, const float* b_val, int64_t b_n, float* acc_sk,
-                              double* acc_nrm, int* status, cudaStream_t st);
+                              double* acc_nrm, int* status, cudaStream_t st,
+                              const int32_t* head_lut = nullptr);
 void csr_workspace_free(CsrWorkspace& w);
+// head columns: count nonzeros per column over the block, select columns with
+// count >= density * rows (slots in column order) -> w.head_lut / w.head_map;
+// *n_head = number of slots (synchronises)
+cudaError_t csr_select_head(CsrWorkspace& w, const int64_t* a_rowptr, const int32_t* a_col, int64_t a_n,
+                            const int64_t* b_rowptr, const int32_t* b_col, int64_t b_n, int64_t rows,
+                            double density, int* n_head, cudaStream_t st);
+// dense bf16 head chunk [rows][ldh] for rows [r0, r0 + rows) of the block
+cudaError_t csr_densify(CsrWorkspace& w, const int64_t* a_rowptr, const int32_t* a_col, const float* a_val,
+                        int64_t a_n, const int64_t* b_rowptr, const int32_t* b_col, const float* b_val,
+                        int64_t b_n, int64_t r0, int64_t rows, int64_t ldh, uint16_t* xh, cudaStream_t st);
 
 // ---- K5/K6 sampling and estimation (omega.cu)
 cudaError_t launch_alpha_beta(const double* a2, int64_t n1, const double* b2, int64_t n2,

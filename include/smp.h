@@ -98,9 +98,16 @@ SMP_API smp_status smp_sketch_block(smp_handle* h, int64_t row0, int64_t rows, c
 SMP_API smp_status smp_sketch_block_host(smp_handle* h, int64_t row0, int64_t rows, const void* A,
                                  int64_t lda, const void* B, int64_t ldb, int64_t chunk_rows);
 
-/* CSR variant (SMP_IN_CSR_F32): row t = row0 + r has entries
- * (col[p], val[p]) for p in [rowptr[r] - rowptr[0], rowptr[r+1] - rowptr[0]).
- * Column indices must lie in [0, n).  Errors: SMP_EINVAL. */
+/* CSR variant (SMP_IN_CSR_F32; bag-of-words inputs, P:9): row
+ * t = row0 + r has entries (col[p], val[p]) for
+ * p in [rowptr[r] - rowptr[0], rowptr[r+1] - rowptr[0]); rowptr has rows+1
+ * entries.  Column indices must lie in [0, n): an out-of-range index is
+ * reported by smp_finalize_norms (SMP_EINVAL).  Columns with density
+ * >= 2% (env SMP_CSR_HEAD_DENSITY) and small-integer values go through the
+ * tensor-core sketch as a dense head; the rest through the sparse kernels
+ * (K3).  Norms² are exact for integer counts.  Synchronises
+ * (head selection and panel sizes are read back).  Errors: SMP_EINVAL
+ * (null arrays, > 2^26 columns), SMP_ECUDA. */
 SMP_API smp_status smp_sketch_block_csr(smp_handle* h, int64_t row0, int64_t rows, const int64_t* a_rowptr,
                                 const int32_t* a_col, const float* a_val, int64_t a_nnz,
                                 const int64_t* b_rowptr, const int32_t* b_col, const float* b_val,

@@ -2,6 +2,7 @@
 // rank r; instantiated in waltmin_r*.cu (split for parallel compilation) and
 // driven by run_waltmin() in waltmin.cu.
 #pragma once
+#include <cstdlib>
 #include "smp_device.cuh"
 #include "smp_kernels.h"
 
@@ -550,7 +551,12 @@ cudaError_t launch_wm(WMParams& p, cudaStream_t st) {
   SMP_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   SMP_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, wm_persistent_kernel<R>, WM_THREADS, smem));
   if (per_sm < 1) return cudaErrorInvalidConfiguration;
-  const int grid = sms;  // one CTA per SM (co-resident: cooperative launch)
+  // one CTA per SM (co-resident: cooperative launch); SMP_WM_CTAS overrides (tuning)
+  static const int env_ctas = [] {
+    const char* e = getenv("SMP_WM_CTAS");
+    return e ? atoi(e) : 0;
+  }();
+  const int grid = (env_ctas > 0 && env_ctas <= sms) ? env_ctas : sms;
   void* args[] = {&p};
   return cudaLaunchCooperativeKernel((const void*)wm_persistent_kernel<R>, dim3(grid), dim3(WM_THREADS),
                                      args, smem, st);

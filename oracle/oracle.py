@@ -18,6 +18,12 @@ _LIB = os.path.join(_HERE, "liboracle.so")
 
 PI_RADEMACHER, PI_GAUSSIAN, PI_HADAMARD = 0, 1, 2
 
+
+def pi_srht(d: int) -> int:
+    """Kind code of the SRHT Π for d rows (16 + L, 2^L >= d; R26)."""
+    L = max(1, int(d - 1).bit_length())
+    return 16 + L
+
 _lib = None
 
 
@@ -47,6 +53,10 @@ def _get():
                                        ctypes.c_int, i64, P, P]
         lib.or_sketch_csr.argtypes = [ctypes.c_int, u64, ctypes.c_int, i64, i64, i64, P, P, P,
                                       P, P]
+        lib.or_srht_row.argtypes = [u64, ctypes.c_int, i64]
+        lib.or_srht_row.restype = i64
+        lib.or_srht_sign.argtypes = [u64, i64]
+        lib.or_srht_sign.restype = f64
         lib.or_colnorms.argtypes = [i64, i64, P, ctypes.c_int, i64, P]
         lib.or_colnorms.restype = None
         lib.or_pairwise_sum.argtypes = [P, i64]
@@ -126,6 +136,16 @@ def sketch_rows(kind, seed, k, X, row0=0, sk=None, norm2=None):
     _get().or_sketch_rows(kind, seed, k, row0, rows, n, _p(X), _dtype_code(X), n, _p(sk),
                           _p(norm2))
     return sk, norm2
+
+
+def srht_row(seed: int, L: int, kappa: int) -> int:
+    """s_κ = F_L(κ): the sampled Hadamard row of SRHT row κ (R26)."""
+    return _get().or_srht_row(seed, L, kappa)
+
+
+def srht_sign(seed: int, t: int) -> float:
+    """D_t of the SRHT (R26)."""
+    return _get().or_srht_sign(seed, t)
 
 
 def colnorms(X, norm2=None):

@@ -175,10 +175,58 @@ double or_pi_hadamard(int64_t kappa, int64_t t)
     return (popcount64((uint64_t)kappa & (uint64_t)t) & 1) ? -1.0 : 1.0;
 }
 
+/* ------------------------------------------------------------------------ */
+/* SRHT (the sketch the paper's Spark code used, P:145 and its footnote;     */
+/* SURVEY §8f NEXT-1; R26):  Π = sqrt(d/k) S H D with H the        */
+/* normalised Sylvester-Hadamard matrix of order 2^L >= d, D = diag(±1) and  */
+/* S k distinct rows of H sampled without replacement.  Unscaled entries:    */
+/*   Π(κ, t) = D_t · (−1)^popcount(s_κ & t),  s_κ = F_L(κ),                 */
+/* D_t: bit of Philox(ctr = (t>>7, 0, t>>39, 6)) in the Rademacher layout;   */
+/* F_L: a bijection of [0, 2^L) — 4-round unbalanced Feistel, halves        */
+/* a = L/2 (high) and b = L − a (low) bits; even rounds hi ^= f(lo) mod 2^a, */
+/* odd rounds lo ^= f(hi) mod 2^b, f(v) = word 0 of                         */
+/* Philox(ctr = (v, round, L, 7)).  Internal kind code: 16 + L.              */
+/* ------------------------------------------------------------------------ */
+int64_t or_srht_row(uint64_t seed, int L, int64_t kappa)
+{
+    const int a = L / 2, b = L - a;
+    const uint64_t mb = b >= 64 ? ~0ull : ((1ull << b) - 1), ma = a >= 64 ? ~0ull : ((1ull << a) - 1);
+    uint64_t lo = (uint64_t)kappa & mb, hi = ((uint64_t)kappa >> b) & ma;
+    for (int r = 0; r < 4; ++r) {
+        uint32_t w[4];
+        if ((r & 1) == 0) {
+            philox_seed(seed, (uint32_t)lo, (uint32_t)r, (uint32_t)L, 7u, w);
+            hi ^= (uint64_t)w[0] & ma;
+        } else {
+            philox_seed(seed, (uint32_t)hi, (uint32_t)r, (uint32_t)L, 7u, w);
+            lo ^= (uint64_t)w[0] & mb;
+        }
+    }
+    return (int64_t)((hi << b) | lo);
+}
+
+double or_srht_sign(uint64_t seed, int64_t t)
+{
+    uint32_t w[4];
+    philox_seed(seed, (uint32_t)((uint64_t)t >> 7), 0u, (uint32_t)((uint64_t)t >> 39), 6u, w);
+    unsigned b = (unsigned)(t & 127);
+    unsigned e = b & 31u;
+    unsigned pos = (e >> 1) + ((e & 1u) << 4);
+    return ((w[b >> 5] >> pos) & 1u) ? -1.0 : 1.0;
+}
+
+double or_pi_srht(uint64_t seed, int L, int64_t kappa, int64_t t)
+{
+    const int64_t s = or_srht_row(seed, L, kappa);
+    const double h = (popcount64((uint64_t)s & (uint64_t)t) & 1) ? -1.0 : 1.0;
+    return or_srht_sign(seed, t) * h;
+}
+
 double or_pi_entry(int kind, uint64_t seed, int64_t kappa, int64_t t)
 {
     if (kind == OR_PI_RADEMACHER) return or_pi_rademacher(seed, kappa, t);
     if (kind == OR_PI_GAUSSIAN) return or_pi_gaussian(seed, kappa, t);
+    if (kind >= 16) return or_pi_srht(seed, kind - 16, kappa, t);
     return or_pi_hadamard(kappa, t);
 }
 

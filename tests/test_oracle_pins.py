@@ -572,3 +572,69 @@ def test_pipeline_error_reported_vs_optimal():
     assert err <= err_svd
     assert err < 0.1
     assert opt <= err + 1e-12
+
+
+# ------------------------------------------------------------------ SRHT (NEXT-1, R26)
+def test_srht_feistel_is_a_bijection():
+    """F_L permutes [0, 2^L): the k sampled Hadamard rows are distinct
+    (sampling without replacement, the S of S·H·D)."""
+    for L in (1, 2, 3, 5, 8, 11):
+        rows = [oracle.srht_row(7, L, i) for i in range(1 << L)]
+        assert sorted(rows) == list(range(1 << L)), L
+
+
+def test_srht_sign_layout_and_balance():
+    """D_t from raw Philox words of stream 6 (the Rademacher bit layout)."""
+    seed = 0x1234
+    for t in (0, 1, 2, 31, 32, 127, 128, 1000, (1 << 40) + 77):
+        w = oracle.philox4x32_10([(t >> 7) & 0xFFFFFFFF, 0, (t >> 39) & 0xFFFFFFFF, 6],
+                                 [seed & 0xFFFFFFFF, seed >> 32])
+        b = t & 127
+        e = b & 31
+        bit = (int(w[b >> 5]) >> ((e >> 1) + ((e & 1) << 4))) & 1
+        assert oracle.srht_sign(seed, t) == (-1.0 if bit else 1.0)
+    s = np.array([oracle.srht_sign(3, t) for t in range(20000)])
+    assert abs(s.mean()) < 4.5 / np.sqrt(len(s))
+
+
+def test_srht_entries_are_signed_hadamard():
+    d = 1000
+    kind = oracle.pi_srht(d)
+    L = kind - 16
+    assert (1 << L) >= d > (1 << (L - 1))
+    H = scipy.linalg.hadamard(1 << L)
+    for kap in (0, 3, 17):
+        s = oracle.srht_row(5, L, kap)
+        for t in (0, 1, 77, 999):
+            assert oracle.pi_entry(kind, 5, kap, t) == oracle.srht_sign(5, t) * H[s, t]
+
+
+def test_srht_full_rank_gives_exact_product():
+    """k = d = 2^L: Π is a row-permuted, column-signed Hadamard matrix, so
+    ΠᵀΠ = d I and the (1/√k-scaled) sketch preserves all inner products:
+    M̃ = AᵀB exactly (the SRHT analogue of north-star check (a))."""
+    d, n = 256, 12
+    kind = oracle.pi_srht(d)
+    rng = np.random.default_rng(2)
+    A = rng.standard_normal((d, n))
+    B = rng.standard_normal((d, n))
+    P = oracle.pi_matrix(kind, 9, d, 0, d)
+    np.testing.assert_allclose(P.T @ P, d * np.eye(d), atol=1e-9)
+    skA, a2 = oracle.sketch_rows(kind, 9, d, A)
+    skB, b2 = oracle.sketch_rows(kind, 9, d, B)
+    As, _, DA = oracle.finalize(d, skA, a2)
+    Bs, _, DB = oracle.finalize(d, skB, b2)
+    I, J = np.meshgrid(np.arange(n, dtype=np.int32), np.arange(n, dtype=np.int32), indexing="ij")
+    M = oracle.estimate(d, I.ravel(), J.ravel(), As, Bs, DA, DB)
+    np.testing.assert_allclose(M.reshape(n, n), A.T @ B, rtol=1e-9, atol=1e-9)
+
+
+def test_srht_jl_band():
+    """Subsampled at k < d, SRHT is still a JL map: ‖Πx‖²/k ≈ ‖x‖²."""
+    d, k, trials = 2048, 256, 40
+    kind = oracle.pi_srht(d)
+    rng = np.random.default_rng(4)
+    X = rng.standard_normal((d, trials))
+    sk, n2 = oracle.sketch_rows(kind, 11, k, X)
+    ratio = (sk ** 2).sum(1) / k / n2
+    assert np.all(np.abs(ratio - 1) < 0.5) and abs(ratio.mean() - 1) < 0.1

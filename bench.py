@@ -153,7 +153,16 @@ def dtype_name(cfg):
 
 
 def pi_code(cfg):
-    return {"rademacher": 0, "gaussian": 1}[cfg["pi"]]
+    """Π kind as the C ABI takes it (SMP_PI_*)."""
+    return {"rademacher": 0, "gaussian": 1, "srht": 3}[cfg["pi"]]
+
+
+def oracle_pi(cfg):
+    """Π kind code of the oracle (SRHT carries its Hadamard order)."""
+    if cfg["pi"] == "srht":
+        import oracle
+        return oracle.pi_srht(cfg["d"])
+    return pi_code(cfg)
 
 
 # --------------------------------------------------------------------- oracle arms
@@ -179,13 +188,13 @@ def oracle_sample_rate(cfgname, cfg, target_s):
         t0 = time.perf_counter()
         if csr:
             for X, n in ((A, n1), (B, n2)):
-                oracle.sketch_csr(pi_code(cfg), cfg["seed"], k, n, X[0].numpy(), X[1].numpy(),
+                oracle.sketch_csr(oracle_pi(cfg), cfg["seed"], k, n, X[0].numpy(), X[1].numpy(),
                                   X[2].numpy(), row0=r0)
             nbytes = csr_bytes(A) + csr_bytes(B)
         else:
-            oracle.sketch_rows(pi_code(cfg), cfg["seed"], k, host(A), row0=r0)
+            oracle.sketch_rows(oracle_pi(cfg), cfg["seed"], k, host(A), row0=r0)
             if not a_is_b:
-                oracle.sketch_rows(pi_code(cfg), cfg["seed"], k, host(B), row0=r0)
+                oracle.sketch_rows(oracle_pi(cfg), cfg["seed"], k, host(B), row0=r0)
             nbytes = A.numel() * A.element_size() + (0 if a_is_b else B.numel() * B.element_size())
         return time.perf_counter() - t0, nbytes
 
@@ -247,6 +256,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--init-iters", type=int, default=30)
+    ap.add_argument("--pi", default=None, choices=["rademacher", "gaussian", "srht"],
+                    help="override the config's Π (e.g. srht, the paper's Spark sketch; NEXT-1)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 0)
 
@@ -254,7 +265,9 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     cfgname = args.config
-    cfg = synth.CONFIGS[cfgname]
+    cfg = dict(synth.CONFIGS[cfgname])
+    if args.pi:
+        cfg["pi"] = args.pi
 
     if args.impl == "reference":
         run_reference(args, cfgname, cfg, world, rank)

@@ -50,7 +50,16 @@ typedef enum {
  * Philox4x32-10 hash of (seed, κ, global row t).
  * HADAMARD_TEST: Π(κ,t) = (-1)^popcount(κ&t)/sqrt(k), requires k = d_total a
  * power of two (then Π is orthonormal and M̃ = AᵀB exactly). */
-typedef enum { SMP_PI_RADEMACHER = 0, SMP_PI_GAUSSIAN = 1, SMP_PI_HADAMARD_TEST = 2 } smp_pi;
+/* Π kinds (R1, R26): Rademacher ±1, Gaussian bf16(Box–Muller),
+ * the Sylvester-Hadamard test matrix (k = d, d a power of 2), and SRHT
+ * (√(d/k)·S·H·D — the sketch of the paper's Spark code; H of order
+ * 2^⌈log2 d_total⌉, k distinct rows; requires k <= that order). */
+typedef enum {
+  SMP_PI_RADEMACHER = 0,
+  SMP_PI_GAUSSIAN = 1,
+  SMP_PI_HADAMARD_TEST = 2,
+  SMP_PI_SRHT = 3
+} smp_pi;
 
 typedef enum {
   SMP_IN_DENSE_BF16 = 0, /* bf16, 16-byte aligned base, ld % 8 == 0 (TMA)     */

@@ -13,7 +13,7 @@ _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_PKG, "libsmp.so")
 
 SMP_OK, SMP_EIO, SMP_EINVAL, SMP_ENUMERIC, SMP_ECUDA, SMP_ECAPACITY, SMP_ENOMEM = 0, 2, 3, 4, 5, 6, 7
-PI_RADEMACHER, PI_GAUSSIAN, PI_HADAMARD_TEST = 0, 1, 2
+PI_RADEMACHER, PI_GAUSSIAN, PI_HADAMARD_TEST, PI_SRHT = 0, 1, 2, 3
 IN_DENSE_BF16, IN_DENSE_F32, IN_CSR_F32 = 0, 1, 2
 EST_RESCALED, EST_PLAIN = 0, 1
 PART_REUSE_ALL = 0

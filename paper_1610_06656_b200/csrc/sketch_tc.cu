@@ -84,10 +84,10 @@ struct RadCache {
 // Word W (global index over 32-row words) of the Rademacher bit string of
 // row κ: group W>>2 = Philox(ctr=(g, κ, g>>32, 1)).
 __device__ __forceinline__ uint32_t rad_word(RadCache& c, uint64_t W, uint32_t kappa,
-                                             uint32_t k0, uint32_t k1) {
+                                             uint32_t k0, uint32_t k1, uint32_t tag = TAG_RADEMACHER) {
   uint64_t g = W >> 2;
   if (g != c.g) {
-    u32x4 w = philox4x32_10((uint32_t)g, kappa, (uint32_t)(g >> 32), TAG_RADEMACHER, k0, k1);
+    u32x4 w = philox4x32_10((uint32_t)g, kappa, (uint32_t)(g >> 32), tag, k0, k1);
     c.g = g; c.w0 = w.x; c.w1 = w.y; c.w2 = w.z; c.w3 = w.w;
   }
   uint32_t i = (uint32_t)(W & 3);
@@ -102,14 +102,23 @@ __device__ __forceinline__ uint32_t rad_pos(uint32_t e) { return (e >> 1) | ((e 
 // Half a κ row of the Π tile, rows t0..t0+31: 32 bf16 packed in 16 words
 // (word p = rows 2p (low half) and 2p+1 (high half)), the TMEM A layout.
 __device__ __forceinline__ void gen_pi_half(int kind, uint64_t seed, uint32_t kappa, bool valid,
-                                            uint64_t t0, RadCache& rc, uint32_t (&o)[16]) {
+                                            uint64_t t0, RadCache& rc, uint32_t (&o)[16],
+                                            uint64_t srht_s, uint32_t srht_walsh) {
   const uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
   if (!valid) {
 #pragma unroll
     for (int i = 0; i < 16; ++i) o[i] = 0u;
     return;
   }
-  if (kind == PI_RADEMACHER && (t0 & 31) == 0) {
+  if (kind >= PI_SRHT_BASE && (t0 & 31) == 0) {
+    // 32 rows: D word (stream 6, κ-independent, cached per 128 rows) XOR the
+    // Walsh pattern of s_κ's low 5 bits XOR parity(s_κ & t0) (t0 32-aligned)
+    const uint32_t dw = rad_word(rc, t0 >> 5, 0u, k0, k1, TAG_SRHT_D);
+    const uint32_t hb = (uint32_t)__popcll((unsigned long long)(srht_s & t0)) & 1u;
+    const uint32_t w = dw ^ srht_walsh ^ (0u - hb);
+#pragma unroll
+    for (int p = 0; p < 16; ++p) o[p] = 0x3F803F80u | ((w * (1u << (15 - p))) & 0x80008000u);
+  } else if (kind == PI_RADEMACHER && (t0 & 31) == 0) {
     const uint32_t w = rad_word(rc, t0 >> 5, kappa, k0, k1);
 #pragma unroll
     for (int p = 0; p < 16; ++p)  // shift as a multiply: IMAD on the FMA pipe, LOP3 on ALU
@@ -136,6 +145,11 @@ __device__ __forceinline__ void gen_pi_half(int kind, uint64_t seed, uint32_t ka
         if (kind == PI_RADEMACHER) {
           const uint32_t w = rad_word(rc, t >> 5, kappa, k0, k1);
           lohi[e] = ((w >> rad_pos((uint32_t)(t & 31))) & 1u) ? 0xBF80u : 0x3F80u;
+        } else if (kind >= PI_SRHT_BASE) {
+          const uint32_t w = rad_word(rc, t >> 5, 0u, k0, k1, TAG_SRHT_D);
+          const uint32_t bit = ((w >> rad_pos((uint32_t)(t & 31))) & 1u) ^
+                               ((uint32_t)__popcll((unsigned long long)(srht_s & t)) & 1u);
+          lohi[e] = bit ? 0xBF80u : 0x3F80u;
         } else {
           lohi[e] = pi_bits(kind, seed, kappa, t);
         }
@@ -262,6 +276,12 @@ sketch_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant
     const int kl = 32 * quad + lane;
     const int kappa = kappa0 + kl;
     RadCache rc{~0ull, 0, 0, 0, 0};
+    uint64_t srht_s = 0;
+    uint32_t srht_walsh = 0;
+    if (p.kind >= PI_SRHT_BASE && kappa < p.k) {
+      srht_s = srht_row(p.seed, p.kind - PI_SRHT_BASE, (uint32_t)kappa);
+      srht_walsh = walsh32_interleaved((uint32_t)(srht_s & 31u));
+    }
     for (int it = 0; it < nkb; ++it) {
       const int ps = it % PI_STAGES;
       const uint64_t t0 = (uint64_t)p.row0 + (uint64_t)(kb_begin + it) * TC_BK + 32 * half;
@@ -270,7 +290,7 @@ sketch_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant
 #pragma unroll
         for (int i = 0; i < 16; ++i) o[i] = 0x3F803F80u;
       } else {
-        gen_pi_half(p.kind, p.seed, (uint32_t)kappa, kappa < p.k, t0, rc, o);
+        gen_pi_half(p.kind, p.seed, (uint32_t)kappa, kappa < p.k, t0, rc, o, srht_s, srht_walsh);
       }
       mbar_wait(&pempty[ps], ((uint32_t)(it / PI_STAGES) & 1u) ^ 1u);
       tc_fence_after();

@@ -120,6 +120,17 @@ cudaError_t ensure(T*& p, int64_t& cap, int64_t need) {
 
 bool is_pow2(int64_t x) { return x > 0 && (x & (x - 1)) == 0; }
 
+int srht_L(int64_t d) {
+  int L = 1;
+  while (L < 62 && ((int64_t)1 << L) < d) ++L;
+  return L;
+}
+
+// Π kind code passed to the kernels (SRHT carries its Hadamard order: 16 + L)
+int pi_code(const smp_handle* h) {
+  return h->d.pi_kind == SMP_PI_SRHT ? 16 + srht_L(h->d.d_total) : h->d.pi_kind;
+}
+
 // split-K factor for the tcgen05 sketch.  Two constraints:
 //  * accuracy: a CTA's fp32 TMEM accumulation chain is at most
 //    K1_MAX_KB K-blocks (64 rows each); measured: 41.7K MMA updates per
@@ -165,7 +176,7 @@ smp_status sketch_dense_bf16(smp_handle* h, int64_t row0, int64_t rows, const vo
   p.kb_total = (int32_t)((rows + 63) / 64);
   p.splits = choose_splits(2 * p.n_tiles * p.k_tiles, p.kb_total,
                            h->d.pi_kind == SMP_PI_GAUSSIAN ? K1_MAX_KB_GAUSS : K1_MAX_KB);
-  p.kind = h->d.pi_kind;
+  p.kind = pi_code(h);
   p.do_norms = do_norms ? 1 : 0;
   { const char* dbg = getenv("SMP_K1_DEBUG"); p.debug = dbg ? atoi(dbg) : 0; }
   p.seed = h->d.seed;
@@ -283,7 +294,7 @@ smp_status sketch_dense_split(smp_handle* h, int64_t row0, int64_t rows, const v
     h->launches += 2;
     if (gauss) {
       const int64_t ld = ((rc + 63) / 64) * 64;
-      CK(h, launch_pi_panel_kmajor(h->d.pi_kind, h->d.seed, h->k, (int)kpad, row0 + r0, ld, ld,
+      CK(h, launch_pi_panel_kmajor(pi_code(h), h->d.seed, h->k, (int)kpad, row0 + r0, ld, ld,
                                    h->panel2[b], aux),
          "pi panel");
       h->launches += 1;
@@ -353,7 +364,8 @@ smp_status smp_sketch_init(smp_handle** out, const smp_sketch_desc* d, void* str
   if (d->k < 1 || d->k > 4096 || d->n1 < 1 || (!d->a_is_b && d->n2 < 1) || d->d_total < 1 ||
       d->row_begin < 0 || d->row_end > d->d_total || d->row_begin > d->row_end)
     return SMP_EINVAL;
-  if (d->pi_kind < 0 || d->pi_kind > 2 || d->input < 0 || d->input > 2) return SMP_EINVAL;
+  if (d->pi_kind < 0 || d->pi_kind > 3 || d->input < 0 || d->input > 2) return SMP_EINVAL;
+  if (d->pi_kind == SMP_PI_SRHT && (int64_t)d->k > ((int64_t)1 << srht_L(d->d_total))) return SMP_EINVAL;
   if (d->pi_kind == SMP_PI_HADAMARD_TEST && (d->k != d->d_total || !is_pow2(d->d_total)))
     return SMP_EINVAL;
   if (d->n1 > (1ll << 31) - 1 || d->n2 > (1ll << 31) - 1) return SMP_EINVAL;
@@ -575,7 +587,7 @@ smp_status smp_sketch_block_csr(smp_handle* h, int64_t row0, int64_t rows, const
     }
   }
   h->csr.ev_pool = h->timing ? &h->ev_pool : nullptr;
-  cudaError_t e = smp::launch_sketch_csr(h->csr, h->d.pi_kind, h->d.seed, h->k, row0, rows, a_rowptr,
+  cudaError_t e = smp::launch_sketch_csr(h->csr, pi_code(h), h->d.seed, h->k, row0, rows, a_rowptr,
                                          a_col, a_val, h->n1, two ? b_rowptr : nullptr,
                                          two ? b_col : nullptr, two ? b_val : nullptr,
                                          two ? h->n2 : 0, h->acc_sk, h->acc_nrm, h->status, h->st, lut);

@@ -29,10 +29,26 @@ __device__ __forceinline__ u32x4 philox4x32_10(uint32_t c0, uint32_t c1, uint32_
   return {c0, c1, c2, c3};
 }
 
-enum : int { PI_RADEMACHER = 0, PI_GAUSSIAN = 1, PI_HADAMARD = 2 };
+enum : int { PI_RADEMACHER = 0, PI_GAUSSIAN = 1, PI_HADAMARD = 2, PI_SRHT_BASE = 16 };
 
 // Stream tags (c3 of the Philox counter), DESIGN.md §3.1.
-enum : uint32_t { TAG_RADEMACHER = 1, TAG_GAUSSIAN = 2, TAG_OMEGA = 3, TAG_INIT = 5 };
+enum : uint32_t { TAG_RADEMACHER = 1, TAG_GAUSSIAN = 2, TAG_OMEGA = 3, TAG_INIT = 5, TAG_SRHT_D = 6,
+                  TAG_SRHT_S = 7 };
+
+// ---------------------------------------------------------------- SRHT
+// Π(κ, t) = D_t (−1)^popcount(s_κ & t) (R26; kind code 16 + L):
+// s_κ = F_L(κ), a 4-round unbalanced Feistel bijection of [0, 2^L) whose
+// round function is word 0 of Philox(ctr = (v, round, L, 7)); D_t from
+// stream 6 in the Rademacher bit layout.
+__device__ __forceinline__ uint64_t srht_row(uint64_t seed, int L, uint32_t kappa);
+__device__ __forceinline__ uint32_t walsh32_interleaved(uint32_t s5) {
+  // bit at (j >> 1) | ((j & 1) << 4) = parity(s5 & j), j = 0..31
+  uint32_t w = 0;
+#pragma unroll
+  for (int j = 0; j < 32; ++j)
+    w |= (uint32_t)(__popc(s5 & (uint32_t)j) & 1) << ((j >> 1) | ((j & 1) << 4));
+  return w;
+}
 
 // ---------------------------------------------------------------- Gaussian G
 // fp32 Box–Muller with stated polynomials.  Every operation
@@ -91,6 +107,19 @@ __device__ __forceinline__ void gauss_pair(uint32_t wa, uint32_t wb, uint16_t& z
   z1 = bf16_rne_bits(__fmul_rn(rho, s));
 }
 
+__device__ __forceinline__ uint64_t srht_row(uint64_t seed, int L, uint32_t kappa) {
+  const int a = L / 2, b = L - a;
+  const uint64_t mb = (1ull << b) - 1ull, ma = (1ull << a) - 1ull;
+  uint64_t lo = (uint64_t)kappa & mb, hi = ((uint64_t)kappa >> b) & ma;
+  const uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    if ((r & 1) == 0) hi ^= (uint64_t)philox4x32_10((uint32_t)lo, (uint32_t)r, (uint32_t)L, TAG_SRHT_S, k0, k1).x & ma;
+    else lo ^= (uint64_t)philox4x32_10((uint32_t)hi, (uint32_t)r, (uint32_t)L, TAG_SRHT_S, k0, k1).x & mb;
+  }
+  return (hi << b) | lo;
+}
+
 // Unscaled Π(κ, t) as bf16 bits (used by the SIMT/CSR paths and tests).
 __device__ __forceinline__ uint16_t pi_bits(int kind, uint64_t seed, uint32_t kappa, uint64_t t) {
   const uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
@@ -105,6 +134,14 @@ __device__ __forceinline__ uint16_t pi_bits(int kind, uint64_t seed, uint32_t ka
     uint16_t z0, z1;
     if ((t & 3) < 2) gauss_pair(w.x, w.y, z0, z1); else gauss_pair(w.z, w.w, z0, z1);
     return (t & 1) ? z1 : z0;
+  } else if (kind >= PI_SRHT_BASE) {
+    const uint64_t sk = srht_row(seed, kind - PI_SRHT_BASE, kappa);
+    const u32x4 w = philox4x32_10((uint32_t)(t >> 7), 0u, (uint32_t)(t >> 39), TAG_SRHT_D, k0, k1);
+    const uint32_t b = (uint32_t)(t & 127), e = b & 31;
+    const uint32_t word = (b >> 5) == 0 ? w.x : (b >> 5) == 1 ? w.y : (b >> 5) == 2 ? w.z : w.w;
+    const uint32_t dbit = (word >> ((e >> 1) | ((e & 1u) << 4))) & 1u;
+    const uint32_t hbit = (uint32_t)__popcll((unsigned long long)(sk & t)) & 1u;
+    return (dbit ^ hbit) ? (uint16_t)0xBF80 : (uint16_t)0x3F80;
   } else {
     return (__popcll((unsigned long long)kappa & t) & 1) ? (uint16_t)0xBF80 : (uint16_t)0x3F80;
   }

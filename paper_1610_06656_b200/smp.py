@@ -14,9 +14,9 @@ import torch
 
 from . import _lib
 from ._lib import (EST_PLAIN, EST_RESCALED, IN_CSR_F32, IN_DENSE_BF16, IN_DENSE_F32,
-                   PI_GAUSSIAN, PI_HADAMARD_TEST, PI_RADEMACHER, SmpError)
+                   PI_GAUSSIAN, PI_HADAMARD_TEST, PI_RADEMACHER, PI_SRHT, SmpError)
 
-__all__ = ["SMPSketch", "smp_pca", "PI_RADEMACHER", "PI_GAUSSIAN", "PI_HADAMARD_TEST",
+__all__ = ["SMPSketch", "smp_pca", "PI_RADEMACHER", "PI_GAUSSIAN", "PI_HADAMARD_TEST", "PI_SRHT",
            "IN_DENSE_BF16", "IN_DENSE_F32", "IN_CSR_F32", "SmpError"]
 
 

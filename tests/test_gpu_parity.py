@@ -327,7 +327,7 @@ def test_sketch_csr_bad_column_rejected():
         sk.finalize()
 
 
-@pytest.mark.parametrize("pi", ["gaussian", "rademacher"])
+@pytest.mark.parametrize("pi", ["gaussian", "rademacher", "srht"])
 def test_pi_bit_exact_sampled_rows(pi):
     """Π itself, bit for bit: X has one 1 per column at a random row t_c over
     a long row range, so Ã[:, c]·√k = Π[:, t_c] exactly (a1, R2/R3)."""
@@ -337,11 +337,60 @@ def test_pi_bit_exact_sampled_rows(pi):
     t = np.sort(rng.choice(d, n, replace=False))
     X = torch.zeros(d, n, dtype=torch.bfloat16)
     X[torch.as_tensor(t), torch.arange(n)] = 1.0
-    sk = smp.SMPSketch(d, n, n, k, pi=PI[pi], seed=seed, a_is_b=True, input=smp.IN_DENSE_BF16)
+    gpu_kind = smp.PI_SRHT if pi == "srht" else PI[pi]
+    or_kind = oracle.pi_srht(d) if pi == "srht" else PI[pi]
+    sk = smp.SMPSketch(d, n, n, k, pi=gpu_kind, seed=seed, a_is_b=True, input=smp.IN_DENSE_BF16)
     sk.block(0, X.cuda())
     fin = sk.finalize()
     got = fin["A_sk"].cpu().numpy()                       # fp32: Π(κ, t_c) · fp32(1/√k), RN
-    want = np.array([[oracle.pi_entry(PI[pi], seed, kap, int(tc)) for kap in range(k)] for tc in t])
+    want = np.array([[oracle.pi_entry(or_kind, seed, kap, int(tc)) for kap in range(k)] for tc in t])
     want32 = want.astype(np.float32) * np.float32(1.0 / np.sqrt(k))
     bad = got != want32
     assert bad.sum() == 0, f"{bad.sum()} of {bad.size} Π entries differ, e.g. {np.argwhere(bad)[:5]}"
+
+
+# ------------------------------------------------------------------ SRHT (NEXT-1, R26)
+@pytest.mark.parametrize("d,n,k,row0,blocks", [
+    (3000, 300, 256, 0, None),            # several n-tiles, Hadamard order 4096
+    (2500, 96, 130, 77, [(900, 2500), (0, 900)]),   # unaligned rows (generic path), ragged k
+])
+def test_sketch_srht_parity(d, n, k, row0, blocks):
+    smp = _smp()
+    A = synth.gaussian_small(d, n, seed=1, scale_cols=True).to(torch.bfloat16)
+    B = synth.gaussian_small(d, n, seed=2).to(torch.bfloat16)
+    dt = row0 + d
+    _, fin = gpu_sketch(A, B, k, smp.PI_SRHT, seed=5, row0=row0, d_total=dt, blocks=blocks)
+    kind = oracle.pi_srht(dt)
+    orc = oracle_sketch(A, B, k, kind, seed=5, row0=row0)
+    check_sketch(fin, orc)
+
+
+def test_sketch_csr_srht_parity():
+    smp = _smp()
+    d, n1, n2, k = 2000, 120, 80, 128
+    A = _csr(d, n1, 10, 5, 0)
+    B = _csr(d, n2, 8, 5, 1)
+    sk, fin = gpu_sketch_csr(d, n1, n2, k, smp.PI_SRHT, 11, A, B)
+    kind = oracle.pi_srht(d)
+    skA, a2 = oracle.sketch_csr(kind, 11, k, n1, A[0].numpy(), A[1].numpy(), A[2].numpy())
+    skB, b2 = oracle.sketch_csr(kind, 11, k, n2, B[0].numpy(), B[1].numpy(), B[2].numpy())
+    As, _, _ = oracle.finalize(k, skA, a2)
+    Bs, _, _ = oracle.finalize(k, skB, b2)
+    assert col_rel_err(fin["A_sk"], As).max() <= 1e-5 and col_rel_err(fin["B_sk"], Bs).max() <= 1e-5
+    assert np.array_equal(fin["a_norm2"].cpu().numpy(), a2)
+
+
+def test_srht_full_rank_exact_product():
+    """SRHT with k = d = 2^L: M̃ = AᵀB (fully sampled), as with Hadamard."""
+    smp = _smp()
+    d, n = 256, 24
+    A = synth.gaussian_small(d, n, seed=11).to(torch.bfloat16)
+    B = synth.gaussian_small(d, n, seed=12).to(torch.bfloat16)
+    sk, fin = gpu_sketch(A, B, d, smp.PI_SRHT, seed=3)
+    I, J, val, qh = sk.sample_estimate(1e12, 0)
+    assert I.numel() == n * n
+    M = (A.double().T @ B.double()).numpy()
+    got = np.zeros((n, n))
+    got[I.cpu().numpy(), J.cpu().numpy()] = val.cpu().numpy()
+    scale = np.outer(np.linalg.norm(A.double().numpy(), axis=0), np.linalg.norm(B.double().numpy(), axis=0))
+    assert np.max(np.abs(got - M) / scale) < 1e-5

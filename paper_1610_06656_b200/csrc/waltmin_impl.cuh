@@ -56,6 +56,8 @@ struct WMParams {
   double* gpart;  // [2][gridDim.x][NG]
   unsigned* bar;  // [2]: arrival count, generation
   uint64_t* trace;  // optional [3 * barriers] (SMP_WM_TRACE)
+  uint64_t* trace2; // optional [64] phase stamps of CTA 0 (SMP_WM_TRACE)
+  int stage_x;      // gathered factor rows staged into SMEM per phase (fits: n·r·8 B small)
   float* Uout;
   float* Vout;
 };
@@ -178,7 +180,7 @@ __device__ __forceinline__ void flush_gram(WMShared<R>& sm, const double (&gl)[(
 template <int R>
 __device__ void reduce_chol(WMShared<R>& sm, const double* gpart_buf) {
   constexpr int NG = WMShared<R>::NG;
-  constexpr int MAXK = 8;  // independent loads in flight per thread
+  constexpr int MAXK = 16;  // independent loads in flight per thread (one L2 round trip at r <= 6)
   const int G = gridDim.x;
   const int groups = blockDim.x / NG;  // >= 1 for NG <= 136 < 256
   const int tid = threadIdx.x;
@@ -267,12 +269,41 @@ __device__ void reduce_chol(WMShared<R>& sm, const double* gpart_buf) {
 template <int R>
 struct WMUnroll { static constexpr int U = R <= 6 ? 4 : (R <= 10 ? 2 : 1); };
 
+// Copy the factor rows X[0 .. n) (n·R doubles, written by other CTAs before
+// the last grid barrier) into this CTA's SMEM, so that the phase's gathers —
+// one per sample, the latency-critical part — are SMEM reads, not L2 trips.
+template <int R>
+__device__ __forceinline__ const double* stage_rows(const double* X, int64_t n, double* xs, bool on) {
+  if (!on) return nullptr;
+  // 16-byte loads, 8 in flight per thread (one L2 round trip for ~32 KB)
+  const int64_t tot2 = (n * R) / 2;
+  const double2* src = reinterpret_cast<const double2*>(X);
+  double2* dst = reinterpret_cast<double2*>(xs);
+  for (int64_t b = threadIdx.x; b < tot2; b += 8 * (int64_t)blockDim.x) {
+    double2 v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int64_t e = b + (int64_t)u * blockDim.x;
+      v[u] = e < tot2 ? __ldcg(src + e) : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int64_t e = b + (int64_t)u * blockDim.x;
+      if (e < tot2) dst[e] = v[u];
+    }
+  }
+  if (((n * R) & 1) && threadIdx.x == 0) xs[n * R - 1] = __ldcg(X + n * R - 1);
+  __syncthreads();
+  return xs;
+}
+
 // out[o] = (Σ_{p in [ptr[o], ptr[o+1])} coef[p] X[other[p]]) · T (samples of
 // row o stored contiguously: CSR order, or the pre-permuted CSC copy)
 template <int R>
 __device__ void spmm_phase(WMShared<R>& sm, const int64_t* __restrict__ ptr,
                            const int32_t* __restrict__ other, const double* __restrict__ coef,
-                           const double* X, int64_t nout, double* out, double* gpart_buf) {
+                           const double* X, int64_t nout, double* out, double* gpart_buf,
+                           const double* Xs) {
   constexpr int NG = WMShared<R>::NG;
   constexpr int U = WMUnroll<R>::U;
   const int lane = threadIdx.x & 31;
@@ -299,7 +330,7 @@ __device__ void spmm_phase(WMShared<R>& sm, const int64_t* __restrict__ ptr,
 #pragma unroll
       for (int u = 0; u < U; ++u)
 #pragma unroll
-        for (int l = 0; l < R; ++l) x[u][l] = __ldcg(X + (int64_t)oi[u] * R + l);
+        for (int l = 0; l < R; ++l) x[u][l] = Xs ? Xs[(int64_t)oi[u] * R + l] : __ldcg(X + (int64_t)oi[u] * R + l);
 #pragma unroll
       for (int u = 0; u < U; ++u)
 #pragma unroll
@@ -343,7 +374,7 @@ template <int R>
 __device__ void als_phase(WMShared<R>& sm, const int64_t* __restrict__ ptr,
                           const int32_t* __restrict__ other, const double* __restrict__ w,
                           const double* __restrict__ wv, const double* X, int64_t nout, double lam,
-                          double* out) {
+                          double* out, const double* Xs) {
   constexpr int NG = WMShared<R>::NG;
   constexpr int U = WMUnroll<R>::U;
   const int lane = threadIdx.x & 31;
@@ -370,7 +401,7 @@ __device__ void als_phase(WMShared<R>& sm, const int64_t* __restrict__ ptr,
 #pragma unroll
       for (int u = 0; u < U; ++u)
 #pragma unroll
-        for (int l = 0; l < R; ++l) x[u][l] = __ldcg(X + (int64_t)oi[u] * R + l);
+        for (int l = 0; l < R; ++l) x[u][l] = Xs ? Xs[(int64_t)oi[u] * R + l] : __ldcg(X + (int64_t)oi[u] * R + l);
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         int e = 0;
@@ -453,6 +484,8 @@ __global__ void __launch_bounds__(WM_THREADS, 1) wm_persistent_kernel(WMParams p
   constexpr int NG = WMShared<R>::NG;
   extern __shared__ __align__(16) uint8_t wm_smem[];
   WMShared<R>& sm = *reinterpret_cast<WMShared<R>*>(wm_smem);
+  double* xs = reinterpret_cast<double*>(wm_smem + ((sizeof(WMShared<R>) + 15) & ~(size_t)15));
+  const bool stg = p.stage_x != 0;
   __shared__ double TZ[R * R];
   const int tid = threadIdx.x;
   if (tid == 0) {
@@ -500,14 +533,23 @@ __global__ void __launch_bounds__(WM_THREADS, 1) wm_persistent_kernel(WMParams p
     __syncthreads();
   };
   const int iters = p.init_iters > 0 ? p.init_iters : 1;
+  // diagnostics (SMP_WM_TRACE): CTA 0's time in the first Z-side SpMM phases
+  auto stamp = [&](int slot) {
+    if (p.trace2 && blockIdx.x == 0 && tid == 0 && slot < 64) p.trace2[slot] = wm_globaltimer();
+  };
   for (int it = 0; it < iters; ++it) {
-    spmm_phase<R>(sm, p.rptr, p.J, p.wv, p.Y, p.n1, p.Z, gp(buf));
+    stamp(4 * it);
+    const double* xsY = stage_rows<R>(p.Y, p.n2, xs, stg);
+    stamp(4 * it + 1);
+    spmm_phase<R>(sm, p.rptr, p.J, p.wv, p.Y, p.n1, p.Z, gp(buf), xsY);
+    stamp(4 * it + 2);
     if (it == iters - 1) {  // the last Y half does not reach U0
       cqr2(p.Z, p.n1);
       break;
     }
     cqr1();
-    spmm_phase<R>(sm, p.cptr, p.cI, p.cwv, p.Z, p.n2, p.Y, gp(buf));
+    stamp(4 * it + 3);
+    spmm_phase<R>(sm, p.cptr, p.cI, p.cwv, p.Z, p.n2, p.Y, gp(buf), stage_rows<R>(p.Z, p.n1, xs, stg));
     cqr1();
   }
   for (int e = tid; e < R * R; e += blockDim.x) TZ[e] = sm.T[e];
@@ -525,9 +567,9 @@ __global__ void __launch_bounds__(WM_THREADS, 1) wm_persistent_kernel(WMParams p
   if (p.T == 0)
     for (int64_t e = (int64_t)blockIdx.x * WM_THREADS + tid; e < p.n2 * R; e += G * WM_THREADS) p.V[e] = 0.0;
   for (int t = 0; t < p.T; ++t) {
-    als_phase<R>(sm, p.cptr, p.cI, p.cw, p.cwv, p.U, p.n2, p.lam, p.V);
+    als_phase<R>(sm, p.cptr, p.cI, p.cw, p.cwv, p.U, p.n2, p.lam, p.V, stage_rows<R>(p.U, p.n1, xs, stg));
     grid_sync(p.bar, p.trace, nbar);
-    als_phase<R>(sm, p.rptr, p.J, p.w, p.wv, p.V, p.n1, p.lam, p.U);
+    als_phase<R>(sm, p.rptr, p.J, p.w, p.wv, p.V, p.n1, p.lam, p.U, stage_rows<R>(p.V, p.n2, xs, stg));
     grid_sync(p.bar, p.trace, nbar);
   }
   // output (Û(T), V̂(T)) in fp32
@@ -539,11 +581,15 @@ __global__ void __launch_bounds__(WM_THREADS, 1) wm_persistent_kernel(WMParams p
 
 template <int R>
 cudaError_t launch_wm(WMParams& p, cudaStream_t st) {
-  const size_t smem = sizeof(WMShared<R>);
+  constexpr size_t XS_MAX = 160 * 1024;  // staged factor rows (n_max · r doubles)
+  const size_t base = (sizeof(WMShared<R>) + 15) & ~(size_t)15;
+  const size_t xs_bytes = (size_t)(p.n1 > p.n2 ? p.n1 : p.n2) * R * 8;
+  p.stage_x = xs_bytes <= XS_MAX ? 1 : 0;
+  const size_t smem = base + (p.stage_x ? xs_bytes : 0);
   static bool attr = false;
   if (!attr) {
     SMP_TRY(cudaFuncSetAttribute(wm_persistent_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem));
+                                 (int)(base + XS_MAX)));
     attr = true;
   }
   int dev = 0, sms = 0, per_sm = 0;

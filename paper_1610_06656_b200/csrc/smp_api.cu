@@ -312,6 +312,68 @@ smp_status sketch_dense_split(smp_handle* h, int64_t row0, int64_t rows, const v
   return SMP_OK;
 }
 
+// fp32 block through K1F (split fused into the sketch kernel): Π panel per
+// row chunk (κ-major, <= 512 MB), K1F, K2 over the 3 planes, norms.
+smp_status sketch_dense_f32_fused(smp_handle* h, int64_t row0, int64_t rows, const float* X, int64_t ldx,
+                                  int64_t n, int64_t col_off) {
+  using namespace smp;
+  const bool gauss = h->d.pi_kind == SMP_PI_GAUSSIAN;
+  const int k = h->k;
+  const int k_tiles = (k + 255) / 256;
+  const int64_t kpad = (int64_t)k_tiles * 256;
+  int64_t chunk = std::min<int64_t>(rows, (512ll << 20) / (kpad * 2));
+  chunk = std::max<int64_t>(64, (chunk / 64) * 64);
+  for (int64_t r0 = 0; r0 < rows; r0 += chunk) {
+    const int64_t rc = std::min(chunk, rows - r0);
+    SketchTCParams p{};
+    p.rows = rc;
+    p.row0 = row0 + r0;
+    p.n = (int32_t)n;
+    p.k = k;
+    p.n_tiles = (int32_t)((n + 127) / 128);
+    p.k_tiles = k_tiles;
+    p.kb_total = (int32_t)((rc + 63) / 64);
+    p.splits = choose_splits(2 * p.n_tiles * p.k_tiles, p.kb_total, gauss ? K1_MAX_KB_GAUSS : K1_MAX_KB);
+    p.kind = pi_code(h);
+    p.do_norms = 1;
+    p.seed = h->d.seed;
+    const int64_t ld = (int64_t)p.kb_total * 64;
+    CK(h, ensure(h->part, h->part_cap, (int64_t)p.splits * 3 * n * k), "alloc partials");
+    CK(h, ensure(h->pnorm, h->pnorm_cap, (int64_t)p.splits * p.k_tiles * n), "alloc pnorm");
+    CK(h, ensure(h->pi_panel, h->pi_panel_cap, kpad * ld), "alloc pi panel");
+    const bool cached = h->panel_row0 == p.row0 && h->panel_ld == ld && h->panel_kpad == kpad;
+    if (!cached) {
+      CK(h, launch_pi_panel_kmajor(p.kind, p.seed, k, (int)kpad, p.row0, ld, ld, h->pi_panel, h->st), "pi panel");
+      h->launches += 1;
+      h->panel_row0 = p.row0;
+      h->panel_ld = ld;
+      h->panel_kpad = kpad;
+    }
+    p.part = h->part;
+    p.pnorm = h->pnorm;
+    p.pi_panel = h->pi_panel;
+    p.pi_ld = ld;
+    p.debug = 0;
+    if (h->timing) {
+      while (h->ev_pool.size() < h->ev_used_n + 2) {
+        cudaEvent_t e;
+        CK(h, cudaEventCreate(&e), "event");
+        h->ev_pool.push_back(e);
+      }
+      CK(h, cudaEventRecord(h->ev_pool[h->ev_used_n], h->st), "event");
+    }
+    CK(h, launch_sketch_tc_f32(X + r0 * ldx, ldx, p, gauss ? 4 : 3, h->st), "sketch_tc_f32");
+    if (h->timing) {
+      CK(h, cudaEventRecord(h->ev_pool[h->ev_used_n + 1], h->st), "event");
+      h->ev_used_n += 2;
+    }
+    CK(h, launch_reduce_sketch(h->part, p.splits, 3, n, k, h->acc_sk + col_off * k, h->st), "reduce_sketch");
+    CK(h, launch_reduce_norms(h->pnorm, p.splits * p.k_tiles, n, h->acc_nrm + col_off, h->st), "reduce_norms");
+    h->launches += 3;
+  }
+  return SMP_OK;
+}
+
 // TMA needs a 16-byte aligned base and row pitch: repack unaligned bf16
 // blocks through the handle's staging buffer (device to device, chunked).
 smp_status sketch_dense_bf16_repack(smp_handle* h, int64_t row0, int64_t rows, const void* X,
@@ -478,6 +540,16 @@ smp_status smp_sketch_block(smp_handle* h, int64_t row0, int64_t rows, const voi
   // fp32
   if (reinterpret_cast<uintptr_t>(A) % 4 != 0 || (two && reinterpret_cast<uintptr_t>(B) % 4 != 0))
     return fail(h, SMP_EINVAL, "fp32 input must be 4-byte aligned");
+  static const bool fused = [] {  // SMP_F32_FUSED=0: materialised planes (reference path)
+    const char* e = getenv("SMP_F32_FUSED");
+    return !(e && atoi(e) == 0);
+  }();
+  auto ok16 = [](const void* q, int64_t ld) { return reinterpret_cast<uintptr_t>(q) % 16 == 0 && ld % 4 == 0; };
+  if (fused && ok16(A, lda) && (!two || ok16(B, ldb))) {
+    s = sketch_dense_f32_fused(h, row0, rows, static_cast<const float*>(A), lda, h->n1, 0);
+    if (s != SMP_OK || !two) return s;
+    return sketch_dense_f32_fused(h, row0, rows, static_cast<const float*>(B), ldb, h->n2, h->n1);
+  }
   s = sketch_dense_split(h, row0, rows, A, 0, lda, h->n1, 0);
   if (s != SMP_OK || !two) return s;
   return sketch_dense_split(h, row0, rows, B, 0, ldb, h->n2, h->n1);

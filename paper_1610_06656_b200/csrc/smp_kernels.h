@@ -29,6 +29,10 @@ cudaError_t launch_pi_panel_kmajor(int kind, uint64_t seed, int k, int kpad, int
                                    int64_t ld, uint16_t* panel, cudaStream_t st);
 cudaError_t launch_sketch_tc(const void* X, int64_t ldx, SketchTCParams p, cudaStream_t st);
 int sketch_tc_smem_bytes();
+// K1F (sketch_tc_f32.cu): fp32 X with the bf16 plane split fused in; Π from
+// p.pi_panel (required); mode 3 (±1 Π, 8+8+8 bits) or 4 (Gaussian, 4+8+8);
+// p.n = input columns, p.n_tiles = ceil(n / 128); part = [splits][3 n][k].
+cudaError_t launch_sketch_tc_f32(const float* X, int64_t ldx, SketchTCParams p, int mode, cudaStream_t st);
 
 // ---- K2 partial reduce, fp32 split, K4 finalize (reduce.cu)
 // acc[c][κ] += Σ_s Σ_pl part[s][pl*n + c][κ]   (planes pl = 0..planes-1)

@@ -497,19 +497,39 @@ cudaError_t csr_densify(CsrWorkspace& w, const int64_t* a_rowptr, const int32_t*
 
 // ---------------------------------------------------------------- driver
 __global__ void csr_bounds_kernel(const int64_t* __restrict__ arp, const int64_t* __restrict__ brp,
-                                  int rows, int rp, int npan, int64_t* __restrict__ out) {
+                                  int64_t rbase, int rows, int rp, int npan, int64_t* __restrict__ out) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i <= npan; i += gridDim.x * blockDim.x) {
-    const int r = i < npan ? i * rp : rows;
+    const int64_t r = rbase + (i < npan ? (int64_t)i * rp : rows);
     out[i] = arp[r] - arp[0];
     out[npan + 1 + i] = brp ? brp[r] - brp[0] : 0;
   }
+}
+
+// out[κ · ld + t_off + t] = pi[t · kp + κ] (κ < k; zero for k <= κ < kpad):
+// the row-major K3 panel transposed into the κ-major layout K1 (PANEL) reads,
+// so the head and the tail of the CSR sketch share one generation of Π.
+__global__ void pi_transpose_kernel(const uint16_t* __restrict__ pi, int kp, int k, int prow, int kpad,
+                                    uint16_t* __restrict__ out, int64_t ld, int64_t t_off) {
+  __shared__ uint16_t tile[64][66];
+  const int t0 = blockIdx.x * 64, c0 = blockIdx.y * 64;
+  for (int i = threadIdx.y; i < 64; i += blockDim.y)
+    for (int j = threadIdx.x; j < 64; j += blockDim.x) {
+      const int t = t0 + i, c = c0 + j;
+      tile[i][j] = (t < prow && c < k) ? pi[(int64_t)t * kp + c] : (uint16_t)0;
+    }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 64; i += blockDim.y)
+    for (int j = threadIdx.x; j < 64; j += blockDim.x) {
+      const int c = c0 + i, t = t0 + j;
+      if (c < kpad && t < prow) out[(int64_t)c * ld + t_off + t] = tile[j][i];
+    }
 }
 
 void csr_workspace_free(CsrWorkspace& w) {
   cudaFree(w.pi); cudaFree(w.keys_in); cudaFree(w.keys_out); cudaFree(w.vals_in);
   cudaFree(w.vals_out); cudaFree(w.cub_tmp); cudaFree(w.bounds_d); cudaFree(w.hist); cudaFree(w.offs);
   cudaFree(w.ne_dev); cudaFree(w.head_lut); cudaFree(w.head_map); cudaFree(w.head_cnt); cudaFree(w.head_flag);
-  cudaFree(w.xhead); cudaFree(w.head_tmp);
+  cudaFree(w.xhead); cudaFree(w.head_tmp); cudaFree(w.kmaj);
   if (w.head_h) cudaFreeHost(w.head_h);
   if (w.bounds_h) cudaFreeHost(w.bounds_h);
   w = CsrWorkspace{};
@@ -521,11 +541,39 @@ static int bits_for(int64_t x) {  // smallest b with 2^b > x
   return b;
 }
 
+int csr_panel_rows(int64_t ntot) {
+  const int cbits = bits_for(ntot - 1 > 0 ? ntot - 1 : 1);
+  return 1 << std::max(0, std::min(15, 32 - cbits));
+}
+
+cudaError_t csr_bounds(CsrWorkspace& w, const int64_t* a_rowptr, const int64_t* b_rowptr, int64_t ntot,
+                       int64_t rows, cudaStream_t st) {
+  const int rp = csr_panel_rows(ntot);
+  const int npan = (int)((rows + rp - 1) / rp);
+  CSR_TRY(grow(w.bounds_d, w.bounds_cap, 2 * (int64_t)(npan + 1)));
+  if (w.bounds_hcap < 2 * (int64_t)(npan + 1)) {
+    if (w.bounds_h) cudaFreeHost(w.bounds_h);
+    w.bounds_h = nullptr;
+    w.bounds_hcap = 0;
+    CSR_TRY(cudaMallocHost(&w.bounds_h, 2 * (size_t)(npan + 1) * 8));
+    w.bounds_hcap = 2 * (int64_t)(npan + 1);
+  }
+  csr_bounds_kernel<<<(npan + 256) / 256, 256, 0, st>>>(a_rowptr, b_rowptr, 0, (int)rows, rp, npan, w.bounds_d);
+  CSR_TRY(cudaMemcpyAsync(w.bounds_h, w.bounds_d, 2 * (size_t)(npan + 1) * 8, cudaMemcpyDeviceToHost, st));
+  CSR_TRY(cudaStreamSynchronize(st));
+  w.bounds_npan = npan;
+  w.bounds_rp = rp;
+  w.bounds_pre = true;
+  return cudaSuccess;
+}
+
+
 cudaError_t launch_sketch_csr(CsrWorkspace& w, int kind, uint64_t seed, int k, int64_t row0,
                               int64_t rows, const int64_t* a_rowptr, const int32_t* a_col,
                               const float* a_val, int64_t a_n, const int64_t* b_rowptr,
                               const int32_t* b_col, const float* b_val, int64_t b_n, float* acc_sk,
-                              double* acc_nrm, int* status, cudaStream_t st, const int32_t* head_lut) {
+                              double* acc_nrm, int* status, cudaStream_t st, const int32_t* head_lut,
+                              int64_t rbase, uint16_t* kmaj, int64_t kmaj_ld, int kpad) {
   if (rows <= 0) return cudaSuccess;
   const int64_t ntot = a_n + (b_rowptr ? b_n : 0);
   const int cbits = bits_for(ntot - 1 > 0 ? ntot - 1 : 1);
@@ -535,20 +583,31 @@ cudaError_t launch_sketch_csr(CsrWorkspace& w, int kind, uint64_t seed, int k, i
   const int rp = 1 << tbits;                      // panel rows
   const int kp = (k + 7) & ~7;
   const int npan = (int)((rows + rp - 1) / rp);
-  // panel entry boundaries (one D2H read per block)
-  CSR_TRY(grow(w.bounds_d, w.bounds_cap, 2 * (int64_t)(npan + 1)));
-  if (w.bounds_hcap < 2 * (int64_t)(npan + 1)) {
-    if (w.bounds_h) cudaFreeHost(w.bounds_h);
-    w.bounds_h = nullptr;
-    w.bounds_hcap = 0;
-    CSR_TRY(cudaMallocHost(&w.bounds_h, 2 * (size_t)(npan + 1) * 8));
-    w.bounds_hcap = 2 * (int64_t)(npan + 1);
+  const int64_t* ab;
+  const int64_t* bb;
+  if (w.bounds_pre) {
+    // boundaries of the whole block, read back once by csr_bounds()
+    if (rbase % rp != 0 || w.bounds_rp != rp) return cudaErrorInvalidValue;
+    const int64_t pb = rbase / rp;
+    ab = w.bounds_h + pb;
+    bb = w.bounds_h + (w.bounds_npan + 1) + pb;
+  } else {
+    // panel entry boundaries (one D2H read per call)
+    CSR_TRY(grow(w.bounds_d, w.bounds_cap, 2 * (int64_t)(npan + 1)));
+    if (w.bounds_hcap < 2 * (int64_t)(npan + 1)) {
+      if (w.bounds_h) cudaFreeHost(w.bounds_h);
+      w.bounds_h = nullptr;
+      w.bounds_hcap = 0;
+      CSR_TRY(cudaMallocHost(&w.bounds_h, 2 * (size_t)(npan + 1) * 8));
+      w.bounds_hcap = 2 * (int64_t)(npan + 1);
+    }
+    csr_bounds_kernel<<<(npan + 256) / 256, 256, 0, st>>>(a_rowptr, b_rowptr, rbase, (int)rows, rp, npan,
+                                                         w.bounds_d);
+    CSR_TRY(cudaMemcpyAsync(w.bounds_h, w.bounds_d, 2 * (size_t)(npan + 1) * 8, cudaMemcpyDeviceToHost, st));
+    CSR_TRY(cudaStreamSynchronize(st));
+    ab = w.bounds_h;
+    bb = w.bounds_h + npan + 1;
   }
-  csr_bounds_kernel<<<(npan + 256) / 256, 256, 0, st>>>(a_rowptr, b_rowptr, (int)rows, rp, npan, w.bounds_d);
-  CSR_TRY(cudaMemcpyAsync(w.bounds_h, w.bounds_d, 2 * (size_t)(npan + 1) * 8, cudaMemcpyDeviceToHost, st));
-  CSR_TRY(cudaStreamSynchronize(st));
-  const int64_t* ab = w.bounds_h;
-  const int64_t* bb = w.bounds_h + npan + 1;
   int64_t max_ent = 0;
   for (int p = 0; p < npan; ++p) max_ent = std::max(max_ent, (ab[p + 1] - ab[p]) + (bb[p + 1] - bb[p]));
   CSR_TRY(grow(w.pi, w.pi_cap, (int64_t)rp * kp));
@@ -598,29 +657,35 @@ cudaError_t launch_sketch_csr(CsrWorkspace& w, int kind, uint64_t seed, int k, i
       const int64_t groups = ((row0 + p0 + prow - 1) / 4 - (row0 + p0) / 4 + 1) * kp;
       const int blocks = (int)std::min<int64_t>((groups + 255) / 256, 148 * 16);
       pi_panel_kernel<<<blocks, 256, 0, st>>>(kind, seed, k, kp, row0 + p0, prow, w.pi);
+      if (kmaj) {
+        dim3 tg((unsigned)((prow + 63) / 64), (unsigned)((kpad + 63) / 64));
+        pi_transpose_kernel<<<tg, dim3(32, 8), 0, st>>>(w.pi, kp, k, prow, kpad, kmaj, kmaj_ld, p0);
+        w.launches += 1;
+      }
     }
+    const int64_t pr = rbase + p0;   // rowptr index of the panel's first row
     if (prof) CSR_TRY(cudaEventRecord(pev[1], st));
     if (ne == 0) continue;
     if (counting) {
       const size_t sm = (size_t)ntot * 4;
       csr_hist_kernel<<<CSR_HIST_CTAS, CSR_T_THREADS, sm, st>>>(a_rowptr, a_col, a_val, a_n, b_rowptr,
-                                                                b_col, b_val, b_n, p0, prow, (int)ntot,
+                                                                b_col, b_val, b_n, pr, prow, (int)ntot,
                                                                 head_lut, w.hist);
       size_t tmp = (size_t)w.cub_cap;
       CSR_TRY(cub::DeviceScan::ExclusiveSum(w.cub_tmp, tmp, w.hist, w.offs,
                                             (int)(ntot * (int64_t)CSR_HIST_CTAS), st));
       csr_scatter_kernel<<<CSR_HIST_CTAS, CSR_T_THREADS, sm, st>>>(a_rowptr, a_col, a_val, a_n, b_rowptr,
-                                                                   b_col, b_val, b_n, p0, prow, (int)ntot,
+                                                                   b_col, b_val, b_n, pr, prow, (int)ntot,
                                                                    tbits, head_lut, w.offs, w.keys_out,
                                                                    w.vals_out, status);
       csr_total_kernel<<<1, 32, 0, st>>>(w.hist, w.offs, ntot * (int64_t)CSR_HIST_CTAS, w.ne_dev);
     } else {
       const int kb_blocks = (int)std::min<int64_t>((prow + 7) / 8, 148 * 16);
       // A: entries ab[p] .. ab[p+1] (relative to a_rowptr[0]) -> keys[0 .. na)
-      csr_keys_kernel<<<kb_blocks, 256, 0, st>>>(a_rowptr, a_col, a_val, p0, prow, ab[p], 0u, tbits,
+      csr_keys_kernel<<<kb_blocks, 256, 0, st>>>(a_rowptr, a_col, a_val, pr, prow, ab[p], 0u, tbits,
                                                  a_n, w.keys_in, w.vals_in, status);
       if (b_rowptr && nb > 0)
-        csr_keys_kernel<<<kb_blocks, 256, 0, st>>>(b_rowptr, b_col, b_val, p0, prow, bb[p] - na,
+        csr_keys_kernel<<<kb_blocks, 256, 0, st>>>(b_rowptr, b_col, b_val, pr, prow, bb[p] - na,
                                                    (uint32_t)a_n, tbits, b_n, w.keys_in, w.vals_in, status);
       size_t tmp = (size_t)w.cub_cap;
       CSR_TRY(cub::DeviceRadixSort::SortPairs(w.cub_tmp, tmp, w.keys_in, w.keys_out, w.vals_in, w.vals_out,

@@ -623,6 +623,7 @@ smp_status smp_sketch_block_csr(smp_handle* h, int64_t row0, int64_t rows, const
   (void)a_nnz; (void)b_nnz;
   h->finalized = false;
   const int64_t l0 = h->csr.launches;
+  h->csr.bounds_pre = false;
   h->csr.ev_pool = nullptr;
   h->csr.ev_used = &h->ev_used_n;
   // tensor-core head (K3): columns with density >= δ whose
@@ -639,23 +640,43 @@ smp_status smp_sketch_block_csr(smp_handle* h, int64_t row0, int64_t rows, const
                                two ? b_col : nullptr, b_n, rows, head_density, &n_head, h->st),
        "csr head");
     if (n_head > 0) {
+      // per head chunk: the tail K3 over the chunk's rows (which generates
+      // each Π panel once and also transposes it into the κ-major head panel),
+      // then densify + K1 (PANEL) on the head with that panel
       lut = h->csr.head_lut;
       const int64_t ldh = ((n_head + 63) / 64) * 64;
       const int64_t kpad = ((h->k + 255) / 256) * 256;
+      const int64_t rp = smp::csr_panel_rows(a_n + b_n);
       int64_t chunk = std::min<int64_t>(rows, (1ll << 30) / (ldh * 2));            // 1 GB dense chunk
       chunk = std::min<int64_t>(chunk, (512ll << 20) / (kpad * 2));                // 512 MB Π panel
-      chunk = std::max<int64_t>(64, (chunk / 64) * 64);
-      CK(h, ensure(h->csr.xhead, h->csr.xhead_cap, ((chunk + 63) / 64) * 64 * ldh), "alloc head");
+      chunk = std::max<int64_t>(rp, (chunk / rp) * rp);
+      const int64_t cpad = ((std::min(chunk, rows) + 63) / 64) * 64;
+      CK(h, ensure(h->csr.xhead, h->csr.xhead_cap, cpad * ldh), "alloc head");
+      CK(h, ensure(h->csr.kmaj, h->csr.kmaj_cap, kpad * cpad), "alloc head panel");
+      h->csr.ev_pool = h->timing ? &h->ev_pool : nullptr;
+      CK(h, smp::csr_bounds(h->csr, a_rowptr, two ? b_rowptr : nullptr, a_n + b_n, rows, h->st), "bounds");
       for (int64_t r0 = 0; r0 < rows; r0 += chunk) {
         const int64_t rc = std::min(chunk, rows - r0);
+        const int64_t ldk = ((rc + 63) / 64) * 64;
+        if (rc != ldk) CK(h, cudaMemsetAsync(h->csr.kmaj, 0, kpad * ldk * 2, h->st), "memset");
+        cudaError_t e1 = smp::launch_sketch_csr(h->csr, pi_code(h), h->d.seed, h->k, row0 + r0, rc, a_rowptr,
+                                                a_col, a_val, h->n1, two ? b_rowptr : nullptr,
+                                                two ? b_col : nullptr, two ? b_val : nullptr, b_n,
+                                                h->acc_sk, h->acc_nrm, h->status, h->st, lut, r0,
+                                                h->csr.kmaj, ldk, (int)kpad);
+        if (e1 != cudaSuccess) h->csr.bounds_pre = false;
+        CK(h, e1, "sketch_csr");
         CK(h, smp::csr_densify(h->csr, a_rowptr, a_col, a_val, a_n, two ? b_rowptr : nullptr,
                                two ? b_col : nullptr, two ? b_val : nullptr, b_n, r0, rc, ldh,
                                h->csr.xhead, h->st),
            "densify");
         smp_status s2 = sketch_dense_bf16(h, row0 + r0, rc, h->csr.xhead, ldh, n_head, 1, 0, true,
-                                          nullptr, h->csr.head_map);
+                                          h->csr.kmaj, h->csr.head_map);
         if (s2 != SMP_OK) return s2;
       }
+      h->csr.bounds_pre = false;
+      h->launches += 2 + (h->csr.launches - l0);
+      return SMP_OK;
     }
   }
   h->csr.ev_pool = h->timing ? &h->ev_pool : nullptr;

@@ -96,13 +96,13 @@ __device__ __forceinline__ void gauss_pair(uint32_t wa, uint32_t wb, uint16_t& z
   float sp = __fmaf_rn(__fmaf_rn(__fmaf_rn(__fmaf_rn(S9, x2, S7), x2, S5), x2, S3), x2, S1);
   float sn = __fmul_rn(x, sp);
   float cs = __fmaf_rn(__fmaf_rn(__fmaf_rn(__fmaf_rn(__fmaf_rn(C10, x2, C8), x2, C6), x2, C4), x2, C2), x2, 1.0f);
-  float c, s;
-  switch (qn & 3u) {
-    case 0: c = cs; s = sn; break;
-    case 1: c = -sn; s = cs; break;
-    case 2: c = -cs; s = -sn; break;
-    default: c = sn; s = -cs; break;
-  }
+  // rotate by the quadrant (branch-free; negation is exact, so the values
+  // equal the case analysis (cs, sn), (−sn, cs), (−cs, −sn), (sn, −cs))
+  const uint32_t qq = qn & 3u;
+  const float a = (qq & 1u) ? sn : cs;
+  const float b = (qq & 1u) ? cs : sn;
+  const float c = ((qq + 1u) & 2u) ? -a : a;
+  const float s = (qq & 2u) ? -b : b;
   z0 = bf16_rne_bits(__fmul_rn(rho, c));
   z1 = bf16_rne_bits(__fmul_rn(rho, s));
 }

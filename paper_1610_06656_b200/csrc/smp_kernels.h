@@ -81,12 +81,17 @@ struct CsrWorkspace {
   int64_t head_lut_cap = 0, head_map_cap = 0, head_cnt_cap = 0, head_flag_cap = 0, head_tmp_cap = 0;
   uint16_t* xhead = nullptr;      // dense head chunk (bf16)
   int64_t xhead_cap = 0;
+  uint16_t* kmaj = nullptr;       // κ-major Π of the head chunk (transposed K3 panels)
+  int64_t kmaj_cap = 0;
   int64_t* head_h = nullptr;      // pinned
 
   int64_t* bounds_d = nullptr;
   int64_t bounds_cap = 0;
   int64_t* bounds_h = nullptr;    // pinned
   int64_t bounds_hcap = 0;
+  bool bounds_pre = false;        // bounds_h holds the whole block's panel boundaries
+  int64_t bounds_npan = 0;
+  int bounds_rp = 0;
   int64_t launches = 0;           // kernels launched (counter for the bench)
   // timing of the dominant kernel (K3d) with CUDA events on the launching
   // stream: pairs appended to *ev_pool from index *ev_used (null: off)
@@ -103,8 +108,17 @@ cudaError_t launch_sketch_csr(CsrWorkspace& w, int kind, uint64_t seed, int k, i
                               const float* a_val, int64_t a_n, const int64_t* b_rowptr,
                               const int32_t* b_col, const float* b_val, int64_t b_n, float* acc_sk,
                               double* acc_nrm, int* status, cudaStream_t st,
-                              const int32_t* head_lut = nullptr);
+                              const int32_t* head_lut = nullptr, int64_t rbase = 0,
+                              uint16_t* kmaj = nullptr, int64_t kmaj_ld = 0, int kpad = 0);
+// (rbase: the call covers rowptr rows [rbase, rbase + rows) of the block,
+// global row0 = the global row of rowptr row rbase; kmaj: also transpose each
+// generated Π panel into kmaj[κ][t - row0] (ld kmaj_ld, kpad κ rows) for K1)
 void csr_workspace_free(CsrWorkspace& w);
+int csr_panel_rows(int64_t ntot);  // rows of one K3 Π panel (2^15 for up to 2^17 columns)
+// read back every panel's entry boundaries for rows [0, rows) of the block
+// once (one sync) so that per-chunk launch_sketch_csr calls need none
+cudaError_t csr_bounds(CsrWorkspace& w, const int64_t* a_rowptr, const int64_t* b_rowptr, int64_t ntot,
+                       int64_t rows, cudaStream_t st);
 // head columns: count nonzeros per column over the block, select columns with
 // count >= density * rows (slots in column order) -> w.head_lut / w.head_map;
 // *n_head = number of slots (synchronises)

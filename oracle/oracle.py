@@ -53,6 +53,8 @@ def _get():
                                        ctypes.c_int, i64, P, P]
         lib.or_sketch_csr.argtypes = [ctypes.c_int, u64, ctypes.c_int, i64, i64, i64, P, P, P,
                                       P, P]
+        lib.or_sample_multinomial.argtypes = [u64, f64, i64, i64, P, P, i64, P, P, P]
+        lib.or_sample_multinomial.restype = i64
         lib.or_srht_row.argtypes = [u64, ctypes.c_int, i64]
         lib.or_srht_row.restype = i64
         lib.or_srht_sign.argtypes = [u64, i64]
@@ -235,6 +237,24 @@ def sample(seed, m, alpha, beta, cap=None):
         J = np.empty(max(cap, 1), np.int32)
         q = np.empty(max(cap, 1), np.float64)
         cnt = lib.or_sample(seed, m, n1, n2, _p(alpha), _p(beta), cap, _p(I), _p(J), _p(q))
+        if cnt <= cap:
+            return I[:cnt].copy(), J[:cnt].copy(), q[:cnt].copy()
+        cap = int(cnt)
+
+
+def sample_multinomial(seed, m, alpha, beta):
+    """Ω by the appendix's row-multinomial sampler (R27): draws
+    with replacement, sorted by (i, j), and q = m(α_i + β_j) unclipped."""
+    alpha = _c(alpha, np.float64)
+    beta = _c(beta, np.float64)
+    n1, n2 = len(alpha), len(beta)
+    lib = _get()
+    cap = int(m + 10 * np.sqrt(max(m, 1.0)) + 1024)
+    while True:
+        I = np.empty(max(cap, 1), np.int32)
+        J = np.empty(max(cap, 1), np.int32)
+        q = np.empty(max(cap, 1), np.float64)
+        cnt = lib.or_sample_multinomial(seed, m, n1, n2, _p(alpha), _p(beta), cap, _p(I), _p(J), _p(q))
         if cnt <= cap:
             return I[:cnt].copy(), J[:cnt].copy(), q[:cnt].copy()
         cap = int(cnt)

@@ -396,6 +396,65 @@ double or_qhat(double m, double alpha_i, double beta_j)
     return q < 1.0 ? q : 1.0;
 }
 
+/* ------------------------------------------------------------------------ */
+/* Row-multinomial sampler (the paper's appendix; SURVEY §8f      */
+/* NEXT-2; R27).  With α, β from or_alpha_beta (Eq. 1, R6):       */
+/*   Bpre[j] = β_0 + ... + β_j (sequential, fp64); T_i = n2·α_i + Bpre[n2-1] */
+/*   m_i = m·T_i (= m(‖A_i‖²/(2‖A‖_F²) + 1/(2n1)), the appendix's m_i);     */
+/*   M_i = floor(m_i + u_i), u_i = U53(Philox(i, 0, 0, 8)) 2^-53;           */
+/*   draw d of row i: u = U53(Philox(i, d, 0, 9)) 2^-53, target = u·T_i,     */
+/*   j = the smallest column with C_i(j) = (j+1)·α_i + Bpre[j] > target      */
+/*   (n2-1 if none): inversion of the CDF of q̃_ij ∝ α_i + β_j.     */
+/* Draws are with replacement; output sorted by (i, j), duplicates kept,     */
+/* q = m(α_i + β_j) unclipped (each draw's weight is 1/q: a pair's expected  */
+/* count is q, the Bernoulli inclusion probability when q <= 1).             */
+/* ------------------------------------------------------------------------ */
+static double u53(uint64_t seed, uint32_t c0, uint32_t c1, uint32_t tag)
+{
+    uint32_t w[4];
+    philox_seed(seed, c0, c1, 0u, tag, w);
+    uint64_t v = (((uint64_t)w[1] << 32) | (uint64_t)w[0]) >> 11;
+    return (double)v * 0x1p-53;
+}
+
+static int cmp_i32(const void *a, const void *b)
+{
+    int32_t x = *(const int32_t *)a, y = *(const int32_t *)b;
+    return (x > y) - (x < y);
+}
+
+int64_t or_sample_multinomial(uint64_t seed, double m, int64_t n1, int64_t n2, const double *alpha,
+                              const double *beta, int64_t cap, int32_t *I, int32_t *J, double *q)
+{
+    double *bpre = (double *)malloc(sizeof(double) * (size_t)(n2 > 0 ? n2 : 1));
+    double acc = 0.0;
+    for (int64_t j = 0; j < n2; ++j) { acc = acc + beta[j]; bpre[j] = acc; }
+    const double btot = n2 > 0 ? bpre[n2 - 1] : 0.0;
+    int64_t cnt = 0;
+    for (int64_t i = 0; i < n1; ++i) {
+        const double T = (double)n2 * alpha[i] + btot;
+        const double mi = m * T;
+        const int64_t Mi = (int64_t)floor(mi + u53(seed, (uint32_t)i, 0u, 8u));
+        const int64_t c0 = cnt;
+        for (int64_t d = 0; d < Mi; ++d) {
+            const double target = u53(seed, (uint32_t)i, (uint32_t)d, 9u) * T;
+            int64_t lo = 0, hi = n2 - 1;            /* first j with C(j) > target, else n2-1 */
+            while (lo < hi) {
+                const int64_t mid = (lo + hi) / 2;
+                const double c = (double)(mid + 1) * alpha[i] + bpre[mid];
+                if (c > target) hi = mid; else lo = mid + 1;
+            }
+            if (cnt < cap) { I[cnt] = (int32_t)i; J[cnt] = (int32_t)lo; }
+            ++cnt;
+        }
+        if (cnt <= cap && cnt > c0) qsort(J + c0, (size_t)(cnt - c0), sizeof(int32_t), cmp_i32);
+    }
+    if (cnt <= cap)
+        for (int64_t s = 0; s < cnt; ++s) q[s] = m * (alpha[I[s]] + beta[J[s]]);
+    free(bpre);
+    return cnt;
+}
+
 /* Bernoulli draw for pair (i,j): U53 from Philox(ctr=(i,j,0,3), key=seed).  */
 int or_draw(uint64_t seed, int64_t i, int64_t j, double qhat)
 {

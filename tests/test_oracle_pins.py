@@ -638,3 +638,72 @@ def test_srht_jl_band():
     sk, n2 = oracle.sketch_rows(kind, 11, k, X)
     ratio = (sk ** 2).sum(1) / k / n2
     assert np.all(np.abs(ratio - 1) < 0.5) and abs(ratio.mean() - 1) < 0.1
+
+
+# ------------------------------------------------------------------ row-multinomial Ω (NEXT-2, R27)
+def _ab(n1, n2, seed):
+    rng = np.random.default_rng(seed)
+    a2 = rng.exponential(size=n1) ** 2
+    b2 = rng.exponential(size=n2) ** 2
+    return oracle.alpha_beta(a2, b2, oracle.pairwise_sum(a2), oracle.pairwise_sum(b2))
+
+
+def test_multinomial_row_counts_match_appendix():
+    """E[M_i] = m_i = m(‖A_i‖²/(2‖A‖_F²) + 1/(2 n1)) and Σ_i m_i = m."""
+    n1, n2, m = 40, 30, 500.0
+    al, be = _ab(n1, n2, 1)
+    mi = m * (n2 * al + be.sum())
+    assert abs(mi.sum() - m) < 1e-9 * m
+    counts = np.zeros(n1)
+    seeds = 400
+    for s in range(seeds):
+        I, J, q = oracle.sample_multinomial(s, m, al, be)
+        counts += np.bincount(I, minlength=n1)
+        assert np.all(np.diff(I) >= 0)
+        same = I[1:] == I[:-1]
+        assert np.all(J[1:][same] >= J[:-1][same])       # sorted by (i, j)
+        np.testing.assert_allclose(q, m * (al[I] + be[J]), rtol=1e-15)
+    est = counts / seeds
+    # M_i = floor(m_i + u): |mean - m_i| within a few standard errors (var <= 1/4)
+    assert np.all(np.abs(est - mi) < 5 * 0.5 / np.sqrt(seeds) + 1e-12)
+
+
+def test_multinomial_draws_follow_q_tilde():
+    """Within a row, columns are drawn ∝ α_i + β_j: expected count of
+    (i, j) per draw-set = m(α_i + β_j) = q_ij; chi-squared over seeds."""
+    n1, n2, m = 3, 25, 2000.0
+    al, be = _ab(n1, n2, 2)
+    freq = np.zeros((n1, n2))
+    seeds = 60
+    for s in range(seeds):
+        I, J, _ = oracle.sample_multinomial(s + 1000, m, al, be)
+        np.add.at(freq, (I, J), 1)
+    expect = seeds * m * (al[:, None] + be[None, :])
+    chi2 = ((freq - expect) ** 2 / expect).sum()
+    dof = n1 * n2
+    assert chi2 < dof + 5 * np.sqrt(2 * dof)
+
+
+def test_multinomial_inversion_matches_linear_search():
+    """The binary search returns the first j with C_i(j) > u T_i — checked
+    against a linear scan of the same fp64 CDF values (the definition)."""
+    n1, n2, m, seed = 6, 50, 300.0, 7
+    al, be = _ab(n1, n2, 3)
+    I, J, _ = oracle.sample_multinomial(seed, m, al, be)
+    bpre = np.cumsum(be)       # sequential fp64 sums, as the definition
+    key = [seed & 0xFFFFFFFF, seed >> 32]
+    got = {}
+    for i in range(n1):
+        T = n2 * al[i] + bpre[-1]
+        w = oracle.philox4x32_10([i, 0, 0, 8], key)
+        Mi = int(np.floor(m * T + ((int(w[1]) << 32 | int(w[0])) >> 11) * 2.0 ** -53))
+        cols = []
+        for d in range(Mi):
+            w = oracle.philox4x32_10([i, d, 0, 9], key)
+            target = ((int(w[1]) << 32 | int(w[0])) >> 11) * 2.0 ** -53 * T
+            C = (np.arange(1, n2 + 1) * al[i]) + bpre
+            hits = np.nonzero(C > target)[0]
+            cols.append(int(hits[0]) if len(hits) else n2 - 1)
+        got[i] = sorted(cols)
+    for i in range(n1):
+        assert list(J[I == i]) == got[i]

@@ -256,6 +256,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--init-iters", type=int, default=30)
+    ap.add_argument("--sampler", default="bernoulli", choices=["bernoulli", "multinomial"],
+                    help="Ω sampler: Alg. 1's Bernoulli sweep or the appendix's row-multinomial (NEXT-2)")
     ap.add_argument("--pi", default=None, choices=["rademacher", "gaussian", "srht"],
                     help="override the config's Π (e.g. srht, the paper's Spark sketch; NEXT-1)")
     args = ap.parse_args()
@@ -330,7 +332,7 @@ def main():
         combine()
         sk.finalize()
         evs[1].record(stream)
-        I, J, val, qh = sk.sample_estimate(m, cfg["seed"])
+        I, J, val, qh = sk.sample_estimate(m, cfg["seed"], sampler=args.sampler)
         U, V = sk.waltmin(I, J, val, qh, r, T, init_iters=args.init_iters, seed=cfg["seed"])
         if host is not None:
             Uh, Vh = U.cpu(), V.cpu()  # D2H of the result
@@ -481,7 +483,7 @@ def main():
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": dtype_name(cfg), "data": "synthetic",
             "config": {"workload": cfgname, "d": d, "n1": n1, "n2": n2, "k": k,
-                       "pi": cfg["pi"], "r": r, "T": T, "m": m, "omega": nomega,
+                       "pi": cfg["pi"], "r": r, "T": T, "m": m, "omega": nomega, "sampler": args.sampler,
                        "init_iters": args.init_iters, "a_is_b": a_is_b,
                        "parallelism": f"row-shard x{world} + NCCL all-reduce" if world > 1 else "1 GPU",
                        "l2": "inputs (%.1f GB) larger than the 126 MB L2; no flush" % (total_bytes / 1e9),

@@ -148,6 +148,17 @@ SMP_API smp_status smp_finalize_norms(smp_handle* h, float* A_sk, float* B_sk, d
  * cap = capacity of the output arrays.  Synchronises (to return *count).
  * Errors: SMP_EINVAL (m <= 0, not finalized), SMP_ECAPACITY (|Ω| > cap;
  * nothing written; call again with cap >= *count). */
+/* Ω samplers: the Bernoulli hash sweep of Alg. 1 line 3 (n1·n2 draws,
+ * bit-exact, q̂ = min(1, q)) or the appendix's row-multinomial sampler
+ * (R27; O(n1 + m log n2): M_i = floor(m_i + u) draws of
+ * row i with replacement, column by CDF inversion of q̃_ij ∝ α_i + β_j;
+ * duplicates kept; qhat = q = m(α_i + β_j) unclipped, each draw weighted
+ * 1/q by smp_waltmin). */
+enum { SMP_SAMPLER_BERNOULLI = 0, SMP_SAMPLER_MULTINOMIAL = 1 };
+SMP_API smp_status smp_sample_estimate_ex(smp_handle* h, double m, uint64_t seed, int32_t est,
+                                          int32_t sampler, int64_t cap, int32_t* I, int32_t* J,
+                                          float* val, double* qhat, int64_t* count);
+
 SMP_API smp_status smp_sample_estimate(smp_handle* h, double m, uint64_t seed, int32_t est, int64_t cap,
                                int32_t* I, int32_t* J, float* val, double* qhat, int64_t* count);
 

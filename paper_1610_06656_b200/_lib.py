@@ -17,12 +17,13 @@ PI_RADEMACHER, PI_GAUSSIAN, PI_HADAMARD_TEST, PI_SRHT = 0, 1, 2, 3
 IN_DENSE_BF16, IN_DENSE_F32, IN_CSR_F32 = 0, 1, 2
 EST_RESCALED, EST_PLAIN = 0, 1
 PART_REUSE_ALL = 0
+SAMPLER_BERNOULLI, SAMPLER_MULTINOMIAL = 0, 1
 
 EXPORTS = [
     "smp_sketch_init", "smp_sketch_block", "smp_sketch_block_host", "smp_sketch_block_csr",
     "smp_sketch_partials", "smp_finalize_norms", "smp_sample_estimate", "smp_waltmin",
     "smp_sketch_reset", "smp_kernel_launches", "smp_destroy", "smp_last_error", "smp_status_str",
-    "smp_set_timing", "smp_kernel_timing",
+    "smp_set_timing", "smp_kernel_timing", "smp_sample_estimate_ex",
 ]
 
 
@@ -75,6 +76,7 @@ def load(path: str = None):
                                         ctypes.POINTER(P), ctypes.POINTER(i64)]
     lib.smp_finalize_norms.argtypes = [H, P, P, P, P, P, P, P]
     lib.smp_sample_estimate.argtypes = [H, f64, u64, i32, i64, P, P, P, P, ctypes.POINTER(i64)]
+    lib.smp_sample_estimate_ex.argtypes = [H, f64, u64, i32, i32, i64, P, P, P, P, ctypes.POINTER(i64)]
     lib.smp_waltmin.argtypes = [H, P, P, P, P, i64, ctypes.POINTER(WaltminDesc), P, P]
     lib.smp_sketch_reset.argtypes = [H]
     lib.smp_set_timing.argtypes = [H, i32]

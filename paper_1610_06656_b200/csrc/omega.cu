@@ -11,6 +11,7 @@
 // q̂ — and therefore Ω — is bit-identical to the written definition.
 // Ω is produced in (i,j) order by a count pass, an exclusive scan of block
 // counts and a write pass that recomputes the same draws.
+#include <cub/device/device_segmented_radix_sort.cuh>
 #include "smp_device.cuh"
 #include "smp_kernels.h"
 
@@ -213,6 +214,107 @@ cudaError_t launch_sddmm(const float* Ask, const float* Bsk, const double* DA, c
   int blocks = (int)std::min<int64_t>((cap + 7) / 8, 148 * 16);
   if (blocks < 1) blocks = 1;
   sddmm_kernel<<<blocks, 256, 0, st>>>(Ask, Bsk, DA, DB, k, I, J, total, cap, plain, val);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- K5m
+// Row-multinomial Ω (the paper's appendix sampler; DESIGN.md
+// R27; NEXT-2): O(n1 + m log n2) work instead of the n1·n2 Bernoulli sweep.
+// fp64 with explicit rounding (no contraction) so the draws are bit-exact
+// with the written definition.
+enum : uint32_t { TAG_MN_COUNT = 8, TAG_MN_DRAW = 9 };
+
+__device__ __forceinline__ double u53_of(uint32_t k0, uint32_t k1, uint32_t c0, uint32_t c1, uint32_t tag) {
+  const u32x4 w = philox4x32_10(c0, c1, 0u, tag, k0, k1);
+  const uint64_t v = (((uint64_t)w.y << 32) | (uint64_t)w.x) >> 11;
+  return __dmul_rn(__ull2double_rn(v), 0x1p-53);
+}
+
+// Bpre[j] = β_0 + ... + β_j, sequential (the definition's order)
+__global__ void mn_prefix_kernel(const double* __restrict__ beta, int64_t n2, double* __restrict__ bpre) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    double acc = 0.0;
+    for (int64_t j = 0; j < n2; ++j) { acc = __dadd_rn(acc, beta[j]); bpre[j] = acc; }
+  }
+}
+
+// counts[i] = M_i = floor(m·T_i + u_i), T_i = n2·α_i + Bpre[n2-1]
+__global__ void mn_count_kernel(const double* __restrict__ alpha, const double* __restrict__ bpre, int64_t n1,
+                                int64_t n2, double m, uint64_t seed, int64_t* __restrict__ counts) {
+  const uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
+  const double btot = n2 > 0 ? bpre[n2 - 1] : 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= n1; i += (int64_t)gridDim.x * blockDim.x) {
+    if (i == n1) { counts[n1] = 0; continue; }   // -> offs[n1] = total after the scan
+    const double T = __dadd_rn(__dmul_rn((double)n2, alpha[i]), btot);
+    const double mi = __dmul_rn(m, T);
+    counts[i] = (int64_t)floor(__dadd_rn(mi, u53_of(k0, k1, (uint32_t)i, 0u, TAG_MN_COUNT)));
+  }
+}
+
+// warp per row, lanes over the row's draws: CDF inversion by binary search
+__global__ void mn_draw_kernel(const double* __restrict__ alpha, const double* __restrict__ bpre, int64_t n1,
+                               int64_t n2, uint64_t seed, const int64_t* __restrict__ offs,
+                               const int64_t* __restrict__ total, int64_t cap, int32_t* __restrict__ I,
+                               int32_t* __restrict__ Jtmp) {
+  if (*total > cap) return;
+  const uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const double btot = n2 > 0 ? bpre[n2 - 1] : 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); i < n1; i += nw) {
+    const int64_t o0 = offs[i], o1 = offs[i + 1];
+    const double ai = alpha[i];
+    const double T = __dadd_rn(__dmul_rn((double)n2, ai), btot);
+    for (int64_t d = lane; d < o1 - o0; d += 32) {
+      const double target = __dmul_rn(u53_of(k0, k1, (uint32_t)i, (uint32_t)d, TAG_MN_DRAW), T);
+      int64_t lo = 0, hi = n2 - 1;
+      while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        const double c = __dadd_rn(__dmul_rn((double)(mid + 1), ai), bpre[mid]);
+        if (c > target) hi = mid; else lo = mid + 1;
+      }
+      I[o0 + d] = (int32_t)i;
+      Jtmp[o0 + d] = (int32_t)lo;
+    }
+  }
+}
+
+// q = m(α_i + β_j), unclipped (the weight of each draw is 1/q)
+__global__ void mn_q_kernel(const double* __restrict__ alpha, const double* __restrict__ beta,
+                            const int32_t* __restrict__ I, const int32_t* __restrict__ J, double m,
+                            const int64_t* __restrict__ total, int64_t cap, double* __restrict__ q) {
+  if (*total > cap) return;
+  const int64_t cnt = *total;
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < cnt; s += (int64_t)gridDim.x * blockDim.x)
+    q[s] = __dmul_rn(m, __dadd_rn(alpha[I[s]], beta[J[s]]));
+}
+
+cudaError_t launch_mn_counts(const double* alpha, const double* beta, int64_t n1, int64_t n2, double m,
+                             uint64_t seed, double* bpre, int64_t* counts, int64_t* total, cudaStream_t st) {
+  mn_prefix_kernel<<<1, 32, 0, st>>>(beta, n2, bpre);
+  const int blocks = (int)std::min<int64_t>((n1 + 256) / 256, 1024);
+  mn_count_kernel<<<std::max(blocks, 1), 256, 0, st>>>(alpha, bpre, n1, n2, m, seed, counts);
+  scan_counts_kernel<<<1, 1024, 0, st>>>(counts, n1 + 1, total);   // -> exclusive offsets, offs[n1] = total
+  return cudaGetLastError();
+}
+
+cudaError_t launch_mn_draws(const double* alpha, const double* beta, const double* bpre, int64_t n1, int64_t n2,
+                            double m, uint64_t seed, const int64_t* offs, const int64_t* total, int64_t cnt,
+                            int64_t cap, int32_t* I, int32_t* J, int32_t* Jtmp, double* qhat, void* tmp,
+                            size_t* tmp_bytes, cudaStream_t st) {
+  // host knows cnt (<= cap) here; tmp == nullptr: query the sort's scratch size
+  if (!tmp) {
+    return cub::DeviceSegmentedRadixSort::SortKeys(nullptr, *tmp_bytes, Jtmp, J, (int)std::max<int64_t>(cnt, 1),
+                                                   (int)n1, offs, offs + 1, 0, 32, st);
+  }
+  const int blocks = (int)std::min<int64_t>((n1 + 7) / 8, 148 * 16);
+  mn_draw_kernel<<<std::max(blocks, 1), 256, 0, st>>>(alpha, bpre, n1, n2, seed, offs, total, cap, I, Jtmp);
+  // row i's draws sorted by column: segments [offs[i], offs[i+1]) (offs[n1] = total)
+  cudaError_t e = cub::DeviceSegmentedRadixSort::SortKeys(tmp, *tmp_bytes, Jtmp, J, (int)cnt, (int)n1, offs,
+                                                          offs + 1, 0, 32, st);
+  if (e != cudaSuccess) return e;
+  const int qb = (int)std::min<int64_t>((cnt + 255) / 256, 148 * 16);
+  mn_q_kernel<<<std::max(qb, 1), 256, 0, st>>>(alpha, beta, I, J, m, total, cap, qhat);
   return cudaGetLastError();
 }
 

@@ -48,6 +48,13 @@ struct smp_handle {
   int64_t panel2_cap[2] = {0, 0};
   cudaEvent_t ev_prep[2] = {nullptr, nullptr}, ev_free[2] = {nullptr, nullptr}, ev_sync = nullptr;
   cudaStream_t aux_st = nullptr;
+  // row-multinomial sampler scratch
+  double* mn_bpre = nullptr;
+  int64_t mn_bpre_cap = 0;
+  int32_t* mn_jtmp = nullptr;
+  int64_t mn_jtmp_cap = 0;
+  uint8_t* mn_tmp = nullptr;
+  int64_t mn_tmp_cap = 0;
   uint16_t* pi_panel = nullptr;  // K1 Gaussian Π panel (κ-major)
   int64_t pi_panel_cap = 0;
   int64_t panel_row0 = -1, panel_ld = 0, panel_kpad = 0;  // rows the panel holds
@@ -483,6 +490,7 @@ void smp_destroy(smp_handle* h) {
   if (!h) return;
   if (h->st) cudaStreamSynchronize(h->st);
   cudaFree(h->acc_sk); cudaFree(h->acc_nrm); cudaFree(h->part); cudaFree(h->pnorm);
+  cudaFree(h->mn_bpre); cudaFree(h->mn_jtmp); cudaFree(h->mn_tmp);
   cudaFree(h->planes); cudaFree(h->pi_panel); cudaFree(h->fin_sk); cudaFree(h->fin_sknorm); cudaFree(h->fin_D);
   cudaFree(h->FAFB); cudaFree(h->status); cudaFree(h->pw_scratch); cudaFree(h->alpha);
   cudaFree(h->blk); cudaFree(h->d_total);
@@ -759,6 +767,50 @@ smp_status smp_finalize_norms(smp_handle* h, float* A_sk, float* B_sk, double* a
   if (!(h->h_fafb[0] > 0.0) || !(h->h_fafb[1] > 0.0))
     return fail(h, SMP_ENUMERIC, "||A||_F = 0 or ||B||_F = 0");
   return SMP_OK;
+}
+
+static smp_status sample_multinomial(smp_handle* h, double m, uint64_t seed, int32_t est, int64_t cap,
+                                     int32_t* I, int32_t* J, float* val, double* qhat, int64_t* count) {
+  using namespace smp;
+  const int64_t n1 = h->n1, n2 = h->n2;
+  const int64_t boff = h->d.a_is_b ? 0 : n1;
+  double* beta = h->alpha + n1;
+  CK(h, launch_alpha_beta(h->acc_nrm, n1, h->acc_nrm + boff, n2, h->FAFB, h->alpha, beta, h->st), "alpha_beta");
+  CK(h, ensure(h->blk, h->blk_cap, n1 + 1), "alloc");
+  CK(h, ensure(h->mn_bpre, h->mn_bpre_cap, std::max<int64_t>(n2, 1)), "alloc");
+  CK(h, launch_mn_counts(h->alpha, beta, n1, n2, m, seed, h->mn_bpre, h->blk, h->d_total, h->st), "mn_counts");
+  CK(h, cudaMemcpyAsync(h->h_total, h->d_total, 8, cudaMemcpyDeviceToHost, h->st), "copy");
+  CK(h, cudaStreamSynchronize(h->st), "sync");
+  const int64_t cnt = *h->h_total;
+  if (count) *count = cnt;
+  h->launches += 4;
+  if (cnt > cap) return fail(h, SMP_ECAPACITY, "|Omega| = %lld > cap = %lld", (long long)cnt, (long long)cap);
+  if (cnt == 0) return SMP_OK;
+  CK(h, ensure(h->mn_jtmp, h->mn_jtmp_cap, cnt), "alloc");
+  size_t need = 0;
+  CK(h, launch_mn_draws(h->alpha, beta, h->mn_bpre, n1, n2, m, seed, h->blk, h->d_total, cnt, cap, I, J,
+                        h->mn_jtmp, qhat, nullptr, &need, h->st), "mn_draws");
+  CK(h, ensure(h->mn_tmp, h->mn_tmp_cap, (int64_t)need + 1), "alloc");
+  size_t have = (size_t)h->mn_tmp_cap;
+  CK(h, launch_mn_draws(h->alpha, beta, h->mn_bpre, n1, n2, m, seed, h->blk, h->d_total, cnt, cap, I, J,
+                        h->mn_jtmp, qhat, h->mn_tmp, &have, h->st), "mn_draws");
+  CK(h, launch_sddmm(h->fin_sk, h->fin_sk + boff * h->k, h->fin_D, h->fin_D + boff, h->k, I, J,
+                     h->d_total, cap, est == SMP_EST_PLAIN, val, h->st), "sddmm");
+  h->launches += 6;
+  CK(h, cudaStreamSynchronize(h->st), "sync");
+  return SMP_OK;
+}
+
+smp_status smp_sample_estimate_ex(smp_handle* h, double m, uint64_t seed, int32_t est, int32_t sampler,
+                                  int64_t cap, int32_t* I, int32_t* J, float* val, double* qhat,
+                                  int64_t* count) {
+  if (!h) return SMP_EINVAL;
+  if (sampler == SMP_SAMPLER_BERNOULLI) return smp_sample_estimate(h, m, seed, est, cap, I, J, val, qhat, count);
+  if (sampler != SMP_SAMPLER_MULTINOMIAL) return fail(h, SMP_EINVAL, "unknown sampler");
+  if (!(m > 0.0)) return fail(h, SMP_EINVAL, "m must be > 0");
+  if (!h->finalized) return fail(h, SMP_EINVAL, "call smp_finalize_norms first");
+  if (cap < 0 || (cap > 0 && (!I || !J || !val || !qhat))) return fail(h, SMP_EINVAL, "bad output");
+  return sample_multinomial(h, m, seed, est, cap, I, J, val, qhat, count);
 }
 
 smp_status smp_sample_estimate(smp_handle* h, double m, uint64_t seed, int32_t est, int64_t cap,

@@ -145,6 +145,16 @@ cudaError_t launch_sddmm(const float* Ask, const float* Bsk, const double* DA, c
                          int k, const int32_t* I, const int32_t* J, const int64_t* total,
                          int64_t cap, int plain, float* val, cudaStream_t st);
 
+// row-multinomial Ω (R27): Bpre, counts -> exclusive offsets (in place) and
+// *total; then draws (cnt = total <= cap, offsets with offs[n1] = total),
+// per-row column sort (CUB segmented; tmp == nullptr queries its size), q
+cudaError_t launch_mn_counts(const double* alpha, const double* beta, int64_t n1, int64_t n2, double m,
+                             uint64_t seed, double* bpre, int64_t* counts, int64_t* total, cudaStream_t st);
+cudaError_t launch_mn_draws(const double* alpha, const double* beta, const double* bpre, int64_t n1, int64_t n2,
+                            double m, uint64_t seed, const int64_t* offs, const int64_t* total, int64_t cnt,
+                            int64_t cap, int32_t* I, int32_t* J, int32_t* Jtmp, double* qhat, void* tmp,
+                            size_t* tmp_bytes, cudaStream_t st);
+
 // ---- K7-K9 WAltMin (waltmin.cu)
 struct WaltminArgs {
   int64_t n1, n2, count;

@@ -155,8 +155,11 @@ class SMPSketch:
                     b_sknorm=bsn)
 
     # ------------------------------------------------------------- Step 2
-    def sample_estimate(self, m, seed, plain=False, cap=None):
-        """Ω (sorted by (i,j)), M̃ on Ω and q̂ (Alg. 1 lines 3-4)."""
+    def sample_estimate(self, m, seed, plain=False, cap=None, sampler="bernoulli"):
+        """Ω (sorted by (i,j)), M̃ on Ω and q̂ (Alg. 1 lines 3-4).  sampler:
+        "bernoulli" (Alg. 1 line 3) or "multinomial" (the appendix's
+        row-multinomial sampler, R27: duplicates kept, q̂ = q)."""
+        smode = {"bernoulli": _lib.SAMPLER_BERNOULLI, "multinomial": _lib.SAMPLER_MULTINOMIAL}[sampler]
         if cap is None:
             cap = int(min(self.n1 * self.n2, m + 10 * math.sqrt(max(m, 1.0)) + 1024))
         dev = self.device
@@ -166,9 +169,9 @@ class SMPSketch:
             val = torch.empty(max(cap, 1), dtype=torch.float32, device=dev)
             qh = torch.empty(max(cap, 1), dtype=torch.float64, device=dev)
             cnt = ctypes.c_int64()
-            st = self.lib.smp_sample_estimate(self.h, float(m), seed,
-                                              EST_PLAIN if plain else EST_RESCALED, cap, _ptr(I),
-                                              _ptr(J), _ptr(val), _ptr(qh), ctypes.byref(cnt))
+            st = self.lib.smp_sample_estimate_ex(self.h, float(m), seed,
+                                                 EST_PLAIN if plain else EST_RESCALED, smode, cap,
+                                                 _ptr(I), _ptr(J), _ptr(val), _ptr(qh), ctypes.byref(cnt))
             if st == _lib.SMP_ECAPACITY:
                 cap = int(cnt.value)
                 continue

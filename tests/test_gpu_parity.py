@@ -394,3 +394,44 @@ def test_srht_full_rank_exact_product():
     got[I.cpu().numpy(), J.cpu().numpy()] = val.cpu().numpy()
     scale = np.outer(np.linalg.norm(A.double().numpy(), axis=0), np.linalg.norm(B.double().numpy(), axis=0))
     assert np.max(np.abs(got - M) / scale) < 1e-5
+
+
+# ------------------------------------------------------------------ row-multinomial Ω (NEXT-2, R27)
+@pytest.mark.parametrize("n1,n2,m_coef", [(100, 100, 0.3), (600, 450, 4.0), (300, 257, 50.0)])
+def test_multinomial_omega_bit_exact(n1, n2, m_coef):
+    d, k = 3000, 128
+    A = synth.gaussian_small(d, n1, seed=21, scale_cols=True).to(torch.bfloat16)
+    B = synth.gaussian_small(d, n2, seed=22, scale_cols=True).to(torch.bfloat16)
+    sk, fin = gpu_sketch(A, B, k, 0, seed=3)
+    orc = oracle_sketch(A, B, k, 0, seed=3)
+    m = m_coef * max(n1, n2) * 5 * math.log(max(n1, n2))
+    I, J, val, qh = sk.sample_estimate(m, 99, sampler="multinomial")
+    al, be = oracle.alpha_beta(orc["a2"], orc["b2"], orc["FA"], orc["FB"])
+    Io, Jo, qo = oracle.sample_multinomial(99, m, al, be)
+    assert np.array_equal(I.cpu().numpy(), Io) and np.array_equal(J.cpu().numpy(), Jo)
+    np.testing.assert_allclose(qh.cpu().numpy(), qo, rtol=2 * NORM_RTOL)
+    Mo = oracle.estimate(k, Io, Jo, orc["As"], orc["Bs"], orc["DA"], orc["DB"])
+    scale = np.sqrt(orc["a2"][Io] * orc["b2"][Jo])
+    assert np.max(np.abs(val.cpu().double().numpy() - Mo) / scale) <= 1e-4
+
+
+def test_multinomial_pipeline_waltmin():
+    """Alg. 1 with the multinomial Ω end to end: the factors agree with the
+    oracle run on the same (oracle) Ω to 1e-3 of ||AᵀB||."""
+    smp = _smp()
+    d, n, r, k = 8192, 256, 5, 256
+    VA = synth.lowrank_factors(n, 20, 1, 0, "cpu")
+    VB = synth.lowrank_factors(n, 20, 1, 1, "cpu")
+    A, B = synth.lowrank_block(0, d, n, 1, VA, VB, device="cpu")
+    sk, fin = gpu_sketch(A, B, k, 0, seed=1)
+    orc = oracle_sketch(A, B, k, 0, seed=1)
+    m = 4 * n * r * math.log(n)
+    I, J, val, qh = sk.sample_estimate(m, 1, sampler="multinomial")
+    Ug, Vg = sk.waltmin(I, J, val, qh, r, 10, init_iters=30, seed=1)
+    al, be = oracle.alpha_beta(orc["a2"], orc["b2"], orc["FA"], orc["FB"])
+    Io, Jo, qo = oracle.sample_multinomial(1, m, al, be)
+    Mo = oracle.estimate(k, Io, Jo, orc["As"], orc["Bs"], orc["DA"], orc["DB"])
+    Uo, Vo = oracle.waltmin(n, n, r, 10, Io, Jo, Mo, qo, np.sqrt(orc["a2"]), math.sqrt(orc["FA"]),
+                            init_iters=30, seed=1)
+    M = (A.double().T @ B.double()).numpy()
+    assert _uvt_err(Ug.cpu().double().numpy(), Vg.cpu().double().numpy(), Uo, Vo, M) <= 1e-3

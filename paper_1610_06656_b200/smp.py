@@ -180,6 +180,17 @@ class SMPSketch:
             return I[:c], J[:c], val[:c], qh[:c]
 
     # ------------------------------------------------------------- Step 3
+    def svd_of_sketch(self, r, T=10, init_iters=30, seed=0):
+        """Rank-r SVD of ÃᵀB̃ — the sketch-only baseline the paper compares
+        against (Figs. 2b/4b), on the GPU through the
+        same C ABI: Ω = every pair (q̂ = 1, w = 1), M̃ = ⟨Ã_i, B̃_j⟩ (the plain JL
+        estimator), then WAltMin without trimming — fully observed ALS
+        from a subspace-iteration start converges to (ÃᵀB̃)_r.  Returns (U, V)."""
+        # q = m(α_i + β_j) >= 1 for every pair with a nonzero column (pairs of two
+        # all-zero columns have (ÃᵀB̃)_ij = 0 and are not needed)
+        I, J, val, qh = self.sample_estimate(1e30, seed, plain=True, cap=self.n1 * self.n2)
+        return self.waltmin(I, J, val, qh, r, T, init_iters=init_iters, trim_c=0.0, seed=seed)
+
     def waltmin(self, I, J, val, qhat, r, T, init_iters=30, trim_c=8.0, ridge=1e-10, seed=0):
         dev = self.device
         U = torch.empty(self.n1, r, dtype=torch.float32, device=dev)

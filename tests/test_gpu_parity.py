@@ -435,3 +435,29 @@ def test_multinomial_pipeline_waltmin():
                             init_iters=30, seed=1)
     M = (A.double().T @ B.double()).numpy()
     assert _uvt_err(Ug.cpu().double().numpy(), Vg.cpu().double().numpy(), Uo, Vo, M) <= 1e-3
+
+
+# ------------------------------------------------------------------ SVD(ÃᵀB̃) baseline (NEXT-4)
+def test_svd_of_sketch_baseline_and_accuracy_claim():
+    """The GPU rank-r SVD of ÃᵀB̃ matches numpy's SVD of the oracle's sketch
+    product, and on a narrow shared-axis cone SMP-PCA beats it."""
+    smp = _smp()
+    d, n, r, k = 4000, 80, 3, 256
+    A64, B64 = synth.cone_shared_axis(d, n, 0.3, seed=5)
+    A, B = A64.float(), B64.float()
+    sk, fin = gpu_sketch(A, B, k, smp.PI_GAUSSIAN, seed=3)
+    orc = oracle_sketch(A, B, k, 1, seed=3)
+    Ms = orc["As"] @ orc["Bs"].T
+    u, sv, vt = np.linalg.svd(Ms)
+    best = (u[:, :r] * sv[:r]) @ vt[:r]
+    M = (A64.T @ B64).numpy()
+    Us, Vs = sk.svd_of_sketch(r, seed=3)
+    Pg = Us.cpu().double().numpy() @ Vs.cpu().double().numpy().T
+    assert np.linalg.norm(Pg - best, 2) / np.linalg.norm(M, 2) <= 1e-3
+    m = 6 * n * r * math.log(n)
+    I, J, val, qh = sk.sample_estimate(m, 3)
+    U, V = sk.waltmin(I, J, val, qh, r, 10, init_iters=30, seed=3)
+    nrm = np.linalg.norm(M, 2)
+    err = np.linalg.norm(U.cpu().double().numpy() @ V.cpu().double().numpy().T - M, 2) / nrm
+    err_svd = np.linalg.norm(Pg - M, 2) / nrm
+    assert err <= err_svd, (err, err_svd)

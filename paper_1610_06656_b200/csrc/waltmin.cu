@@ -11,6 +11,7 @@
 #include <cstdlib>
 #include <vector>
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_select.cuh>
 #include "waltmin_impl.cuh"
 
 namespace smp {
@@ -60,6 +61,16 @@ __global__ void wm_iota_kernel(int32_t* __restrict__ p, int64_t cnt) {
   for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < cnt;
        s += (int64_t)gridDim.x * blockDim.x)
     p[s] = (int32_t)s;
+}
+
+// heavy[o] = 1 iff output row o has more than thr samples; idx[o] = o
+__global__ void wm_heavy_flags_kernel(const int64_t* __restrict__ ptr, int64_t nout, int64_t thr,
+                                      uint8_t* __restrict__ flag, int32_t* __restrict__ idx) {
+  for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < nout;
+       o += (int64_t)gridDim.x * blockDim.x) {
+    flag[o] = (ptr[o + 1] - ptr[o]) > thr ? 1 : 0;
+    idx[o] = (int32_t)o;
+  }
 }
 
 template <int R>
@@ -134,6 +145,39 @@ cudaError_t run_waltmin(const WaltminArgs& a, cudaStream_t st) {
   wm_ptr_kernel<<<grid_for(n2 + 1, 256), 256, 0, st>>>(jsorted, cnt, n2, cptr);
   wm_gather_csc_kernel<<<grid_for(cnt, 256), 256, 0, st>>>(perm, a.I, w, wv, cnt, cI, cw, cwv);
 
+  // heavy rows / columns: stable compaction (fixed order -> fixed CTA
+  // assignment -> deterministic Gram partials)
+  const int64_t nmax = std::max<int64_t>(std::max<int64_t>(n1, n2), 1);
+  // Split a row over a CTA only when it is long in absolute terms AND several
+  // times a warp's average share: the CTA runs its heavy rows before its light
+  // ones, so splitting rows near the average only serialises work (cfg1:
+  // rows <= 564 samples, 119 per warp -> none split).  SMP_WM_HEAVY overrides
+  // the threshold (0 = warp-per-row only; tuning).
+  const char* hv = getenv("SMP_WM_HEAVY");
+  const int64_t avg_warp = cnt / ((int64_t)gctas * WM_WARPS) + 1;
+  const int64_t heavy_thr = hv ? atoll(hv) : std::max<int64_t>(WM_HEAVY, 4 * avg_warp);
+  uint8_t *hfr, *hfc;
+  int32_t *hidx, *hlr, *hlc, *nh;
+  void* sel_tmp = nullptr;
+  size_t sel_bytes = 0;
+  SMP_TRY(cudaMallocAsync(&hfr, n1 + 1, st));
+  SMP_TRY(cudaMallocAsync(&hfc, n2 + 1, st));
+  SMP_TRY(cudaMallocAsync(&hidx, nmax * 4, st));
+  SMP_TRY(cudaMallocAsync(&hlr, (n1 + 1) * 4, st));
+  SMP_TRY(cudaMallocAsync(&hlc, (n2 + 1) * 4, st));
+  SMP_TRY(cudaMallocAsync(&nh, 2 * 4, st));
+  SMP_TRY(cub::DeviceSelect::Flagged(nullptr, sel_bytes, hidx, hfr, hlr, nh, (int)nmax, st));
+  SMP_TRY(cudaMallocAsync(&sel_tmp, sel_bytes > 0 ? sel_bytes : 1, st));
+  SMP_TRY(cudaMemsetAsync(nh, 0, 2 * 4, st));
+  if (n1 > 0) {
+    wm_heavy_flags_kernel<<<grid_for(n1, 256), 256, 0, st>>>(rptr, n1, heavy_thr, hfr, hidx);
+    SMP_TRY(cub::DeviceSelect::Flagged(sel_tmp, sel_bytes, hidx, hfr, hlr, nh, (int)n1, st));
+  }
+  if (n2 > 0) {
+    wm_heavy_flags_kernel<<<grid_for(n2, 256), 256, 0, st>>>(cptr, n2, heavy_thr, hfc, hidx);
+    SMP_TRY(cub::DeviceSelect::Flagged(sel_tmp, sel_bytes, hidx, hfc, hlc, nh + 1, (int)n2, st));
+  }
+
   // lines 5-10: one cooperative persistent kernel
   SMP_TRY(cudaMemsetAsync(bar, 0, 2 * sizeof(unsigned), st));
   WMParams p{};
@@ -144,6 +188,12 @@ cudaError_t run_waltmin(const WaltminArgs& a, cudaStream_t st) {
   p.a2 = a.a_norm2; p.FA = a.FA;
   p.Y = Y; p.Z = Z; p.U = U; p.V = V; p.gpart = gpart; p.bar = bar;
   p.Uout = a.U; p.Vout = a.V;
+  const char* xl = getenv("SMP_WM_L1");  // 0: L2-only gathers (A/B switch)
+  p.x_l1 = (xl && atoi(xl) == 0) ? 0 : 1;
+  if (heavy_thr > 0) {
+    p.heavy_r = hlr; p.nheavy_r = nh; p.hflag_r = hfr;
+    p.heavy_c = hlc; p.nheavy_c = nh + 1; p.hflag_c = hfc;
+  }
   const char* tr = getenv("SMP_WM_TRACE");
   uint64_t* trace = nullptr;
   const int max_bar = 2 * (a.init_iters + 4) + 2 * a.T + 8;
@@ -175,6 +225,8 @@ cudaError_t run_waltmin(const WaltminArgs& a, cudaStream_t st) {
   cudaFreeAsync(U, st); cudaFreeAsync(V, st); cudaFreeAsync(gpart, st); cudaFreeAsync(bar, st);
   cudaFreeAsync(rptr, st); cudaFreeAsync(cptr, st); cudaFreeAsync(iota, st);
   cudaFreeAsync(perm, st); cudaFreeAsync(jsorted, st); cudaFreeAsync(cub_tmp, st);
+  cudaFreeAsync(hfr, st); cudaFreeAsync(hfc, st); cudaFreeAsync(hidx, st); cudaFreeAsync(hlr, st);
+  cudaFreeAsync(hlc, st); cudaFreeAsync(nh, st); cudaFreeAsync(sel_tmp, st);
   return cudaGetLastError();
 }
 

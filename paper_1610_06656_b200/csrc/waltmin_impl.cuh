@@ -32,6 +32,7 @@ namespace smp {
 // SpMM's output (Σ c (x T) = (Σ c x) T), so each half-iteration of the
 // subspace iteration costs two grid barriers.
 constexpr int WM_THREADS = 256;
+constexpr int WM_HEAVY = 1024;  // minimum samples for a row to be split over a CTA
 constexpr int WM_WARPS = WM_THREADS / 32;
 
 struct WMParams {
@@ -58,6 +59,14 @@ struct WMParams {
   uint64_t* trace;  // optional [3 * barriers] (SMP_WM_TRACE)
   uint64_t* trace2; // optional [64] phase stamps of CTA 0 (SMP_WM_TRACE)
   int stage_x;      // gathered factor rows staged into SMEM per phase (fits: n·r·8 B small)
+  // heavy rows (> WM_HEAVY samples): compacted lists, counts, per-row flags
+  int x_l1;         // gathers of non-staged factor rows through L1 (else L2-only)
+  const int32_t* heavy_r;
+  const int32_t* nheavy_r;
+  const uint8_t* hflag_r;
+  const int32_t* heavy_c;
+  const int32_t* nheavy_c;
+  const uint8_t* hflag_c;
   float* Uout;
   float* Vout;
 };
@@ -102,6 +111,7 @@ struct WMShared {
   double red[WM_THREADS];     // reduction scratch
   double wg[WM_WARPS][NG];    // per-warp Gram partials
   double ys[WM_WARPS][R];     // per-warp row broadcast
+  double hred[WM_WARPS][R * (R + 1) / 2 + R];  // heavy-row partials (SpMM: first R)
   int ea[NG], eb[NG];
 };
 
@@ -297,49 +307,112 @@ __device__ __forceinline__ const double* stage_rows(const double* X, int64_t n, 
   return xs;
 }
 
+// one gathered factor row x = X[oi, 0:R]: from the SMEM stage when present,
+// else from global memory — L1-cached (l1: the grid barrier's fences order it
+// after the producing phase) in 16-byte pieces for even R, or L2-only scalars
+template <int R>
+__device__ __forceinline__ void gather_row(const double* X, const double* Xs, int32_t oi, bool l1,
+                                           double (&x)[R]) {
+  if (Xs) {
+#pragma unroll
+    for (int l = 0; l < R; ++l) x[l] = Xs[(int64_t)oi * R + l];
+  } else if (l1) {
+    if constexpr ((R & 1) == 0) {
+      const double2* s2 = reinterpret_cast<const double2*>(X + (int64_t)oi * R);
+#pragma unroll
+      for (int l = 0; l < R / 2; ++l) {
+        const double2 v = s2[l];
+        x[2 * l] = v.x;
+        x[2 * l + 1] = v.y;
+      }
+    } else {
+#pragma unroll
+      for (int l = 0; l < R; ++l) x[l] = X[(int64_t)oi * R + l];
+    }
+  } else {
+#pragma unroll
+    for (int l = 0; l < R; ++l) x[l] = __ldcg(X + (int64_t)oi * R + l);
+  }
+}
+
+// lane-strided partial sum over the samples [q0, q1): acc += Σ coef X[other]
+template <int R>
+__device__ __forceinline__ void spmm_accum(int64_t q0, int64_t q1, const int32_t* __restrict__ other,
+                                           const double* __restrict__ coef, const double* X,
+                                           const double* Xs, bool l1, double (&acc)[R]) {
+  constexpr int U = WMUnroll<R>::U;
+  const int lane = threadIdx.x & 31;
+  for (int64_t base = q0 + lane; base < q1; base += 32 * U) {
+    double c[U];
+    int32_t oi[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t q = base + 32 * u;
+      const bool ok = q < q1;
+      c[u] = ok ? coef[q] : 0.0;
+      oi[u] = ok ? other[q] : 0;
+    }
+    double x[U][R];
+#pragma unroll
+    for (int u = 0; u < U; ++u) gather_row<R>(X, Xs, oi[u], l1, x[u]);
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int l = 0; l < R; ++l) acc[l] = fma(c[u], x[u][l], acc[l]);
+  }
+#pragma unroll
+  for (int l = 0; l < R; ++l)
+#pragma unroll
+    for (int sh = 16; sh > 0; sh >>= 1) acc[l] += __shfl_xor_sync(0xffffffffu, acc[l], sh);
+}
+
 // out[o] = (Σ_{p in [ptr[o], ptr[o+1])} coef[p] X[other[p]]) · T (samples of
-// row o stored contiguously: CSR order, or the pre-permuted CSC copy)
+// row o stored contiguously: CSR order, or the pre-permuted CSC copy).
+// Rows with more than WM_HEAVY samples (listed in heavy[0 .. *n_heavy)) are
+// split over the 8 warps of one CTA and combined in SMEM in warp order; the
+// others take one warp each.  Deterministic either way.
 template <int R>
 __device__ void spmm_phase(WMShared<R>& sm, const int64_t* __restrict__ ptr,
                            const int32_t* __restrict__ other, const double* __restrict__ coef,
                            const double* X, int64_t nout, double* out, double* gpart_buf,
-                           const double* Xs) {
+                           const double* Xs, const int32_t* heavy, const int32_t* n_heavy,
+                           const uint8_t* hflag, bool l1) {
   constexpr int NG = WMShared<R>::NG;
-  constexpr int U = WMUnroll<R>::U;
-  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t W = (int64_t)gridDim.x * WM_WARPS;
   double gl[(NG + 31) / 32];
 #pragma unroll
   for (int q = 0; q < (NG + 31) / 32; ++q) gl[q] = 0.0;
-  for (int64_t o = (int64_t)blockIdx.x * WM_WARPS + (threadIdx.x >> 5); o < nout; o += W) {
+  const int nh = heavy ? *n_heavy : 0;
+  for (int hi = blockIdx.x; hi < nh; hi += gridDim.x) {
+    const int64_t o = heavy[hi];
+    const int64_t p0 = ptr[o], p1 = ptr[o + 1];
+    const int64_t len = p1 - p0;
     double acc[R];
 #pragma unroll
     for (int l = 0; l < R; ++l) acc[l] = 0.0;
-    const int64_t p0 = ptr[o], p1 = ptr[o + 1];
-    for (int64_t base = p0 + lane; base < p1; base += 32 * U) {
-      double c[U];
-      int32_t oi[U];
+    spmm_accum<R>(p0 + (len * warp) / WM_WARPS, p0 + (len * (warp + 1)) / WM_WARPS, other, coef, X, Xs, l1, acc);
+    if (lane == 0)
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int64_t q = base + 32 * u;
-        const bool ok = q < p1;
-        c[u] = ok ? coef[q] : 0.0;
-        oi[u] = ok ? other[q] : 0;
+      for (int l = 0; l < R; ++l) sm.hred[warp][l] = acc[l];
+    __syncthreads();
+    if (warp == 0) {
+#pragma unroll
+      for (int l = 0; l < R; ++l) {
+        double t = sm.hred[0][l];
+        for (int w2 = 1; w2 < WM_WARPS; ++w2) t += sm.hred[w2][l];
+        acc[l] = t;
       }
-      double x[U][R];
-#pragma unroll
-      for (int u = 0; u < U; ++u)
-#pragma unroll
-        for (int l = 0; l < R; ++l) x[u][l] = Xs ? Xs[(int64_t)oi[u] * R + l] : __ldcg(X + (int64_t)oi[u] * R + l);
-#pragma unroll
-      for (int u = 0; u < U; ++u)
-#pragma unroll
-        for (int l = 0; l < R; ++l) acc[l] = fma(c[u], x[u][l], acc[l]);
+      emit_row<R>(sm, o, acc, sm.T, out, -1.0, gl);
     }
+    __syncthreads();
+  }
+  for (int64_t o = (int64_t)blockIdx.x * WM_WARPS + warp; o < nout; o += W) {
+    if (hflag && hflag[o]) continue;
+    double acc[R];
 #pragma unroll
-    for (int l = 0; l < R; ++l)
-#pragma unroll
-      for (int sh = 16; sh > 0; sh >>= 1) acc[l] += __shfl_xor_sync(0xffffffffu, acc[l], sh);
+    for (int l = 0; l < R; ++l) acc[l] = 0.0;
+    spmm_accum<R>(ptr[o], ptr[o + 1], other, coef, X, Xs, l1, acc);
     emit_row<R>(sm, o, acc, sm.T, out, -1.0, gl);
   }
   flush_gram<R>(sm, gl, gpart_buf);
@@ -366,116 +439,175 @@ __device__ void transform_phase(WMShared<R>& sm, const double* X, int64_t n, con
   if (gpart_buf) flush_gram<R>(sm, gl, gpart_buf);
 }
 
+// lane-strided partial normal equations over the samples [q0, q1):
+// g += Σ w x xᵀ (upper triangle), h += Σ w M̃ x, then a fixed xor-butterfly
+template <int R>
+__device__ __forceinline__ void als_accum(int64_t q0, int64_t q1, const int32_t* __restrict__ other,
+                                          const double* __restrict__ w, const double* __restrict__ wv,
+                                          const double* X, const double* Xs, bool l1,
+                                          double (&g)[R * (R + 1) / 2],
+                                          double (&h)[R]) {
+  constexpr int NG = R * (R + 1) / 2;
+  constexpr int U = WMUnroll<R>::U;
+  const int lane = threadIdx.x & 31;
+  for (int64_t base = q0 + lane; base < q1; base += 32 * U) {
+    double ws[U], vs[U];
+    int32_t oi[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t q = base + 32 * u;
+      const bool ok = q < q1;
+      ws[u] = ok ? w[q] : 0.0;
+      vs[u] = ok ? wv[q] : 0.0;
+      oi[u] = ok ? other[q] : 0;
+    }
+    double x[U][R];
+#pragma unroll
+    for (int u = 0; u < U; ++u) gather_row<R>(X, Xs, oi[u], l1, x[u]);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      int e = 0;
+#pragma unroll
+      for (int a = 0; a < R; ++a) {
+        const double wa = ws[u] * x[u][a];
+        h[a] = fma(vs[u], x[u][a], h[a]);
+#pragma unroll
+        for (int b = a; b < R; ++b) { g[e] = fma(wa, x[u][b], g[e]); ++e; }
+      }
+    }
+  }
+#pragma unroll
+  for (int e = 0; e < NG; ++e)
+#pragma unroll
+    for (int sh = 16; sh > 0; sh >>= 1) g[e] += __shfl_xor_sync(0xffffffffu, g[e], sh);
+#pragma unroll
+  for (int a = 0; a < R; ++a)
+#pragma unroll
+    for (int sh = 16; sh > 0; sh >>= 1) h[a] += __shfl_xor_sync(0xffffffffu, h[a], sh);
+}
+
+// ridge Cholesky solve of one output row from its normal equations gh =
+// [G upper triangle | h] in SMEM (called by one lane).  Not inlined: one copy
+// serves the light- and heavy-row paths (two inlined copies spill at R >= 4).
+template <int R>
+__device__ __noinline__ void als_solve(const double* gh, double lam, double* out, int64_t o) {
+  constexpr int NG = R * (R + 1) / 2;
+  const double* g = gh;
+  const double* h = gh + NG;
+  // ridge Cholesky solve (G + lam tr(G)/r I) x = h; empty/singular -> 0
+  // (R14).  Fully unrolled: registers only.
+  double L[R][R], xs[R], y[R], inv[R];
+  double tr = 0.0;
+  {
+    int e = 0;
+#pragma unroll
+    for (int a = 0; a < R; ++a)
+#pragma unroll
+      for (int b = a; b < R; ++b) {
+        L[b][a] = g[e];
+        if (a == b) tr += g[e];
+        ++e;
+      }
+  }
+  bool ok = tr > 0.0;
+  const double shift = lam * tr / (double)R;
+#pragma unroll
+  for (int a = 0; a < R; ++a) L[a][a] += shift;
+#pragma unroll
+  for (int j = 0; j < R; ++j) {
+    double s = L[j][j];
+#pragma unroll
+    for (int q = 0; q < j; ++q) s -= L[j][q] * L[j][q];
+    ok = ok && (s > 0.0);
+    const double d = sqrt(s > 0.0 ? s : 1.0);
+    inv[j] = 1.0 / d;
+    L[j][j] = d;
+#pragma unroll
+    for (int i = j + 1; i < R; ++i) {
+      double t = L[i][j];
+#pragma unroll
+      for (int q = 0; q < j; ++q) t -= L[i][q] * L[j][q];
+      L[i][j] = t * inv[j];
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < R; ++i) {
+    double t = h[i];
+#pragma unroll
+    for (int q = 0; q < i; ++q) t -= L[i][q] * y[q];
+    y[i] = t * inv[i];
+  }
+#pragma unroll
+  for (int i = R - 1; i >= 0; --i) {
+    double t = y[i];
+#pragma unroll
+    for (int q = i + 1; q < R; ++q) t -= L[q][i] * xs[q];
+    xs[i] = t * inv[i];
+  }
+#pragma unroll
+  for (int a = 0; a < R; ++a) out[o * R + a] = ok ? xs[a] : 0.0;
+}
+
 // one weighted least-squares half step (lines 8/9; R14):
 // out[o] = (G_o + lam tr(G_o)/r I)^{-1} h_o over the samples of output row o,
-// G_o = Σ w x xᵀ, h_o = Σ w M̃ x (lanes accumulate their samples in registers,
-// then a fixed xor-butterfly reduction; lane 0 solves by Cholesky)
+// G_o = Σ w x xᵀ, h_o = Σ w M̃ x.  Heavy rows (> WM_HEAVY samples) are split
+// over a CTA's 8 warps and combined in SMEM in warp order.
 template <int R>
 __device__ void als_phase(WMShared<R>& sm, const int64_t* __restrict__ ptr,
                           const int32_t* __restrict__ other, const double* __restrict__ w,
                           const double* __restrict__ wv, const double* X, int64_t nout, double lam,
-                          double* out, const double* Xs) {
+                          double* out, const double* Xs, const int32_t* heavy, const int32_t* n_heavy,
+                          const uint8_t* hflag, bool l1) {
   constexpr int NG = WMShared<R>::NG;
-  constexpr int U = WMUnroll<R>::U;
-  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t W = (int64_t)gridDim.x * WM_WARPS;
-  for (int64_t o = (int64_t)blockIdx.x * WM_WARPS + (threadIdx.x >> 5); o < nout; o += W) {
+  const int nh = heavy ? *n_heavy : 0;
+  for (int hi = blockIdx.x; hi < nh; hi += gridDim.x) {
+    const int64_t o = heavy[hi];
+    const int64_t p0 = ptr[o], p1 = ptr[o + 1];
+    const int64_t len = p1 - p0;
     double g[NG], h[R];
 #pragma unroll
     for (int e = 0; e < NG; ++e) g[e] = 0.0;
 #pragma unroll
     for (int a = 0; a < R; ++a) h[a] = 0.0;
-    const int64_t p0 = ptr[o], p1 = ptr[o + 1];
-    for (int64_t base = p0 + lane; base < p1; base += 32 * U) {
-      double ws[U], vs[U];
-      int32_t oi[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int64_t q = base + 32 * u;
-        const bool ok = q < p1;
-        ws[u] = ok ? w[q] : 0.0;
-        vs[u] = ok ? wv[q] : 0.0;
-        oi[u] = ok ? other[q] : 0;
-      }
-      double x[U][R];
-#pragma unroll
-      for (int u = 0; u < U; ++u)
-#pragma unroll
-        for (int l = 0; l < R; ++l) x[u][l] = Xs ? Xs[(int64_t)oi[u] * R + l] : __ldcg(X + (int64_t)oi[u] * R + l);
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        int e = 0;
-#pragma unroll
-        for (int a = 0; a < R; ++a) {
-          const double wa = ws[u] * x[u][a];
-          h[a] = fma(vs[u], x[u][a], h[a]);
-#pragma unroll
-          for (int b = a; b < R; ++b) { g[e] = fma(wa, x[u][b], g[e]); ++e; }
-        }
-      }
-    }
-#pragma unroll
-    for (int e = 0; e < NG; ++e)
-#pragma unroll
-      for (int sh = 16; sh > 0; sh >>= 1) g[e] += __shfl_xor_sync(0xffffffffu, g[e], sh);
-#pragma unroll
-    for (int a = 0; a < R; ++a)
-#pragma unroll
-      for (int sh = 16; sh > 0; sh >>= 1) h[a] += __shfl_xor_sync(0xffffffffu, h[a], sh);
+    als_accum<R>(p0 + (len * warp) / WM_WARPS, p0 + (len * (warp + 1)) / WM_WARPS, other, w, wv, X, Xs, l1, g, h);
     if (lane == 0) {
-      // ridge Cholesky solve (G + lam tr(G)/r I) x = h; empty/singular -> 0
-      // (R14).  Fully unrolled: registers only.
-      double L[R][R], xs[R], y[R], inv[R];
-      double tr = 0.0;
-      {
-        int e = 0;
 #pragma unroll
-        for (int a = 0; a < R; ++a)
+      for (int e = 0; e < NG; ++e) sm.hred[warp][e] = g[e];
 #pragma unroll
-          for (int b = a; b < R; ++b) {
-            L[b][a] = g[e];
-            if (a == b) tr += g[e];
-            ++e;
-          }
-      }
-      bool ok = tr > 0.0;
-      const double shift = lam * tr / (double)R;
-#pragma unroll
-      for (int a = 0; a < R; ++a) L[a][a] += shift;
-#pragma unroll
-      for (int j = 0; j < R; ++j) {
-        double s = L[j][j];
-#pragma unroll
-        for (int q = 0; q < j; ++q) s -= L[j][q] * L[j][q];
-        ok = ok && (s > 0.0);
-        const double d = sqrt(s > 0.0 ? s : 1.0);
-        inv[j] = 1.0 / d;
-        L[j][j] = d;
-#pragma unroll
-        for (int i = j + 1; i < R; ++i) {
-          double t = L[i][j];
-#pragma unroll
-          for (int q = 0; q < j; ++q) t -= L[i][q] * L[j][q];
-          L[i][j] = t * inv[j];
-        }
-      }
-#pragma unroll
-      for (int i = 0; i < R; ++i) {
-        double t = h[i];
-#pragma unroll
-        for (int q = 0; q < i; ++q) t -= L[i][q] * y[q];
-        y[i] = t * inv[i];
-      }
-#pragma unroll
-      for (int i = R - 1; i >= 0; --i) {
-        double t = y[i];
-#pragma unroll
-        for (int q = i + 1; q < R; ++q) t -= L[q][i] * xs[q];
-        xs[i] = t * inv[i];
-      }
-#pragma unroll
-      for (int a = 0; a < R; ++a) out[o * R + a] = ok ? xs[a] : 0.0;
+      for (int a = 0; a < R; ++a) sm.hred[warp][NG + a] = h[a];
     }
+    __syncthreads();
+    // entry e summed over the warps in warp order by thread e (fixed order)
+    double t = 0.0;
+    if (threadIdx.x < NG + R) {
+      t = sm.hred[0][threadIdx.x];
+#pragma unroll
+      for (int w2 = 1; w2 < WM_WARPS; ++w2) t += sm.hred[w2][threadIdx.x];
+    }
+    __syncthreads();
+    if (threadIdx.x < NG + R) sm.hred[0][threadIdx.x] = t;
+    __syncthreads();
+    if (threadIdx.x == 0) als_solve<R>(sm.hred[0], lam, out, o);
+    __syncthreads();
+  }
+  for (int64_t o = (int64_t)blockIdx.x * WM_WARPS + warp; o < nout; o += W) {
+    if (hflag && hflag[o]) continue;
+    double g[NG], h[R];
+#pragma unroll
+    for (int e = 0; e < NG; ++e) g[e] = 0.0;
+#pragma unroll
+    for (int a = 0; a < R; ++a) h[a] = 0.0;
+    als_accum<R>(ptr[o], ptr[o + 1], other, w, wv, X, Xs, l1, g, h);
+    if (lane == 0) {
+#pragma unroll
+      for (int e = 0; e < NG; ++e) sm.hred[warp][e] = g[e];
+#pragma unroll
+      for (int a = 0; a < R; ++a) sm.hred[warp][NG + a] = h[a];
+      als_solve<R>(sm.hred[warp], lam, out, o);
+    }
+    __syncwarp();
   }
 }
 
@@ -541,7 +673,7 @@ __global__ void __launch_bounds__(WM_THREADS, 1) wm_persistent_kernel(WMParams p
     stamp(4 * it);
     const double* xsY = stage_rows<R>(p.Y, p.n2, xs, stg);
     stamp(4 * it + 1);
-    spmm_phase<R>(sm, p.rptr, p.J, p.wv, p.Y, p.n1, p.Z, gp(buf), xsY);
+    spmm_phase<R>(sm, p.rptr, p.J, p.wv, p.Y, p.n1, p.Z, gp(buf), xsY, p.heavy_r, p.nheavy_r, p.hflag_r, p.x_l1);
     stamp(4 * it + 2);
     if (it == iters - 1) {  // the last Y half does not reach U0
       cqr2(p.Z, p.n1);
@@ -549,7 +681,8 @@ __global__ void __launch_bounds__(WM_THREADS, 1) wm_persistent_kernel(WMParams p
     }
     cqr1();
     stamp(4 * it + 3);
-    spmm_phase<R>(sm, p.cptr, p.cI, p.cwv, p.Z, p.n2, p.Y, gp(buf), stage_rows<R>(p.Z, p.n1, xs, stg));
+    spmm_phase<R>(sm, p.cptr, p.cI, p.cwv, p.Z, p.n2, p.Y, gp(buf), stage_rows<R>(p.Z, p.n1, xs, stg),
+                  p.heavy_c, p.nheavy_c, p.hflag_c, p.x_l1);
     cqr1();
   }
   for (int e = tid; e < R * R; e += blockDim.x) TZ[e] = sm.T[e];
@@ -567,9 +700,11 @@ __global__ void __launch_bounds__(WM_THREADS, 1) wm_persistent_kernel(WMParams p
   if (p.T == 0)
     for (int64_t e = (int64_t)blockIdx.x * WM_THREADS + tid; e < p.n2 * R; e += G * WM_THREADS) p.V[e] = 0.0;
   for (int t = 0; t < p.T; ++t) {
-    als_phase<R>(sm, p.cptr, p.cI, p.cw, p.cwv, p.U, p.n2, p.lam, p.V, stage_rows<R>(p.U, p.n1, xs, stg));
+    als_phase<R>(sm, p.cptr, p.cI, p.cw, p.cwv, p.U, p.n2, p.lam, p.V, stage_rows<R>(p.U, p.n1, xs, stg),
+                 p.heavy_c, p.nheavy_c, p.hflag_c, p.x_l1);
     grid_sync(p.bar, p.trace, nbar);
-    als_phase<R>(sm, p.rptr, p.J, p.w, p.wv, p.V, p.n1, p.lam, p.U, stage_rows<R>(p.V, p.n2, xs, stg));
+    als_phase<R>(sm, p.rptr, p.J, p.w, p.wv, p.V, p.n1, p.lam, p.U, stage_rows<R>(p.V, p.n2, xs, stg),
+                 p.heavy_r, p.nheavy_r, p.hflag_r, p.x_l1);
     grid_sync(p.bar, p.trace, nbar);
   }
   // output (Û(T), V̂(T)) in fp32
@@ -584,7 +719,11 @@ cudaError_t launch_wm(WMParams& p, cudaStream_t st) {
   constexpr size_t XS_MAX = 160 * 1024;  // staged factor rows (n_max · r doubles)
   const size_t base = (sizeof(WMShared<R>) + 15) & ~(size_t)15;
   const size_t xs_bytes = (size_t)(p.n1 > p.n2 ? p.n1 : p.n2) * R * 8;
-  p.stage_x = xs_bytes <= XS_MAX ? 1 : 0;
+  static const int env_stage = [] {  // SMP_WM_STAGE=0: never stage (tuning)
+    const char* e = getenv("SMP_WM_STAGE");
+    return e ? atoi(e) : 1;
+  }();
+  p.stage_x = (env_stage && xs_bytes <= XS_MAX) ? 1 : 0;
   const size_t smem = base + (p.stage_x ? xs_bytes : 0);
   static bool attr = false;
   if (!attr) {

@@ -237,6 +237,67 @@ def test_waltmin_parity_identical_inputs(n1, n2, r, m_coef):
     assert err <= 1e-3, err
 
 
+@pytest.mark.parametrize("thr", ["40", "0"])
+def test_waltmin_heavy_rows_parity(thr, monkeypatch):
+    """WAltMin with rows split over a CTA's warps (SMP_WM_HEAVY = split
+    threshold; 40 forces most rows and columns of this skewed Ω through the
+    CTA-cooperative path, 0 disables it): agrees with the oracle on identical
+    inputs to 1e-3 of ||AᵀB||, and both GPU paths agree to 1e-9."""
+    n1, n2, r, d, k = 200, 150, 6, 2000, 256
+    Z = synth.gaussian_small(d, r, seed=51).double()
+    # column scales 1/sqrt(i+1): skewed norms -> a few long rows/columns in Ω
+    sa = torch.arange(1, n1 + 1, dtype=torch.float64).rsqrt()
+    sb = torch.arange(1, n2 + 1, dtype=torch.float64).rsqrt()
+    A = ((Z @ synth.gaussian_small(r, n1, seed=52).double() + 0.1 * synth.gaussian_small(d, n1, seed=53).double())
+         * sa).to(torch.bfloat16)
+    B = ((Z @ synth.gaussian_small(r, n2, seed=54).double() + 0.1 * synth.gaussian_small(d, n2, seed=55).double())
+         * sb).to(torch.bfloat16)
+    sk, fin = gpu_sketch(A, B, k, 0, seed=1)
+    orc = oracle_sketch(A, B, k, 0, seed=1)
+    m = 2.0 * n1 * r * math.log(n1)
+    al, be = oracle.alpha_beta(orc["a2"], orc["b2"], orc["FA"], orc["FB"])
+    Io, Jo, qo = oracle.sample(5, m, al, be)
+    rows = np.bincount(Io, minlength=n1)
+    assert (rows > 40).sum() >= 20 and (rows <= 40).sum() >= 20, rows  # both paths exercised
+    Mo = oracle.estimate(k, Io, Jo, orc["As"], orc["Bs"], orc["DA"], orc["DB"]).astype(np.float32)
+    Uo, Vo = oracle.waltmin(n1, n2, r, 10, Io, Jo, Mo.astype(np.float64), qo, np.sqrt(orc["a2"]),
+                            math.sqrt(orc["FA"]), init_iters=30, seed=9)
+    dev = torch.device("cuda")
+    args = (torch.tensor(Io, device=dev), torch.tensor(Jo, device=dev), torch.tensor(Mo, device=dev),
+            torch.tensor(qo, device=dev), r, 10)
+    monkeypatch.setenv("SMP_WM_HEAVY", thr)
+    Ug, Vg = sk.waltmin(*args, init_iters=30, seed=9)
+    M = (A.double().T @ B.double()).numpy()
+    Pg = Ug.cpu().double().numpy() @ Vg.cpu().double().numpy().T
+    err = _uvt_err(Ug.cpu().double().numpy(), Vg.cpu().double().numpy(), Uo, Vo, M)
+    assert err <= 1e-3, err
+    monkeypatch.setenv("SMP_WM_HEAVY", "0")
+    U0, V0 = sk.waltmin(*args, init_iters=30, seed=9)
+    P0 = U0.cpu().double().numpy() @ V0.cpu().double().numpy().T
+    assert np.linalg.norm(Pg - P0, 2) / np.linalg.norm(M, 2) <= 1e-9
+
+
+@pytest.mark.parametrize("r", [5, 10])
+def test_waltmin_gather_paths_bit_identical(r, monkeypatch):
+    """Factor-row gathers through L1 (16-byte pieces for even r) and L2-only
+    give bit-identical factors when the rows are too many to stage in SMEM
+    (n r 8 B > 160 KB): the grid barrier's fences make L1 reads coherent."""
+    n = 2304
+    d, k = 4096, 256
+    Z = synth.gaussian_small(d, r, seed=61)
+    A = (Z @ synth.gaussian_small(r, n, seed=62) + 0.1 * synth.gaussian_small(d, n, seed=63)).to(torch.bfloat16)
+    B = (Z @ synth.gaussian_small(r, n, seed=64) + 0.1 * synth.gaussian_small(d, n, seed=65)).to(torch.bfloat16)
+    sk, fin = gpu_sketch(A, B, k, 0, seed=2)
+    I, J, val, qh = sk.sample_estimate(4 * n * r * math.log(n), 3)
+    out = {}
+    for mode in ("1", "0"):
+        monkeypatch.setenv("SMP_WM_L1", mode)
+        U, V = sk.waltmin(I, J, val, qh, r, 10, init_iters=30, seed=3)
+        out[mode] = (U.cpu(), V.cpu())
+    assert torch.equal(out["1"][0], out["0"][0]) and torch.equal(out["1"][1], out["0"][1])
+    assert float(out["1"][0].abs().sum()) > 0
+
+
 def test_pipeline_end_to_end_vs_oracle():
     """Alg. 1 end to end from the same A, B on both sides (cfg1-like regime,
     m = 4 n r ln n): factors within 1e-3 of ||AᵀB||_2."""

@@ -33,6 +33,10 @@ def main():
     sk.finalize()
     I, J, val, qh = sk.sample_estimate(synth.m_of(cfg), cfg["seed"])
     del A, B
+    for key, X, n in (("rows", I, cfg["n1"]), ("cols", J, cfg["n2"])):
+        c = torch.bincount(X.long(), minlength=n)
+        print(f"{name} {key}: n={n} max={int(c.max())} mean={float(c.float().mean()):.1f} "
+              + " ".join(f">{t}:{int((c > t).sum())}" for t in (128, 256, 512, 1024)))
     for iters, T in settings:
         sk.waltmin(I, J, val, qh, cfg["r"], T, init_iters=iters, seed=cfg["seed"])
         torch.cuda.synchronize()

@@ -89,6 +89,12 @@ def main():
     e[3].record()
     torch.cuda.synchronize()
     wall = time.time() - t0
+    # warm re-run of Step 3 alone (the first call also grows the memory pool)
+    w0, w1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    w0.record()
+    sk.waltmin(I, J, val, qh, r, T, init_iters=30, seed=7)
+    w1.record()
+    torch.cuda.synchronize()
     sk.close()
     s = top_singular(A, B)
     nrm = float(s[0])
@@ -97,7 +103,7 @@ def main():
     out = dict(d=d, n=n, k=k, r=r, T=T, m=m, omega=int(I.numel()), sampler=sampler, pi=pi_name,
                optimal=opt, smp_pca=err, paper={"optimal": 0.0271, "lela": 0.0274, "smp_pca": 0.0280},
                ms={"sketch+finalize": e[0].elapsed_time(e[1]), "omega+mtilde": e[1].elapsed_time(e[2]),
-                   "waltmin": e[2].elapsed_time(e[3])}, wall_s=wall)
+                   "waltmin": e[2].elapsed_time(e[3]), "waltmin_warm": w0.elapsed_time(w1)}, wall_s=wall)
     print(json.dumps(out), flush=True)
 
 

@@ -181,7 +181,7 @@ cudaError_t run_waltmin(const WaltminArgs& a, cudaStream_t st) {
   // lines 5-10: one cooperative persistent kernel
   SMP_TRY(cudaMemsetAsync(bar, 0, 2 * sizeof(unsigned), st));
   WMParams p{};
-  p.n1 = n1; p.n2 = n2; p.T = a.T; p.init_iters = a.init_iters;
+  p.n1 = n1; p.n2 = n2; p.count = cnt; p.T = a.T; p.init_iters = a.init_iters;
   p.trim_c = a.trim_c; p.lam = a.lam; p.seed = a.seed;
   p.rptr = rptr; p.J = a.J; p.w = w; p.wv = wv;
   p.cptr = cptr; p.cI = cI; p.cw = cw; p.cwv = cwv;

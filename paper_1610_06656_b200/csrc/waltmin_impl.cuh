@@ -67,6 +67,8 @@ struct WMParams {
   const int32_t* heavy_c;
   const int32_t* nheavy_c;
   const uint8_t* hflag_c;
+  int64_t count;        // |Ω|
+  int64_t cache_bytes;  // dynamic SMEM reserved for the two WMCache copies (0: off)
   float* Uout;
   float* Vout;
 };
@@ -77,30 +79,51 @@ __device__ __forceinline__ uint64_t wm_globaltimer() {
   return t;
 }
 
-// Sense-reversing grid barrier (all CTAs are co-resident: cooperative launch).
+// Grid barrier on one monotonically increasing arrival counter (all CTAs are
+// co-resident: cooperative launch; the counter is zeroed before the launch).
+// Barrier nb completes when the counter reaches (nb + 1)·grid: thread 0
+// arrives with a release reduction (orders the CTA's writes, published to it
+// by the bar.sync before) and polls with acquire loads (orders the CTA's
+// later reads after the other CTAs' writes).  No generation word, no reset,
+// one L2 round trip from the last arrival to the release.
 // trace (diagnostics, SMP_WM_TRACE): per barrier, CTA 0's arrival, the last
 // arrival and CTA 0's release (globaltimer ns).
 __device__ __forceinline__ void grid_sync(unsigned* bar, uint64_t* trace, int& nb) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    volatile unsigned* vgen = bar + 1;
-    const unsigned gen = *vgen;
-    if (trace && blockIdx.x == 0) trace[3 * nb] = wm_globaltimer();
-    __threadfence();
-    if (atomicAdd(bar, 1u) == gridDim.x - 1) {
-      if (trace) trace[3 * nb + 1] = wm_globaltimer();
-      bar[0] = 0u;
-      __threadfence();
-      atomicAdd(bar + 1, 1u);
+    const unsigned target = (unsigned)(nb + 1) * gridDim.x;
+    if (trace) {
+      if (blockIdx.x == 0) trace[3 * nb] = wm_globaltimer();
+      unsigned old;
+      asm volatile("atom.release.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(bar) : "memory");
+      if (old == target - 1) trace[3 * nb + 1] = wm_globaltimer();
     } else {
-      while (*vgen == gen) {}
+      asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
     }
-    __threadfence();
+    unsigned v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
+    } while (v < target);
     if (trace && blockIdx.x == 0) trace[3 * nb + 2] = wm_globaltimer();
   }
   ++nb;
   __syncthreads();
 }
+
+// SMEM copy of one side of Ω restricted to the light rows this CTA owns
+// (row o belongs to warp (o mod W) mod 8 of CTA (o mod W) / 8, W = 8·grid):
+// the sample structure is the same in every phase, so after one copy the
+// phases read their indices and weights from SMEM instead of L2 (the
+// per-row latency that dominates small instances such as cfg1).
+struct WMCache {
+  int on;
+  int soff[WM_WARPS];  // warp's first sample
+  int roff[WM_WARPS];  // warp's first row-length entry (-1: heavy row, skipped)
+  const int32_t* other;
+  const double* w;
+  const double* wv;
+  const int32_t* len;
+};
 
 template <int R>
 struct WMShared {
@@ -113,6 +136,8 @@ struct WMShared {
   double ys[WM_WARPS][R];     // per-warp row broadcast
   double hred[WM_WARPS][R * (R + 1) / 2 + R];  // heavy-row partials (SpMM: first R)
   int ea[NG], eb[NG];
+  WMCache cache[2];           // [0]: rows of U/Z (CSR side), [1]: rows of V/Y (CSC side)
+  int scan[2][WM_WARPS];
 };
 
 template <int R>
@@ -279,6 +304,67 @@ __device__ void reduce_chol(WMShared<R>& sm, const double* gpart_buf) {
 template <int R>
 struct WMUnroll { static constexpr int U = R <= 6 ? 4 : (R <= 10 ? 2 : 1); };
 
+// Fill sm.cache[sd] for this CTA's light rows of one side, if they fit in
+// the remaining region [*region, end); all threads of the CTA call this.
+static __device__ void build_cache(WMCache& c, int (&scan)[2][WM_WARPS], const int64_t* __restrict__ ptr,
+                            const int32_t* __restrict__ other, const double* __restrict__ w,
+                            const double* __restrict__ wv, int64_t nout, const uint8_t* hflag,
+                            uint8_t*& region, const uint8_t* end) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t W = (int64_t)gridDim.x * WM_WARPS;
+  const int64_t o0 = (int64_t)blockIdx.x * WM_WARPS + warp;
+  const int nrows = o0 < nout ? (int)((nout - 1 - o0) / W + 1) : 0;
+  int64_t ns = 0;
+  for (int k = lane; k < nrows; k += 32) {
+    const int64_t o = o0 + (int64_t)k * W;
+    if (!(hflag && hflag[o])) ns += ptr[o + 1] - ptr[o];
+  }
+#pragma unroll
+  for (int sh = 16; sh > 0; sh >>= 1) ns += __shfl_xor_sync(0xffffffffu, ns, sh);
+  if (lane == 0) { scan[0][warp] = (int)(ns < (1 << 30) ? ns : (1 << 30)); scan[1][warp] = nrows; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int64_t S = 0, Rr = 0;
+    for (int q = 0; q < WM_WARPS; ++q) {
+      c.soff[q] = (int)S; c.roff[q] = (int)Rr;
+      S += scan[0][q]; Rr += scan[1][q];
+    }
+    const int64_t bytes = S * 16 + ((S * 4 + Rr * 4 + 15) & ~(int64_t)15);
+    c.on = (region + bytes <= end) ? 1 : 0;
+    if (c.on) {
+      double* d = reinterpret_cast<double*>(region);
+      c.w = d;
+      c.wv = d + S;
+      int32_t* i = reinterpret_cast<int32_t*>(d + 2 * S);
+      c.other = i;
+      c.len = i + S;
+      region += bytes;
+    }
+  }
+  __syncthreads();
+  if (!c.on) return;
+  double* cw = const_cast<double*>(c.w);
+  double* cwv = const_cast<double*>(c.wv);
+  int32_t* co = const_cast<int32_t*>(c.other);
+  int32_t* cl = const_cast<int32_t*>(c.len);
+  int64_t q = c.soff[warp];
+  for (int k = 0; k < nrows; ++k) {
+    const int64_t o = o0 + (int64_t)k * W;
+    const bool hv = hflag && hflag[o];
+    const int64_t p0 = ptr[o], p1 = ptr[o + 1];
+    if (lane == 0) cl[c.roff[warp] + k] = hv ? -1 : (int)(p1 - p0);
+    if (hv) continue;
+    for (int64_t e = p0 + lane; e < p1; e += 32) {
+      const int64_t t = q + (e - p0);
+      co[t] = other[e];
+      cw[t] = w[e];
+      cwv[t] = wv[e];
+    }
+    q += p1 - p0;
+  }
+  __syncthreads();
+}
+
 // Copy the factor rows X[0 .. n) (n·R doubles, written by other CTAs before
 // the last grid barrier) into this CTA's SMEM, so that the phase's gathers —
 // one per sample, the latency-critical part — are SMEM reads, not L2 trips.
@@ -376,7 +462,7 @@ __device__ void spmm_phase(WMShared<R>& sm, const int64_t* __restrict__ ptr,
                            const int32_t* __restrict__ other, const double* __restrict__ coef,
                            const double* X, int64_t nout, double* out, double* gpart_buf,
                            const double* Xs, const int32_t* heavy, const int32_t* n_heavy,
-                           const uint8_t* hflag, bool l1) {
+                           const uint8_t* hflag, bool l1, const WMCache& cc) {
   constexpr int NG = WMShared<R>::NG;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t W = (int64_t)gridDim.x * WM_WARPS;
@@ -407,12 +493,26 @@ __device__ void spmm_phase(WMShared<R>& sm, const int64_t* __restrict__ ptr,
     }
     __syncthreads();
   }
-  for (int64_t o = (int64_t)blockIdx.x * WM_WARPS + warp; o < nout; o += W) {
-    if (hflag && hflag[o]) continue;
+  const bool cached = cc.on != 0;
+  int64_t cq = cached ? cc.soff[warp] : 0;
+  const int32_t* clen = cached ? cc.len + cc.roff[warp] : nullptr;
+  const int32_t* src_o = cached ? cc.other : other;
+  const double* src_c = cached ? cc.wv : coef;
+  int k = 0;
+  for (int64_t o = (int64_t)blockIdx.x * WM_WARPS + warp; o < nout; o += W, ++k) {
+    int64_t q0, q1;
+    if (cached) {
+      const int len = clen[k];
+      if (len < 0) continue;
+      q0 = cq; q1 = cq + len; cq = q1;
+    } else {
+      if (hflag && hflag[o]) continue;
+      q0 = ptr[o]; q1 = ptr[o + 1];
+    }
     double acc[R];
 #pragma unroll
     for (int l = 0; l < R; ++l) acc[l] = 0.0;
-    spmm_accum<R>(ptr[o], ptr[o + 1], other, coef, X, Xs, l1, acc);
+    spmm_accum<R>(q0, q1, src_o, src_c, X, Xs, l1, acc);
     emit_row<R>(sm, o, acc, sm.T, out, -1.0, gl);
   }
   flush_gram<R>(sm, gl, gpart_buf);
@@ -557,7 +657,7 @@ __device__ void als_phase(WMShared<R>& sm, const int64_t* __restrict__ ptr,
                           const int32_t* __restrict__ other, const double* __restrict__ w,
                           const double* __restrict__ wv, const double* X, int64_t nout, double lam,
                           double* out, const double* Xs, const int32_t* heavy, const int32_t* n_heavy,
-                          const uint8_t* hflag, bool l1) {
+                          const uint8_t* hflag, bool l1, const WMCache& cc) {
   constexpr int NG = WMShared<R>::NG;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t W = (int64_t)gridDim.x * WM_WARPS;
@@ -592,14 +692,29 @@ __device__ void als_phase(WMShared<R>& sm, const int64_t* __restrict__ ptr,
     if (threadIdx.x == 0) als_solve<R>(sm.hred[0], lam, out, o);
     __syncthreads();
   }
-  for (int64_t o = (int64_t)blockIdx.x * WM_WARPS + warp; o < nout; o += W) {
-    if (hflag && hflag[o]) continue;
+  const bool cached = cc.on != 0;
+  int64_t cq = cached ? cc.soff[warp] : 0;
+  const int32_t* clen = cached ? cc.len + cc.roff[warp] : nullptr;
+  const int32_t* src_o = cached ? cc.other : other;
+  const double* src_w = cached ? cc.w : w;
+  const double* src_v = cached ? cc.wv : wv;
+  int k = 0;
+  for (int64_t o = (int64_t)blockIdx.x * WM_WARPS + warp; o < nout; o += W, ++k) {
+    int64_t q0, q1;
+    if (cached) {
+      const int len = clen[k];
+      if (len < 0) continue;
+      q0 = cq; q1 = cq + len; cq = q1;
+    } else {
+      if (hflag && hflag[o]) continue;
+      q0 = ptr[o]; q1 = ptr[o + 1];
+    }
     double g[NG], h[R];
 #pragma unroll
     for (int e = 0; e < NG; ++e) g[e] = 0.0;
 #pragma unroll
     for (int a = 0; a < R; ++a) h[a] = 0.0;
-    als_accum<R>(ptr[o], ptr[o + 1], other, w, wv, X, Xs, l1, g, h);
+    als_accum<R>(q0, q1, src_o, src_w, src_v, X, Xs, l1, g, h);
     if (lane == 0) {
 #pragma unroll
       for (int e = 0; e < NG; ++e) sm.hred[warp][e] = g[e];
@@ -626,7 +741,15 @@ __global__ void __launch_bounds__(WM_THREADS, 1) wm_persistent_kernel(WMParams p
       for (int b = a; b < R; ++b) { sm.ea[e] = a; sm.eb[e] = b; ++e; }
   }
   set_identity<R>(sm.T);
+  sm.cache[0].on = 0;
+  sm.cache[1].on = 0;
   __syncthreads();
+  if (p.cache_bytes > 0) {
+    uint8_t* region = reinterpret_cast<uint8_t*>(xs) + (stg ? ((size_t)(p.n1 > p.n2 ? p.n1 : p.n2) * R * 8) : 0);
+    const uint8_t* end = region + p.cache_bytes;
+    build_cache(sm.cache[0], sm.scan, p.rptr, p.J, p.w, p.wv, p.n1, p.hflag_r, region, end);
+    build_cache(sm.cache[1], sm.scan, p.cptr, p.cI, p.cw, p.cwv, p.n2, p.hflag_c, region, end);
+  }
   const int64_t G = gridDim.x;
   int buf = 0;
   int nbar = 0;
@@ -673,7 +796,7 @@ __global__ void __launch_bounds__(WM_THREADS, 1) wm_persistent_kernel(WMParams p
     stamp(4 * it);
     const double* xsY = stage_rows<R>(p.Y, p.n2, xs, stg);
     stamp(4 * it + 1);
-    spmm_phase<R>(sm, p.rptr, p.J, p.wv, p.Y, p.n1, p.Z, gp(buf), xsY, p.heavy_r, p.nheavy_r, p.hflag_r, p.x_l1);
+    spmm_phase<R>(sm, p.rptr, p.J, p.wv, p.Y, p.n1, p.Z, gp(buf), xsY, p.heavy_r, p.nheavy_r, p.hflag_r, p.x_l1, sm.cache[0]);
     stamp(4 * it + 2);
     if (it == iters - 1) {  // the last Y half does not reach U0
       cqr2(p.Z, p.n1);
@@ -682,7 +805,7 @@ __global__ void __launch_bounds__(WM_THREADS, 1) wm_persistent_kernel(WMParams p
     cqr1();
     stamp(4 * it + 3);
     spmm_phase<R>(sm, p.cptr, p.cI, p.cwv, p.Z, p.n2, p.Y, gp(buf), stage_rows<R>(p.Z, p.n1, xs, stg),
-                  p.heavy_c, p.nheavy_c, p.hflag_c, p.x_l1);
+                  p.heavy_c, p.nheavy_c, p.hflag_c, p.x_l1, sm.cache[1]);
     cqr1();
   }
   for (int e = tid; e < R * R; e += blockDim.x) TZ[e] = sm.T[e];
@@ -701,10 +824,10 @@ __global__ void __launch_bounds__(WM_THREADS, 1) wm_persistent_kernel(WMParams p
     for (int64_t e = (int64_t)blockIdx.x * WM_THREADS + tid; e < p.n2 * R; e += G * WM_THREADS) p.V[e] = 0.0;
   for (int t = 0; t < p.T; ++t) {
     als_phase<R>(sm, p.cptr, p.cI, p.cw, p.cwv, p.U, p.n2, p.lam, p.V, stage_rows<R>(p.U, p.n1, xs, stg),
-                 p.heavy_c, p.nheavy_c, p.hflag_c, p.x_l1);
+                 p.heavy_c, p.nheavy_c, p.hflag_c, p.x_l1, sm.cache[1]);
     grid_sync(p.bar, p.trace, nbar);
     als_phase<R>(sm, p.rptr, p.J, p.w, p.wv, p.V, p.n1, p.lam, p.U, stage_rows<R>(p.V, p.n2, xs, stg),
-                 p.heavy_r, p.nheavy_r, p.hflag_r, p.x_l1);
+                 p.heavy_r, p.nheavy_r, p.hflag_r, p.x_l1, sm.cache[0]);
     grid_sync(p.bar, p.trace, nbar);
   }
   // output (Û(T), V̂(T)) in fp32
@@ -724,16 +847,36 @@ cudaError_t launch_wm(WMParams& p, cudaStream_t st) {
     return e ? atoi(e) : 1;
   }();
   p.stage_x = (env_stage && xs_bytes <= XS_MAX) ? 1 : 0;
-  const size_t smem = base + (p.stage_x ? xs_bytes : 0);
-  static bool attr = false;
-  if (!attr) {
-    SMP_TRY(cudaFuncSetAttribute(wm_persistent_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)(base + XS_MAX)));
-    attr = true;
-  }
-  int dev = 0, sms = 0, per_sm = 0;
+  int dev = 0, sms = 0, per_sm = 0, optin = 0;
   SMP_TRY(cudaGetDevice(&dev));
   SMP_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  SMP_TRY(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  cudaFuncAttributes fa;
+  SMP_TRY(cudaFuncGetAttributes(&fa, wm_persistent_kernel<R>));
+  optin -= (int)fa.sharedSizeBytes;  // dynamic limit = opt-in total - static
+  size_t smem = base + (p.stage_x ? xs_bytes : 0);
+  // sample cache (WMCache): reserve twice the average per-CTA need of both
+  // sides (20 B per sample and side + row lengths) when that fits beside the
+  // stage — otherwise leave the SMEM to L1, which the unstaged gathers use.
+  // SMP_WM_CACHE=0 disables it (tuning).
+  static const int env_cache = [] {
+    const char* e = getenv("SMP_WM_CACHE");
+    return e ? atoi(e) : 1;
+  }();
+  p.cache_bytes = 0;
+  if (env_cache && sms > 0) {
+    const int64_t avg = (2 * 20 * p.count + 4 * (p.n1 + p.n2)) / sms;
+    const int64_t want = 2 * avg + 4096;
+    if ((int64_t)smem + want <= (int64_t)optin) {
+      p.cache_bytes = want;
+      smem += (size_t)want;
+    }
+  }
+  static bool attr = false;
+  if (!attr) {
+    SMP_TRY(cudaFuncSetAttribute(wm_persistent_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+    attr = true;
+  }
   SMP_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, wm_persistent_kernel<R>, WM_THREADS, smem));
   if (per_sm < 1) return cudaErrorInvalidConfiguration;
   // one CTA per SM (co-resident: cooperative launch); SMP_WM_CTAS overrides (tuning)

@@ -277,12 +277,14 @@ def test_waltmin_heavy_rows_parity(thr, monkeypatch):
     assert np.linalg.norm(Pg - P0, 2) / np.linalg.norm(M, 2) <= 1e-9
 
 
-@pytest.mark.parametrize("r", [5, 10])
-def test_waltmin_gather_paths_bit_identical(r, monkeypatch):
-    """Factor-row gathers through L1 (16-byte pieces for even r) and L2-only
-    give bit-identical factors when the rows are too many to stage in SMEM
-    (n r 8 B > 160 KB): the grid barrier's fences make L1 reads coherent."""
-    n = 2304
+@pytest.mark.parametrize("r,n,switch", [(5, 2304, "SMP_WM_L1"), (10, 2304, "SMP_WM_L1"),
+                                        (5, 1024, "SMP_WM_CACHE"), (10, 600, "SMP_WM_CACHE")])
+def test_waltmin_gather_paths_bit_identical(r, n, switch, monkeypatch):
+    """Data-path switches that must not change a bit of the factors:
+    SMP_WM_L1 — factor-row gathers through L1 (16-byte pieces for even r) vs
+    L2-only, when the rows are too many to stage in SMEM (n r 8 B > 160 KB):
+    the grid barrier's fences make L1 reads coherent; SMP_WM_CACHE — each
+    CTA's sample indices/weights read from its SMEM copy vs from global."""
     d, k = 4096, 256
     Z = synth.gaussian_small(d, r, seed=61)
     A = (Z @ synth.gaussian_small(r, n, seed=62) + 0.1 * synth.gaussian_small(d, n, seed=63)).to(torch.bfloat16)
@@ -291,7 +293,7 @@ def test_waltmin_gather_paths_bit_identical(r, monkeypatch):
     I, J, val, qh = sk.sample_estimate(4 * n * r * math.log(n), 3)
     out = {}
     for mode in ("1", "0"):
-        monkeypatch.setenv("SMP_WM_L1", mode)
+        monkeypatch.setenv(switch, mode)
         U, V = sk.waltmin(I, J, val, qh, r, 10, init_iters=30, seed=3)
         out[mode] = (U.cpu(), V.cpu())
     assert torch.equal(out["1"][0], out["0"][0]) and torch.equal(out["1"][1], out["0"][1])

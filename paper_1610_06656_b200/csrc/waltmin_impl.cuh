@@ -138,6 +138,7 @@ struct WMShared {
   int ea[NG], eb[NG];
   WMCache cache[2];           // [0]: rows of U/Z (CSR side), [1]: rows of V/Y (CSC side)
   int scan[2][WM_WARPS];
+  int nh[2];                  // heavy-row counts (constant during the kernel)
 };
 
 template <int R>
@@ -212,13 +213,26 @@ __device__ __forceinline__ void flush_gram(WMShared<R>& sm, const double (&gl)[(
 
 // G = Σ_cta gpart[buf][cta] (identical fixed order in every CTA), then
 // R^{-1} of the upper Cholesky factor into sm.Rinv (dead pivots -> zero columns)
+// Optionally also stages X[0 .. sn) into xs (see stage_rows): its first
+// chunk of loads is issued together with the Gram loads (one L2 round trip
+// for both on small instances).
 template <int R>
-__device__ void reduce_chol(WMShared<R>& sm, const double* gpart_buf) {
+__device__ void reduce_chol(WMShared<R>& sm, const double* gpart_buf, const double* SX = nullptr,
+                            int64_t sn = 0, double* xs = nullptr) {
   constexpr int NG = WMShared<R>::NG;
   constexpr int MAXK = 16;  // independent loads in flight per thread (one L2 round trip at r <= 6)
+  constexpr int SU = 8;     // stage loads (16 B) per thread in the first chunk
   const int G = gridDim.x;
   const int groups = blockDim.x / NG;  // >= 1 for NG <= 136 < 256
   const int tid = threadIdx.x;
+  const int64_t tot2 = SX ? (sn * R) / 2 : 0;
+  const double2* src2 = reinterpret_cast<const double2*>(SX);
+  double2 sv[SU];
+#pragma unroll
+  for (int u = 0; u < SU; ++u) {
+    const int64_t e = tid + (int64_t)u * blockDim.x;
+    sv[u] = e < tot2 ? __ldcg(src2 + e) : make_double2(0.0, 0.0);
+  }
   if (tid < groups * NG) {
     // thread (g, e) sums CTAs b = g, g + groups, ... in increasing order
     const int e = tid % NG, g = tid / NG;
@@ -234,6 +248,28 @@ __device__ void reduce_chol(WMShared<R>& sm, const double* gpart_buf) {
       for (int q = 0; q < MAXK; ++q) s += v[q];
     }
     sm.red[tid] = s;
+  }
+  if (SX) {
+    double2* dst = reinterpret_cast<double2*>(xs);
+#pragma unroll
+    for (int u = 0; u < SU; ++u) {
+      const int64_t e = tid + (int64_t)u * blockDim.x;
+      if (e < tot2) dst[e] = sv[u];
+    }
+    // the rest (large stages) in batches of SU loads in flight, as stage_rows
+    for (int64_t b = tid + (int64_t)SU * blockDim.x; b < tot2; b += (int64_t)SU * blockDim.x) {
+#pragma unroll
+      for (int u = 0; u < SU; ++u) {
+        const int64_t e = b + (int64_t)u * blockDim.x;
+        sv[u] = e < tot2 ? __ldcg(src2 + e) : make_double2(0.0, 0.0);
+      }
+#pragma unroll
+      for (int u = 0; u < SU; ++u) {
+        const int64_t e = b + (int64_t)u * blockDim.x;
+        if (e < tot2) dst[e] = sv[u];
+      }
+    }
+    if (((sn * R) & 1) && tid == 0) xs[sn * R - 1] = __ldcg(SX + sn * R - 1);
   }
   __syncthreads();
   if (tid < NG) {
@@ -461,7 +497,7 @@ template <int R>
 __device__ void spmm_phase(WMShared<R>& sm, const int64_t* __restrict__ ptr,
                            const int32_t* __restrict__ other, const double* __restrict__ coef,
                            const double* X, int64_t nout, double* out, double* gpart_buf,
-                           const double* Xs, const int32_t* heavy, const int32_t* n_heavy,
+                           const double* Xs, const int32_t* heavy, int n_heavy,
                            const uint8_t* hflag, bool l1, const WMCache& cc) {
   constexpr int NG = WMShared<R>::NG;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -469,7 +505,7 @@ __device__ void spmm_phase(WMShared<R>& sm, const int64_t* __restrict__ ptr,
   double gl[(NG + 31) / 32];
 #pragma unroll
   for (int q = 0; q < (NG + 31) / 32; ++q) gl[q] = 0.0;
-  const int nh = heavy ? *n_heavy : 0;
+  const int nh = heavy ? n_heavy : 0;
   for (int hi = blockIdx.x; hi < nh; hi += gridDim.x) {
     const int64_t o = heavy[hi];
     const int64_t p0 = ptr[o], p1 = ptr[o + 1];
@@ -656,12 +692,12 @@ template <int R>
 __device__ void als_phase(WMShared<R>& sm, const int64_t* __restrict__ ptr,
                           const int32_t* __restrict__ other, const double* __restrict__ w,
                           const double* __restrict__ wv, const double* X, int64_t nout, double lam,
-                          double* out, const double* Xs, const int32_t* heavy, const int32_t* n_heavy,
+                          double* out, const double* Xs, const int32_t* heavy, int n_heavy,
                           const uint8_t* hflag, bool l1, const WMCache& cc) {
   constexpr int NG = WMShared<R>::NG;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t W = (int64_t)gridDim.x * WM_WARPS;
-  const int nh = heavy ? *n_heavy : 0;
+  const int nh = heavy ? n_heavy : 0;
   for (int hi = blockIdx.x; hi < nh; hi += gridDim.x) {
     const int64_t o = heavy[hi];
     const int64_t p0 = ptr[o], p1 = ptr[o + 1];
@@ -743,6 +779,10 @@ __global__ void __launch_bounds__(WM_THREADS, 1) wm_persistent_kernel(WMParams p
   set_identity<R>(sm.T);
   sm.cache[0].on = 0;
   sm.cache[1].on = 0;
+  if (tid == 0) {
+    sm.nh[0] = p.heavy_r ? *p.nheavy_r : 0;
+    sm.nh[1] = p.heavy_c ? *p.nheavy_c : 0;
+  }
   __syncthreads();
   if (p.cache_bytes > 0) {
     uint8_t* region = reinterpret_cast<uint8_t*>(xs) + (stg ? ((size_t)(p.n1 > p.n2 ? p.n1 : p.n2) * R * 8) : 0);
@@ -780,9 +820,9 @@ __global__ void __launch_bounds__(WM_THREADS, 1) wm_persistent_kernel(WMParams p
   // subspace iteration (R12): Z = R Y, Y = Rᵀ Z, each orthonormalised by
   // one CholeskyQR whose triangular factor is folded into the next SpMM
   // (stored rows · T is the orthonormal basis); the final Z gets CholeskyQR2
-  auto cqr1 = [&]() {
+  auto cqr1 = [&](const double* SX, int64_t sn) {
     grid_sync(p.bar, p.trace, nbar);
-    reduce_chol<R>(sm, gp(buf));
+    reduce_chol<R>(sm, gp(buf), stg ? SX : nullptr, sn, xs);
     buf ^= 1;
     for (int e = tid; e < R * R; e += blockDim.x) sm.T[e] = sm.Rinv[e];
     __syncthreads();
@@ -794,19 +834,20 @@ __global__ void __launch_bounds__(WM_THREADS, 1) wm_persistent_kernel(WMParams p
   };
   for (int it = 0; it < iters; ++it) {
     stamp(4 * it);
-    const double* xsY = stage_rows<R>(p.Y, p.n2, xs, stg);
+    // Y rows: staged with the previous reduction, except before the first half
+    const double* xsY = it == 0 ? stage_rows<R>(p.Y, p.n2, xs, stg) : (stg ? xs : nullptr);
     stamp(4 * it + 1);
-    spmm_phase<R>(sm, p.rptr, p.J, p.wv, p.Y, p.n1, p.Z, gp(buf), xsY, p.heavy_r, p.nheavy_r, p.hflag_r, p.x_l1, sm.cache[0]);
+    spmm_phase<R>(sm, p.rptr, p.J, p.wv, p.Y, p.n1, p.Z, gp(buf), xsY, p.heavy_r, sm.nh[0], p.hflag_r, p.x_l1, sm.cache[0]);
     stamp(4 * it + 2);
     if (it == iters - 1) {  // the last Y half does not reach U0
       cqr2(p.Z, p.n1);
       break;
     }
-    cqr1();
+    cqr1(p.Z, p.n1);
     stamp(4 * it + 3);
-    spmm_phase<R>(sm, p.cptr, p.cI, p.cwv, p.Z, p.n2, p.Y, gp(buf), stage_rows<R>(p.Z, p.n1, xs, stg),
-                  p.heavy_c, p.nheavy_c, p.hflag_c, p.x_l1, sm.cache[1]);
-    cqr1();
+    spmm_phase<R>(sm, p.cptr, p.cI, p.cwv, p.Z, p.n2, p.Y, gp(buf), stg ? xs : nullptr,
+                  p.heavy_c, sm.nh[1], p.hflag_c, p.x_l1, sm.cache[1]);
+    cqr1(it + 1 < iters ? p.Y : nullptr, p.n2);
   }
   for (int e = tid; e < R * R; e += blockDim.x) TZ[e] = sm.T[e];
   __syncthreads();
@@ -824,10 +865,10 @@ __global__ void __launch_bounds__(WM_THREADS, 1) wm_persistent_kernel(WMParams p
     for (int64_t e = (int64_t)blockIdx.x * WM_THREADS + tid; e < p.n2 * R; e += G * WM_THREADS) p.V[e] = 0.0;
   for (int t = 0; t < p.T; ++t) {
     als_phase<R>(sm, p.cptr, p.cI, p.cw, p.cwv, p.U, p.n2, p.lam, p.V, stage_rows<R>(p.U, p.n1, xs, stg),
-                 p.heavy_c, p.nheavy_c, p.hflag_c, p.x_l1, sm.cache[1]);
+                 p.heavy_c, sm.nh[1], p.hflag_c, p.x_l1, sm.cache[1]);
     grid_sync(p.bar, p.trace, nbar);
     als_phase<R>(sm, p.rptr, p.J, p.w, p.wv, p.V, p.n1, p.lam, p.U, stage_rows<R>(p.V, p.n2, xs, stg),
-                 p.heavy_r, p.nheavy_r, p.hflag_r, p.x_l1, sm.cache[0]);
+                 p.heavy_r, sm.nh[0], p.hflag_r, p.x_l1, sm.cache[0]);
     grid_sync(p.bar, p.trace, nbar);
   }
   // output (Û(T), V̂(T)) in fp32

@@ -211,6 +211,59 @@ __device__ __forceinline__ void flush_gram(WMShared<R>& sm, const double (&gl)[(
   }
 }
 
+// upper Cholesky of the reduced Gram sm.G = RᵀR and out = R^{-1} (one thread)
+template <int R>
+__device__ __noinline__ void chol_rinv(const WMShared<R>& sm, double* out) {
+  // upper Cholesky G = RᵀR (L = Rᵀ), then Rinv = (Lᵀ)^{-1}; dead pivots
+  // (rank deficiency) give zero columns.  Fully unrolled: registers only.
+  double L[R][R], Ri[R][R], inv[R];
+  bool dead[R];
+  double tr = 0.0;
+  {
+    int e = 0;
+#pragma unroll
+    for (int a = 0; a < R; ++a)
+#pragma unroll
+      for (int b = a; b < R; ++b) {
+        L[b][a] = sm.G[e];  // lower triangle holds G
+        if (a == b) tr += sm.G[e];
+        ++e;
+      }
+  }
+  const double tol = 1e-28 * (tr > 0.0 ? tr : 1.0);
+#pragma unroll
+  for (int j = 0; j < R; ++j) {
+    double s = L[j][j];
+#pragma unroll
+    for (int q = 0; q < j; ++q) s -= L[j][q] * L[j][q];
+    dead[j] = !(s > tol);
+    const double d = dead[j] ? 0.0 : sqrt(s);
+    inv[j] = dead[j] ? 0.0 : 1.0 / d;
+    L[j][j] = d;
+#pragma unroll
+    for (int i = j + 1; i < R; ++i) {
+      double t = L[i][j];
+#pragma unroll
+      for (int q = 0; q < j; ++q) t -= L[i][q] * L[j][q];
+      L[i][j] = t * inv[j];
+    }
+  }
+  // Ri = (Lᵀ)^{-1} (upper): back substitution per column c
+#pragma unroll
+  for (int c = 0; c < R; ++c)
+#pragma unroll
+    for (int i = R - 1; i >= 0; --i) {
+      double t = (i == c) ? 1.0 : 0.0;
+#pragma unroll
+      for (int q = i + 1; q < R; ++q) t -= L[q][i] * Ri[q][c];
+      Ri[i][c] = (dead[i] || dead[c]) ? 0.0 : t * inv[i];
+    }
+#pragma unroll
+  for (int i = 0; i < R; ++i)
+#pragma unroll
+    for (int c = 0; c < R; ++c) out[i * R + c] = Ri[i][c];
+}
+
 // G = Σ_cta gpart[buf][cta] (identical fixed order in every CTA), then
 // R^{-1} of the upper Cholesky factor into sm.Rinv (dead pivots -> zero columns)
 // Optionally also stages X[0 .. sn) into xs (see stage_rows): its first
@@ -218,7 +271,7 @@ __device__ __forceinline__ void flush_gram(WMShared<R>& sm, const double (&gl)[(
 // for both on small instances).
 template <int R>
 __device__ void reduce_chol(WMShared<R>& sm, const double* gpart_buf, const double* SX = nullptr,
-                            int64_t sn = 0, double* xs = nullptr) {
+                            int64_t sn = 0, double* xs = nullptr, bool do_chol = true) {
   constexpr int NG = WMShared<R>::NG;
   constexpr int MAXK = 16;  // independent loads in flight per thread (one L2 round trip at r <= 6)
   constexpr int SU = 8;     // stage loads (16 B) per thread in the first chunk
@@ -278,56 +331,8 @@ __device__ void reduce_chol(WMShared<R>& sm, const double* gpart_buf, const doub
     sm.G[tid] = s;  // packed upper triangle, row-major (ea/eb order)
   }
   __syncthreads();
-  if (tid == 0) {
-    // upper Cholesky G = RᵀR (L = Rᵀ), then Rinv = (Lᵀ)^{-1}; dead pivots
-    // (rank deficiency) give zero columns.  Fully unrolled: registers only.
-    double L[R][R], Ri[R][R], inv[R];
-    bool dead[R];
-    double tr = 0.0;
-    {
-      int e = 0;
-#pragma unroll
-      for (int a = 0; a < R; ++a)
-#pragma unroll
-        for (int b = a; b < R; ++b) {
-          L[b][a] = sm.G[e];  // lower triangle holds G
-          if (a == b) tr += sm.G[e];
-          ++e;
-        }
-    }
-    const double tol = 1e-28 * (tr > 0.0 ? tr : 1.0);
-#pragma unroll
-    for (int j = 0; j < R; ++j) {
-      double s = L[j][j];
-#pragma unroll
-      for (int q = 0; q < j; ++q) s -= L[j][q] * L[j][q];
-      dead[j] = !(s > tol);
-      const double d = dead[j] ? 0.0 : sqrt(s);
-      inv[j] = dead[j] ? 0.0 : 1.0 / d;
-      L[j][j] = d;
-#pragma unroll
-      for (int i = j + 1; i < R; ++i) {
-        double t = L[i][j];
-#pragma unroll
-        for (int q = 0; q < j; ++q) t -= L[i][q] * L[j][q];
-        L[i][j] = t * inv[j];
-      }
-    }
-    // Ri = (Lᵀ)^{-1} (upper): back substitution per column c
-#pragma unroll
-    for (int c = 0; c < R; ++c)
-#pragma unroll
-      for (int i = R - 1; i >= 0; --i) {
-        double t = (i == c) ? 1.0 : 0.0;
-#pragma unroll
-        for (int q = i + 1; q < R; ++q) t -= L[q][i] * Ri[q][c];
-        Ri[i][c] = (dead[i] || dead[c]) ? 0.0 : t * inv[i];
-      }
-#pragma unroll
-    for (int i = 0; i < R; ++i)
-#pragma unroll
-      for (int c = 0; c < R; ++c) sm.Rinv[i * R + c] = Ri[i][c];
-  }
+  if (!do_chol) return;  // caller overlaps chol_rinv with other work
+  if (tid == 0) chol_rinv<R>(sm, sm.Rinv);
   __syncthreads();
 }
 
@@ -498,7 +503,7 @@ __device__ void spmm_phase(WMShared<R>& sm, const int64_t* __restrict__ ptr,
                            const int32_t* __restrict__ other, const double* __restrict__ coef,
                            const double* X, int64_t nout, double* out, double* gpart_buf,
                            const double* Xs, const int32_t* heavy, int n_heavy,
-                           const uint8_t* hflag, bool l1, const WMCache& cc) {
+                           const uint8_t* hflag, bool l1, const WMCache& cc, bool chol_pending = false) {
   constexpr int NG = WMShared<R>::NG;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t W = (int64_t)gridDim.x * WM_WARPS;
@@ -506,6 +511,20 @@ __device__ void spmm_phase(WMShared<R>& sm, const int64_t* __restrict__ ptr,
 #pragma unroll
   for (int q = 0; q < (NG + 31) / 32; ++q) gl[q] = 0.0;
   const int nh = heavy ? n_heavy : 0;
+  // chol_pending: sm.T (= R^{-1} of the reduced Gram in sm.G) is not computed
+  // yet.  Thread 0 computes it while the other warps accumulate their first
+  // row (the sums do not need T); every warp meets once at named barrier 1
+  // before its first emit.  With heavy rows (CTA-wide, need T at once) it is
+  // computed up front.
+  bool wait_t = chol_pending;
+  if (chol_pending && nh > 0) {
+    if (threadIdx.x == 0) chol_rinv<R>(sm, sm.T);
+    __syncthreads();
+    wait_t = false;
+  } else if (chol_pending && warp == 0) {
+    if (lane == 0) chol_rinv<R>(sm, sm.T);
+    __syncwarp();
+  }
   for (int hi = blockIdx.x; hi < nh; hi += gridDim.x) {
     const int64_t o = heavy[hi];
     const int64_t p0 = ptr[o], p1 = ptr[o + 1];
@@ -549,8 +568,13 @@ __device__ void spmm_phase(WMShared<R>& sm, const int64_t* __restrict__ ptr,
 #pragma unroll
     for (int l = 0; l < R; ++l) acc[l] = 0.0;
     spmm_accum<R>(q0, q1, src_o, src_c, X, Xs, l1, acc);
+    if (wait_t) {
+      asm volatile("bar.sync 1, %0;" ::"r"(WM_THREADS) : "memory");
+      wait_t = false;
+    }
     emit_row<R>(sm, o, acc, sm.T, out, -1.0, gl);
   }
+  if (wait_t) asm volatile("bar.sync 1, %0;" ::"r"(WM_THREADS) : "memory");
   flush_gram<R>(sm, gl, gpart_buf);
 }
 
@@ -820,12 +844,12 @@ __global__ void __launch_bounds__(WM_THREADS, 1) wm_persistent_kernel(WMParams p
   // subspace iteration (R12): Z = R Y, Y = Rᵀ Z, each orthonormalised by
   // one CholeskyQR whose triangular factor is folded into the next SpMM
   // (stored rows · T is the orthonormal basis); the final Z gets CholeskyQR2
-  auto cqr1 = [&](const double* SX, int64_t sn) {
+  // defer: leave the Cholesky to the next spmm_phase (chol_pending), which
+  // overlaps it with the first row's accumulation
+  auto cqr1_defer = [&](const double* SX, int64_t sn) {
     grid_sync(p.bar, p.trace, nbar);
-    reduce_chol<R>(sm, gp(buf), stg ? SX : nullptr, sn, xs);
+    reduce_chol<R>(sm, gp(buf), stg ? SX : nullptr, sn, xs, false);
     buf ^= 1;
-    for (int e = tid; e < R * R; e += blockDim.x) sm.T[e] = sm.Rinv[e];
-    __syncthreads();
   };
   const int iters = p.init_iters > 0 ? p.init_iters : 1;
   // diagnostics (SMP_WM_TRACE): CTA 0's time in the first Z-side SpMM phases
@@ -837,17 +861,18 @@ __global__ void __launch_bounds__(WM_THREADS, 1) wm_persistent_kernel(WMParams p
     // Y rows: staged with the previous reduction, except before the first half
     const double* xsY = it == 0 ? stage_rows<R>(p.Y, p.n2, xs, stg) : (stg ? xs : nullptr);
     stamp(4 * it + 1);
-    spmm_phase<R>(sm, p.rptr, p.J, p.wv, p.Y, p.n1, p.Z, gp(buf), xsY, p.heavy_r, sm.nh[0], p.hflag_r, p.x_l1, sm.cache[0]);
+    spmm_phase<R>(sm, p.rptr, p.J, p.wv, p.Y, p.n1, p.Z, gp(buf), xsY, p.heavy_r, sm.nh[0], p.hflag_r, p.x_l1,
+                  sm.cache[0], it > 0);
     stamp(4 * it + 2);
     if (it == iters - 1) {  // the last Y half does not reach U0
       cqr2(p.Z, p.n1);
       break;
     }
-    cqr1(p.Z, p.n1);
+    cqr1_defer(p.Z, p.n1);
     stamp(4 * it + 3);
     spmm_phase<R>(sm, p.cptr, p.cI, p.cwv, p.Z, p.n2, p.Y, gp(buf), stg ? xs : nullptr,
-                  p.heavy_c, sm.nh[1], p.hflag_c, p.x_l1, sm.cache[1]);
-    cqr1(it + 1 < iters ? p.Y : nullptr, p.n2);
+                  p.heavy_c, sm.nh[1], p.hflag_c, p.x_l1, sm.cache[1], true);
+    cqr1_defer(p.Y, p.n2);  // it + 1 < iters here; its Cholesky runs in the next row SpMM
   }
   for (int e = tid; e < R * R; e += blockDim.x) TZ[e] = sm.T[e];
   __syncthreads();

@@ -929,9 +929,28 @@ cudaError_t launch_wm(WMParams& p, cudaStream_t st) {
     const char* e = getenv("SMP_WM_CACHE");
     return e ? atoi(e) : 1;
   }();
+  // one CTA per SM at most (co-resident: cooperative launch), and no more CTAs
+  // than needed for the per-warp row count a full grid would give: the same
+  // critical path with fewer barrier participants and Gram partials (cfg1:
+  // 1024 rows -> 128 CTAs of one row per warp; cfg4 2.85 -> 2.60 ms).
+  // SMP_WM_CTAS overrides (tuning).
+  static const int env_ctas = [] {
+    const char* e = getenv("SMP_WM_CTAS");
+    return e ? atoi(e) : 0;
+  }();
+  int grid = sms;
+  {
+    const int64_t nmax = p.n1 > p.n2 ? p.n1 : p.n2;
+    const int64_t per_warp = (nmax + (int64_t)sms * WM_WARPS - 1) / ((int64_t)sms * WM_WARPS);
+    if (per_warp > 0) {
+      const int64_t need = (nmax + per_warp * WM_WARPS - 1) / (per_warp * WM_WARPS);
+      grid = (int)(need < 1 ? 1 : (need < sms ? need : sms));
+    }
+  }
+  if (env_ctas > 0 && env_ctas <= sms) grid = env_ctas;
   p.cache_bytes = 0;
-  if (env_cache && sms > 0) {
-    const int64_t avg = (2 * 20 * p.count + 4 * (p.n1 + p.n2)) / sms;
+  if (env_cache && grid > 0) {
+    const int64_t avg = (2 * 20 * p.count + 4 * (p.n1 + p.n2)) / grid;
     const int64_t want = 2 * avg + 4096;
     if ((int64_t)smem + want <= (int64_t)optin) {
       p.cache_bytes = want;
@@ -945,12 +964,6 @@ cudaError_t launch_wm(WMParams& p, cudaStream_t st) {
   }
   SMP_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, wm_persistent_kernel<R>, WM_THREADS, smem));
   if (per_sm < 1) return cudaErrorInvalidConfiguration;
-  // one CTA per SM (co-resident: cooperative launch); SMP_WM_CTAS overrides (tuning)
-  static const int env_ctas = [] {
-    const char* e = getenv("SMP_WM_CTAS");
-    return e ? atoi(e) : 0;
-  }();
-  const int grid = (env_ctas > 0 && env_ctas <= sms) ? env_ctas : sms;
   void* args[] = {&p};
   return cudaLaunchCooperativeKernel((const void*)wm_persistent_kernel<R>, dim3(grid), dim3(WM_THREADS),
                                      args, smem, st);

@@ -198,21 +198,22 @@ cudaError_t run_waltmin(const WaltminArgs& a, cudaStream_t st) {
   uint64_t* trace = nullptr;
   const int max_bar = 2 * (a.init_iters + 4) + 2 * a.T + 8;
   if (tr && atoi(tr)) {
-    SMP_TRY(cudaMalloc(&trace, 3 * 8 * (size_t)max_bar + 64 * 8));
-    SMP_TRY(cudaMemsetAsync(trace, 0, 3 * 8 * (size_t)max_bar + 64 * 8, st));
+    SMP_TRY(cudaMalloc(&trace, 4 * 8 * (size_t)max_bar + 64 * 8));
+    SMP_TRY(cudaMemsetAsync(trace, 0, 4 * 8 * (size_t)max_bar + 64 * 8, st));
   }
   p.trace = trace;
-  p.trace2 = trace ? trace + 3 * max_bar : nullptr;
+  p.trace2 = trace ? trace + 4 * max_bar : nullptr;
   SMP_TRY(launch_wm_r(r, p, st));
   if (trace) {
-    std::vector<uint64_t> t(3 * (size_t)max_bar + 64);
+    std::vector<uint64_t> t(4 * (size_t)max_bar + 64);
     SMP_TRY(cudaMemcpyAsync(t.data(), trace, t.size() * 8, cudaMemcpyDeviceToHost, st));
     SMP_TRY(cudaStreamSynchronize(st));
-    for (int b = 0; b < max_bar && t[3 * b]; ++b)
-      fprintf(stderr, "wm barrier %3d: cta0 work %8.2f us, skew to last %8.2f us, release %6.2f us\n", b,
-              b ? (t[3 * b] - t[3 * (b - 1) + 2]) * 1e-3 : 0.0, ((int64_t)t[3 * b + 1] - (int64_t)t[3 * b]) * 1e-3,
-              ((int64_t)t[3 * b + 2] - (int64_t)t[3 * b + 1]) * 1e-3);
-    const uint64_t* t2 = t.data() + 3 * max_bar;
+    for (int b = 0; b < max_bar && t[4 * b]; ++b)
+      fprintf(stderr, "wm barrier %3d: cta0 work %8.2f us, skew to last %8.2f us (cta %3d), release %6.2f us\n",
+              b, b ? (t[4 * b] - t[4 * (b - 1) + 2]) * 1e-3 : 0.0,
+              ((int64_t)t[4 * b + 1] - (int64_t)t[4 * b]) * 1e-3, (int)t[4 * b + 3],
+              ((int64_t)t[4 * b + 2] - (int64_t)t[4 * b + 1]) * 1e-3);
+    const uint64_t* t2 = t.data() + 4 * max_bar;
     for (int i = 0; i + 4 < 64 && t2[i + 4]; i += 4)
       fprintf(stderr, "wm iter %2d: stage %.2f us, Z-SpMM+flush %.2f us, barrier+chol %.2f us, Y half %.2f us\n",
               i / 4, (t2[i + 1] - t2[i]) * 1e-3, (t2[i + 2] - t2[i + 1]) * 1e-3, (t2[i + 3] - t2[i + 2]) * 1e-3,

@@ -56,7 +56,7 @@ struct WMParams {
   double* V;
   double* gpart;  // [2][gridDim.x][NG]
   unsigned* bar;  // [2]: arrival count, generation
-  uint64_t* trace;  // optional [3 * barriers] (SMP_WM_TRACE)
+  uint64_t* trace;  // optional [4 * barriers] (SMP_WM_TRACE)
   uint64_t* trace2; // optional [64] phase stamps of CTA 0 (SMP_WM_TRACE)
   int stage_x;      // gathered factor rows staged into SMEM per phase (fits: n·r·8 B small)
   // heavy rows (> WM_HEAVY samples): compacted lists, counts, per-row flags
@@ -87,16 +87,19 @@ __device__ __forceinline__ uint64_t wm_globaltimer() {
 // later reads after the other CTAs' writes).  No generation word, no reset,
 // one L2 round trip from the last arrival to the release.
 // trace (diagnostics, SMP_WM_TRACE): per barrier, CTA 0's arrival, the last
-// arrival and CTA 0's release (globaltimer ns).
+// arrival, CTA 0's release (globaltimer ns) and the last arriving CTA.
 __device__ __forceinline__ void grid_sync(unsigned* bar, uint64_t* trace, int& nb) {
   __syncthreads();
   if (threadIdx.x == 0) {
     const unsigned target = (unsigned)(nb + 1) * gridDim.x;
     if (trace) {
-      if (blockIdx.x == 0) trace[3 * nb] = wm_globaltimer();
+      if (blockIdx.x == 0) trace[4 * nb] = wm_globaltimer();
       unsigned old;
       asm volatile("atom.release.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(bar) : "memory");
-      if (old == target - 1) trace[3 * nb + 1] = wm_globaltimer();
+      if (old == target - 1) {
+        trace[4 * nb + 1] = wm_globaltimer();
+        trace[4 * nb + 3] = blockIdx.x;
+      }
     } else {
       asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
     }
@@ -104,7 +107,7 @@ __device__ __forceinline__ void grid_sync(unsigned* bar, uint64_t* trace, int& n
     do {
       asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
     } while (v < target);
-    if (trace && blockIdx.x == 0) trace[3 * nb + 2] = wm_globaltimer();
+    if (trace && blockIdx.x == 0) trace[4 * nb + 2] = wm_globaltimer();
   }
   ++nb;
   __syncthreads();

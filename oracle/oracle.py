@@ -17,6 +17,7 @@ _SRC = os.path.join(_HERE, "smp_oracle.c")
 _LIB = os.path.join(_HERE, "liboracle.so")
 
 PI_RADEMACHER, PI_GAUSSIAN, PI_HADAMARD = 0, 1, 2
+PART_REUSE_ALL, PART_FRESH_2T1 = 0, 1
 
 
 def pi_srht(d: int) -> int:
@@ -74,7 +75,15 @@ def _get():
         lib.or_estimate.argtypes = [ctypes.c_int, i64, P, P, P, P, P, P, ctypes.c_int, P]
         lib.or_als_half.argtypes = [ctypes.c_int, i64, i64, P, P, P, P, P, f64, P]
         lib.or_waltmin.argtypes = [i64, i64, ctypes.c_int, ctypes.c_int, ctypes.c_int, f64, f64,
-                                   u64, i64, P, P, P, P, P, f64, P, P]
+                                   u64, ctypes.c_int, i64, P, P, P, P, P, f64, P, P]
+        lib.or_multinomial_draws.argtypes = [u64, f64, i64, i64, P, P, i64, P, P, P]
+        lib.or_mn_rows.argtypes = [f64, i64, i64, P, P, P, P]
+        lib.or_mn_rows.restype = None
+        lib.or_multinomial_draws.restype = i64
+        lib.or_mn_qhat.argtypes = [f64, f64, f64, f64]
+        lib.or_mn_qhat.restype = f64
+        lib.or_partition.argtypes = [u64, ctypes.c_int, i64, P, P, P]
+        lib.or_partition.restype = None
         _lib = lib
     return _lib
 
@@ -242,9 +251,38 @@ def sample(seed, m, alpha, beta, cap=None):
         cap = int(cnt)
 
 
+def multinomial_draws(seed, m, alpha, beta):
+    """Raw draws of the row-multinomial sampler's unsaturated part (P:633-639;
+    R27): with replacement, sorted by (i, j), duplicates kept."""
+    alpha = _c(alpha, np.float64)
+    beta = _c(beta, np.float64)
+    n1, n2 = len(alpha), len(beta)
+    lib = _get()
+    cnt = lib.or_multinomial_draws(seed, m, n1, n2, _p(alpha), _p(beta), 0, None, None, None)
+    I = np.empty(max(cnt, 1), np.int32)
+    J = np.empty(max(cnt, 1), np.int32)
+    lib.or_multinomial_draws(seed, m, n1, n2, _p(alpha), _p(beta), cnt, _p(I), _p(J), None)
+    return I[:cnt].copy(), J[:cnt].copy()
+
+
+def mn_rows(m, alpha, beta):
+    """(s_i, T_i) per row: saturated-prefix length and unsaturated mass (R27)."""
+    alpha = _c(alpha, np.float64)
+    beta = _c(beta, np.float64)
+    s = np.empty(len(alpha), np.int64)
+    T = np.empty(len(alpha), np.float64)
+    _get().or_mn_rows(m, len(alpha), len(beta), _p(alpha), _p(beta), _p(s), _p(T))
+    return s, T
+
+
+def mn_qhat(m, alpha_i, beta_j, T_i) -> float:
+    """Inclusion probability of (i, j) in the multinomial Ω (R27)."""
+    return _get().or_mn_qhat(m, alpha_i, beta_j, T_i)
+
+
 def sample_multinomial(seed, m, alpha, beta):
-    """Ω by the appendix's row-multinomial sampler (R27): draws
-    with replacement, sorted by (i, j), and q = m(α_i + β_j) unclipped."""
+    """Ω by the appendix's row-multinomial sampler (R27): the SET
+    of drawn pairs, sorted by (i, j), with q̂ = P((i, j) ∈ Ω)."""
     alpha = _c(alpha, np.float64)
     beta = _c(beta, np.float64)
     n1, n2 = len(alpha), len(beta)
@@ -258,6 +296,15 @@ def sample_multinomial(seed, m, alpha, beta):
         if cnt <= cap:
             return I[:cnt].copy(), J[:cnt].copy(), q[:cnt].copy()
         cap = int(cnt)
+
+
+def partition(seed, T, I, J):
+    """Alg. 2 line 3 (R11 FRESH_2T1): subset id in [0, 2T+1) per sample."""
+    I = _c(I, np.int32)
+    J = _c(J, np.int32)
+    sub = np.empty(max(len(I), 1), np.int32)
+    _get().or_partition(seed, 2 * T + 1, len(I), _p(I), _p(J), _p(sub))
+    return sub[:len(I)].copy()
 
 
 def estimate(k, I, J, Ask, Bsk, DA, DB, plain=False):
@@ -290,7 +337,8 @@ def als_half(r, n_out, side, other, val, w, X_other, lam=1e-10):
 
 
 def waltmin(n1, n2, r, T, I, J, val, qhat_, a_norm, frobA, init_iters=50, trim_c=8.0,
-            lam=1e-10, seed=0):
+            lam=1e-10, seed=0, partition=PART_REUSE_ALL):
+    """Alg. 2; partition per R11 (REUSE_ALL or FRESH_2T1)."""
     I = _c(I, np.int32)
     J = _c(J, np.int32)
     val = _c(val, np.float64)
@@ -298,7 +346,7 @@ def waltmin(n1, n2, r, T, I, J, val, qhat_, a_norm, frobA, init_iters=50, trim_c
     a_norm = _c(a_norm, np.float64)
     U = np.zeros((n1, r), np.float64)
     V = np.zeros((n2, r), np.float64)
-    _get().or_waltmin(n1, n2, r, T, init_iters, trim_c, lam, seed, len(I), _p(I), _p(J),
+    _get().or_waltmin(n1, n2, r, T, init_iters, trim_c, lam, seed, int(partition), len(I), _p(I), _p(J),
                       _p(val), _p(qhat_), _p(a_norm), frobA, _p(U), _p(V))
     return U, V
 
@@ -307,7 +355,8 @@ def waltmin(n1, n2, r, T, I, J, val, qhat_, a_norm, frobA, init_iters=50, trim_c
 # Whole pipeline (Alg. 1) on in-memory inputs (small configs only)
 # --------------------------------------------------------------------------
 def smp_pca(A, B, k, r, m, T, pi_kind=PI_RADEMACHER, seed=0, omega_seed=None,
-            wm_seed=None, init_iters=50, trim_c=8.0, lam=1e-10, plain=False, a_is_b=False):
+            wm_seed=None, init_iters=50, trim_c=8.0, lam=1e-10, plain=False, a_is_b=False,
+            sampler="bernoulli", partition=PART_REUSE_ALL):
     """Alg. 1 end to end.  Returns a dict with every intermediate."""
     omega_seed = seed if omega_seed is None else omega_seed
     wm_seed = seed if wm_seed is None else wm_seed
@@ -320,10 +369,13 @@ def smp_pca(A, B, k, r, m, T, pi_kind=PI_RADEMACHER, seed=0, omega_seed=None,
     Ask, As, DA = finalize(k, skA, a2)
     Bsk, Bs, DB = finalize(k, skB, b2)
     al, be = alpha_beta(a2, b2, FA, FB)
-    I, J, q = sample(omega_seed, m, al, be)
+    if sampler == "multinomial":
+        I, J, q = sample_multinomial(omega_seed, m, al, be)
+    else:
+        I, J, q = sample(omega_seed, m, al, be)
     Mt = estimate(k, I, J, Ask, Bsk, DA, DB, plain=plain)
     U, V = waltmin(len(a2), len(b2), r, T, I, J, Mt, q, np.sqrt(a2), np.sqrt(FA),
-                   init_iters=init_iters, trim_c=trim_c, lam=lam, seed=wm_seed)
+                   init_iters=init_iters, trim_c=trim_c, lam=lam, seed=wm_seed, partition=partition)
     return dict(Ask=Ask, Bsk=Bsk, a2=a2, b2=b2, FA=FA, FB=FB, As=As, Bs=Bs, DA=DA, DB=DB,
                 alpha=al, beta=be, I=I, J=J, qhat=q, Mt=Mt, U=U, V=V)
 

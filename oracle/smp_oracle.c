@@ -397,17 +397,29 @@ double or_qhat(double m, double alpha_i, double beta_j)
 }
 
 /* ------------------------------------------------------------------------ */
-/* Row-multinomial sampler (the paper's appendix; SURVEY §8f      */
-/* NEXT-2; R27).  With α, β from or_alpha_beta (Eq. 1, R6):       */
-/*   Bpre[j] = β_0 + ... + β_j (sequential, fp64); T_i = n2·α_i + Bpre[n2-1] */
-/*   m_i = m·T_i (= m(‖A_i‖²/(2‖A‖_F²) + 1/(2n1)), the appendix's m_i);     */
-/*   M_i = floor(m_i + u_i), u_i = U53(Philox(i, 0, 0, 8)) 2^-53;           */
-/*   draw d of row i: u = U53(Philox(i, d, 0, 9)) 2^-53, target = u·T_i,     */
-/*   j = the smallest column with C_i(j) = (j+1)·α_i + Bpre[j] > target      */
-/*   (n2-1 if none): inversion of the CDF of q̃_ij ∝ α_i + β_j.     */
-/* Draws are with replacement; output sorted by (i, j), duplicates kept,     */
-/* q = m(α_i + β_j) unclipped (each draw's weight is 1/q: a pair's expected  */
-/* count is q, the Bernoulli inclusion probability when q <= 1).             */
+/* Row-multinomial sampler (the paper's appendix, with Alg. 1     */
+/* line 3's saturation q̂ = min(1, q)     */
+/* R27).  With α, β from or_alpha_beta and q_ij = m(α_i + β_j) (Eq. 1, R6):  */
+/*  * σ orders the columns by β descending (ties: column index ascending);   */
+/*    Bp[p] = β_σ(0) + ... + β_σ(p) (sequential, fp64), Btot = Bp[n2-1].     */
+/*  * Row i's saturated pairs — q_ij >= 1, always in Ω with q̂ = 1 as in the  */
+/*    Bernoulli model — are the prefix p < s_i of σ (q is non-increasing     */
+/*    in p): s_i = the first p with m(α_i + β_σ(p)) < 1 (binary search).     */
+/*  * The unsaturated mass T_i = (n2 − s_i)·α_i + (Btot − Bp[s_i−1]) (the     */
+/*    appendix's m_i/m restricted to unsaturated columns; Bp[−1] = 0) is      */
+/*    drawn row-wise multinomially: m_i = m·T_i, M_i = floor(m_i + u_i),      */
+/*    u_i = U53(Philox(i, 0, 0, 8)) 2^-53; draw d: target = U53(Philox(i, d,   */
+/*    0, 9)) 2^-53 · T_i, p = the first p >= s_i with                        */
+/*    C_i(p) = (p − s_i + 1)·α_i + (Bp[p] − Bp[s_i−1]) > target (n2−1 if       */
+/*    none): inversion of the affine CDF of q̃_ij ∝ α_i + β_j ("only   */
+/*    update the linear shift and scale"); column j = σ(p).                   */
+/*  * Ω = saturated pairs ∪ the SET of drawn pairs, sorted by (i, j).  A      */
+/*    drawn pair's inclusion probability, with π = (α_i + β_j)/T_i,          */
+/*    F = floor(m_i), f = m_i − F (M_i = F + 1 w.p. f):                       */
+/*      q̂_ij = 1 − (1−π)^F (1 − fπ) = −expm1(F·log1p(−π) + log1p(−fπ))      */
+/*    (π >= 1: q̂ = 1 if F >= 1, else f); WAltMin weights it 1/q̂ (Alg. 2    */
+/*    line 2).  For q ≪ 1, q̂ → q (the Bernoulli marginal).                  */
+/* O(n2 log n2 + n1 log n2 + m log n2) work (P:633-639's O(m log n)).        */
 /* ------------------------------------------------------------------------ */
 static double u53(uint64_t seed, uint32_t c0, uint32_t c1, uint32_t tag)
 {
@@ -423,36 +435,161 @@ static int cmp_i32(const void *a, const void *b)
     return (x > y) - (x < y);
 }
 
-int64_t or_sample_multinomial(uint64_t seed, double m, int64_t n1, int64_t n2, const double *alpha,
-                              const double *beta, int64_t cap, int32_t *I, int32_t *J, double *q)
+typedef struct { double b; int64_t j; } beta_rec;
+
+static int cmp_beta_desc(const void *a, const void *b)
 {
-    double *bpre = (double *)malloc(sizeof(double) * (size_t)(n2 > 0 ? n2 : 1));
+    const beta_rec *x = (const beta_rec *)a, *y = (const beta_rec *)b;
+    if (x->b != y->b) return x->b > y->b ? -1 : 1;
+    return (x->j > y->j) - (x->j < y->j);
+}
+
+typedef struct {
+    int64_t n2;
+    int64_t *sig;   /* σ */
+    double *bp;     /* Bp */
+    double btot;
+} mn_ctx;
+
+static void mn_setup(mn_ctx *c, int64_t n2, const double *beta)
+{
+    beta_rec *r = (beta_rec *)malloc(sizeof(beta_rec) * (size_t)(n2 > 0 ? n2 : 1));
+    for (int64_t j = 0; j < n2; ++j) { r[j].b = beta[j]; r[j].j = j; }
+    qsort(r, (size_t)n2, sizeof(beta_rec), cmp_beta_desc);
+    c->n2 = n2;
+    c->sig = (int64_t *)malloc(sizeof(int64_t) * (size_t)(n2 > 0 ? n2 : 1));
+    c->bp = (double *)malloc(sizeof(double) * (size_t)(n2 > 0 ? n2 : 1));
     double acc = 0.0;
-    for (int64_t j = 0; j < n2; ++j) { acc = acc + beta[j]; bpre[j] = acc; }
-    const double btot = n2 > 0 ? bpre[n2 - 1] : 0.0;
+    for (int64_t p = 0; p < n2; ++p) {
+        c->sig[p] = r[p].j;
+        acc = acc + r[p].b;
+        c->bp[p] = acc;
+    }
+    c->btot = n2 > 0 ? c->bp[n2 - 1] : 0.0;
+    free(r);
+}
+
+static void mn_free(mn_ctx *c) { free(c->sig); free(c->bp); }
+
+/* s_i and T_i of row i */
+static void mn_row(const mn_ctx *c, double m, double alpha_i, const double *beta, int64_t *s_out,
+                   double *T_out)
+{
+    int64_t lo = 0, hi = c->n2;                 /* first p with q < 1, n2 if none */
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) / 2;
+        const double q = m * (alpha_i + beta[c->sig[mid]]);
+        if (q < 1.0) hi = mid; else lo = mid + 1;
+    }
+    const double base = lo > 0 ? c->bp[lo - 1] : 0.0;
+    *s_out = lo;
+    *T_out = (double)(c->n2 - lo) * alpha_i + (c->btot - base);
+}
+
+/* column of draw d of row i (given s_i, T_i) */
+static int64_t mn_draw(const mn_ctx *c, uint64_t seed, int64_t i, int64_t d, double alpha_i, int64_t s,
+                       double T)
+{
+    const double target = u53(seed, (uint32_t)i, (uint32_t)d, 9u) * T;
+    const double base = s > 0 ? c->bp[s - 1] : 0.0;
+    int64_t lo = s, hi = c->n2 - 1;             /* first p >= s with C(p) > target, else n2-1 */
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) / 2;
+        const double cdf = (double)(mid - s + 1) * alpha_i + (c->bp[mid] - base);
+        if (cdf > target) hi = mid; else lo = mid + 1;
+    }
+    return c->sig[lo];
+}
+
+static int64_t mn_count(uint64_t seed, double m, int64_t i, double T)
+{
+    return (int64_t)floor(m * T + u53(seed, (uint32_t)i, 0u, 8u));
+}
+
+/* Raw multinomial draws of the unsaturated part (with replacement, sorted   */
+/* by (i, j), duplicates kept); sat[i] (optional) receives s_i.              */
+int64_t or_multinomial_draws(uint64_t seed, double m, int64_t n1, int64_t n2, const double *alpha,
+                             const double *beta, int64_t cap, int32_t *I, int32_t *J, int64_t *sat)
+{
+    mn_ctx c;
+    mn_setup(&c, n2, beta);
     int64_t cnt = 0;
     for (int64_t i = 0; i < n1; ++i) {
-        const double T = (double)n2 * alpha[i] + btot;
-        const double mi = m * T;
-        const int64_t Mi = (int64_t)floor(mi + u53(seed, (uint32_t)i, 0u, 8u));
+        int64_t s;
+        double T;
+        mn_row(&c, m, alpha[i], beta, &s, &T);
+        if (sat) sat[i] = s;
+        const int64_t Mi = s < n2 ? mn_count(seed, m, i, T) : 0;
         const int64_t c0 = cnt;
         for (int64_t d = 0; d < Mi; ++d) {
-            const double target = u53(seed, (uint32_t)i, (uint32_t)d, 9u) * T;
-            int64_t lo = 0, hi = n2 - 1;            /* first j with C(j) > target, else n2-1 */
-            while (lo < hi) {
-                const int64_t mid = (lo + hi) / 2;
-                const double c = (double)(mid + 1) * alpha[i] + bpre[mid];
-                if (c > target) hi = mid; else lo = mid + 1;
-            }
-            if (cnt < cap) { I[cnt] = (int32_t)i; J[cnt] = (int32_t)lo; }
+            const int64_t j = mn_draw(&c, seed, i, d, alpha[i], s, T);
+            if (cnt < cap) { I[cnt] = (int32_t)i; J[cnt] = (int32_t)j; }
             ++cnt;
         }
         if (cnt <= cap && cnt > c0) qsort(J + c0, (size_t)(cnt - c0), sizeof(int32_t), cmp_i32);
     }
-    if (cnt <= cap)
-        for (int64_t s = 0; s < cnt; ++s) q[s] = m * (alpha[I[s]] + beta[J[s]]);
-    free(bpre);
+    mn_free(&c);
     return cnt;
+}
+
+/* q̂_ij of a drawn (unsaturated) pair; T_i as above. */
+double or_mn_qhat(double m, double alpha_i, double beta_j, double T_i)
+{
+    const double mi = m * T_i;
+    const double F = floor(mi);
+    const double f = mi - F;
+    const double pi = (alpha_i + beta_j) / T_i;
+    if (!(pi > 0.0)) return 0.0;
+    if (pi >= 1.0) return F >= 1.0 ? 1.0 : f;
+    return -expm1(F * log1p(-pi) + log1p(-f * pi));
+}
+
+/* Ω of the multinomial model; returns |Ω|, writes at most cap entries.     */
+int64_t or_sample_multinomial(uint64_t seed, double m, int64_t n1, int64_t n2, const double *alpha,
+                              const double *beta, int64_t cap, int32_t *I, int32_t *J, double *q)
+{
+    mn_ctx c;
+    mn_setup(&c, n2, beta);
+    int32_t *row = (int32_t *)malloc(sizeof(int32_t) * 64);
+    int64_t rcap = 64;
+    int64_t cnt = 0;
+    for (int64_t i = 0; i < n1; ++i) {
+        int64_t s;
+        double T;
+        mn_row(&c, m, alpha[i], beta, &s, &T);
+        const int64_t Mi = s < n2 ? mn_count(seed, m, i, T) : 0;
+        if (s + Mi > rcap) {
+            rcap = s + Mi;
+            row = (int32_t *)realloc(row, sizeof(int32_t) * (size_t)rcap);
+        }
+        for (int64_t p = 0; p < s; ++p) row[p] = (int32_t)c.sig[p];
+        for (int64_t d = 0; d < Mi; ++d) row[s + d] = (int32_t)mn_draw(&c, seed, i, d, alpha[i], s, T);
+        qsort(row, (size_t)(s + Mi), sizeof(int32_t), cmp_i32);
+        for (int64_t e = 0; e < s + Mi; ++e) {
+            if (e > 0 && row[e] == row[e - 1]) continue;          /* the set Ω */
+            if (cnt < cap) {
+                const int32_t j = row[e];
+                const double qq = m * (alpha[i] + beta[j]);
+                I[cnt] = (int32_t)i;
+                J[cnt] = j;
+                q[cnt] = qq >= 1.0 ? 1.0 : or_mn_qhat(m, alpha[i], beta[j], T);
+            }
+            ++cnt;
+        }
+    }
+    free(row);
+    mn_free(&c);
+    return cnt;
+}
+
+/* s_i and T_i per row (tests) */
+void or_mn_rows(double m, int64_t n1, int64_t n2, const double *alpha, const double *beta, int64_t *s,
+                double *T)
+{
+    mn_ctx c;
+    mn_setup(&c, n2, beta);
+    for (int64_t i = 0; i < n1; ++i) mn_row(&c, m, alpha[i], beta, &s[i], &T[i]);
+    mn_free(&c);
 }
 
 /* Bernoulli draw for pair (i,j): U53 from Philox(ctr=(i,j,0,3), key=seed).  */
@@ -609,20 +746,75 @@ void or_als_half(int r, int64_t n_out, int64_t cnt, const int32_t *side, const i
     free(G); free(h);
 }
 
-/* Full WAltMin with the REUSE_ALL partition (R11):              */
-/*   R = w .* P_Ω(M̃) (Alg. 2 lines 2, 4);                                  */
+/* Alg. 2 line 3: "Divide Ω in 2T+1 equal uniformly random subsets"  */
+/* (R11, the FRESH_2T1 partition).  Sample s = (i, j) gets the key  */
+/* K_s = (w1 << 32) | w0 of Philox(ctr = (i, j, 0, 4), key = seed); samples   */
+/* are ranked by (K_s, i, j, s) and the sample of rank p goes to subset       */
+/* p mod nsub (nsub = 2T+1): subset sizes differ by at most one, and the      */
+/* assignment is a uniformly random equal split (keys i.i.d. uniform).        */
+typedef struct { uint64_t key; int32_t i, j; int64_t s; } part_rec;
+
+static int cmp_part(const void *a, const void *b)
+{
+    const part_rec *x = (const part_rec *)a, *y = (const part_rec *)b;
+    if (x->key != y->key) return x->key < y->key ? -1 : 1;
+    if (x->i != y->i) return x->i < y->i ? -1 : 1;
+    if (x->j != y->j) return x->j < y->j ? -1 : 1;
+    return (x->s > y->s) - (x->s < y->s);
+}
+
+void or_partition(uint64_t seed, int nsub, int64_t cnt, const int32_t *I, const int32_t *J, int32_t *sub)
+{
+    part_rec *r = (part_rec *)malloc(sizeof(part_rec) * (size_t)(cnt > 0 ? cnt : 1));
+    for (int64_t s = 0; s < cnt; ++s) {
+        uint32_t w[4];
+        philox_seed(seed, (uint32_t)I[s], (uint32_t)J[s], 0u, 4u, w);
+        r[s].key = ((uint64_t)w[1] << 32) | (uint64_t)w[0];
+        r[s].i = I[s];
+        r[s].j = J[s];
+        r[s].s = s;
+    }
+    qsort(r, (size_t)cnt, sizeof(part_rec), cmp_part);
+    for (int64_t p = 0; p < cnt; ++p) sub[r[p].s] = (int32_t)(p % nsub);
+    free(r);
+}
+
+/* Samples of phase ph: all of Ω (REUSE_ALL) or subset Ω_ph (FRESH_2T1),   */
+/* compacted in their original (i, j) order.                                 */
+static int64_t phase_samples(int partition, int ph, int64_t cnt, const int32_t *sub, const int32_t *I,
+                             const int32_t *J, const double *val, const double *w, int32_t *pI,
+                             int32_t *pJ, double *pv, double *pw)
+{
+    int64_t c = 0;
+    for (int64_t s = 0; s < cnt; ++s) {
+        if (partition != 0 && sub[s] != ph) continue;
+        pI[c] = I[s]; pJ[c] = J[s]; pv[c] = val[s]; pw[c] = w[s];
+        ++c;
+    }
+    return c;
+}
+
+/* Full WAltMin (Alg. 2).  partition 0 = REUSE_ALL (all of Ω in */
+/* every phase, as the deployed ALS; R11), 1 = FRESH_2T1    */
+/* (line 3: Ω_0 for the init, Ω_{2t+1} / Ω_{2t+2} for iteration t):          */
+/*   w = 1/q̂ (line 2); R = w .* P_Ω0(M̃) (line 4);                          */
 /*   U0 = top-r left singular subspace of R by subspace iteration from a     */
 /*        Rademacher start (line 5; R12), init_iters iterations;    */
 /*   trim rows of U0 with norm > trim_c sqrt(r) ||A_i||/||A||_F (line 6,     */
 /*        P:237; R13), re-orthonormalise;                          */
-/*   T x { V = argmin (line 8); U = argmin (line 9) }; output (U, V).       */
+/*   T x { V = argmin on Ω_{2t+1} (line 8); U = argmin on Ω_{2t+2} (l. 9) }. */
 void or_waltmin(int64_t n1, int64_t n2, int r, int T, int init_iters, double trim_c,
-                double lam, uint64_t seed, int64_t cnt, const int32_t *I, const int32_t *J,
-                const double *val, const double *qhat, const double *a_norm, double frobA,
-                double *U, double *V)
+                double lam, uint64_t seed, int partition, int64_t cnt, const int32_t *I,
+                const int32_t *J, const double *val, const double *qhat, const double *a_norm,
+                double frobA, double *U, double *V)
 {
-    double *w = (double *)malloc(sizeof(double) * (size_t)(cnt > 0 ? cnt : 1));
+    const size_t c1 = (size_t)(cnt > 0 ? cnt : 1);
+    double *w = (double *)malloc(sizeof(double) * c1);
     for (int64_t s = 0; s < cnt; ++s) w[s] = qhat[s] > 0.0 ? 1.0 / qhat[s] : 0.0;
+    int32_t *sub = (int32_t *)calloc(c1, sizeof(int32_t));
+    if (partition != 0) or_partition(seed, 2 * T + 1, cnt, I, J, sub);
+    int32_t *pI = (int32_t *)malloc(sizeof(int32_t) * c1), *pJ = (int32_t *)malloc(sizeof(int32_t) * c1);
+    double *pv = (double *)malloc(sizeof(double) * c1), *pw = (double *)malloc(sizeof(double) * c1);
     double *Y = (double *)calloc((size_t)n2 * r, sizeof(double));
     double *Z = (double *)calloc((size_t)n1 * r, sizeof(double));
     /* Y0[j][l] = ±1 from Philox(ctr=(j,l,0,5), key=seed), bit 0 of word 0 */
@@ -632,14 +824,15 @@ void or_waltmin(int64_t n1, int64_t n2, int r, int T, int init_iters, double tri
             philox_seed(seed, (uint32_t)j, (uint32_t)l, 0u, 5u, o);
             Y[j * r + l] = (o[0] & 1u) ? -1.0 : 1.0;
         }
+    int64_t pc = phase_samples(partition, 0, cnt, sub, I, J, val, w, pI, pJ, pv, pw);
     for (int it = 0; it < init_iters; ++it) {
         for (int64_t i = 0; i < n1 * r; ++i) Z[i] = 0.0;
-        for (int64_t s = 0; s < cnt; ++s)
-            for (int l = 0; l < r; ++l) Z[(int64_t)I[s] * r + l] += w[s] * val[s] * Y[(int64_t)J[s] * r + l];
+        for (int64_t s = 0; s < pc; ++s)
+            for (int l = 0; l < r; ++l) Z[(int64_t)pI[s] * r + l] += pw[s] * pv[s] * Y[(int64_t)pJ[s] * r + l];
         householder_q(n1, r, Z);
         for (int64_t j = 0; j < n2 * r; ++j) Y[j] = 0.0;
-        for (int64_t s = 0; s < cnt; ++s)
-            for (int l = 0; l < r; ++l) Y[(int64_t)J[s] * r + l] += w[s] * val[s] * Z[(int64_t)I[s] * r + l];
+        for (int64_t s = 0; s < pc; ++s)
+            for (int l = 0; l < r; ++l) Y[(int64_t)pJ[s] * r + l] += pw[s] * pv[s] * Z[(int64_t)pI[s] * r + l];
         householder_q(n2, r, Y);
     }
     /* trim */
@@ -655,11 +848,15 @@ void or_waltmin(int64_t n1, int64_t n2, int r, int T, int init_iters, double tri
         householder_q(n1, r, Z);
     }
     memcpy(U, Z, sizeof(double) * (size_t)n1 * r);
+    if (T == 0)
+        for (int64_t j = 0; j < n2 * r; ++j) V[j] = 0.0;
     for (int t = 0; t < T; ++t) {
-        or_als_half(r, n2, cnt, J, I, val, w, U, lam, V);
-        or_als_half(r, n1, cnt, I, J, val, w, V, lam, U);
+        pc = phase_samples(partition, 2 * t + 1, cnt, sub, I, J, val, w, pI, pJ, pv, pw);
+        or_als_half(r, n2, pc, pJ, pI, pv, pw, U, lam, V);
+        pc = phase_samples(partition, 2 * t + 2, cnt, sub, I, J, val, w, pI, pJ, pv, pw);
+        or_als_half(r, n1, pc, pI, pJ, pv, pw, V, lam, U);
     }
-    free(w); free(Y); free(Z);
+    free(w); free(sub); free(pI); free(pJ); free(pv); free(pw); free(Y); free(Z);
 }
 
 /* Threads the oracle's OpenMP loops use (reported as the CPU baseline's cores). */

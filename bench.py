@@ -218,6 +218,26 @@ def oracle_sample_rate(cfgname, cfg, target_s):
     return nbytes / secs / 1e9, info
 
 
+def config_dict(cfgname, cfg, args, world, extra=None):
+    """The workload description both arms print (identical keys and values)."""
+    d, n1, n2, k = cfg["d"], cfg["n1"], cfg["n2"], cfg["k"]
+    a_is_b = cfg.get("a_is_b", False)
+    csr = cfg["dtype"] == "csr"
+    es = {"bf16": 2, "f32": 4}.get(cfg["dtype"], 0)
+    out = {"workload": cfgname, "d": d, "n1": n1, "n2": n2, "k": k, "pi": cfg["pi"], "r": cfg["r"],
+           "T": cfg["T"], "m": synth.m_of(cfg), "sampler": args.sampler, "partition": args.partition,
+           "init_iters": args.init_iters, "a_is_b": a_is_b,
+           "parallelism": f"row-shard x{world} + one NCCL all-reduce" if world > 1 else "1 GPU",
+           "l2": ("CSR inputs (11.6 GB)" if csr else "inputs (%.1f GB)" % (d * (n1 + (0 if a_is_b else n2)) * es / 1e9))
+           + " larger than the 126 MB L2; no flush",
+           "value_scope": "A+B bytes / (sketch_block .. finalize) time; ms_per_step = whole Alg. 1"}
+    if csr:
+        out["input"] = "CSR int64 rowptr / int32 col / fp32 val"
+    if extra:
+        out.update(extra)
+    return out
+
+
 def run_reference(args, cfgname, cfg, world, rank):
     if rank != 0:
         return
@@ -235,10 +255,9 @@ def run_reference(args, cfgname, cfg, world, rank):
         "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * statistics.mean(per_step), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": cfgname, "d": cfg["d"], "n1": cfg["n1"], "n2": cfg["n2"],
-                   "k": cfg["k"], "sample_rows_per_step": info["rows"]},
+        "config": config_dict(cfgname, cfg, args, world),
         "cpu_baseline": {"value": value, "unit": "GB/s", "cores": info["cores"], "kind": "oracle",
-                         "sample": info["sample"]},
+                         "sample": info["sample"] + f"; {info['rows']} rows per step"},
         "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(out), flush=True)
@@ -250,7 +269,8 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="cfg1")
+    ap.add_argument("--config", default="cfg2",
+                    help="workload (default cfg2: the largest single-GPU config of BASELINE.json)")
     ap.add_argument("--impl", default="smp", choices=["smp", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -260,10 +280,24 @@ def main():
                     help="Ω sampler: Alg. 1's Bernoulli sweep or the appendix's row-multinomial (NEXT-2)")
     ap.add_argument("--pi", default=None, choices=["rademacher", "gaussian", "srht"],
                     help="override the config's Π (e.g. srht, the paper's Spark sketch; NEXT-1)")
+    ap.add_argument("--partition", default="reuse_all", choices=["reuse_all", "fresh_2t1"],
+                    help="Alg. 2 line 3 reading (DESIGN.md R11)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 0)
 
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: re-launch under torch.distributed.run
+        import socket
+        so = socket.socket()
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+        so.close()
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+        sys.exit(subprocess.call(cmd))
     world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus and "WORLD_SIZE" in os.environ:
+        raise SystemExit(f"bench.py: WORLD_SIZE={world} but --gpus {args.gpus}")
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     cfgname = args.config
@@ -309,11 +343,11 @@ def main():
     sk = SMPSketch(d, n1, n2, k, pi=pi_code(cfg), seed=cfg["seed"], a_is_b=a_is_b, input=inp,
                    row_begin=r0, row_end=r1, stream=stream, device=dev)
 
+    from paper_1610_06656_b200 import dist as smp_dist
+
     def combine():
-        if world > 1:
-            a, b = sk.partials()
-            dist.all_reduce(a)
-            dist.all_reduce(b)
+        if world > 1:   # ONE coalesced all-reduce of the packed partials
+            smp_dist.combine(sk)
 
     def step(evs, host=None):
         sk.reset()
@@ -333,7 +367,8 @@ def main():
         sk.finalize()
         evs[1].record(stream)
         I, J, val, qh = sk.sample_estimate(m, cfg["seed"], sampler=args.sampler)
-        U, V = sk.waltmin(I, J, val, qh, r, T, init_iters=args.init_iters, seed=cfg["seed"])
+        U, V = sk.waltmin(I, J, val, qh, r, T, init_iters=args.init_iters, seed=cfg["seed"],
+                          partition=args.partition)
         if host is not None:
             Uh, Vh = U.cpu(), V.cpu()  # D2H of the result
         evs[2].record(stream)
@@ -398,26 +433,29 @@ def main():
                 "algorithmic_per_step": {"flops": flops_step, "nnz": nnz}}
         roofline_time = max(total_bytes / (pk["hbm"] * 1e9), 2.0 * k * total_nnz / (pk["tc"] * 1e12))
     else:
-        # roofline of K1 (per launch = one matrix over this rank's rows)
+        # roofline of K1 (per launch = one matrix over this rank's rows),
+        # from the ALGORITHMIC work of the method: 2k FLOP and
+        # one read of the input element (2 B bf16, 4 B fp32) per element.  The
+        # bf16 planes K1F executes for fp32 inputs (R21) are reported beside
+        # it as "executed", not counted as useful work.
         rows = r1 - r0
-        # bf16 planes per input element (R21): fp32 -> 3; bf16 with a
-        # Gaussian Π -> 2
-        gauss = cfg["pi"] == "gaussian"
-        planes = 3 if inp == IN_DENSE_F32 else (2 if gauss else 1)
+        es_in = A.element_size()
+        planes = 3 if inp == IN_DENSE_F32 else (2 if cfg["pi"] == "gaussian" else 1)
         launches_per_step = max(k1_n // max(args.steps, 1), 1)
         ncols_total = (n1 + (0 if a_is_b else n2))
-        flops_launch = 2.0 * k * rows * ncols_total * planes / launches_per_step
-        bytes_launch = rows * ncols_total * 2 * planes / launches_per_step
+        flops_launch = 2.0 * k * rows * ncols_total / launches_per_step
+        bytes_launch = rows * ncols_total * es_in / launches_per_step
         t_hbm = bytes_launch / (pk["hbm"] * 1e9)
         t_tc = flops_launch / (pk["tc"] * 1e12)
         traffic = None
         tfile = os.path.join(ROOT, "profiles", "k1_traffic.json")
         if os.path.exists(tfile):
             traffic = json.load(open(tfile)).get(cfgname)
+        kname = "sketch_tc_f32_kernel (K1F)" if inp == IN_DENSE_F32 else "sketch_tc_kernel (K1)"
         if t_tc >= t_hbm:
             ach = flops_launch / (k1_avg * 1e-3) / 1e12
             roof = {"bound": "tensor", "achieved": ach, "peak": pk["tc"], "unit": "TFLOP/s",
-                    "frac": ach / pk["tc"], "traffic": traffic, "kernel": "sketch_tc_kernel",
+                    "frac": ach / pk["tc"], "traffic": traffic, "kernel": kname,
                     "peak_source": pk["src"] + " burst bf16 dense (MEASURED_PEAKS.json)"}
             alt_ach = bytes_launch / (k1_avg * 1e-3) / 1e9
             roof["hbm_view"] = {"achieved": alt_ach, "peak": pk["hbm"], "unit": "GB/s",
@@ -425,15 +463,21 @@ def main():
         else:
             ach = bytes_launch / (k1_avg * 1e-3) / 1e9
             roof = {"bound": "hbm", "achieved": ach, "peak": pk["hbm"], "unit": "GB/s",
-                    "frac": ach / pk["hbm"], "traffic": traffic, "kernel": "sketch_tc_kernel",
+                    "frac": ach / pk["hbm"], "traffic": traffic, "kernel": kname,
                     "peak_source": pk["src"] + " HBM copy bandwidth (MEASURED_PEAKS.json)"}
             alt = flops_launch / (k1_avg * 1e-3) / 1e12
             roof["tensor_view"] = {"achieved": alt, "peak": pk["tc"], "unit": "TFLOP/s",
                                    "frac": alt / pk["tc"]}
+        roof["sustained_view"] = {"peak": pk["tc_sust"], "unit": "TFLOP/s",
+                                  "frac": flops_launch / (k1_avg * 1e-3) / 1e12 / pk["tc_sust"]}
+        if planes > 1:
+            exe = flops_launch * planes / (k1_avg * 1e-3) / 1e12
+            roof["executed"] = {"planes": planes, "achieved": exe, "unit": "TFLOP/s", "frac": exe / pk["tc"],
+                                "note": "bf16 plane-split tensor work actually issued (R21); not useful work"}
         roof["k1_ms_per_launch"] = k1_avg
         roof["algorithmic_per_launch"] = {"flops": flops_launch, "bytes": bytes_launch}
         roofline_time = max(total_bytes / (pk["hbm"] * 1e9),
-                            2.0 * k * d * ncols_total * planes / (pk["tc"] * 1e12))
+                            2.0 * k * d * ncols_total / (pk["tc"] * 1e12))
 
     # e2e through the C ABI with pinned host buffers
     e2e = None
@@ -482,13 +526,9 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_step,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": dtype_name(cfg), "data": "synthetic",
-            "config": {"workload": cfgname, "d": d, "n1": n1, "n2": n2, "k": k,
-                       "pi": cfg["pi"], "r": r, "T": T, "m": m, "omega": nomega, "sampler": args.sampler,
-                       "init_iters": args.init_iters, "a_is_b": a_is_b,
-                       "parallelism": f"row-shard x{world} + NCCL all-reduce" if world > 1 else "1 GPU",
-                       "l2": "inputs (%.1f GB) larger than the 126 MB L2; no flush" % (total_bytes / 1e9),
-                       **({"nnz": int(total_nnz), "input": "CSR int64 rowptr / int32 col / fp32 val"} if csr else {}),
-                       "value_scope": "A+B bytes / (sketch_block .. finalize) time; ms_per_step = whole Alg. 1"},
+            "config": config_dict(cfgname, cfg, args, world),
+            "omega": nomega,
+            **({"nnz": int(total_nnz)} if csr else {}),
             "smp_pca_sec": t_step * 1e-3,
             "sketch_ms": t_sketch,
             "roofline_pct_of_stage": 100.0 * roofline_time / (t_sketch * 1e-3),

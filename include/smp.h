@@ -150,10 +150,14 @@ SMP_API smp_status smp_finalize_norms(smp_handle* h, float* A_sk, float* B_sk, d
  * nothing written; call again with cap >= *count). */
 /* Ω samplers: the Bernoulli hash sweep of Alg. 1 line 3 (n1·n2 draws,
  * bit-exact, q̂ = min(1, q)) or the appendix's row-multinomial sampler
- * (R27; O(n1 + m log n2): M_i = floor(m_i + u) draws of
- * row i with replacement, column by CDF inversion of q̃_ij ∝ α_i + β_j;
- * duplicates kept; qhat = q = m(α_i + β_j) unclipped, each draw weighted
- * 1/q by smp_waltmin). */
+ * (P:633-639 with line 3's saturation; R27; O(n2 log n2 + m log n2)):
+ * pairs with q_ij >= 1 are always in Ω (q̂ = 1); the unsaturated mass of row
+ * i, T_i, is drawn M_i = floor(m T_i + u) times with replacement by CDF
+ * inversion of q̃_ij ∝ α_i + β_j over the unsaturated columns; Ω holds each
+ * drawn pair once, with qhat = its inclusion probability
+ * 1 − (1 − π)^F (1 − fπ), π = (α_i + β_j)/T_i, F = ⌊m T_i⌋, f = m T_i − F.
+ * Synchronises twice.  Errors as smp_sample_estimate, plus SMP_EINVAL when
+ * the draws exceed 2^31 entries. */
 enum { SMP_SAMPLER_BERNOULLI = 0, SMP_SAMPLER_MULTINOMIAL = 1 };
 SMP_API smp_status smp_sample_estimate_ex(smp_handle* h, double m, uint64_t seed, int32_t est,
                                           int32_t sampler, int64_t cap, int32_t* I, int32_t* J,
@@ -162,7 +166,13 @@ SMP_API smp_status smp_sample_estimate_ex(smp_handle* h, double m, uint64_t seed
 SMP_API smp_status smp_sample_estimate(smp_handle* h, double m, uint64_t seed, int32_t est, int64_t cap,
                                int32_t* I, int32_t* J, float* val, double* qhat, int64_t* count);
 
-typedef enum { SMP_PART_REUSE_ALL = 0 } smp_part;
+/* Alg. 2 line 3, R11.  REUSE_ALL: all of Ω for the init
+ * and every half step (the deployed ALS).  FRESH_2T1: Ω divided into
+ * 2T+1 equal random subsets — sample (i, j) keyed by Philox(ctr = (i, j, 0,
+ * 4), key = waltmin seed), ranked by (key, position), rank p -> subset
+ * p mod (2T+1) — Ω_0 for lines 4-5, Ω_{2t+1} for line 8 and Ω_{2t+2} for
+ * line 9 of iteration t. */
+typedef enum { SMP_PART_REUSE_ALL = 0, SMP_PART_FRESH_2T1 = 1 } smp_part;
 
 typedef struct {
   int32_t r;          /* rank, 1 <= r <= 16, r <= min(n1, n2)                 */
@@ -175,12 +185,32 @@ typedef struct {
 } smp_waltmin_desc;
 
 /* Step 3: WAltMin (Alg. 2) on (I, J, val, qhat) as
- * produced by smp_sample_estimate (sorted by (i,j)); uses the handle's
- * ||A_i|| and ||A||_F for the trim.  Outputs U (n1×r) and V (n2×r) fp32
- * row-major with ÛV̂ᵀ ≈ (AᵀB)_r.  Synchronises.  Errors: SMP_EINVAL. */
+ * produced by smp_sample_estimate (sorted by (i,j), distinct pairs); uses
+ * the handle's ||A_i|| and ||A||_F for the trim.  Outputs U (n1×r) and V
+ * (n2×r) fp32 row-major with ÛV̂ᵀ ≈ (AᵀB)_r.  Synchronises.  Errors:
+ * SMP_EINVAL (r outside [1, min(16, n1, n2)], T < 1, init_iters < 1, unknown
+ * partition, FRESH_2T1 with count < 2T+1, null arrays), SMP_ECUDA. */
 SMP_API smp_status smp_waltmin(smp_handle* h, const int32_t* I, const int32_t* J, const float* val,
                        const double* qhat, int64_t count, const smp_waltmin_desc* w, float* U,
                        float* V);
+
+/* LELA (Bhojanapalli et al.; the paper's two-pass comparison system, P:78,
+ * P:145, Table 1, runtime P:191-192; DESIGN.md NEXT-3).  Pass 1:
+ * smp_norms_block accumulates ONLY the exact column norms² (fp64) of rows
+ * [row0, row0+rows) into the handle (no sketch; blocks in any order), after
+ * which smp_finalize_norms and smp_sample_estimate give Ω and q̂ by Eq. 1
+ * exactly as for SMP-PCA (its M̃ values are then 0 and unused).  Pass 2:
+ * smp_exact_entries_block adds Σ_{t in block} A[t, I_s]·B[t, J_s] (fp64) to
+ * acc[s] for the count samples (I, J device int32, acc device fp64, zeroed by
+ * the caller before the first block); after every row block, acc = (AᵀB)_Ω,
+ * the exact entries smp_waltmin then completes (as fp32 val).  Dense inputs
+ * only (bf16 or fp32, any leading dimension >= n).  Errors: SMP_EINVAL (rows
+ * outside [row_begin, row_end), CSR handle, null arrays, ld < n), SMP_ECUDA. */
+SMP_API smp_status smp_norms_block(smp_handle* h, int64_t row0, int64_t rows, const void* A, int64_t lda,
+                                   const void* B, int64_t ldb);
+SMP_API smp_status smp_exact_entries_block(smp_handle* h, int64_t row0, int64_t rows, const void* A,
+                                           int64_t lda, const void* B, int64_t ldb, const int32_t* I,
+                                           const int32_t* J, int64_t count, double* acc);
 
 /* Reset the accumulators to zero (reuse the handle for another pass). */
 SMP_API smp_status smp_sketch_reset(smp_handle* h);

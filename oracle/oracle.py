@@ -82,6 +82,8 @@ def _get():
         lib.or_multinomial_draws.restype = i64
         lib.or_mn_qhat.argtypes = [f64, f64, f64, f64]
         lib.or_mn_qhat.restype = f64
+        lib.or_exact_entries.argtypes = [i64, P, ctypes.c_int, i64, P, ctypes.c_int, i64, i64, P, P, P]
+        lib.or_exact_entries.restype = None
         lib.or_partition.argtypes = [u64, ctypes.c_int, i64, P, P, P]
         lib.or_partition.restype = None
         _lib = lib
@@ -378,6 +380,39 @@ def smp_pca(A, B, k, r, m, T, pi_kind=PI_RADEMACHER, seed=0, omega_seed=None,
                    init_iters=init_iters, trim_c=trim_c, lam=lam, seed=wm_seed, partition=partition)
     return dict(Ask=Ask, Bsk=Bsk, a2=a2, b2=b2, FA=FA, FB=FB, As=As, Bs=Bs, DA=DA, DB=DB,
                 alpha=al, beta=be, I=I, J=J, qhat=q, Mt=Mt, U=U, V=V)
+
+
+# --------------------------------------------------------------------------
+# LELA: the two-pass comparison system (NEXT-3)
+# --------------------------------------------------------------------------
+def exact_entries(A, B, I, J, out=None):
+    """Pass 2 of LELA: out[s] += Σ_t A[t, I_s] B[t, J_s] over the rows of the
+    block (fp64), i.e. (AᵀB)_{I_s J_s} once every row block has been seen."""
+    A = np.ascontiguousarray(A)
+    B = np.ascontiguousarray(B)
+    I = _c(I, np.int32)
+    J = _c(J, np.int32)
+    if out is None:
+        out = np.zeros(len(I), np.float64)
+    _get().or_exact_entries(A.shape[0], _p(A), _dtype_code(A), A.shape[1], _p(B), _dtype_code(B),
+                            B.shape[1], len(I), _p(I), _p(J), _p(out))
+    return out
+
+
+def lela(A, B, r, m, T, seed=0, wm_seed=None, init_iters=50, trim_c=8.0, lam=1e-10,
+         partition=PART_REUSE_ALL):
+    """LELA end to end: pass 1 exact column norms, Ω by Eq. 1 (same sampler
+    and hash as SMP-PCA), pass 2 exact entries on Ω, WAltMin."""
+    wm_seed = seed if wm_seed is None else wm_seed
+    a2 = colnorms(A)
+    b2 = colnorms(B)
+    FA, FB = pairwise_sum(a2), pairwise_sum(b2)
+    al, be = alpha_beta(a2, b2, FA, FB)
+    I, J, q = sample(seed, m, al, be)
+    M = exact_entries(A, B, I, J)
+    U, V = waltmin(len(a2), len(b2), r, T, I, J, M, q, np.sqrt(a2), np.sqrt(FA), init_iters=init_iters,
+                   trim_c=trim_c, lam=lam, seed=wm_seed, partition=partition)
+    return dict(a2=a2, b2=b2, FA=FA, FB=FB, I=I, J=J, qhat=q, M=M, U=U, V=V)
 
 
 def num_threads() -> int:

@@ -859,6 +859,26 @@ void or_waltmin(int64_t n1, int64_t n2, int r, int T, int init_iters, double tri
     free(w); free(sub); free(pI); free(pJ); free(pv); free(pw); free(Y); free(Z);
 }
 
+/* ------------------------------------------------------------------------ */
+/* LELA (Bhojanapalli et al.; the paper's two-pass comparison system,  */
+/* P:145, Table 1): pass 1 = the column  */
+/* norms (or_colnorms), Ω from the same Eq. 1 (or_sample); pass 2 computes   */
+/* the EXACT entries of AᵀB on Ω ("needs a second pass to compute the  */
+/* sampled entries"):  out[s] += Σ_t A[t, I_s] · B[t, J_s]  (fp64), over the  */
+/* rows of the block; then WAltMin on (Ω, exact entries, q̂) (or_waltmin).   */
+/* ------------------------------------------------------------------------ */
+void or_exact_entries(int64_t rows, const void *A, int adtype, int64_t lda, const void *B, int bdtype,
+                      int64_t ldb, int64_t cnt, const int32_t *I, const int32_t *J, double *out)
+{
+    #pragma omp parallel for schedule(static)
+    for (int64_t s = 0; s < cnt; ++s) {
+        double acc = out[s];
+        for (int64_t t = 0; t < rows; ++t)
+            acc += load_elem(A, adtype, t * lda + I[s]) * load_elem(B, bdtype, t * ldb + J[s]);
+        out[s] = acc;
+    }
+}
+
 /* Threads the oracle's OpenMP loops use (reported as the CPU baseline's cores). */
 #ifdef _OPENMP
 #include <omp.h>

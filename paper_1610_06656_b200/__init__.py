@@ -5,4 +5,4 @@ The one-pass sketch ΠA, ΠB with fused exact column norms, the biased sample
 libsmp.so (include/smp.h).  See DESIGN.md.
 """
 from .smp import (IN_CSR_F32, IN_DENSE_BF16, IN_DENSE_F32, PI_GAUSSIAN, PI_HADAMARD_TEST, PI_SRHT,  # noqa: F401
-                  PI_RADEMACHER, SMPSketch, SmpError, smp_pca)
+                  PI_RADEMACHER, SMPSketch, SmpError, lela, smp_pca)

@@ -16,14 +16,15 @@ SMP_OK, SMP_EIO, SMP_EINVAL, SMP_ENUMERIC, SMP_ECUDA, SMP_ECAPACITY, SMP_ENOMEM 
 PI_RADEMACHER, PI_GAUSSIAN, PI_HADAMARD_TEST, PI_SRHT = 0, 1, 2, 3
 IN_DENSE_BF16, IN_DENSE_F32, IN_CSR_F32 = 0, 1, 2
 EST_RESCALED, EST_PLAIN = 0, 1
-PART_REUSE_ALL = 0
+PART_REUSE_ALL, PART_FRESH_2T1 = 0, 1
 SAMPLER_BERNOULLI, SAMPLER_MULTINOMIAL = 0, 1
 
 EXPORTS = [
     "smp_sketch_init", "smp_sketch_block", "smp_sketch_block_host", "smp_sketch_block_csr",
     "smp_sketch_partials", "smp_finalize_norms", "smp_sample_estimate", "smp_waltmin",
     "smp_sketch_reset", "smp_kernel_launches", "smp_destroy", "smp_last_error", "smp_status_str",
-    "smp_set_timing", "smp_kernel_timing", "smp_sample_estimate_ex",
+    "smp_set_timing", "smp_kernel_timing", "smp_sample_estimate_ex", "smp_norms_block",
+    "smp_exact_entries_block",
 ]
 
 
@@ -78,6 +79,8 @@ def load(path: str = None):
     lib.smp_sample_estimate.argtypes = [H, f64, u64, i32, i64, P, P, P, P, ctypes.POINTER(i64)]
     lib.smp_sample_estimate_ex.argtypes = [H, f64, u64, i32, i32, i64, P, P, P, P, ctypes.POINTER(i64)]
     lib.smp_waltmin.argtypes = [H, P, P, P, P, i64, ctypes.POINTER(WaltminDesc), P, P]
+    lib.smp_norms_block.argtypes = [H, i64, i64, P, i64, P, i64]
+    lib.smp_exact_entries_block.argtypes = [H, i64, i64, P, i64, P, i64, P, P, i64, P]
     lib.smp_sketch_reset.argtypes = [H]
     lib.smp_set_timing.argtypes = [H, i32]
     lib.smp_kernel_timing.argtypes = [H, ctypes.POINTER(f64), ctypes.POINTER(i64)]

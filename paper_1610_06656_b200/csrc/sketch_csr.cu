@@ -457,12 +457,10 @@ cudaError_t csr_select_head(CsrWorkspace& w, const int64_t* a_rowptr, const int3
   CSR_TRY(grow(w.head_lut, w.head_lut_cap, ntot));
   CSR_TRY(grow(w.head_map, w.head_map_cap, ntot));
   CSR_TRY(cudaMemsetAsync(w.head_cnt, 0, ntot * 4, st));
-  static bool attr = false;
-  if (!attr) {
+  static PerDeviceOnce attr;
+  if (attr.need())
     CSR_TRY(cudaFuncSetAttribute(csr_colcount_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  CSR_HIST_MAX_COLS * 4));
-    attr = true;
-  }
   csr_colcount_kernel<<<148, CSR_T_THREADS, ntot * 4, st>>>(a_rowptr, a_col, a_n, b_rowptr, b_col, b_n,
                                                            (int)rows, (int)ntot, w.head_cnt);
   const uint32_t thr = (uint32_t)std::max(1.0, std::ceil(density * (double)rows));
@@ -627,13 +625,12 @@ cudaError_t launch_sketch_csr(CsrWorkspace& w, int kind, uint64_t seed, int k, i
     CSR_TRY(grow(w.offs, w.offs_cap, nh));
     CSR_TRY(grow(w.ne_dev, w.ne_cap, 1));
     CSR_TRY(cub::DeviceScan::ExclusiveSum(nullptr, need, w.hist, w.offs, (int)nh, st));
-    static bool attr = false;
-    if (!attr) {
+    static PerDeviceOnce attr;
+    if (attr.need()) {
       CSR_TRY(cudaFuncSetAttribute(csr_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    CSR_HIST_MAX_COLS * 4));
       CSR_TRY(cudaFuncSetAttribute(csr_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    CSR_HIST_MAX_COLS * 4));
-      attr = true;
     }
   } else {
     CSR_TRY(cub::DeviceRadixSort::SortPairs(nullptr, need, w.keys_in, w.keys_out, w.vals_in, w.vals_out,

@@ -517,15 +517,14 @@ cudaError_t launch_sketch_tc(const void* X, int64_t ldx, SketchTCParams p, cudaS
   } else {
     tmap_pi = tmap;
   }
-  static bool attr_set[2] = {false, false};
+  static PerDeviceOnce attr_set[2];
   const int smem = panel ? P_SMEM : TC_SMEM;
-  if (!attr_set[panel]) {
+  if (attr_set[panel].need()) {
     cudaError_t e = panel ? cudaFuncSetAttribute(sketch_tc_kernel<true>,
                                                  cudaFuncAttributeMaxDynamicSharedMemorySize, P_SMEM)
                           : cudaFuncSetAttribute(sketch_tc_kernel<false>,
                                                  cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM);
     if (e != cudaSuccess) return e;
-    attr_set[panel] = true;
   }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(2u * (unsigned)(p.n_tiles * p.k_tiles * p.splits));

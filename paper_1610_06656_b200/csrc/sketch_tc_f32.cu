@@ -324,12 +324,11 @@ cudaError_t launch_sketch_tc_f32(const float* X, int64_t ldx, SketchTCParams p, 
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return cudaErrorInvalidValue;
   }
-  static bool attr = false;
-  if (!attr) {
+  static PerDeviceOnce attr;
+  if (attr.need()) {
     cudaError_t e = cudaFuncSetAttribute(sketch_tc_f32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          f32k::SMEM);
     if (e != cudaSuccess) return e;
-    attr = true;
   }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(2u * (unsigned)(p.n_tiles * p.k_tiles * p.splits));

@@ -11,6 +11,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/smp.h"
 #include "smp_device.cuh"
 #include "smp_kernels.h"
@@ -49,15 +51,16 @@ struct smp_handle {
   cudaEvent_t ev_prep[2] = {nullptr, nullptr}, ev_free[2] = {nullptr, nullptr}, ev_sync = nullptr;
   cudaStream_t aux_st = nullptr;
   // row-multinomial sampler scratch
-  double* mn_bpre = nullptr;
-  int64_t mn_bpre_cap = 0;
-  int32_t* mn_jtmp = nullptr;
-  int64_t mn_jtmp_cap = 0;
-  uint8_t* mn_tmp = nullptr;
-  int64_t mn_tmp_cap = 0;
+  smp::MnWorkspace mn;
   uint16_t* pi_panel = nullptr;  // K1 Gaussian Π panel (κ-major)
   int64_t pi_panel_cap = 0;
   int64_t panel_row0 = -1, panel_ld = 0, panel_kpad = 0;  // rows the panel holds
+  // LELA pass 2 transposed chunks
+  float* lela_at = nullptr;
+  float* lela_bt = nullptr;
+  int64_t lela_at_cap = 0, lela_bt_cap = 0;
+  double* lela_pn = nullptr;
+  int64_t lela_pn_cap = 0;
   // finalized state
   float* fin_sk = nullptr;     // [ntot][k]
   double* fin_sknorm = nullptr;
@@ -91,6 +94,12 @@ struct smp_handle {
 };
 
 namespace {
+
+// NVTX range over one ABI call (visible in nsys / ncu --nvtx timelines)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 smp_status fail(smp_handle* h, smp_status s, const char* fmt, ...) {
   if (h) {
@@ -428,6 +437,7 @@ const char* smp_last_error(const smp_handle* h) { return h ? h->err.c_str() : "n
 int64_t smp_kernel_launches(const smp_handle* h) { return h ? h->launches : 0; }
 
 smp_status smp_sketch_init(smp_handle** out, const smp_sketch_desc* d, void* stream) {
+  NvtxRange nvtx_("smp_sketch_init");
   if (!out || !d) return SMP_EINVAL;
   *out = nullptr;
   if (d->k < 1 || d->k > 4096 || d->n1 < 1 || (!d->a_is_b && d->n2 < 1) || d->d_total < 1 ||
@@ -478,6 +488,7 @@ smp_status smp_sketch_init(smp_handle** out, const smp_sketch_desc* d, void* str
 }
 
 smp_status smp_sketch_reset(smp_handle* h) {
+  NvtxRange nvtx_("smp_sketch_reset");
   if (!h) return SMP_EINVAL;
   CK(h, cudaMemsetAsync(h->acc_sk, 0, h->ntot * (int64_t)h->k * 4, h->st), "memset");
   CK(h, cudaMemsetAsync(h->acc_nrm, 0, h->ntot * 8, h->st), "memset");
@@ -490,7 +501,8 @@ void smp_destroy(smp_handle* h) {
   if (!h) return;
   if (h->st) cudaStreamSynchronize(h->st);
   cudaFree(h->acc_sk); cudaFree(h->acc_nrm); cudaFree(h->part); cudaFree(h->pnorm);
-  cudaFree(h->mn_bpre); cudaFree(h->mn_jtmp); cudaFree(h->mn_tmp);
+  smp::mn_workspace_free(h->mn);
+  cudaFree(h->lela_at); cudaFree(h->lela_bt); cudaFree(h->lela_pn);
   cudaFree(h->planes); cudaFree(h->pi_panel); cudaFree(h->fin_sk); cudaFree(h->fin_sknorm); cudaFree(h->fin_D);
   cudaFree(h->FAFB); cudaFree(h->status); cudaFree(h->pw_scratch); cudaFree(h->alpha);
   cudaFree(h->blk); cudaFree(h->d_total);
@@ -517,6 +529,7 @@ void smp_destroy(smp_handle* h) {
 
 smp_status smp_sketch_block(smp_handle* h, int64_t row0, int64_t rows, const void* A, int64_t lda,
                             const void* B, int64_t ldb) {
+  NvtxRange nvtx_("smp_sketch_block");
   if (!h) return SMP_EINVAL;
   smp_status s = check_rows(h, row0, rows);
   if (s != SMP_OK) return s;
@@ -565,6 +578,7 @@ smp_status smp_sketch_block(smp_handle* h, int64_t row0, int64_t rows, const voi
 
 smp_status smp_sketch_block_host(smp_handle* h, int64_t row0, int64_t rows, const void* A,
                                  int64_t lda, const void* B, int64_t ldb, int64_t chunk_rows) {
+  NvtxRange nvtx_("smp_sketch_block_host");
   if (!h) return SMP_EINVAL;
   smp_status s = check_rows(h, row0, rows);
   if (s != SMP_OK) return s;
@@ -619,6 +633,7 @@ smp_status smp_sketch_block_csr(smp_handle* h, int64_t row0, int64_t rows, const
                                 const int32_t* a_col, const float* a_val, int64_t a_nnz,
                                 const int64_t* b_rowptr, const int32_t* b_col, const float* b_val,
                                 int64_t b_nnz) {
+  NvtxRange nvtx_("smp_sketch_block_csr");
   if (!h) return SMP_EINVAL;
   smp_status s = check_rows(h, row0, rows);
   if (s != SMP_OK) return s;
@@ -699,6 +714,61 @@ smp_status smp_sketch_block_csr(smp_handle* h, int64_t row0, int64_t rows, const
   return SMP_OK;
 }
 
+// LELA pass 1: exact column norms only, accumulated into the same
+// fp64 norm accumulators the sketch pass fills (no sketch).
+smp_status smp_norms_block(smp_handle* h, int64_t row0, int64_t rows, const void* A, int64_t lda, const void* B,
+                           int64_t ldb) {
+  NvtxRange nvtx_("smp_norms_block");
+  if (!h) return SMP_EINVAL;
+  smp_status s = check_rows(h, row0, rows);
+  if (s != SMP_OK) return s;
+  if (h->d.input == SMP_IN_CSR_F32) return fail(h, SMP_EINVAL, "smp_norms_block: dense inputs only");
+  if (rows == 0) return SMP_OK;
+  const bool two = !h->d.a_is_b;
+  if (!A || lda < h->n1 || (two && (!B || ldb < h->n2)))
+    return fail(h, SMP_EINVAL, "null pointer or leading dimension smaller than n");
+  const int bf = h->d.input == SMP_IN_DENSE_BF16 ? 1 : 0;
+  h->finalized = false;
+  for (int side = 0; side < (two ? 2 : 1); ++side) {
+    const void* X = side ? B : A;
+    const int64_t ld = side ? ldb : lda, n = side ? h->n2 : h->n1, off = side ? h->n1 : 0;
+    const int64_t chunk = 1ll << 26;  // rows per launch (<= 65535 segments)
+    for (int64_t r0 = 0; r0 < rows; r0 += chunk) {
+      const int64_t rc = std::min(chunk, rows - r0);
+      CK(h, ensure(h->lela_pn, h->lela_pn_cap, ((rc + 1023) / 1024) * n), "alloc");
+      int segs = 0;
+      CK(h, smp::launch_colnorms(static_cast<const uint8_t*>(X) + r0 * ld * (bf ? 2 : 4), bf, ld, rc, n,
+                                 h->lela_pn, &segs, h->st), "colnorms");
+      CK(h, smp::launch_reduce_norms(h->lela_pn, segs, n, h->acc_nrm + off, h->st), "reduce_norms");
+      h->launches += 2;
+    }
+  }
+  return SMP_OK;
+}
+
+// LELA pass 2: acc[s] += Σ_{t in block} A[t, I_s] B[t, J_s].
+smp_status smp_exact_entries_block(smp_handle* h, int64_t row0, int64_t rows, const void* A, int64_t lda,
+                                   const void* B, int64_t ldb, const int32_t* I, const int32_t* J,
+                                   int64_t count, double* acc) {
+  NvtxRange nvtx_("smp_exact_entries_block");
+  if (!h) return SMP_EINVAL;
+  smp_status s = check_rows(h, row0, rows);
+  if (s != SMP_OK) return s;
+  if (h->d.input == SMP_IN_CSR_F32) return fail(h, SMP_EINVAL, "smp_exact_entries_block: dense inputs only");
+  if (count < 0 || (count > 0 && (!I || !J || !acc))) return fail(h, SMP_EINVAL, "bad sample arrays");
+  if (rows == 0 || count == 0) return SMP_OK;
+  const bool two = !h->d.a_is_b;
+  if (!A || lda < h->n1 || (two && (!B || ldb < h->n2)))
+    return fail(h, SMP_EINVAL, "null pointer or leading dimension smaller than n");
+  const int bf = h->d.input == SMP_IN_DENSE_BF16 ? 1 : 0;
+  const int64_t R = smp::lela_chunk_rows();
+  CK(h, ensure(h->lela_at, h->lela_at_cap, h->n1 * R), "alloc");
+  CK(h, ensure(h->lela_bt, h->lela_bt_cap, h->n2 * R), "alloc");
+  CK(h, smp::launch_exact_entries(A, lda, two ? B : A, two ? ldb : lda, bf, rows, h->n1, h->n2, I, J, count, acc,
+                                  h->lela_at, h->lela_bt, &h->launches, h->st), "exact_entries");
+  return SMP_OK;
+}
+
 smp_status smp_set_timing(smp_handle* h, int32_t enable) {
   if (!h) return SMP_EINVAL;
   h->timing = enable != 0;
@@ -732,6 +802,7 @@ smp_status smp_sketch_partials(smp_handle* h, float** sk, int64_t* sk_count, dou
 
 smp_status smp_finalize_norms(smp_handle* h, float* A_sk, float* B_sk, double* a_norm2,
                               double* b_norm2, double* frob2, float* a_sknorm, float* b_sknorm) {
+  NvtxRange nvtx_("smp_finalize_norms");
   using namespace smp;
   if (!h) return SMP_EINVAL;
   const int k = h->k;
@@ -761,11 +832,14 @@ smp_status smp_finalize_norms(smp_handle* h, float* A_sk, float* B_sk, double* a
   CK(h, cudaMemcpyAsync(h->h_status, h->status, sizeof(int), cudaMemcpyDeviceToHost, h->st), "copy");
   CK(h, cudaMemcpyAsync(h->h_fafb, h->FAFB, 16, cudaMemcpyDeviceToHost, h->st), "copy");
   CK(h, cudaStreamSynchronize(h->st), "sync");
-  h->finalized = true;
+  // the finalized state is usable by sample_estimate / waltmin only when every
+  // check passes (a zero Frobenius norm would divide by zero in q̂)
+  h->finalized = false;
   if (*h->h_status & 2) return fail(h, SMP_EINVAL, "CSR column index out of range (S:123)");
   if (*h->h_status) return fail(h, SMP_ENUMERIC, "NaN/Inf in the column norms or sketch");
   if (!(h->h_fafb[0] > 0.0) || !(h->h_fafb[1] > 0.0))
     return fail(h, SMP_ENUMERIC, "||A||_F = 0 or ||B||_F = 0");
+  h->finalized = true;
   return SMP_OK;
 }
 
@@ -776,27 +850,18 @@ static smp_status sample_multinomial(smp_handle* h, double m, uint64_t seed, int
   const int64_t boff = h->d.a_is_b ? 0 : n1;
   double* beta = h->alpha + n1;
   CK(h, launch_alpha_beta(h->acc_nrm, n1, h->acc_nrm + boff, n2, h->FAFB, h->alpha, beta, h->st), "alpha_beta");
-  CK(h, ensure(h->blk, h->blk_cap, n1 + 1), "alloc");
-  CK(h, ensure(h->mn_bpre, h->mn_bpre_cap, std::max<int64_t>(n2, 1)), "alloc");
-  CK(h, launch_mn_counts(h->alpha, beta, n1, n2, m, seed, h->mn_bpre, h->blk, h->d_total, h->st), "mn_counts");
-  CK(h, cudaMemcpyAsync(h->h_total, h->d_total, 8, cudaMemcpyDeviceToHost, h->st), "copy");
-  CK(h, cudaStreamSynchronize(h->st), "sync");
-  const int64_t cnt = *h->h_total;
+  h->launches += 1;
+  int64_t cnt = 0;
+  cudaError_t e = run_sample_multinomial(h->mn, h->alpha, beta, n1, n2, m, seed, cap, I, J, qhat, &cnt,
+                                         &h->launches, h->st);
+  if (e == cudaErrorInvalidValue) return fail(h, SMP_EINVAL, "multinomial sampler: >= 2^31 entries");
+  CK(h, e, "multinomial sampler");
   if (count) *count = cnt;
-  h->launches += 4;
   if (cnt > cap) return fail(h, SMP_ECAPACITY, "|Omega| = %lld > cap = %lld", (long long)cnt, (long long)cap);
   if (cnt == 0) return SMP_OK;
-  CK(h, ensure(h->mn_jtmp, h->mn_jtmp_cap, cnt), "alloc");
-  size_t need = 0;
-  CK(h, launch_mn_draws(h->alpha, beta, h->mn_bpre, n1, n2, m, seed, h->blk, h->d_total, cnt, cap, I, J,
-                        h->mn_jtmp, qhat, nullptr, &need, h->st), "mn_draws");
-  CK(h, ensure(h->mn_tmp, h->mn_tmp_cap, (int64_t)need + 1), "alloc");
-  size_t have = (size_t)h->mn_tmp_cap;
-  CK(h, launch_mn_draws(h->alpha, beta, h->mn_bpre, n1, n2, m, seed, h->blk, h->d_total, cnt, cap, I, J,
-                        h->mn_jtmp, qhat, h->mn_tmp, &have, h->st), "mn_draws");
   CK(h, launch_sddmm(h->fin_sk, h->fin_sk + boff * h->k, h->fin_D, h->fin_D + boff, h->k, I, J,
-                     h->d_total, cap, est == SMP_EST_PLAIN, val, h->st), "sddmm");
-  h->launches += 6;
+                     h->mn.total, cap, est == SMP_EST_PLAIN, val, h->st), "sddmm");
+  h->launches += 1;
   CK(h, cudaStreamSynchronize(h->st), "sync");
   return SMP_OK;
 }
@@ -804,6 +869,7 @@ static smp_status sample_multinomial(smp_handle* h, double m, uint64_t seed, int
 smp_status smp_sample_estimate_ex(smp_handle* h, double m, uint64_t seed, int32_t est, int32_t sampler,
                                   int64_t cap, int32_t* I, int32_t* J, float* val, double* qhat,
                                   int64_t* count) {
+  NvtxRange nvtx_("smp_sample_estimate_ex");
   if (!h) return SMP_EINVAL;
   if (sampler == SMP_SAMPLER_BERNOULLI) return smp_sample_estimate(h, m, seed, est, cap, I, J, val, qhat, count);
   if (sampler != SMP_SAMPLER_MULTINOMIAL) return fail(h, SMP_EINVAL, "unknown sampler");
@@ -815,6 +881,7 @@ smp_status smp_sample_estimate_ex(smp_handle* h, double m, uint64_t seed, int32_
 
 smp_status smp_sample_estimate(smp_handle* h, double m, uint64_t seed, int32_t est, int64_t cap,
                                int32_t* I, int32_t* J, float* val, double* qhat, int64_t* count) {
+  NvtxRange nvtx_("smp_sample_estimate");
   using namespace smp;
   if (!h) return SMP_EINVAL;
   if (!(m > 0.0)) return fail(h, SMP_EINVAL, "m must be > 0");
@@ -845,18 +912,22 @@ smp_status smp_sample_estimate(smp_handle* h, double m, uint64_t seed, int32_t e
 smp_status smp_waltmin(smp_handle* h, const int32_t* I, const int32_t* J, const float* val,
                        const double* qhat, int64_t count, const smp_waltmin_desc* w, float* U,
                        float* V) {
+  NvtxRange nvtx_("smp_waltmin");
   if (!h || !w) return SMP_EINVAL;
   if (!h->finalized) return fail(h, SMP_EINVAL, "call smp_finalize_norms first");
   if (w->r < 1 || w->r > 16 || w->r > h->n1 || w->r > h->n2)
     return fail(h, SMP_EINVAL, "r must satisfy 1 <= r <= min(16, n1, n2)");
   if (w->T < 1) return fail(h, SMP_EINVAL, "T must be >= 1");
   if (w->init_iters < 1) return fail(h, SMP_EINVAL, "init_iters must be >= 1");
-  if (w->partition != SMP_PART_REUSE_ALL) return fail(h, SMP_EINVAL, "unsupported partition");
+  if (w->partition != SMP_PART_REUSE_ALL && w->partition != SMP_PART_FRESH_2T1)
+    return fail(h, SMP_EINVAL, "unknown partition");
+  if (w->partition == SMP_PART_FRESH_2T1 && count < 2 * (int64_t)w->T + 1)
+    return fail(h, SMP_EINVAL, "FRESH_2T1 needs |Omega| >= 2T+1 (Alg. 2 line 3)");
   if (count < 0 || count > (1ll << 31) - 1 || (count > 0 && (!I || !J || !val || !qhat)) || !U || !V)
     return fail(h, SMP_EINVAL, "bad sample arrays");
   smp::WaltminArgs a{};
   a.n1 = h->n1; a.n2 = h->n2; a.count = count;
-  a.r = w->r; a.T = w->T; a.init_iters = w->init_iters;
+  a.r = w->r; a.T = w->T; a.init_iters = w->init_iters; a.partition = w->partition;
   a.trim_c = w->trim_c; a.lam = w->ridge; a.seed = w->seed;
   a.I = I; a.J = J; a.val = val; a.qhat = qhat;
   a.a_norm2 = h->acc_nrm; a.FA = h->FAFB;

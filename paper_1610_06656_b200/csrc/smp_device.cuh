@@ -13,6 +13,21 @@
 
 namespace smp {
 
+// cudaFuncSetAttribute is a per-device setting: remember, per call site, the
+// devices it has been applied to (a process may drive several GPUs).
+struct PerDeviceOnce {
+  unsigned long long mask = 0;
+  bool need() {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev >= 64) return true;
+    const unsigned long long bit = 1ull << dev;
+    if (mask & bit) return false;
+    mask |= bit;
+    return true;
+  }
+};
+
+
 // ---------------------------------------------------------------- hash
 struct u32x4 { uint32_t x, y, z, w; };
 
@@ -32,7 +47,7 @@ __device__ __forceinline__ u32x4 philox4x32_10(uint32_t c0, uint32_t c1, uint32_
 enum : int { PI_RADEMACHER = 0, PI_GAUSSIAN = 1, PI_HADAMARD = 2, PI_SRHT_BASE = 16 };
 
 // Stream tags (c3 of the Philox counter), DESIGN.md §3.1.
-enum : uint32_t { TAG_RADEMACHER = 1, TAG_GAUSSIAN = 2, TAG_OMEGA = 3, TAG_INIT = 5, TAG_SRHT_D = 6,
+enum : uint32_t { TAG_RADEMACHER = 1, TAG_GAUSSIAN = 2, TAG_OMEGA = 3, TAG_PART = 4, TAG_INIT = 5, TAG_SRHT_D = 6,
                   TAG_SRHT_S = 7 };
 
 // ---------------------------------------------------------------- SRHT

@@ -145,20 +145,47 @@ cudaError_t launch_sddmm(const float* Ask, const float* Bsk, const double* DA, c
                          int k, const int32_t* I, const int32_t* J, const int64_t* total,
                          int64_t cap, int plain, float* val, cudaStream_t st);
 
-// row-multinomial Ω (R27): Bpre, counts -> exclusive offsets (in place) and
-// *total; then draws (cnt = total <= cap, offsets with offs[n1] = total),
-// per-row column sort (CUB segmented; tmp == nullptr queries its size), q
-cudaError_t launch_mn_counts(const double* alpha, const double* beta, int64_t n1, int64_t n2, double m,
-                             uint64_t seed, double* bpre, int64_t* counts, int64_t* total, cudaStream_t st);
-cudaError_t launch_mn_draws(const double* alpha, const double* beta, const double* bpre, int64_t n1, int64_t n2,
-                            double m, uint64_t seed, const int64_t* offs, const int64_t* total, int64_t cnt,
-                            int64_t cap, int32_t* I, int32_t* J, int32_t* Jtmp, double* qhat, void* tmp,
-                            size_t* tmp_bytes, cudaStream_t st);
+// row-multinomial Ω (R27, omega.cu): handle-owned scratch
+struct MnWorkspace {
+  int32_t* sig = nullptr; int64_t sig_cap = 0;        // σ (columns by β descending)
+  int32_t* iota = nullptr; int64_t iota_cap = 0;
+  double* bsorted = nullptr; int64_t bsorted_cap = 0; // β_σ
+  double* bp = nullptr; int64_t bp_cap = 0;           // sequential prefix of β_σ
+  int64_t* sat = nullptr; int64_t sat_cap = 0;        // s_i
+  double* Tr = nullptr; int64_t Tr_cap = 0;           // T_i
+  int64_t* offs = nullptr; int64_t offs_cap = 0;      // row entry offsets (n1 + 1)
+  int32_t* jtmp = nullptr; int64_t jtmp_cap = 0;      // saturated + drawn columns
+  int32_t* jsrt = nullptr; int64_t jsrt_cap = 0;      // sorted per row
+  int32_t* flag = nullptr; int64_t flag_cap = 0;      // first occurrence
+  int32_t* pos = nullptr; int64_t pos_cap = 0;        // output position
+  uint8_t* tmp = nullptr; int64_t tmp_cap = 0;        // CUB scratch
+  int64_t* total = nullptr;
+  int64_t* total_h = nullptr;                         // pinned
+};
+void mn_workspace_free(MnWorkspace& w);
+// Ω (sorted by (i, j)) with q̂; *count = |Ω| (written even when > cap, in
+// which case nothing is written).  Synchronises twice.
+cudaError_t run_sample_multinomial(MnWorkspace& w, const double* alpha, const double* beta, int64_t n1,
+                                   int64_t n2, double m, uint64_t seed, int64_t cap, int32_t* I, int32_t* J,
+                                   double* qhat, int64_t* count, int64_t* launches, cudaStream_t st);
+
+// ---- LELA (lela.cu): pass 1 column norms, pass 2 exact entries on Ω
+// pnorm[seg][c] = Σ_{t in seg} X[t, c]² (fp64, NORM_SEG-row segments; *segs set)
+cudaError_t launch_colnorms(const void* X, int x_bf16, int64_t ldx, int64_t rows, int64_t n, double* pnorm,
+                            int* segs, cudaStream_t st);
+// acc[s] += Σ_{t < rows} A[t, I_s] B[t, J_s]; At / Bt: scratch of n1 · R / n2 · R
+// floats (R = lela_chunk_rows())
+cudaError_t launch_exact_entries(const void* A, int64_t lda, const void* B, int64_t ldb, int x_bf16,
+                                 int64_t rows, int64_t n1, int64_t n2, const int32_t* I, const int32_t* J,
+                                 int64_t cnt, double* acc, float* At, float* Bt, int64_t* launches,
+                                 cudaStream_t st);
+int lela_chunk_rows();
 
 // ---- K7-K9 WAltMin (waltmin.cu)
 struct WaltminArgs {
   int64_t n1, n2, count;
   int r, T, init_iters;
+  int partition;          // 0 REUSE_ALL, 1 FRESH_2T1 (Alg. 2 line 3; R11)
   double trim_c, lam;
   uint64_t seed;
   const int32_t* I;

@@ -1,5 +1,5 @@
 // K7-K9: WAltMin (Alg. 2; Step 3, Eq. 3) with
-// the REUSE_ALL partition (R11):
+// the REUSE_ALL or FRESH_2T1 partition of line 3 (R11):
 //   w = 1/q̂ (line 2); R = w .* P_Ω(M̃) (line 4);
 //   U0 = top-r left subspace of R by subspace iteration from a Rademacher
 //        start (line 5; R12), CholeskyQR2 orthonormalisation;
@@ -29,17 +29,23 @@ __global__ void wm_weights_kernel(const double* __restrict__ qhat, const float* 
   }
 }
 
-// ptr[o] = lower_bound(keys, o) for o in [0, nout]
-__global__ void wm_ptr_kernel(const int32_t* __restrict__ keys, int64_t cnt, int64_t nout,
+// ptr[g·(nout+1) + o] = lower_bound(keys, g·nout + o) for o in [0, nout],
+// g in [0, groups): row pointers of every subset of a (subset, row)-sorted key
+// sequence (groups = 1: plain CSR pointers)
+template <class K>
+__global__ void wm_ptr_kernel(const K* __restrict__ keys, int64_t cnt, int64_t nout, int groups,
                               int64_t* __restrict__ ptr) {
-  for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o <= nout;
-       o += (int64_t)gridDim.x * blockDim.x) {
+  const int64_t tot = (int64_t)groups * (nout + 1);
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t g = e / (nout + 1), o = e - g * (nout + 1);
+    const int64_t target = g * nout + o;
     int64_t lo = 0, hi = cnt;
     while (lo < hi) {
       int64_t mid = (lo + hi) >> 1;
-      if (keys[mid] < o) lo = mid + 1; else hi = mid;
+      if ((int64_t)keys[mid] < target) lo = mid + 1; else hi = mid;
     }
-    ptr[o] = lo;
+    ptr[e] = lo;
   }
 }
 
@@ -73,6 +79,69 @@ __global__ void wm_heavy_flags_kernel(const int64_t* __restrict__ ptr, int64_t n
   }
 }
 
+// ---- FRESH_2T1 partition (Alg. 2 line 3; R11):
+// key_s = (w1 << 32) | w0 of Philox(ctr = (i, j, 0, 4), key = seed); the
+// sample of rank p in (key, s) order goes to subset p mod nsub.
+__global__ void wm_part_key_kernel(const int32_t* __restrict__ I, const int32_t* __restrict__ J, int64_t cnt,
+                                   uint64_t seed, uint64_t* __restrict__ key) {
+  const uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < cnt;
+       s += (int64_t)gridDim.x * blockDim.x) {
+    const u32x4 w = philox4x32_10((uint32_t)I[s], (uint32_t)J[s], 0u, TAG_PART, k0, k1);
+    key[s] = ((uint64_t)w.y << 32) | (uint64_t)w.x;
+  }
+}
+
+__global__ void wm_sub_kernel(const int32_t* __restrict__ rank_to_s, int64_t cnt, int nsub,
+                              int32_t* __restrict__ sub) {
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < cnt;
+       p += (int64_t)gridDim.x * blockDim.x)
+    sub[rank_to_s[p]] = (int32_t)(p % nsub);
+}
+
+// subset-major copy: sample q of the new order is original sample ord[q];
+// rk = sub·n1 + i (CSR key), ck = sub·n2 + j (CSC key)
+__global__ void wm_fresh_gather_kernel(const int32_t* __restrict__ ord, const int32_t* __restrict__ sub,
+                                       const int32_t* __restrict__ I, const int32_t* __restrict__ J,
+                                       const float* __restrict__ val, const double* __restrict__ qhat,
+                                       int64_t cnt, int64_t n1, int64_t n2, int32_t* __restrict__ I2,
+                                       int32_t* __restrict__ J2, float* __restrict__ val2,
+                                       double* __restrict__ q2, int64_t* __restrict__ rk,
+                                       int64_t* __restrict__ ck) {
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < cnt;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t s = ord[q];
+    const int64_t g = sub[s];
+    I2[q] = I[s];
+    J2[q] = J[s];
+    val2[q] = val[s];
+    q2[q] = qhat[s];
+    rk[q] = g * n1 + I[s];
+    ck[q] = g * n2 + J[s];
+  }
+}
+
+// stream-ordered workspace, released on every return path
+struct WmScratch {
+  cudaStream_t st;
+  std::vector<void*> ptrs;
+  explicit WmScratch(cudaStream_t s) : st(s) {}
+  template <class T>
+  cudaError_t alloc(T*& p, int64_t bytes) {
+    void* q = nullptr;
+    cudaError_t e = cudaMallocAsync(&q, (size_t)(bytes > 0 ? bytes : 1), st);
+    if (e == cudaSuccess) { ptrs.push_back(q); p = static_cast<T*>(q); }
+    return e;
+  }
+  ~WmScratch() { for (void* q : ptrs) cudaFreeAsync(q, st); }
+};
+
+static int bits_for(int64_t v) {  // bits needed to represent values < v (at least 1)
+  int b = 1;
+  while (b < 63 && ((int64_t)1 << b) < v) ++b;
+  return b;
+}
+
 template <int R>
 cudaError_t launch_wm(WMParams& p, cudaStream_t st);  // waltmin_r*.cu
 
@@ -100,53 +169,117 @@ static int grid_for(int64_t n, int threads) {
   return (int)std::min<int64_t>(b, 148 * 16);
 }
 
+static int env_int(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e ? atoi(e) : dflt;
+}
+
 cudaError_t run_waltmin(const WaltminArgs& a, cudaStream_t st) {
   const int64_t cnt = a.count, n1 = a.n1, n2 = a.n2;
   const int r = a.r;
   if (r < 1 || r > 16) return cudaErrorInvalidValue;
-  // workspace
+  const bool fresh = a.partition == 1;
+  const int nsub = fresh ? 2 * a.T + 1 : 1;
+  WmScratch ws(st);
   double *w, *wv, *cw, *cwv, *Y, *Z, *U, *V, *gpart;
   unsigned* bar;
   int64_t *rptr, *cptr;
-  int32_t *iota, *perm, *jsorted, *cI;
-  void* cub_tmp = nullptr;
-  size_t cub_bytes = 0;
+  int32_t *iota, *perm, *cI;
   const int64_t c1 = cnt > 0 ? cnt : 1;
   const int gctas = waltmin_grid_ctas();
   if (gctas < 1) return cudaErrorNoDevice;
-  SMP_TRY(cudaMallocAsync(&w, c1 * 8, st));
-  SMP_TRY(cudaMallocAsync(&wv, c1 * 8, st));
-  SMP_TRY(cudaMallocAsync(&cw, c1 * 8, st));
-  SMP_TRY(cudaMallocAsync(&cwv, c1 * 8, st));
-  SMP_TRY(cudaMallocAsync(&cI, c1 * 4, st));
-  SMP_TRY(cudaMallocAsync(&Y, n2 * r * 8, st));
-  SMP_TRY(cudaMallocAsync(&Z, n1 * r * 8, st));
-  SMP_TRY(cudaMallocAsync(&U, n1 * r * 8, st));
-  SMP_TRY(cudaMallocAsync(&V, n2 * r * 8, st));
-  SMP_TRY(cudaMallocAsync(&gpart, (int64_t)2 * gctas * r * (r + 1) / 2 * 8, st));
-  SMP_TRY(cudaMallocAsync(&bar, 64, st));
-  SMP_TRY(cudaMallocAsync(&rptr, (n1 + 1) * 8, st));
-  SMP_TRY(cudaMallocAsync(&cptr, (n2 + 1) * 8, st));
-  SMP_TRY(cudaMallocAsync(&iota, c1 * 4, st));
-  SMP_TRY(cudaMallocAsync(&perm, c1 * 4, st));
-  SMP_TRY(cudaMallocAsync(&jsorted, c1 * 4, st));
+  SMP_TRY(ws.alloc(w, c1 * 8));
+  SMP_TRY(ws.alloc(wv, c1 * 8));
+  SMP_TRY(ws.alloc(cw, c1 * 8));
+  SMP_TRY(ws.alloc(cwv, c1 * 8));
+  SMP_TRY(ws.alloc(cI, c1 * 4));
+  SMP_TRY(ws.alloc(Y, n2 * r * 8));
+  SMP_TRY(ws.alloc(Z, n1 * r * 8));
+  SMP_TRY(ws.alloc(U, n1 * r * 8));
+  SMP_TRY(ws.alloc(V, n2 * r * 8));
+  SMP_TRY(ws.alloc(gpart, (int64_t)2 * gctas * r * (r + 1) / 2 * 8));
+  SMP_TRY(ws.alloc(bar, 64));
+  SMP_TRY(ws.alloc(rptr, (int64_t)nsub * (n1 + 1) * 8));
+  SMP_TRY(ws.alloc(cptr, (int64_t)nsub * (n2 + 1) * 8));
+  SMP_TRY(ws.alloc(iota, c1 * 4));
+  SMP_TRY(ws.alloc(perm, c1 * 4));
+  void* cub_tmp = nullptr;
+  size_t cub_bytes = 0;
+  auto cub_scratch = [&](size_t need) -> cudaError_t {
+    if (need <= cub_bytes && cub_tmp) return cudaSuccess;
+    void* q = nullptr;
+    SMP_TRY(ws.alloc(q, (int64_t)need));
+    cub_tmp = q;
+    cub_bytes = need;
+    return cudaSuccess;
+  };
+  const int gc = grid_for(cnt, 256);
 
-  wm_weights_kernel<<<grid_for(cnt, 256), 256, 0, st>>>(a.qhat, a.val, cnt, w, wv);
-  wm_ptr_kernel<<<grid_for(n1 + 1, 256), 256, 0, st>>>(a.I, cnt, n1, rptr);
-  // CSC: stable radix sort of (J, s) -> perm; column pointers on sorted J
-  wm_iota_kernel<<<grid_for(cnt, 256), 256, 0, st>>>(iota, cnt);
-  int end_bit = 1;
-  while (end_bit < 32 && ((int64_t)1 << end_bit) <= n2) ++end_bit;
-  SMP_TRY(cub::DeviceRadixSort::SortPairs(nullptr, cub_bytes, a.J, jsorted, iota, perm, (int)cnt, 0,
-                                          end_bit, st));
-  SMP_TRY(cudaMallocAsync(&cub_tmp, cub_bytes > 0 ? cub_bytes : 1, st));
-  SMP_TRY(cub::DeviceRadixSort::SortPairs(cub_tmp, cub_bytes, a.J, jsorted, iota, perm, (int)cnt, 0,
-                                          end_bit, st));
-  wm_ptr_kernel<<<grid_for(n2 + 1, 256), 256, 0, st>>>(jsorted, cnt, n2, cptr);
-  wm_gather_csc_kernel<<<grid_for(cnt, 256), 256, 0, st>>>(perm, a.I, w, wv, cnt, cI, cw, cwv);
+  // the sample arrays the phases read: Ω as given (REUSE_ALL) or its
+  // subset-major copy (FRESH_2T1)
+  const int32_t* sI = a.I;
+  const int32_t* sJ = a.J;
+  const float* sval = a.val;
+  const double* sq = a.qhat;
+  int64_t *rk = nullptr, *ck = nullptr;
+  wm_iota_kernel<<<gc, 256, 0, st>>>(iota, cnt);
+  if (fresh && cnt > 0) {
+    uint64_t *key, *key_s;
+    int32_t *sub, *sub_s, *ord, *I2, *J2;
+    float* val2;
+    double* q2;
+    SMP_TRY(ws.alloc(key, c1 * 8));
+    SMP_TRY(ws.alloc(key_s, c1 * 8));
+    SMP_TRY(ws.alloc(sub, c1 * 4));
+    SMP_TRY(ws.alloc(sub_s, c1 * 4));
+    SMP_TRY(ws.alloc(ord, c1 * 4));
+    SMP_TRY(ws.alloc(I2, c1 * 4));
+    SMP_TRY(ws.alloc(J2, c1 * 4));
+    SMP_TRY(ws.alloc(val2, c1 * 4));
+    SMP_TRY(ws.alloc(q2, c1 * 8));
+    SMP_TRY(ws.alloc(rk, c1 * 8));
+    SMP_TRY(ws.alloc(ck, c1 * 8));
+    wm_part_key_kernel<<<gc, 256, 0, st>>>(a.I, a.J, cnt, a.seed, key);
+    size_t need = 0;
+    SMP_TRY(cub::DeviceRadixSort::SortPairs(nullptr, need, key, key_s, iota, perm, (int)cnt, 0, 64, st));
+    SMP_TRY(cub_scratch(need));
+    SMP_TRY(cub::DeviceRadixSort::SortPairs(cub_tmp, need, key, key_s, iota, perm, (int)cnt, 0, 64, st));
+    wm_sub_kernel<<<gc, 256, 0, st>>>(perm, cnt, nsub, sub);
+    // stable by subset: within a subset the (i, j) order of Ω is kept
+    SMP_TRY(cub::DeviceRadixSort::SortPairs(nullptr, need, sub, sub_s, iota, ord, (int)cnt, 0, bits_for(nsub), st));
+    SMP_TRY(cub_scratch(need));
+    SMP_TRY(cub::DeviceRadixSort::SortPairs(cub_tmp, need, sub, sub_s, iota, ord, (int)cnt, 0, bits_for(nsub), st));
+    wm_fresh_gather_kernel<<<gc, 256, 0, st>>>(ord, sub, a.I, a.J, a.val, a.qhat, cnt, n1, n2, I2, J2, val2, q2,
+                                                rk, ck);
+    sI = I2; sJ = J2; sval = val2; sq = q2;
+  }
+  wm_weights_kernel<<<gc, 256, 0, st>>>(sq, sval, cnt, w, wv);
+  // CSR pointers (per subset); CSC: stable radix sort of the column key
+  if (fresh) {
+    wm_ptr_kernel<int64_t><<<grid_for((int64_t)nsub * (n1 + 1), 256), 256, 0, st>>>(rk, cnt, n1, nsub, rptr);
+    int64_t* ck_s;
+    SMP_TRY(ws.alloc(ck_s, c1 * 8));
+    const int eb = bits_for((int64_t)nsub * n2 + 1);
+    size_t need = 0;
+    SMP_TRY(cub::DeviceRadixSort::SortPairs(nullptr, need, ck, ck_s, iota, perm, (int)cnt, 0, eb, st));
+    SMP_TRY(cub_scratch(need));
+    SMP_TRY(cub::DeviceRadixSort::SortPairs(cub_tmp, need, ck, ck_s, iota, perm, (int)cnt, 0, eb, st));
+    wm_ptr_kernel<int64_t><<<grid_for((int64_t)nsub * (n2 + 1), 256), 256, 0, st>>>(ck_s, cnt, n2, nsub, cptr);
+  } else {
+    wm_ptr_kernel<int32_t><<<grid_for(n1 + 1, 256), 256, 0, st>>>(sI, cnt, n1, 1, rptr);
+    int32_t* jsorted;
+    SMP_TRY(ws.alloc(jsorted, c1 * 4));
+    const int end_bit = bits_for(n2 + 1);
+    size_t need = 0;
+    SMP_TRY(cub::DeviceRadixSort::SortPairs(nullptr, need, sJ, jsorted, iota, perm, (int)cnt, 0, end_bit, st));
+    SMP_TRY(cub_scratch(need));
+    SMP_TRY(cub::DeviceRadixSort::SortPairs(cub_tmp, need, sJ, jsorted, iota, perm, (int)cnt, 0, end_bit, st));
+    wm_ptr_kernel<int32_t><<<grid_for(n2 + 1, 256), 256, 0, st>>>(jsorted, cnt, n2, 1, cptr);
+  }
+  wm_gather_csc_kernel<<<gc, 256, 0, st>>>(perm, sI, w, wv, cnt, cI, cw, cwv);
 
-  // heavy rows / columns: stable compaction (fixed order -> fixed CTA
-  // assignment -> deterministic Gram partials)
+  // heavy rows / columns (REUSE_ALL only): stable compaction (fixed order ->
+  // fixed CTA assignment -> deterministic Gram partials)
   const int64_t nmax = std::max<int64_t>(std::max<int64_t>(n1, n2), 1);
   // Split a row over a CTA only when it is long in absolute terms AND several
   // times a warp's average share: the CTA runs its heavy rows before its light
@@ -155,27 +288,30 @@ cudaError_t run_waltmin(const WaltminArgs& a, cudaStream_t st) {
   // the threshold (0 = warp-per-row only; tuning).
   const char* hv = getenv("SMP_WM_HEAVY");
   const int64_t avg_warp = cnt / ((int64_t)gctas * WM_WARPS) + 1;
-  const int64_t heavy_thr = hv ? atoll(hv) : std::max<int64_t>(WM_HEAVY, 4 * avg_warp);
-  uint8_t *hfr, *hfc;
-  int32_t *hidx, *hlr, *hlc, *nh;
-  void* sel_tmp = nullptr;
-  size_t sel_bytes = 0;
-  SMP_TRY(cudaMallocAsync(&hfr, n1 + 1, st));
-  SMP_TRY(cudaMallocAsync(&hfc, n2 + 1, st));
-  SMP_TRY(cudaMallocAsync(&hidx, nmax * 4, st));
-  SMP_TRY(cudaMallocAsync(&hlr, (n1 + 1) * 4, st));
-  SMP_TRY(cudaMallocAsync(&hlc, (n2 + 1) * 4, st));
-  SMP_TRY(cudaMallocAsync(&nh, 2 * 4, st));
-  SMP_TRY(cub::DeviceSelect::Flagged(nullptr, sel_bytes, hidx, hfr, hlr, nh, (int)nmax, st));
-  SMP_TRY(cudaMallocAsync(&sel_tmp, sel_bytes > 0 ? sel_bytes : 1, st));
-  SMP_TRY(cudaMemsetAsync(nh, 0, 2 * 4, st));
-  if (n1 > 0) {
-    wm_heavy_flags_kernel<<<grid_for(n1, 256), 256, 0, st>>>(rptr, n1, heavy_thr, hfr, hidx);
-    SMP_TRY(cub::DeviceSelect::Flagged(sel_tmp, sel_bytes, hidx, hfr, hlr, nh, (int)n1, st));
-  }
-  if (n2 > 0) {
-    wm_heavy_flags_kernel<<<grid_for(n2, 256), 256, 0, st>>>(cptr, n2, heavy_thr, hfc, hidx);
-    SMP_TRY(cub::DeviceSelect::Flagged(sel_tmp, sel_bytes, hidx, hfc, hlc, nh + 1, (int)n2, st));
+  const int64_t heavy_thr = fresh ? 0 : (hv ? atoll(hv) : std::max<int64_t>(WM_HEAVY, 4 * avg_warp));
+  uint8_t *hfr = nullptr, *hfc = nullptr;
+  int32_t *hidx = nullptr, *hlr = nullptr, *hlc = nullptr, *nh = nullptr;
+  if (heavy_thr > 0) {
+    SMP_TRY(ws.alloc(hfr, n1 + 1));
+    SMP_TRY(ws.alloc(hfc, n2 + 1));
+    SMP_TRY(ws.alloc(hidx, nmax * 4));
+    SMP_TRY(ws.alloc(hlr, (n1 + 1) * 4));
+    SMP_TRY(ws.alloc(hlc, (n2 + 1) * 4));
+    SMP_TRY(ws.alloc(nh, 2 * 4));
+    size_t need = 0;
+    SMP_TRY(cub::DeviceSelect::Flagged(nullptr, need, hidx, hfr, hlr, nh, (int)nmax, st));
+    SMP_TRY(cub_scratch(need));
+    SMP_TRY(cudaMemsetAsync(nh, 0, 2 * 4, st));
+    if (n1 > 0) {
+      wm_heavy_flags_kernel<<<grid_for(n1, 256), 256, 0, st>>>(rptr, n1, heavy_thr, hfr, hidx);
+      size_t h1 = cub_bytes;
+      SMP_TRY(cub::DeviceSelect::Flagged(cub_tmp, h1, hidx, hfr, hlr, nh, (int)n1, st));
+    }
+    if (n2 > 0) {
+      wm_heavy_flags_kernel<<<grid_for(n2, 256), 256, 0, st>>>(cptr, n2, heavy_thr, hfc, hidx);
+      size_t h2 = cub_bytes;
+      SMP_TRY(cub::DeviceSelect::Flagged(cub_tmp, h2, hidx, hfc, hlc, nh + 1, (int)n2, st));
+    }
   }
 
   // lines 5-10: one cooperative persistent kernel
@@ -183,13 +319,18 @@ cudaError_t run_waltmin(const WaltminArgs& a, cudaStream_t st) {
   WMParams p{};
   p.n1 = n1; p.n2 = n2; p.count = cnt; p.T = a.T; p.init_iters = a.init_iters;
   p.trim_c = a.trim_c; p.lam = a.lam; p.seed = a.seed;
-  p.rptr = rptr; p.J = a.J; p.w = w; p.wv = wv;
+  p.rptr = rptr; p.J = sJ; p.w = w; p.wv = wv;
   p.cptr = cptr; p.cI = cI; p.cw = cw; p.cwv = cwv;
   p.a2 = a.a_norm2; p.FA = a.FA;
   p.Y = Y; p.Z = Z; p.U = U; p.V = V; p.gpart = gpart; p.bar = bar;
   p.Uout = a.U; p.Vout = a.V;
-  const char* xl = getenv("SMP_WM_L1");  // 0: L2-only gathers (A/B switch)
-  p.x_l1 = (xl && atoi(xl) == 0) ? 0 : 1;
+  p.rstride = fresh ? n1 + 1 : 0;
+  p.cstride = fresh ? n2 + 1 : 0;
+  // tuning switches, read on every call
+  p.x_l1 = env_int("SMP_WM_L1", 1) == 0 ? 0 : 1;  // 0: L2-only gathers (A/B switch)
+  p.env_stage = env_int("SMP_WM_STAGE", 1);
+  p.env_cache = env_int("SMP_WM_CACHE", 1);
+  p.env_ctas = env_int("SMP_WM_CTAS", 0);
   if (heavy_thr > 0) {
     p.heavy_r = hlr; p.nheavy_r = nh; p.hflag_r = hfr;
     p.heavy_c = hlc; p.nheavy_c = nh + 1; p.hflag_c = hfc;
@@ -198,7 +339,7 @@ cudaError_t run_waltmin(const WaltminArgs& a, cudaStream_t st) {
   uint64_t* trace = nullptr;
   const int max_bar = 2 * (a.init_iters + 4) + 2 * a.T + 8;
   if (tr && atoi(tr)) {
-    SMP_TRY(cudaMalloc(&trace, 4 * 8 * (size_t)max_bar + 64 * 8));
+    SMP_TRY(ws.alloc(trace, 4 * 8 * (int64_t)max_bar + 64 * 8));
     SMP_TRY(cudaMemsetAsync(trace, 0, 4 * 8 * (size_t)max_bar + 64 * 8, st));
   }
   p.trace = trace;
@@ -218,16 +359,7 @@ cudaError_t run_waltmin(const WaltminArgs& a, cudaStream_t st) {
       fprintf(stderr, "wm iter %2d: stage %.2f us, Z-SpMM+flush %.2f us, barrier+chol %.2f us, Y half %.2f us\n",
               i / 4, (t2[i + 1] - t2[i]) * 1e-3, (t2[i + 2] - t2[i + 1]) * 1e-3, (t2[i + 3] - t2[i + 2]) * 1e-3,
               (t2[i + 4] - t2[i + 3]) * 1e-3);
-    cudaFree(trace);
   }
-  SMP_TRY(cudaGetLastError());
-  cudaFreeAsync(w, st); cudaFreeAsync(wv, st); cudaFreeAsync(cw, st); cudaFreeAsync(cwv, st);
-  cudaFreeAsync(cI, st); cudaFreeAsync(Y, st); cudaFreeAsync(Z, st);
-  cudaFreeAsync(U, st); cudaFreeAsync(V, st); cudaFreeAsync(gpart, st); cudaFreeAsync(bar, st);
-  cudaFreeAsync(rptr, st); cudaFreeAsync(cptr, st); cudaFreeAsync(iota, st);
-  cudaFreeAsync(perm, st); cudaFreeAsync(jsorted, st); cudaFreeAsync(cub_tmp, st);
-  cudaFreeAsync(hfr, st); cudaFreeAsync(hfc, st); cudaFreeAsync(hidx, st); cudaFreeAsync(hlr, st);
-  cudaFreeAsync(hlc, st); cudaFreeAsync(nh, st); cudaFreeAsync(sel_tmp, st);
   return cudaGetLastError();
 }
 

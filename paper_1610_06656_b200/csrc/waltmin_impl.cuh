@@ -69,6 +69,12 @@ struct WMParams {
   const uint8_t* hflag_c;
   int64_t count;        // |Ω|
   int64_t cache_bytes;  // dynamic SMEM reserved for the two WMCache copies (0: off)
+  // FRESH_2T1 (Alg. 2 line 3): phase ph (0 = init, 2t+1 = V-solve t,
+  // 2t+2 = U-solve t) reads rptr + ph·rstride / cptr + ph·cstride (positions
+  // into the subset-major sample arrays); 0 = REUSE_ALL (every phase, all of Ω)
+  int64_t rstride, cstride;
+  // tuning switches, read per call by the host (SMP_WM_STAGE / _CACHE / _CTAS)
+  int env_stage, env_cache, env_ctas;
   float* Uout;
   float* Vout;
 };
@@ -892,11 +898,11 @@ __global__ void __launch_bounds__(WM_THREADS, 1) wm_persistent_kernel(WMParams p
   if (p.T == 0)
     for (int64_t e = (int64_t)blockIdx.x * WM_THREADS + tid; e < p.n2 * R; e += G * WM_THREADS) p.V[e] = 0.0;
   for (int t = 0; t < p.T; ++t) {
-    als_phase<R>(sm, p.cptr, p.cI, p.cw, p.cwv, p.U, p.n2, p.lam, p.V, stage_rows<R>(p.U, p.n1, xs, stg),
-                 p.heavy_c, sm.nh[1], p.hflag_c, p.x_l1, sm.cache[1]);
+    als_phase<R>(sm, p.cptr + (2 * t + 1) * p.cstride, p.cI, p.cw, p.cwv, p.U, p.n2, p.lam, p.V,
+                 stage_rows<R>(p.U, p.n1, xs, stg), p.heavy_c, sm.nh[1], p.hflag_c, p.x_l1, sm.cache[1]);
     grid_sync(p.bar, p.trace, nbar);
-    als_phase<R>(sm, p.rptr, p.J, p.w, p.wv, p.V, p.n1, p.lam, p.U, stage_rows<R>(p.V, p.n2, xs, stg),
-                 p.heavy_r, sm.nh[0], p.hflag_r, p.x_l1, sm.cache[0]);
+    als_phase<R>(sm, p.rptr + (2 * t + 2) * p.rstride, p.J, p.w, p.wv, p.V, p.n1, p.lam, p.U,
+                 stage_rows<R>(p.V, p.n2, xs, stg), p.heavy_r, sm.nh[0], p.hflag_r, p.x_l1, sm.cache[0]);
     grid_sync(p.bar, p.trace, nbar);
   }
   // output (Û(T), V̂(T)) in fp32
@@ -911,11 +917,7 @@ cudaError_t launch_wm(WMParams& p, cudaStream_t st) {
   constexpr size_t XS_MAX = 160 * 1024;  // staged factor rows (n_max · r doubles)
   const size_t base = (sizeof(WMShared<R>) + 15) & ~(size_t)15;
   const size_t xs_bytes = (size_t)(p.n1 > p.n2 ? p.n1 : p.n2) * R * 8;
-  static const int env_stage = [] {  // SMP_WM_STAGE=0: never stage (tuning)
-    const char* e = getenv("SMP_WM_STAGE");
-    return e ? atoi(e) : 1;
-  }();
-  p.stage_x = (env_stage && xs_bytes <= XS_MAX) ? 1 : 0;
+  p.stage_x = (p.env_stage && xs_bytes <= XS_MAX) ? 1 : 0;  // SMP_WM_STAGE=0: never stage
   int dev = 0, sms = 0, per_sm = 0, optin = 0;
   SMP_TRY(cudaGetDevice(&dev));
   SMP_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
@@ -927,20 +929,15 @@ cudaError_t launch_wm(WMParams& p, cudaStream_t st) {
   // sample cache (WMCache): reserve twice the average per-CTA need of both
   // sides (20 B per sample and side + row lengths) when that fits beside the
   // stage — otherwise leave the SMEM to L1, which the unstaged gathers use.
-  // SMP_WM_CACHE=0 disables it (tuning).
-  static const int env_cache = [] {
-    const char* e = getenv("SMP_WM_CACHE");
-    return e ? atoi(e) : 1;
-  }();
+  // SMP_WM_CACHE=0 disables it (tuning); FRESH_2T1 phases read different
+  // subsets, so the (whole-Ω) cache is off there.
+  const int env_cache = p.env_cache && p.rstride == 0;
   // one CTA per SM at most (co-resident: cooperative launch), and no more CTAs
   // than needed for the per-warp row count a full grid would give: the same
   // critical path with fewer barrier participants and Gram partials (cfg1:
   // 1024 rows -> 128 CTAs of one row per warp; cfg4 2.85 -> 2.60 ms).
   // SMP_WM_CTAS overrides (tuning).
-  static const int env_ctas = [] {
-    const char* e = getenv("SMP_WM_CTAS");
-    return e ? atoi(e) : 0;
-  }();
+  const int env_ctas = p.env_ctas;
   int grid = sms;
   {
     const int64_t nmax = p.n1 > p.n2 ? p.n1 : p.n2;
@@ -960,11 +957,8 @@ cudaError_t launch_wm(WMParams& p, cudaStream_t st) {
       smem += (size_t)want;
     }
   }
-  static bool attr = false;
-  if (!attr) {
-    SMP_TRY(cudaFuncSetAttribute(wm_persistent_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
-    attr = true;
-  }
+  // per device (cheap; a process may drive several GPUs)
+  SMP_TRY(cudaFuncSetAttribute(wm_persistent_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
   SMP_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, wm_persistent_kernel<R>, WM_THREADS, smem));
   if (per_sm < 1) return cudaErrorInvalidConfiguration;
   void* args[] = {&p};

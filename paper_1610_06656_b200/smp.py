@@ -16,7 +16,7 @@ from . import _lib
 from ._lib import (EST_PLAIN, EST_RESCALED, IN_CSR_F32, IN_DENSE_BF16, IN_DENSE_F32,
                    PI_GAUSSIAN, PI_HADAMARD_TEST, PI_RADEMACHER, PI_SRHT, SmpError)
 
-__all__ = ["SMPSketch", "smp_pca", "PI_RADEMACHER", "PI_GAUSSIAN", "PI_HADAMARD_TEST", "PI_SRHT",
+__all__ = ["SMPSketch", "smp_pca", "lela", "PI_RADEMACHER", "PI_GAUSSIAN", "PI_HADAMARD_TEST", "PI_SRHT",
            "IN_DENSE_BF16", "IN_DENSE_F32", "IN_CSR_F32", "SmpError"]
 
 
@@ -122,6 +122,26 @@ class SMPSketch:
                                             0 if self.a_is_b else B.stride(0), chunk_rows)
         self._check(st, "smp_sketch_block_host")
 
+    def norms_block(self, row0, A, B=None):
+        """LELA pass 1: exact column norms of rows [row0, row0 + A.shape[0])."""
+        _check_dense(A, "A")
+        if not self.a_is_b:
+            _check_dense(B, "B")
+        st = self.lib.smp_norms_block(self.h, row0, A.shape[0], _ptr(A), A.stride(0),
+                                      _ptr(None if self.a_is_b else B), 0 if self.a_is_b else B.stride(0))
+        self._check(st, "smp_norms_block")
+
+    def exact_entries_block(self, row0, A, B, I, J, acc):
+        """LELA pass 2: acc[s] += Σ_t A[t, I_s] B[t, J_s] over this block."""
+        _check_dense(A, "A")
+        if not self.a_is_b:
+            _check_dense(B, "B")
+        st = self.lib.smp_exact_entries_block(self.h, row0, A.shape[0], _ptr(A), A.stride(0),
+                                              _ptr(None if self.a_is_b else B),
+                                              0 if self.a_is_b else B.stride(0), _ptr(I), _ptr(J),
+                                              I.numel(), _ptr(acc))
+        self._check(st, "smp_exact_entries_block")
+
     def block_csr(self, row0, rows, a_rowptr, a_col, a_val, b_rowptr=None, b_col=None, b_val=None):
         st = self.lib.smp_sketch_block_csr(
             self.h, row0, rows, _ptr(a_rowptr), _ptr(a_col), _ptr(a_val), a_col.numel(),
@@ -158,7 +178,8 @@ class SMPSketch:
     def sample_estimate(self, m, seed, plain=False, cap=None, sampler="bernoulli"):
         """Ω (sorted by (i,j)), M̃ on Ω and q̂ (Alg. 1 lines 3-4).  sampler:
         "bernoulli" (Alg. 1 line 3) or "multinomial" (the appendix's
-        row-multinomial sampler, R27: duplicates kept, q̂ = q)."""
+        row-multinomial sampler with line 3's saturation, R27:
+        each drawn pair once, q̂ = its inclusion probability)."""
         smode = {"bernoulli": _lib.SAMPLER_BERNOULLI, "multinomial": _lib.SAMPLER_MULTINOMIAL}[sampler]
         if cap is None:
             cap = int(min(self.n1 * self.n2, m + 10 * math.sqrt(max(m, 1.0)) + 1024))
@@ -191,20 +212,53 @@ class SMPSketch:
         I, J, val, qh = self.sample_estimate(1e30, seed, plain=True, cap=self.n1 * self.n2)
         return self.waltmin(I, J, val, qh, r, T, init_iters=init_iters, trim_c=0.0, seed=seed)
 
-    def waltmin(self, I, J, val, qhat, r, T, init_iters=30, trim_c=8.0, ridge=1e-10, seed=0):
+    def waltmin(self, I, J, val, qhat, r, T, init_iters=30, trim_c=8.0, ridge=1e-10, seed=0,
+                partition="reuse_all"):
+        """Alg. 2.  partition: "reuse_all" or "fresh_2t1" (line 3,
+        2T+1 random subsets; R11)."""
         dev = self.device
         U = torch.empty(self.n1, r, dtype=torch.float32, device=dev)
         V = torch.empty(self.n2, r, dtype=torch.float32, device=dev)
-        w = _lib.WaltminDesc(r, T, _lib.PART_REUSE_ALL, init_iters, trim_c, ridge, seed)
+        part = {"reuse_all": _lib.PART_REUSE_ALL, "fresh_2t1": _lib.PART_FRESH_2T1}[partition]
+        w = _lib.WaltminDesc(r, T, part, init_iters, trim_c, ridge, seed)
         st = self.lib.smp_waltmin(self.h, _ptr(I), _ptr(J), _ptr(val), _ptr(qhat), I.numel(),
                                   ctypes.byref(w), _ptr(U), _ptr(V))
         self._check(st, "smp_waltmin")
         return U, V
 
 
+def lela(A, B, r, m, T, seed=0, wm_seed=None, init_iters=30, trim_c=8.0, ridge=1e-10, a_is_b=False,
+         partition="reuse_all", row_block=None):
+    """LELA (the paper's two-pass comparison system) on
+    device-resident dense A (and B), through the same C ABI: pass 1 exact
+    column norms, Ω and q̂ by Eq. 1 (the SMP-PCA sampler), pass 2 exact
+    entries (AᵀB)_Ω, WAltMin.  row_block streams each pass in row blocks."""
+    inp = IN_DENSE_BF16 if A.dtype == torch.bfloat16 else IN_DENSE_F32
+    d = A.shape[0]
+    n2 = A.shape[1] if a_is_b else B.shape[1]
+    sk = SMPSketch(d, A.shape[1], n2, 1, pi=PI_RADEMACHER, seed=seed, a_is_b=a_is_b, input=inp,
+                   device=A.device)
+    rb = d if row_block is None else int(row_block)
+    try:
+        for r0 in range(0, d, rb):
+            sk.norms_block(r0, A[r0:r0 + rb], None if a_is_b else B[r0:r0 + rb])
+        fin = sk.finalize()
+        I, J, _, qh = sk.sample_estimate(m, seed)
+        acc = torch.zeros(I.numel(), dtype=torch.float64, device=A.device)
+        for r0 in range(0, d, rb):
+            sk.exact_entries_block(r0, A[r0:r0 + rb], None if a_is_b else B[r0:r0 + rb], I, J, acc)
+        val = acc.float()
+        U, V = sk.waltmin(I, J, val, qh, r, T, init_iters=init_iters, trim_c=trim_c, ridge=ridge,
+                          seed=seed if wm_seed is None else wm_seed, partition=partition)
+        fin.update(I=I, J=J, val=val, acc=acc, qhat=qh, U=U, V=V, launches=sk.kernel_launches)
+        return fin
+    finally:
+        sk.close()
+
+
 def smp_pca(A, B, k, r, m, T, pi=PI_RADEMACHER, seed=0, omega_seed=None, wm_seed=None,
             init_iters=30, trim_c=8.0, ridge=1e-10, a_is_b=False, plain=False, row0=0,
-            d_total=None):
+            d_total=None, sampler="bernoulli", partition="reuse_all"):
     """Alg. 1 end to end on device-resident dense A (and B): returns a dict
     with the finalized sketch state, Ω, M̃, q̂ and the factors (U, V)."""
     inp = IN_DENSE_BF16 if A.dtype == torch.bfloat16 else IN_DENSE_F32
@@ -214,9 +268,10 @@ def smp_pca(A, B, k, r, m, T, pi=PI_RADEMACHER, seed=0, omega_seed=None, wm_seed
     try:
         sk.block(row0, A, None if a_is_b else B)
         fin = sk.finalize()
-        I, J, val, qh = sk.sample_estimate(m, seed if omega_seed is None else omega_seed, plain=plain)
+        I, J, val, qh = sk.sample_estimate(m, seed if omega_seed is None else omega_seed, plain=plain,
+                                           sampler=sampler)
         U, V = sk.waltmin(I, J, val, qh, r, T, init_iters=init_iters, trim_c=trim_c, ridge=ridge,
-                          seed=seed if wm_seed is None else wm_seed)
+                          seed=seed if wm_seed is None else wm_seed, partition=partition)
         fin.update(I=I, J=J, val=val, qhat=qh, U=U, V=V, launches=sk.kernel_launches)
         return fin
     finally:

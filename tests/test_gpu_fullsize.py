@@ -5,8 +5,12 @@ checked against the CPU oracle on sampled outputs it can compute exactly:
   * sketch columns Ã_i, B̃_j for a sample of columns over the full d
     (columns are independent, so this is exact per column; SURVEY §7.2-9);
   * their column norms;
-  * cfg1 and cfg3: Ω bit-exact over all n1·n2 pairs from the oracle's own
-    full column norms, and M̃ on Ω ∩ (sampled A columns × sampled B columns).
+  * cfg1-cfg4: Ω bit-exact over all n1·n2 pairs from the oracle's own full
+    column norms, and M̃ on Ω ∩ (sampled A columns × sampled B columns);
+  * cfg1-cfg4: WAltMin (bench's r, T, init_iters) on identical inputs — the
+    GPU's Ω, M̃, q̂ fed to oracle.waltmin — with
+    ||UVᵀ_gpu − UVᵀ_or||_2 / ||AᵀB||_2 <= 1e-3, ||AᵀB||_2 of the implicit
+    product by power iteration (north-star factor tolerance).
 
 Tolerances as in test_gpu_parity.py.
 """
@@ -57,14 +61,61 @@ def _oracle_full_norms(X, block=1 << 16):
     return n2
 
 
+def _lowrank_diff_norm(U1, V1, U2, V2):
+    """||U1 V1ᵀ − U2 V2ᵀ||_2 from the factors (rank <= 2r, no n1 x n2 matrix)."""
+    Qa, Ra = np.linalg.qr(np.hstack([U1, U2]))
+    Qb, Rb = np.linalg.qr(np.hstack([V1, -V2]))
+    return np.linalg.norm(Ra @ Rb.T, 2)
+
+
+def _power_norm(matvec, rmatvec, n, iters=40, seed=0):
+    """||M||_2 of an implicit M (n columns) by power iteration on MᵀM."""
+    v = torch.randn(n, generator=torch.Generator().manual_seed(seed), dtype=torch.float64)
+    v /= v.norm()
+    lam = 0.0
+    for _ in range(iters):
+        w = rmatvec(matvec(v))
+        lam = float(w.norm())
+        v = w / lam
+    return math.sqrt(lam)
+
+
+def _dense_ops(A, B, chunk=1 << 18):
+    """x -> AᵀB x and y -> BᵀA y on device-resident row-major A, B (fp32
+    accumulation, fp64 vectors; test infrastructure, not the method)."""
+    dev = A.device
+
+    def mv(X, Y, x):  # Xᵀ (Y x)
+        xd = x.to(dev, torch.float32)
+        out = torch.zeros(X.shape[1], dtype=torch.float64, device=dev)
+        for r0 in range(0, X.shape[0], chunk):
+            t = Y[r0:r0 + chunk].float() @ xd
+            out += (X[r0:r0 + chunk].float().T @ t).double()
+        return out.cpu()
+    return (lambda x: mv(A, B, x)), (lambda y: mv(B, A, y))
+
+
+def _check_waltmin_identical(sk, cfg, I, J, val, qh, a2, FA, normM, tag):
+    """GPU WAltMin vs oracle WAltMin on the GPU's own Ω, M̃, q̂ (bench's r, T,
+    init_iters = 30, seed)."""
+    r, T, n1, n2 = cfg["r"], cfg["T"], cfg["n1"], cfg["n2"]
+    Ug, Vg = sk.waltmin(I, J, val, qh, r, T, init_iters=30, seed=cfg["seed"])
+    Uo, Vo = oracle.waltmin(n1, n2, r, T, I.cpu().numpy(), J.cpu().numpy(),
+                            val.cpu().double().numpy(), qh.cpu().numpy(), np.sqrt(a2), math.sqrt(FA),
+                            init_iters=30, seed=cfg["seed"])
+    err = _lowrank_diff_norm(Ug.cpu().double().numpy(), Vg.cpu().double().numpy(), Uo, Vo) / normM
+    assert err <= 1e-3, f"{tag}: factor parity {err:.3e}"
+    return err
+
+
 def _free(*xs):
     for x in xs:
         del x
     torch.cuda.empty_cache()
 
 
-@pytest.mark.parametrize("cfgname,ns,full_omega", [("cfg1", 16, True), ("cfg4", 12, False),
-                                                     ("cfg2", 8, False)])
+@pytest.mark.parametrize("cfgname,ns,full_omega", [("cfg1", 16, True), ("cfg4", 12, True),
+                                                     ("cfg2", 8, True)])
 def test_dense_full_size(cfgname, ns, full_omega):
     smp = _smp()
     cfg = synth.CONFIGS[cfgname]
@@ -92,7 +143,9 @@ def test_dense_full_size(cfgname, ns, full_omega):
 
     if full_omega:
         a2 = _oracle_full_norms(A)
-        b2 = _oracle_full_norms(B)
+        b2 = a2 if a_is_b else _oracle_full_norms(B)
+        if a_is_b:
+            cb, Bs, DB = ca, As, DA
         np.testing.assert_allclose(fin["a_norm2"].cpu().numpy(), a2, rtol=NORM_RTOL)
         np.testing.assert_allclose(fin["b_norm2"].cpu().numpy(), b2, rtol=NORM_RTOL)
         m = synth.m_of(cfg)
@@ -113,6 +166,10 @@ def test_dense_full_size(cfgname, ns, full_omega):
             scale = np.sqrt(a2[Ih[sel]] * b2[Jh[sel]])
             err = np.abs(val.cpu().double().numpy()[sel] - Mo) / scale
             assert err.max() <= 1e-4, err.max()
+        Bx = A if a_is_b else B
+        mv, rmv = _dense_ops(A, Bx)
+        normM = _power_norm(mv, rmv, n2)
+        _check_waltmin_identical(sk, cfg, I, J, val, qh, a2, oracle.pairwise_sum(a2), normM, cfgname)
     sk.close()
     _free(A, B)
 
@@ -175,5 +232,21 @@ def test_csr_full_size_cfg3():
     al, be = oracle.alpha_beta(a2, b2, oracle.pairwise_sum(a2), oracle.pairwise_sum(b2))
     Io, Jo, qo = oracle.sample(cfg["seed"], m, al, be)
     assert np.array_equal(I.cpu().numpy(), Io) and np.array_equal(J.cpu().numpy(), Jo)
+    # WAltMin on identical inputs; ||AᵀB||_2 by power iteration with CSR SpMVs
+    def csr_t(X, n):
+        rp, col, val = X
+        return torch.sparse_csr_tensor(rp, col.long(), val.double(), size=(d, n))
+    SA, SB = csr_t(A, n1), csr_t(B, n2)
+
+    SAc = SA.to_sparse_coo().t().coalesce()
+    SBc = SB.to_sparse_coo().t().coalesce()
+
+    def mv(x):
+        return torch.mv(SAc, torch.mv(SB, x.to(dev))).cpu()
+
+    def rmv(y):
+        return torch.mv(SBc, torch.mv(SA, y.to(dev))).cpu()
+    normM = _power_norm(mv, rmv, n2)
+    _check_waltmin_identical(sk, cfg, I, J, val, qh, a2, oracle.pairwise_sum(a2), normM, "cfg3")
     sk.close()
     _free(A, B)

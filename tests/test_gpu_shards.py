@@ -1,0 +1,81 @@
+"""Row sharding on ONE GPU: G handles, each
+restricted to its row range [row_begin, row_end) = shard_rows(d, G, g), sketch
+their own rows; their packed partials (smp_sketch_partials) are summed on the
+device — what the single NCCL all-reduce computes across GPUs — and one handle
+finalizes.  The result must equal the single-handle pass (sketch within 1e-5
+per column, norms within 1e-12, Ω bit-exact) and the oracle.  This runs the
+library's multi-GPU data path (row-ranged handles, partial buffers, combine,
+finalize) without a second GPU; the collective itself is covered by the gloo
+test (test_dist_cpu.py)."""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from paper_1610_06656_b200.dist import shard_rows
+from test_gpu_parity import NORM_RTOL, col_rel_err
+
+pytestmark = pytest.mark.gpu
+
+
+def _smp():
+    import paper_1610_06656_b200 as smp
+    return smp
+
+
+@pytest.mark.parametrize("G", [2, 4, 8])
+def test_row_sharded_handles_sum_to_single_pass(G):
+    smp = _smp()
+    d, n, k = 8 * synth.GEN_BLOCK, 256, 256
+    dev = torch.device("cuda", 0)
+    VA = synth.lowrank_factors(n, 20, 1, 0, dev)
+    VB = synth.lowrank_factors(n, 20, 1, 1, dev)
+    A, B = synth.lowrank_block(0, d, n, 1, VA, VB, device=dev)
+    # single pass
+    one = smp.SMPSketch(d, n, n, k, pi=smp.PI_RADEMACHER, seed=7, device=dev)
+    one.block(0, A, B)
+    f1 = one.finalize()
+    # G row-ranged handles, blocks delivered out of order inside each shard
+    hs = []
+    for g in range(G):
+        r0, r1 = shard_rows(d, G, g)
+        h = smp.SMPSketch(d, n, n, k, pi=smp.PI_RADEMACHER, seed=7, row_begin=r0, row_end=r1, device=dev)
+        mid = (r0 + r1) // 2
+        h.block(mid, A[mid:r1], B[mid:r1])
+        h.block(r0, A[r0:mid], B[r0:mid])
+        out = r1 if r1 < d else 0                  # a row outside [r0, r1)
+        with pytest.raises(smp.SmpError):          # rows outside the handle's range are rejected
+            h.block(out, A[out:out + 64], B[out:out + 64])
+        hs.append(h)
+    sk0, nr0 = hs[0].partials()
+    for h in hs[1:]:
+        sk, nr = h.partials()
+        sk0 += sk
+        nr0 += nr
+    fG = hs[0].finalize()
+    e = col_rel_err(fG["A_sk"], f1["A_sk"].cpu().double().numpy())
+    assert e.max() <= 1e-5, e.max()
+    e = col_rel_err(fG["B_sk"], f1["B_sk"].cpu().double().numpy())
+    assert e.max() <= 1e-5, e.max()
+    np.testing.assert_allclose(fG["a_norm2"].cpu().numpy(), f1["a_norm2"].cpu().numpy(), rtol=1e-12)
+    np.testing.assert_allclose(fG["b_norm2"].cpu().numpy(), f1["b_norm2"].cpu().numpy(), rtol=1e-12)
+    # oracle on a few columns over all d rows
+    cols = np.array([0, 17, 100, 255])
+    sub = A[:, torch.as_tensor(cols, device=dev)].contiguous()
+    skc, n2c = oracle.sketch_rows(0, 7, k, synth.bf16_bits(sub))
+    S, _, _ = oracle.finalize(k, skc, n2c)
+    assert col_rel_err(fG["A_sk"][torch.as_tensor(cols, device=dev)], S).max() <= 1e-5
+    np.testing.assert_allclose(fG["a_norm2"].cpu().numpy()[cols], n2c, rtol=NORM_RTOL)
+    # Ω from the combined handle == Ω from the single pass (bit-exact)
+    m = 4 * n * 5 * math.log(n)
+    I1, J1, v1, q1 = one.sample_estimate(m, 3)
+    IG, JG, vG, qG = hs[0].sample_estimate(m, 3)
+    assert torch.equal(I1, IG) and torch.equal(J1, JG)
+    scale = torch.sqrt(f1["a_norm2"][I1.long()] * f1["b_norm2"][J1.long()])
+    assert float(((v1.double() - vG.double()).abs() / scale).max()) <= 1e-4
+    for h in hs:
+        h.close()
+    one.close()

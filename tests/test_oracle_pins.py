@@ -1034,3 +1034,56 @@ def test_theorem1_implied_eta_below_one_and_shrinks():
              for c in (1.5, 3.0, 8.0)]
     assert eta_m[2] < 1.0
     assert eta_m[0] > eta_m[1] > eta_m[2], eta_m
+
+
+# ------------------------------------------------------------------ LELA (NEXT-3)
+def test_exact_entries_equal_matmul_and_block_additivity():
+    """LELA's pass 2 against the library matmul (AᵀB)[I, J]; fp32 and bf16
+    inputs read exactly; row blocks in any order sum to the whole."""
+    rng = np.random.default_rng(51)
+    d, n1, n2 = 700, 40, 30
+    A = rng.standard_normal((d, n1))
+    B = rng.standard_normal((d, n2))
+    I = rng.integers(0, n1, 200).astype(np.int32)
+    J = rng.integers(0, n2, 200).astype(np.int32)
+    ref = (A.T @ B)[I, J]
+    np.testing.assert_allclose(oracle.exact_entries(A, B, I, J), ref, rtol=1e-12, atol=1e-12)
+    out = np.zeros(200)
+    for r0, r1 in [(300, 700), (0, 120), (120, 300)]:
+        oracle.exact_entries(A[r0:r1], B[r0:r1], I, J, out)
+    np.testing.assert_allclose(out, ref, rtol=1e-12, atol=1e-12)
+    A32 = A.astype(np.float32)
+    Abf = (A32.view(np.uint32) >> 16).astype(np.uint16)
+    Aval = (Abf.astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+    np.testing.assert_allclose(oracle.exact_entries(Abf, B, I, J), (Aval.T @ B)[I, J], rtol=1e-12, atol=1e-12)
+    np.testing.assert_allclose(oracle.exact_entries(A32, B, I, J), (A32.astype(np.float64).T @ B)[I, J],
+                               rtol=1e-12, atol=1e-12)
+
+
+def test_lela_exact_rank_saturated_and_beats_smp_pca():
+    """LELA with saturated sampling on an exact rank-r product recovers it
+    (exact entries, full observation); on a noisy GD instance LELA's
+    error is at most SMP-PCA's ("LELA always achieves a smaller spectral
+    norm error than SMP-PCA"), both above the optimal rank-r error."""
+    rng = np.random.default_rng(52)
+    d, n, r = 300, 30, 3
+    Z = rng.standard_normal((d, r))
+    A = Z @ rng.standard_normal((r, n))
+    B = Z @ rng.standard_normal((r, n))
+    res = oracle.lela(A, B, r, 1e12, 5, trim_c=0.0)
+    assert len(res["I"]) == n * n
+    np.testing.assert_allclose(res["U"] @ res["V"].T, A.T @ B, rtol=1e-7, atol=1e-7 * np.abs(A.T @ B).max())
+    d, n, r = 2000, 80, 5
+    G = rng.standard_normal((d, n))
+    A = G * (1.0 / np.arange(1, n + 1))
+    M = A.T @ A
+    s = np.linalg.svd(M, compute_uv=False)
+    m = 4 * n * r * math.log(n)
+    el, es = [], []
+    for sd in range(3):
+        L = oracle.lela(A, A, r, m, 10, seed=sd)
+        S = oracle.smp_pca(A, A, k=128, r=r, m=m, T=10, pi_kind=oracle.PI_GAUSSIAN, seed=sd, a_is_b=True)
+        el.append(np.linalg.norm(L["U"] @ L["V"].T - M, 2) / s[0])
+        es.append(np.linalg.norm(S["U"] @ S["V"].T - M, 2) / s[0])
+    assert s[r] / s[0] <= np.median(el) + 1e-9
+    assert np.median(el) <= np.median(es) + 1e-9, (el, es)

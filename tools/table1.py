@@ -9,9 +9,12 @@ sketch size k = 2,000 — through the library's C ABI (fp32 inputs: K1F; the
 against ‖AᵀB‖₂ next to the optimal rank-r error σ_{r+1}/σ_1, both estimated
 by block power iteration on the implicit product (AᵀB is never formed; the
 evaluation uses torch GEMMs on the resident A, B — it is not part of the
-method).  Printed numbers: Optimal 0.0271, SMP-PCA 0.0280.
+method).  Printed numbers: Optimal 0.0271, LELA 0.0274,
+SMP-PCA 0.0280.  LELA (the two-pass comparison) runs through the same
+C ABI: pass 1 smp_norms_block, Ω by Eq. 1 (Bernoulli), pass 2
+smp_exact_entries_block, WAltMin.
 
-    python tools/table1.py [n] [k] [multinomial|bernoulli] [gaussian|srht|rademacher]
+    python tools/table1.py [n] [k] [multinomial|bernoulli] [gaussian|srht|rademacher] [lela|nolela]
 """
 import json
 import math
@@ -70,6 +73,7 @@ def main():
     sampler = sys.argv[3] if len(sys.argv) > 3 else "multinomial"
     pi_name = sys.argv[4] if len(sys.argv) > 4 else "gaussian"
     pi = {"gaussian": PI_GAUSSIAN, "srht": PI_SRHT, "rademacher": PI_RADEMACHER}[pi_name]
+    run_lela = (sys.argv[5] if len(sys.argv) > 5 else "lela") == "lela"
     d, r, T = n, 5, 10
     m = 4 * n * r * math.log(n)
     dev = torch.device("cuda", 0)
@@ -96,12 +100,37 @@ def main():
     w1.record()
     torch.cuda.synchronize()
     sk.close()
+    lela = None
+    if run_lela:
+        # LELA: two passes over A, same sampler and WAltMin
+        le = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+        sl = SMPSketch(d, n, n, 1, pi=PI_RADEMACHER, seed=7, a_is_b=True, input=IN_DENSE_F32, device=dev)
+        le[0].record()
+        sl.norms_block(0, A)
+        sl.finalize()
+        le[1].record()
+        Il, Jl, _, ql = sl.sample_estimate(m, 7)
+        le[2].record()
+        acc = torch.zeros(Il.numel(), dtype=torch.float64, device=dev)
+        sl.exact_entries_block(0, A, None, Il, Jl, acc)
+        le[3].record()
+        Ul, Vl = sl.waltmin(Il, Jl, acc.float(), ql, r, T, init_iters=30, seed=7)
+        le[4].record()
+        torch.cuda.synchronize()
+        sl.close()
+        lela = dict(omega=int(Il.numel()), ms={"pass1_norms": le[0].elapsed_time(le[1]),
+                                               "omega": le[1].elapsed_time(le[2]),
+                                               "pass2_exact_entries": le[2].elapsed_time(le[3]),
+                                               "waltmin": le[3].elapsed_time(le[4])})
     s = top_singular(A, B)
     nrm = float(s[0])
     opt = float(s[r]) / nrm
     err = err_norm(A, B, U, V) / nrm
+    if lela is not None:
+        lela["error"] = err_norm(A, B, Ul, Vl) / nrm
     out = dict(d=d, n=n, k=k, r=r, T=T, m=m, omega=int(I.numel()), sampler=sampler, pi=pi_name,
-               optimal=opt, smp_pca=err, paper={"optimal": 0.0271, "lela": 0.0274, "smp_pca": 0.0280},
+               optimal=opt, smp_pca=err, lela=lela,
+               paper={"optimal": 0.0271, "lela": 0.0274, "smp_pca": 0.0280},
                ms={"sketch+finalize": e[0].elapsed_time(e[1]), "omega+mtilde": e[1].elapsed_time(e[2]),
                    "waltmin": e[2].elapsed_time(e[3]), "waltmin_warm": w0.elapsed_time(w1)}, wall_s=wall)
     print(json.dumps(out), flush=True)

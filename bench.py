@@ -238,6 +238,34 @@ def config_dict(cfgname, cfg, args, world, extra=None):
     return out
 
 
+def oracle_rest_seconds(fin, cfg, m, args):
+    """Time the oracle's steps after the pass (finalize, Ω, M̃, WAltMin) on the
+    workload's full n-sized data — the finalized GPU sketch and norms as its
+    input data (values are not compared here) — for metric part 2's CPU
+    counterpart.  Returns (seconds, |Ω|)."""
+    import oracle
+    k = cfg["k"]
+    t0 = time.perf_counter()
+    skA = fin["A_sk"].double().cpu().numpy() * math.sqrt(k)
+    skB = fin["B_sk"].double().cpu().numpy() * math.sqrt(k)
+    a2 = fin["a_norm2"].cpu().numpy().copy()
+    b2 = fin["b_norm2"].cpu().numpy().copy()
+    t0 = time.perf_counter()
+    As, _, DA = oracle.finalize(k, skA, a2)
+    Bs, _, DB = oracle.finalize(k, skB, b2)
+    FA, FB = oracle.pairwise_sum(a2), oracle.pairwise_sum(b2)
+    al, be = oracle.alpha_beta(a2, b2, FA, FB)
+    if args.sampler == "multinomial":
+        I, J, q = oracle.sample_multinomial(cfg["seed"], m, al, be)
+    else:
+        I, J, q = oracle.sample(cfg["seed"], m, al, be)
+    Mt = oracle.estimate(k, I, J, As, Bs, DA, DB)
+    oracle.waltmin(len(a2), len(b2), cfg["r"], cfg["T"], I, J, Mt, q, np.sqrt(a2), math.sqrt(FA),
+                   init_iters=args.init_iters, seed=cfg["seed"],
+                   partition=1 if args.partition == "fresh_2t1" else 0)
+    return time.perf_counter() - t0, len(I)
+
+
 def run_reference(args, cfgname, cfg, world, rank):
     if rank != 0:
         return
@@ -519,6 +547,16 @@ def main():
         rate, info = oracle_sample_rate(cfgname, cfg, 20.0)
         cpu = {"value": rate, "unit": "GB/s", "cores": info["cores"], "kind": "oracle",
                "sample": info["sample"]}
+        if not csr:
+            # metric part 2 on the CPU: the pass extrapolated from the sampled
+            # rate, the n-sized steps (finalize, Ω, M̃, WAltMin) run in full
+            sk.reset()
+            sk.block(r0, A, B)
+            fin = sk.finalize()
+            rest, nom = oracle_rest_seconds(fin, cfg, m, args)
+            cpu["smp_pca_sec"] = total_bytes / (rate * 1e9) + rest
+            cpu["smp_pca_sec_parts"] = {"pass_extrapolated_s": total_bytes / (rate * 1e9),
+                                        "finalize_omega_mtilde_waltmin_s": rest, "omega": nom}
 
     if rank == 0:
         out = {

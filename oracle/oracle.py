@@ -204,9 +204,12 @@ def pairwise_sum(x) -> float:
 
 
 def finalize(k, sk, norm2):
-    """Scale by 1/sqrt(k) (N(0,1/k)); ||Ã_i||; D = ||X_i|| / ||Ã_i||."""
+    """Scale by 1/sqrt(k) (N(0,1/k)); ||Ã_i||; D = ||X_i|| / ||Ã_i||.
+    norm2 is flushed IN PLACE where below 2^-200 (R25) when it is a float64
+    array (the caller's a2 then feeds Eq. 1 with the same zero)."""
     sk = _c(sk, np.float64)
-    norm2 = _c(norm2, np.float64)
+    if not (isinstance(norm2, np.ndarray) and norm2.dtype == np.float64 and norm2.flags.c_contiguous):
+        norm2 = _c(norm2, np.float64)
     n = sk.shape[0]
     out = np.empty_like(sk)
     sknorm = np.empty(n, np.float64)
@@ -367,9 +370,9 @@ def smp_pca(A, B, k, r, m, T, pi_kind=PI_RADEMACHER, seed=0, omega_seed=None,
         skB, b2 = skA, a2
     else:
         skB, b2 = sketch_rows(pi_kind, seed, k, B)
-    FA, FB = pairwise_sum(a2), pairwise_sum(b2)
-    Ask, As, DA = finalize(k, skA, a2)
+    Ask, As, DA = finalize(k, skA, a2)    # flushes a2 < 2^-200 in place (R25)
     Bsk, Bs, DB = finalize(k, skB, b2)
+    FA, FB = pairwise_sum(a2), pairwise_sum(b2)
     al, be = alpha_beta(a2, b2, FA, FB)
     if sampler == "multinomial":
         I, J, q = sample_multinomial(omega_seed, m, al, be)

@@ -360,7 +360,9 @@ double or_pairwise_sum(const double *x, int64_t n)
 
 /* Scales the unscaled sketch sk (n x k) by 1/sqrt(k) into out (n x k),      */
 /* and computes sknorm[c] = ||Ã_c|| and D[c] = ||X_c|| / ||Ã_c|| (0 if 0).  */
-void or_finalize(int k, int64_t n, const double *sk, const double *norm2,
+/* DESIGN.md R25: a column whose norm² is below 2^-200 is the zero column     */
+/* (norm2[c] is set to 0, so Eq. 1 and D see an exact zero).                 */
+void or_finalize(int k, int64_t n, const double *sk, double *norm2,
                  double *out, double *sknorm, double *D)
 {
     double scale = 1.0 / sqrt((double)k);
@@ -371,6 +373,7 @@ void or_finalize(int k, int64_t n, const double *sk, const double *norm2,
             out[c * k + kp] = v;
             s2 += v * v;
         }
+        if (norm2[c] < 0x1p-200) norm2[c] = 0.0;
         sknorm[c] = sqrt(s2);
         D[c] = sknorm[c] > 0.0 ? sqrt(norm2[c]) / sknorm[c] : 0.0;
     }

@@ -36,7 +36,7 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False, defines=(), out: str = None) -> str:
+def build(force: bool = False, verbose: bool = False, defines=(), out: str = None, only=()) -> str:
     """Compile csrc/*.cu (in parallel) and link libsmp.so.  `defines` and
     `out` produce tuning variants (e.g. libsmp_x4p3.so) next to the default."""
     out = out or LIB
@@ -48,13 +48,24 @@ def build(force: bool = False, verbose: bool = False, defines=(), out: str = Non
     os.makedirs(objdir, exist_ok=True)
     dflags = [f"-D{d}" for d in defines]
     procs = []
+    default_objs = os.path.join(PKG, "build", "libsmp")
     for src in sources():
         obj = os.path.join(objdir, os.path.basename(src).replace(".cu", ".o"))
+        if only and os.path.basename(src) not in only:
+            # tuning variant: reuse the default build's object for this source
+            ref = os.path.join(default_objs, os.path.basename(obj))
+            if not os.path.exists(ref):
+                raise RuntimeError(f"variant build needs the default object {ref}")
+            procs.append((src, ref, None))
+            continue
         cmd = [nvcc, *NVCC_FLAGS, *dflags, "-c", src, "-o", obj, "-I", os.path.join(ROOT, "include")]
         procs.append((src, obj, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE,
                                                  text=True)))
     objs = []
     for src, obj, pr in procs:
+        if pr is None:
+            objs.append(obj)
+            continue
         so, se = pr.communicate()
         if pr.returncode != 0:
             sys.stderr.write(so + se)
@@ -73,5 +84,7 @@ if __name__ == "__main__":
     args = [a for a in sys.argv[1:] if not a.startswith("--")]
     defs = [a[2:] for a in args if a.startswith("-D")]
     outs = [a for a in sys.argv[1:] if a.startswith("--out=")]
+    only = [a[7:] for a in sys.argv[1:] if a.startswith("--only=")]
     print(build(force="--force" in sys.argv or bool(defs), verbose="--quiet" not in sys.argv,
-                defines=defs, out=os.path.join(PKG, outs[0][6:]) if outs else None))
+                defines=defs, out=os.path.join(PKG, outs[0][6:]) if outs else None,
+                only=tuple(x for o in only for x in o.split(","))))

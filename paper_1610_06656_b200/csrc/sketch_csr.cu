@@ -205,13 +205,26 @@ csr_accumulate_kernel(const uint32_t* __restrict__ keys, const float* __restrict
         }
         const float v = vv[u];
         nrm = fma((double)v, (double)v, nrm);
+        const uint32_t vbits = __float_as_uint(v);
+        if ((vbits & 0xFFFFu) == 0u) {
+          // v is bf16-exact (e.g. integer counts < 256): v·π is exact and one
+          // FHFMA.BF16 per entry accumulates it in fp32 without unpacking π
+          const uint32_t vb = vbits >> 16;
 #pragma unroll
-        for (int i = 0; i < KV; ++i) {
-          const uint32_t w[4] = {q[u][i].x, q[u][i].y, q[u][i].z, q[u][i].w};
+          for (int i = 0; i < KV; ++i) {
+            const uint32_t w[4] = {q[u][i].x, q[u][i].y, q[u][i].z, q[u][i].w};
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            acc[i][2 * j] = fmaf(v, __uint_as_float(w[j] << 16), acc[i][2 * j]);
-            acc[i][2 * j + 1] = fmaf(v, __uint_as_float(w[j] & 0xFFFF0000u), acc[i][2 * j + 1]);
+            for (int j = 0; j < 4; ++j) fma_bf16s_x2_f32(vb, w[j], acc[i][2 * j], acc[i][2 * j + 1]);
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < KV; ++i) {
+            const uint32_t w[4] = {q[u][i].x, q[u][i].y, q[u][i].z, q[u][i].w};
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              acc[i][2 * j] = fmaf(v, __uint_as_float(w[j] << 16), acc[i][2 * j]);
+              acc[i][2 * j + 1] = fmaf(v, __uint_as_float(w[j] & 0xFFFF0000u), acc[i][2 * j + 1]);
+            }
           }
         }
       }

@@ -11,8 +11,8 @@
 // that run on both SMs.  Per SM:
 //   * X half tile (64 rows × 128 cols bf16) arrives by TMA as two 64×64
 //     128B-swizzled boxes: the B operand, MN-major (8-stage SMEM ring).
-//   * Π half tile (128 κ × 64 t) is regenerated from the Philox hash by 4
-//     generator warps and written straight into TMEM with tcgen05.st: the A
+//   * Π half tile (128 κ × 64 t) is regenerated from the Philox hash by 2
+//     sets of 4 generator warps and written straight into TMEM with tcgen05.st: the A
 //     operand lives in TMEM (4-stage ring of 32 columns), so Π costs no SMEM
 //     bandwidth and is stored nowhere else.
 //   * 8 norm warps read the X stage once from SMEM: exact fp32 squares
@@ -54,8 +54,9 @@ constexpr int PI_COLS = TC_BK / 2;                // 64 bf16 per lane = 32 colum
 constexpr int TMEM_COLS = 512;
 static_assert(ACC_COLS + PI_STAGES * PI_COLS <= TMEM_COLS, "TMEM budget");
 // Warp roles: 0 TMA, 1 MMA (leader) + TMEM alloc, 2 relay, 3 spare,
-// 4..7 and 16..19 Π generators (two per TMEM lane quadrant, one per 32-row
-// half of a K-block), 8..15 norm warps + TMEM epilogue.
+// 4..7 and 16..19 Π generators (two sets, one warp per TMEM lane quadrant
+// each; the sets take alternate pairs of K-blocks), 8..15 norm warps + TMEM
+// epilogue.
 constexpr int NUM_GEN_WARPS = 8;
 constexpr int NUM_NORM_WARPS = 8;                 // warps 8..15
 constexpr int NORM_RG = (32 * NUM_NORM_WARPS) / 16;   // row groups (16 chunks per row)
@@ -198,7 +199,7 @@ sketch_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant
       mbar_init(&ready[s], 2);
     }
     for (int s = 0; s < PI_STAGES; ++s) {
-      mbar_init(&pfull[s], NUM_GEN_WARPS);
+      mbar_init(&pfull[s], NUM_GEN_WARPS / 2);   // one set of 4 warps writes a stage
       mbar_init(&pempty[s], 1);
     }
     mbar_init(tmem_full, 1);
@@ -267,39 +268,62 @@ sketch_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant
       }
     }
   } else if ((warp >= 4 && warp < 8) || warp >= 16) {
-    // ---------------- Π generators: thread owns TMEM lane 32*quad + lane,
-    // rows 32*half .. 32*half+31 of every K-block (idle in PANEL mode: Π
-    // arrives by TMA)
+    // ---------------- Π generators: thread owns TMEM lane 32*quad + lane (one
+    // κ); set 0 (warps 4..7) and set 1 (warps 16..19) take alternate PAIRS of
+    // K-blocks (2jp, 2jp+1), all 64 rows of each, so that one Philox call
+    // (128 rows of one κ) serves the whole pair when the rows are 128-aligned;
+    // the next pair's call is issued between the TMEM store and its wait, so
+    // its latency overlaps the store (idle in PANEL mode: Π arrives by TMA)
     if (PANEL) goto role_done;
     const int quad = warp & 3;
-    const int half = warp >= 16 ? 1 : 0;
+    const int set = warp >= 16 ? 1 : 0;
     const int kl = 32 * quad + lane;
     const int kappa = kappa0 + kl;
+    const bool valid = kappa < p.k;
+    const uint32_t k0 = (uint32_t)p.seed, k1 = (uint32_t)(p.seed >> 32);
     RadCache rc{~0ull, 0, 0, 0, 0};
     uint64_t srht_s = 0;
     uint32_t srht_walsh = 0;
-    if (p.kind >= PI_SRHT_BASE && kappa < p.k) {
+    if (p.kind >= PI_SRHT_BASE && valid) {
       srht_s = srht_row(p.seed, p.kind - PI_SRHT_BASE, (uint32_t)kappa);
       srht_walsh = walsh32_interleaved((uint32_t)(srht_s & 31u));
     }
-    for (int it = 0; it < nkb; ++it) {
-      const int ps = it % PI_STAGES;
-      const uint64_t t0 = (uint64_t)p.row0 + (uint64_t)(kb_begin + it) * TC_BK + 32 * half;
-      uint32_t o[16];
-      if (p.debug & 2) {
+    const bool word_kind = p.kind == PI_RADEMACHER || p.kind >= PI_SRHT_BASE;
+    const uint32_t taddr = tbase + ((uint32_t)(32 * quad) << 16) + ACC_COLS;
+    for (int jp = set; 2 * jp < nkb; jp += 2) {
+      for (int h = 0; h < 2; ++h) {
+        const int it = 2 * jp + h;
+        if (it >= nkb) break;
+        const int ps = it % PI_STAGES;
+        const uint64_t t0 = (uint64_t)p.row0 + (uint64_t)(kb_begin + it) * TC_BK;
+        uint32_t o[16], o2[16];
+        if (p.debug & 2) {
 #pragma unroll
-        for (int i = 0; i < 16; ++i) o[i] = 0x3F803F80u;
-      } else {
-        gen_pi_half(p.kind, p.seed, (uint32_t)kappa, kappa < p.k, t0, rc, o, srht_s, srht_walsh);
+          for (int i = 0; i < 16; ++i) o[i] = o2[i] = 0x3F803F80u;
+        } else {
+          gen_pi_half(p.kind, p.seed, (uint32_t)kappa, valid, t0, rc, o, srht_s, srht_walsh);
+          gen_pi_half(p.kind, p.seed, (uint32_t)kappa, valid, t0 + 32, rc, o2, srht_s, srht_walsh);
+        }
+        mbar_wait(&pempty[ps], ((uint32_t)(it / PI_STAGES) & 1u) ^ 1u);
+        tc_fence_after();
+        tmem_st_32x32b_x16(taddr + ps * PI_COLS, o);
+        tmem_st_32x32b_x16(taddr + ps * PI_COLS + 16, o2);
+        if (h == 1 || it + 1 == nkb) {
+          // prefetch the Philox words of this set's next pair
+          const int itn = 2 * (jp + 2);
+          if (word_kind && valid && itn < nkb && !(p.debug & 2)) {
+            const uint64_t tn = (uint64_t)p.row0 + (uint64_t)(kb_begin + itn) * TC_BK;
+            if ((tn & 31) == 0) {
+              if (p.kind == PI_RADEMACHER) (void)rad_word(rc, tn >> 5, (uint32_t)kappa, k0, k1);
+              else (void)rad_word(rc, tn >> 5, 0u, k0, k1, TAG_SRHT_D);
+            }
+          }
+        }
+        tc_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&pfull[ps]);
       }
-      mbar_wait(&pempty[ps], ((uint32_t)(it / PI_STAGES) & 1u) ^ 1u);
-      tc_fence_after();
-      tmem_st_32x32b_x16(
-          tbase + ((uint32_t)(32 * quad) << 16) + ACC_COLS + ps * PI_COLS + 16 * half, o);
-      tc_wait_st();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&pfull[ps]);
     }
   } else if (warp >= 8) {
     // ---------------- norm warps (fp64 Σx²), then TMEM epilogue
@@ -332,22 +356,16 @@ sketch_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant
         }
         // exact fp32 squares (bf16 has 8 significant bits), summed over the
         // thread's NORM_ROWS rows in fp32, then one fp64 add per column
-        // (R4: relative error <= 3·2^-24 worst case per chunk)
+        // (R4: relative error <= 3·2^-24 worst case per chunk);
+        // one FHFMA.BF16 per element (no unpack)
         float sq[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) sq[e] = 0.f;
 #pragma unroll
         for (int rr = 0; rr < NORM_ROWS; ++rr) {
           const uint32_t w[4] = {v[rr].x, v[rr].y, v[rr].z, v[rr].w};
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const float lo = __uint_as_float(w[e] << 16), hi = __uint_as_float(w[e] & 0xFFFF0000u);
-            if (rr == 0) {
-              sq[2 * e] = __fmul_rn(lo, lo);
-              sq[2 * e + 1] = __fmul_rn(hi, hi);
-            } else {
-              sq[2 * e] = __fmaf_rn(lo, lo, sq[2 * e]);
-              sq[2 * e + 1] = __fmaf_rn(hi, hi, sq[2 * e + 1]);
-            }
-          }
+          for (int e = 0; e < 4; ++e) fma_bf16x2_f32(w[e], w[e], sq[2 * e], sq[2 * e + 1]);
         }
 #pragma unroll
         for (int e = 0; e < 8; ++e) acc[e] += (double)sq[e];

@@ -164,6 +164,28 @@ __device__ __forceinline__ uint16_t pi_bits(int kind, uint64_t seed, uint32_t ka
 
 __device__ __forceinline__ float bf16_bits_to_float(uint32_t b) { return __uint_as_float(b << 16); }
 
+// ---------------------------------------------------------------- mixed-precision FMA
+// acc + lo(x)·lo(y) and acc + hi(x)·hi(y) for packed bf16 pairs, accumulated
+// in fp32 with one rounding (fma.rn.f32.bf16 -> FHFMA.BF16 with .H0/.H1
+// operand selection: no unpack instructions).  A bf16 × bf16 product has at
+// most 16 significant bits, so it is exact and each step equals
+// fmaf(float(a), float(b), acc) bit for bit.
+__device__ __forceinline__ void fma_bf16x2_f32(uint32_t x, uint32_t y, float& acc_lo, float& acc_hi) {
+  asm("{\n\t.reg .b16 xl, xh, yl, yh;\n\t"
+      "mov.b32 {xl, xh}, %2;\n\tmov.b32 {yl, yh}, %3;\n\t"
+      "fma.rn.f32.bf16 %0, xl, yl, %0;\n\tfma.rn.f32.bf16 %1, xh, yh, %1;\n\t}"
+      : "+f"(acc_lo), "+f"(acc_hi)
+      : "r"(x), "r"(y));
+}
+// acc + v·lo(y), acc + v·hi(y) for a bf16 scalar v (in the low half of vb)
+__device__ __forceinline__ void fma_bf16s_x2_f32(uint32_t vb, uint32_t y, float& acc_lo, float& acc_hi) {
+  asm("{\n\t.reg .b16 vl, vh, yl, yh;\n\t"
+      "mov.b32 {vl, vh}, %2;\n\tmov.b32 {yl, yh}, %3;\n\t"
+      "fma.rn.f32.bf16 %0, vl, yl, %0;\n\tfma.rn.f32.bf16 %1, vl, yh, %1;\n\t}"
+      : "+f"(acc_lo), "+f"(acc_hi)
+      : "r"(vb), "r"(y));
+}
+
 // ---------------------------------------------------------------- PTX: misc
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));

@@ -139,12 +139,14 @@ def test_zero_and_sparse_columns():
     A[:, 3] = 0.0
     A[:, 5] = 0.0
     A[100, 5] = 2.5
+    A[:, 7] = 2.0 ** -110          # norm² ~ 2^-210: the zero column of R25 on both sides
     A = A.to(torch.bfloat16)
     B = synth.gaussian_small(d, n, seed=14).to(torch.bfloat16)
     sk, fin = gpu_sketch(A, B, k, 0, seed=1)
     orc = oracle_sketch(A, B, k, 0, seed=1)
     check_sketch(fin, orc)
     assert float(fin["a_norm2"][3]) == 0.0 and float(fin["a_norm2"][5]) == 6.25
+    assert float(fin["a_norm2"][7]) == 0.0 and orc["a2"][7] == 0.0
     I, J, val, qh = sk.sample_estimate(500.0, 4)
     al, be = oracle.alpha_beta(orc["a2"], orc["b2"], orc["FA"], orc["FB"])
     Io, Jo, qo = oracle.sample(4, 500.0, al, be)

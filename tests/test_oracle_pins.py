@@ -1087,3 +1087,16 @@ def test_lela_exact_rank_saturated_and_beats_smp_pca():
         es.append(np.linalg.norm(S["U"] @ S["V"].T - M, 2) / s[0])
     assert s[r] / s[0] <= np.median(el) + 1e-9
     assert np.median(el) <= np.median(es) + 1e-9, (el, es)
+
+
+def test_finalize_flushes_negligible_norms_r25():
+    """R25: a column whose norm² is below 2^-200 is the zero column: D = 0 and
+    its norm² becomes an exact 0 (so Eq. 1 gives α = 0); a column just above
+    the threshold keeps its value."""
+    k = 8
+    sk = np.ones((3, k))
+    norm2 = np.array([2.0 ** -210, 2.0 ** -190, 4.0])
+    out, sn, D = oracle.finalize(k, sk, norm2)
+    assert norm2[0] == 0.0 and D[0] == 0.0
+    assert norm2[1] == 2.0 ** -190 and D[1] > 0
+    np.testing.assert_allclose(D[2], 2.0 / np.sqrt(k * (1.0 / k)), rtol=1e-15)

@@ -91,6 +91,64 @@ __global__ void pi_panel_kernel(int kind, uint64_t seed, int k, int kp, int64_t 
   }
 }
 
+// K3a' (Gaussian Π with a tensor-core head): one generation of a 32-row ×
+// 64-κ tile into SMEM, written out in BOTH layouts — row-major for the tail
+// (pi[(t - t0) * kp + κ], κ < kp) and κ-major for K1's head panel
+// (kmaj[κ * ld + t_off + t - t0], κ < kpad) — with coalesced stores on both
+// sides (no second pass over the panel).  t0 % 4 == 0.
+constexpr int DUAL_ROWS = 32, DUAL_K = 64;
+__global__ void __launch_bounds__(256)
+pi_panel_dual_kernel(uint64_t seed, int k, int kp, int kpad, int64_t t0, int rows, uint16_t* __restrict__ pi,
+                     uint16_t* __restrict__ kmaj, int64_t ld, int64_t t_off) {
+  __shared__ uint16_t tile[DUAL_ROWS][DUAL_K + 2];
+  const int tid = threadIdx.x;
+  const int r0 = blockIdx.x * DUAL_ROWS, c0 = blockIdx.y * DUAL_K;
+  const uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
+  {
+    const int kq = tid & (DUAL_K - 1);
+    const int kappa = c0 + kq;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int g = (tid >> 6) + 4 * h;              // 4-row group 0..7 of the tile
+      const int rt = r0 + 4 * g;
+      uint16_t z[4] = {0, 0, 0, 0};
+      if (kappa < k && rt < rows) {
+        const uint64_t tq = (uint64_t)(t0 + rt) >> 2;
+        const u32x4 w = philox4x32_10((uint32_t)tq, (uint32_t)kappa, (uint32_t)(tq >> 32), TAG_GAUSSIAN, k0, k1);
+        gauss_pair(w.x, w.y, z[0], z[1]);
+        gauss_pair(w.z, w.w, z[2], z[3]);
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) tile[4 * g + j][kq] = z[j];
+    }
+  }
+  __syncthreads();
+  // row-major: 32 rows x 64 κ, 4-byte stores (2 κ), 128 B per row
+  for (int e = tid; e < DUAL_ROWS * (DUAL_K / 2); e += blockDim.x) {
+    const int r = e / (DUAL_K / 2), cp = e % (DUAL_K / 2);
+    const int kappa = c0 + 2 * cp;
+    if (r0 + r < rows && kappa < kp)
+      *reinterpret_cast<uint32_t*>(pi + (int64_t)(r0 + r) * kp + kappa) =
+          *reinterpret_cast<const uint32_t*>(&tile[r][2 * cp]);
+  }
+  // κ-major: 64 κ x 32 rows, 4-byte stores (2 rows), 64 B per κ
+  if (kmaj) {
+    for (int e = tid; e < DUAL_K * (DUAL_ROWS / 2); e += blockDim.x) {
+      const int c = e / (DUAL_ROWS / 2), rp2 = e % (DUAL_ROWS / 2);
+      const int kappa = c0 + c, r = r0 + 2 * rp2;
+      if (kappa < kpad && r < rows) {
+        uint16_t* dst = kmaj + (int64_t)kappa * ld + t_off + r;
+        const uint32_t v = (uint32_t)tile[2 * rp2][c] | ((uint32_t)tile[2 * rp2 + 1][c] << 16);
+        if (r + 1 < rows && ((reinterpret_cast<uintptr_t>(dst) & 3) == 0)) *reinterpret_cast<uint32_t*>(dst) = v;
+        else {
+          dst[0] = (uint16_t)v;
+          if (r + 1 < rows) dst[1] = (uint16_t)(v >> 16);
+        }
+      }
+    }
+  }
+}
+
 // ---------------------------------------------------------------- K3b
 // keys[o] = (c_glob << tbits) | (t - p0), vals[o] = v for the nonzeros of
 // rows [p0, p0 + rows) of one matrix; warp per row; o = (entry index
@@ -245,6 +303,12 @@ __device__ __forceinline__ bool is_4bit(float v) {
 __device__ __forceinline__ bool is_head(const int32_t* __restrict__ lut, uint32_t cg, float v) {
   return lut != nullptr && lut[cg] >= 0 && is_4bit(v);
 }
+// same test with the head-column flags staged in SMEM (hfl != nullptr)
+__device__ __forceinline__ bool is_head_s(const int32_t* __restrict__ lut, const uint8_t* hfl, uint32_t cg,
+                                          float v) {
+  if (lut == nullptr) return false;
+  return (hfl ? hfl[cg] != 0 : lut[cg] >= 0) && is_4bit(v);
+}
 
 // ---------------------------------------------------------------- K3c counting sort
 // CTA b owns panel rows [b·rows/G, (b+1)·rows/G) of both matrices.
@@ -262,10 +326,14 @@ __global__ void __launch_bounds__(CSR_T_THREADS)
 csr_hist_kernel(const int64_t* __restrict__ arp, const int32_t* __restrict__ acol,
                 const float* __restrict__ aval, int64_t a_n, const int64_t* __restrict__ brp,
                 const int32_t* __restrict__ bcol, const float* __restrict__ bval, int64_t b_n,
-                int64_t p0, int rows, int ntot, const int32_t* __restrict__ lut,
+                int64_t p0, int rows, int ntot, const int32_t* __restrict__ lut, int sflags,
                 uint32_t* __restrict__ histT) {
   extern __shared__ uint32_t hist[];
-  for (int c = threadIdx.x; c < ntot; c += blockDim.x) hist[c] = 0u;
+  uint8_t* hfl = (lut && sflags) ? reinterpret_cast<uint8_t*>(hist + ntot) : nullptr;
+  for (int c = threadIdx.x; c < ntot; c += blockDim.x) {
+    hist[c] = 0u;
+    if (hfl) hfl[c] = lut[c] >= 0 ? 1 : 0;
+  }
   __syncthreads();
   int r0, r1;
   cta_rows(rows, r0, r1);
@@ -292,7 +360,7 @@ csr_hist_kernel(const int64_t* __restrict__ arp, const int32_t* __restrict__ aco
         for (int u = 0; u < 4; ++u)
           if (eb + 32 * u < e1) {
             const uint32_t cg = (uint32_t)(c[u] < 0 || c[u] >= ncols ? 0 : c[u]) + cofs;
-            if (!is_head(lut, cg, v[u])) atomicAdd(&hist[cg], 1u);
+            if (!is_head_s(lut, hfl, cg, v[u])) atomicAdd(&hist[cg], 1u);
           }
       }
     }
@@ -306,11 +374,15 @@ __global__ void __launch_bounds__(CSR_T_THREADS)
 csr_scatter_kernel(const int64_t* __restrict__ arp, const int32_t* __restrict__ acol,
                    const float* __restrict__ aval, int64_t a_n, const int64_t* __restrict__ brp,
                    const int32_t* __restrict__ bcol, const float* __restrict__ bval, int64_t b_n,
-                   int64_t p0, int rows, int ntot, int tbits, const int32_t* __restrict__ lut,
+                   int64_t p0, int rows, int ntot, int tbits, const int32_t* __restrict__ lut, int sflags,
                    const uint32_t* __restrict__ offsT, uint32_t* __restrict__ keys,
                    float* __restrict__ vals, int* __restrict__ status) {
   extern __shared__ uint32_t cur[];
-  for (int c = threadIdx.x; c < ntot; c += blockDim.x) cur[c] = offsT[(int64_t)c * gridDim.x + blockIdx.x];
+  uint8_t* hfl = (lut && sflags) ? reinterpret_cast<uint8_t*>(cur + ntot) : nullptr;
+  for (int c = threadIdx.x; c < ntot; c += blockDim.x) {
+    cur[c] = offsT[(int64_t)c * gridDim.x + blockIdx.x];
+    if (hfl) hfl[c] = lut[c] >= 0 ? 1 : 0;
+  }
   __syncthreads();
   int r0, r1;
   cta_rows(rows, r0, r1);
@@ -339,7 +411,7 @@ csr_scatter_kernel(const int64_t* __restrict__ arp, const int32_t* __restrict__ 
           if (eb + 32 * u < e1) {
             if (c[u] < 0 || c[u] >= ncols) atomicOr(status, 2);  // out-of-range column
             const uint32_t cg = (uint32_t)(c[u] < 0 || c[u] >= ncols ? 0 : c[u]) + cofs;
-            if (is_head(lut, cg, v[u])) continue;  // densified for the tensor cores
+            if (is_head_s(lut, hfl, cg, v[u])) continue;  // densified for the tensor cores
             const uint32_t pos = atomicAdd(&cur[cg], 1u);
             keys[pos] = (cg << tbits) | (uint32_t)r;
             vals[pos] = v[u];
@@ -663,7 +735,13 @@ cudaError_t launch_sketch_csr(CsrWorkspace& w, int kind, uint64_t seed, int k, i
     const int prow = (int)std::min<int64_t>(rp, rows - p0);
     const int64_t na = ab[p + 1] - ab[p], nb = bb[p + 1] - bb[p];
     const int64_t ne = na + nb;
-    {
+    if (kind == PI_GAUSSIAN && ((row0 + p0) & 3) == 0 && (kp & 1) == 0) {
+      // one generation, both layouts (the head panel when kmaj is given)
+      const int kcols = std::max(kp, kmaj ? kpad : 0);
+      dim3 dg((unsigned)((prow + DUAL_ROWS - 1) / DUAL_ROWS), (unsigned)((kcols + DUAL_K - 1) / DUAL_K));
+      pi_panel_dual_kernel<<<dg, 256, 0, st>>>(seed, k, kp, kmaj ? kpad : 0, row0 + p0, prow, w.pi, kmaj,
+                                               kmaj_ld, p0);
+    } else {
       const int64_t groups = ((row0 + p0 + prow - 1) / 4 - (row0 + p0) / 4 + 1) * kp;
       const int blocks = (int)std::min<int64_t>((groups + 255) / 256, 148 * 16);
       pi_panel_kernel<<<blocks, 256, 0, st>>>(kind, seed, k, kp, row0 + p0, prow, w.pi);
@@ -677,16 +755,19 @@ cudaError_t launch_sketch_csr(CsrWorkspace& w, int kind, uint64_t seed, int k, i
     if (prof) CSR_TRY(cudaEventRecord(pev[1], st));
     if (ne == 0) continue;
     if (counting) {
-      const size_t sm = (size_t)ntot * 4;
+      // head-column flags in SMEM beside the counters when they fit (no
+      // global lut gather per nonzero)
+      const int sflags = (head_lut && ntot * 5 <= (int64_t)CSR_HIST_MAX_COLS * 4) ? 1 : 0;
+      const size_t sm = (size_t)ntot * 4 + (sflags ? (((size_t)ntot + 15) & ~(size_t)15) : 0);
       csr_hist_kernel<<<CSR_HIST_CTAS, CSR_T_THREADS, sm, st>>>(a_rowptr, a_col, a_val, a_n, b_rowptr,
                                                                 b_col, b_val, b_n, pr, prow, (int)ntot,
-                                                                head_lut, w.hist);
+                                                                head_lut, sflags, w.hist);
       size_t tmp = (size_t)w.cub_cap;
       CSR_TRY(cub::DeviceScan::ExclusiveSum(w.cub_tmp, tmp, w.hist, w.offs,
                                             (int)(ntot * (int64_t)CSR_HIST_CTAS), st));
       csr_scatter_kernel<<<CSR_HIST_CTAS, CSR_T_THREADS, sm, st>>>(a_rowptr, a_col, a_val, a_n, b_rowptr,
                                                                    b_col, b_val, b_n, pr, prow, (int)ntot,
-                                                                   tbits, head_lut, w.offs, w.keys_out,
+                                                                   tbits, head_lut, sflags, w.offs, w.keys_out,
                                                                    w.vals_out, status);
       csr_total_kernel<<<1, 32, 0, st>>>(w.hist, w.offs, ntot * (int64_t)CSR_HIST_CTAS, w.ne_dev);
     } else {

@@ -216,14 +216,18 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
                "r"(bytes)
                : "memory");
 }
+// try_wait with a suspend-time hint: the warp is parked by the hardware
+// until the phase completes (or the hint expires) instead of re-issuing the
+// test in a loop — a spinning warp costs issue slots and power that the
+// generator, norm and MMA warps sharing the SM need.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   uint32_t addr = smem_u32(bar);
   asm volatile(
       "{\n\t.reg .pred P1;\n\t"
       "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
       "@!P1 bra WAIT_%=;\n\t}" ::"r"(addr),
-      "r"(parity)
+      "r"(parity), "r"(0x989680u)
       : "memory");
 }
 

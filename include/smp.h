@@ -124,7 +124,7 @@ SMP_API smp_status smp_sketch_block_csr(smp_handle* h, int64_t row0, int64_t row
 
 /* Expose the packed partial accumulators (fp32 UNSCALED sketch sums, n_tot×k
  * with n_tot = n1 + n2 (n1 if a_is_b), then fp64 column norms² n_tot) so the
- * caller can combine shards with ONE all-reduce-sum in place (Spark's
+ * caller can combine shards with an all-reduce-sum in place (Spark's
  * treeAggregate, P:145 → NCCL over NVLink).  Not needed with a
  * single shard.  Pointers stay valid until smp_destroy. */
 SMP_API smp_status smp_sketch_partials(smp_handle* h, float** sk, int64_t* sk_count, double** nrm,

@@ -175,8 +175,14 @@ __global__ void csr_keys_kernel(const int64_t* __restrict__ rowptr, const int32_
 }
 
 // ---------------------------------------------------------------- K3d
-constexpr int CSR_CHUNK = 128;  // sorted nonzeros per warp task
-constexpr int CSR_U = 4;        // π rows in flight per lane
+#ifndef SMP_CSR_U
+#define SMP_CSR_U 4
+#endif
+#ifndef SMP_CSR_CHUNK
+#define SMP_CSR_CHUNK 128
+#endif
+constexpr int CSR_CHUNK = SMP_CSR_CHUNK;  // sorted nonzeros per warp task
+constexpr int CSR_U = SMP_CSR_U;          // π rows in flight per lane
 
 __device__ __forceinline__ void red_add_v4(float* addr, float a, float b, float c, float d) {
   asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(addr), "f"(a), "f"(b), "f"(c),
@@ -317,10 +323,13 @@ __device__ __forceinline__ void cta_rows(int rows, int& r0, int& r1) {
   r1 = (int)(((int64_t)(blockIdx.x + 1) * rows) / gridDim.x);
 }
 
-// histT[c * G + b] = nonzeros of column c in CTA b's rows (c of B offset by a_n).
-// Warp per row; each lane issues its (up to 4) column loads before the SMEM
-// atomics so a row costs one memory round trip.
+// histT[b * ntot + c] = tail nonzeros of column c in CTA b's rows (c of B
+// offset by a_n).  A CTA's rows [r0, r1) own the CONTIGUOUS entry range
+// [rp[r0], rp[r1]) of each matrix, so the entries are streamed linearly
+// (coalesced, CSR_MLP independent loads in flight per thread); the row of an
+// entry is not needed for the histogram.
 constexpr int CSR_T_THREADS = 1024;
+constexpr int CSR_MLP = 4;
 
 __global__ void __launch_bounds__(CSR_T_THREADS)
 csr_hist_kernel(const int64_t* __restrict__ arp, const int32_t* __restrict__ acol,
@@ -337,7 +346,6 @@ csr_hist_kernel(const int64_t* __restrict__ arp, const int32_t* __restrict__ aco
   __syncthreads();
   int r0, r1;
   cta_rows(rows, r0, r1);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (int mat = 0; mat < 2; ++mat) {
     const int64_t* rp = mat == 0 ? arp : brp;
     if (!rp) continue;
@@ -346,30 +354,46 @@ csr_hist_kernel(const int64_t* __restrict__ arp, const int32_t* __restrict__ aco
     const int64_t ncols = mat == 0 ? a_n : b_n;
     const uint32_t cofs = mat == 0 ? 0u : (uint32_t)a_n;
     const int64_t base = rp[0];
-    for (int r = r0 + warp; r < r1; r += nw) {
-      const int64_t e0 = rp[p0 + r] - base, e1 = rp[p0 + r + 1] - base;
-      for (int64_t eb = e0 + lane; eb < e1; eb += 128) {
-        int32_t c[4];
-        float v[4];
+    const int64_t e0 = rp[p0 + r0] - base, e1 = rp[p0 + r1] - base;
+    for (int64_t eb = e0 + threadIdx.x; eb < e1; eb += (int64_t)CSR_MLP * blockDim.x) {
+      int32_t c[CSR_MLP];
+      float v[CSR_MLP];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          c[u] = eb + 32 * u < e1 ? col[eb + 32 * u] : -1;
-          v[u] = (lut && eb + 32 * u < e1) ? val[eb + 32 * u] : 0.f;
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-          if (eb + 32 * u < e1) {
-            const uint32_t cg = (uint32_t)(c[u] < 0 || c[u] >= ncols ? 0 : c[u]) + cofs;
-            if (!is_head_s(lut, hfl, cg, v[u])) atomicAdd(&hist[cg], 1u);
-          }
+      for (int u = 0; u < CSR_MLP; ++u) {
+        const int64_t e = eb + (int64_t)u * blockDim.x;
+        c[u] = e < e1 ? col[e] : -1;
+        v[u] = (lut && e < e1) ? val[e] : 0.f;
       }
+#pragma unroll
+      for (int u = 0; u < CSR_MLP; ++u)
+        if (eb + (int64_t)u * blockDim.x < e1) {
+          const uint32_t cg = (uint32_t)(c[u] < 0 || c[u] >= ncols ? 0 : c[u]) + cofs;
+          if (!is_head_s(lut, hfl, cg, v[u])) atomicAdd(&hist[cg], 1u);
+        }
     }
   }
   __syncthreads();
-  for (int c = threadIdx.x; c < ntot; c += blockDim.x) histT[(int64_t)c * gridDim.x + blockIdx.x] = hist[c];
+  // CTA-major (coalesced): histB[b * ntot + c]
+  for (int c = threadIdx.x; c < ntot; c += blockDim.x) histT[(int64_t)blockIdx.x * ntot + c] = hist[c];
 }
 
-// keys/vals at offsT[c * G + b] + (rank within the CTA's column c, SMEM atomic order)
+// per column c: pre[b][c] = Σ_{b' < b} histB[b'][c] (in place) and
+// colsum[c] = Σ_b histB[b][c]; one thread per column, coalesced across columns
+__global__ void csr_colscan_kernel(uint32_t* __restrict__ histB, int ntot, int G, uint32_t* __restrict__ colsum) {
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < ntot; c += gridDim.x * blockDim.x) {
+    uint32_t run = 0;
+    for (int b = 0; b < G; ++b) {
+      const uint32_t v = histB[(int64_t)b * ntot + c];
+      histB[(int64_t)b * ntot + c] = run;
+      run += v;
+    }
+    colsum[c] = run;
+  }
+}
+
+// keys/vals at offsT[c * G + b] + (rank within the CTA's column c, SMEM atomic
+// order); entries streamed linearly as in csr_hist_kernel, the row of an entry
+// found by binary search in the CTA's row pointers staged in SMEM.
 __global__ void __launch_bounds__(CSR_T_THREADS)
 csr_scatter_kernel(const int64_t* __restrict__ arp, const int32_t* __restrict__ acol,
                    const float* __restrict__ aval, int64_t a_n, const int64_t* __restrict__ brp,
@@ -378,15 +402,18 @@ csr_scatter_kernel(const int64_t* __restrict__ arp, const int32_t* __restrict__ 
                    const uint32_t* __restrict__ offsT, uint32_t* __restrict__ keys,
                    float* __restrict__ vals, int* __restrict__ status) {
   extern __shared__ uint32_t cur[];
-  uint8_t* hfl = (lut && sflags) ? reinterpret_cast<uint8_t*>(cur + ntot) : nullptr;
-  for (int c = threadIdx.x; c < ntot; c += blockDim.x) {
-    cur[c] = offsT[(int64_t)c * gridDim.x + blockIdx.x];
-    if (hfl) hfl[c] = lut[c] >= 0 ? 1 : 0;
-  }
-  __syncthreads();
   int r0, r1;
   cta_rows(rows, r0, r1);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int nr = r1 - r0;
+  // layout: cur[ntot] | srp[nr + 1] (int64, 8-byte aligned) | hfl[ntot]
+  int64_t* srp = reinterpret_cast<int64_t*>(cur + ((ntot + 1) & ~1));
+  uint8_t* hfl = (lut && sflags) ? reinterpret_cast<uint8_t*>(srp + nr + 1) : nullptr;
+  // cursor = column base (exclusive scan of the column totals) + this CTA's
+  // prefix within the column (csr_colscan_kernel): offsT = [colbase | pre]
+  for (int c = threadIdx.x; c < ntot; c += blockDim.x) {
+    cur[c] = offsT[c] + offsT[ntot + (int64_t)blockIdx.x * ntot + c];
+    if (hfl) hfl[c] = lut[c] >= 0 ? 1 : 0;
+  }
   for (int mat = 0; mat < 2; ++mat) {
     const int64_t* rp = mat == 0 ? arp : brp;
     if (!rp) continue;
@@ -395,35 +422,42 @@ csr_scatter_kernel(const int64_t* __restrict__ arp, const int32_t* __restrict__ 
     const int64_t ncols = mat == 0 ? a_n : b_n;
     const uint32_t cofs = mat == 0 ? 0u : (uint32_t)a_n;
     const int64_t base = rp[0];
-    for (int r = r0 + warp; r < r1; r += nw) {
-      const int64_t e0 = rp[p0 + r] - base, e1 = rp[p0 + r + 1] - base;
-      for (int64_t eb = e0 + lane; eb < e1; eb += 128) {
-        int32_t c[4];
-        float v[4];
+    __syncthreads();  // cur / hfl ready; srp free for this matrix
+    for (int i = threadIdx.x; i <= nr; i += blockDim.x) srp[i] = rp[p0 + r0 + i] - base;
+    __syncthreads();
+    const int64_t e0 = srp[0], e1 = srp[nr];
+    for (int64_t eb = e0 + threadIdx.x; eb < e1; eb += (int64_t)CSR_MLP * blockDim.x) {
+      int32_t c[CSR_MLP];
+      float v[CSR_MLP];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const bool ok = eb + 32 * u < e1;
-          c[u] = ok ? col[eb + 32 * u] : 0;
-          v[u] = ok ? val[eb + 32 * u] : 0.f;
+      for (int u = 0; u < CSR_MLP; ++u) {
+        const int64_t e = eb + (int64_t)u * blockDim.x;
+        c[u] = e < e1 ? col[e] : 0;
+        v[u] = e < e1 ? val[e] : 0.f;
+      }
+#pragma unroll
+      for (int u = 0; u < CSR_MLP; ++u) {
+        const int64_t e = eb + (int64_t)u * blockDim.x;
+        if (e >= e1) continue;
+        if (c[u] < 0 || c[u] >= ncols) atomicOr(status, 2);  // out-of-range column
+        const uint32_t cg = (uint32_t)(c[u] < 0 || c[u] >= ncols ? 0 : c[u]) + cofs;
+        if (is_head_s(lut, hfl, cg, v[u])) continue;  // densified for the tensor cores
+        int lo = 0, hi = nr;                          // row: last i with srp[i] <= e
+        while (hi - lo > 1) {
+          const int mid = (lo + hi) >> 1;
+          if (srp[mid] <= e) lo = mid; else hi = mid;
         }
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-          if (eb + 32 * u < e1) {
-            if (c[u] < 0 || c[u] >= ncols) atomicOr(status, 2);  // out-of-range column
-            const uint32_t cg = (uint32_t)(c[u] < 0 || c[u] >= ncols ? 0 : c[u]) + cofs;
-            if (is_head_s(lut, hfl, cg, v[u])) continue;  // densified for the tensor cores
-            const uint32_t pos = atomicAdd(&cur[cg], 1u);
-            keys[pos] = (cg << tbits) | (uint32_t)r;
-            vals[pos] = v[u];
-          }
+        const uint32_t pos = atomicAdd(&cur[cg], 1u);
+        keys[pos] = (cg << tbits) | (uint32_t)(r0 + lo);
+        vals[pos] = v[u];
       }
     }
   }
 }
 
-__global__ void csr_total_kernel(const uint32_t* __restrict__ hist, const uint32_t* __restrict__ offs,
-                                 int64_t nh, uint32_t* __restrict__ total) {
-  if (threadIdx.x == 0 && blockIdx.x == 0) *total = nh > 0 ? offs[nh - 1] + hist[nh - 1] : 0u;
+__global__ void csr_total_kernel(const uint32_t* __restrict__ colsum, const uint32_t* __restrict__ colbase,
+                                 int64_t ntot, uint32_t* __restrict__ total) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) *total = ntot > 0 ? colbase[ntot - 1] + colsum[ntot - 1] : 0u;
 }
 
 constexpr int CSR_HIST_CTAS = 148;
@@ -705,17 +739,18 @@ cudaError_t launch_sketch_csr(CsrWorkspace& w, int kind, uint64_t seed, int k, i
   CSR_TRY(grow(w.vals_out, w.ent_cap_vo, max_ent));
   size_t need = 0;
   if (counting) {
+    // w.offs = [colbase (ntot) | pre (G x ntot)], w.hist = colsum (ntot) scratch
     const int64_t nh = ntot * (int64_t)CSR_HIST_CTAS;
-    CSR_TRY(grow(w.hist, w.hist_cap, nh));
-    CSR_TRY(grow(w.offs, w.offs_cap, nh));
+    CSR_TRY(grow(w.hist, w.hist_cap, ntot));
+    CSR_TRY(grow(w.offs, w.offs_cap, ntot + nh));
     CSR_TRY(grow(w.ne_dev, w.ne_cap, 1));
-    CSR_TRY(cub::DeviceScan::ExclusiveSum(nullptr, need, w.hist, w.offs, (int)nh, st));
+    CSR_TRY(cub::DeviceScan::ExclusiveSum(nullptr, need, w.hist, w.offs, (int)ntot, st));
     static PerDeviceOnce attr;
     if (attr.need()) {
       CSR_TRY(cudaFuncSetAttribute(csr_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   CSR_HIST_MAX_COLS * 4));
+                                   227 * 1024));
       CSR_TRY(cudaFuncSetAttribute(csr_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   CSR_HIST_MAX_COLS * 4));
+                                   227 * 1024));
     }
   } else {
     CSR_TRY(cub::DeviceRadixSort::SortPairs(nullptr, need, w.keys_in, w.keys_out, w.vals_in, w.vals_out,
@@ -757,19 +792,24 @@ cudaError_t launch_sketch_csr(CsrWorkspace& w, int kind, uint64_t seed, int k, i
     if (counting) {
       // head-column flags in SMEM beside the counters when they fit (no
       // global lut gather per nonzero)
-      const int sflags = (head_lut && ntot * 5 <= (int64_t)CSR_HIST_MAX_COLS * 4) ? 1 : 0;
+      const int64_t srp_bytes = (int64_t)((prow + CSR_HIST_CTAS - 1) / CSR_HIST_CTAS + 2) * 8;
+      const int sflags = (head_lut && ntot * 5 + 8 + srp_bytes <= 227 * 1024) ? 1 : 0;
       const size_t sm = (size_t)ntot * 4 + (sflags ? (((size_t)ntot + 15) & ~(size_t)15) : 0);
       csr_hist_kernel<<<CSR_HIST_CTAS, CSR_T_THREADS, sm, st>>>(a_rowptr, a_col, a_val, a_n, b_rowptr,
                                                                 b_col, b_val, b_n, pr, prow, (int)ntot,
-                                                                head_lut, sflags, w.hist);
+                                                                head_lut, sflags, w.offs + ntot);
+      csr_colscan_kernel<<<(int)((ntot + 255) / 256), 256, 0, st>>>(w.offs + ntot, (int)ntot, CSR_HIST_CTAS,
+                                                                    w.hist);
       size_t tmp = (size_t)w.cub_cap;
-      CSR_TRY(cub::DeviceScan::ExclusiveSum(w.cub_tmp, tmp, w.hist, w.offs,
-                                            (int)(ntot * (int64_t)CSR_HIST_CTAS), st));
-      csr_scatter_kernel<<<CSR_HIST_CTAS, CSR_T_THREADS, sm, st>>>(a_rowptr, a_col, a_val, a_n, b_rowptr,
+      CSR_TRY(cub::DeviceScan::ExclusiveSum(w.cub_tmp, tmp, w.hist, w.offs, (int)ntot, st));
+      const int max_rows_cta = (prow + CSR_HIST_CTAS - 1) / CSR_HIST_CTAS + 1;
+      const size_t sm_sc = (size_t)((ntot + 1) & ~1) * 4 + (size_t)(max_rows_cta + 1) * 8 +
+                           (sflags ? (size_t)ntot : 0);
+      csr_scatter_kernel<<<CSR_HIST_CTAS, CSR_T_THREADS, sm_sc, st>>>(a_rowptr, a_col, a_val, a_n, b_rowptr,
                                                                    b_col, b_val, b_n, pr, prow, (int)ntot,
                                                                    tbits, head_lut, sflags, w.offs, w.keys_out,
                                                                    w.vals_out, status);
-      csr_total_kernel<<<1, 32, 0, st>>>(w.hist, w.offs, ntot * (int64_t)CSR_HIST_CTAS, w.ne_dev);
+      csr_total_kernel<<<1, 32, 0, st>>>(w.hist, w.offs, ntot, w.ne_dev);
     } else {
       const int kb_blocks = (int)std::min<int64_t>((prow + 7) / 8, 148 * 16);
       // A: entries ab[p] .. ab[p+1] (relative to a_rowptr[0]) -> keys[0 .. na)
@@ -806,7 +846,9 @@ cudaError_t launch_sketch_csr(CsrWorkspace& w, int kind, uint64_t seed, int k, i
       CSR_TRY(cudaEventRecord((*w.ev_pool)[*w.ev_used + 1], st));
       *w.ev_used += 2;
     }
-    w.launches += 4 + (b_rowptr && nb > 0 ? 1 : 0) + 3;
+    // Π panel + (counting: hist, colscan, 2 CUB scan kernels, scatter, total;
+    // radix: 1-2 key kernels + CUB sort passes) + accumulate
+    w.launches += counting ? 1 + 6 + 1 : 1 + 1 + (b_rowptr && nb > 0 ? 1 : 0) + 4 + 1;
     if (prof) {
       CSR_TRY(cudaEventRecord(pev[3], st));
       CSR_TRY(cudaEventSynchronize(pev[3]));

@@ -678,6 +678,13 @@ smp_status smp_sketch_block_csr(smp_handle* h, int64_t row0, int64_t rows, const
       CK(h, ensure(h->csr.kmaj, h->csr.kmaj_cap, kpad * cpad), "alloc head panel");
       h->csr.ev_pool = h->timing ? &h->ev_pool : nullptr;
       CK(h, smp::csr_bounds(h->csr, a_rowptr, two ? b_rowptr : nullptr, a_n + b_n, rows, h->st), "bounds");
+      // SMP_CSR_PROFILE=1: device time of the head (densify, K1 + K2) per call
+      const char* hp = getenv("SMP_CSR_PROFILE");
+      const bool hprof = hp && atoi(hp);
+      cudaEvent_t hev[3] = {};
+      float hms[2] = {0.f, 0.f};
+      if (hprof)
+        for (int i = 0; i < 3; ++i) CK(h, cudaEventCreate(&hev[i]), "event");
       for (int64_t r0 = 0; r0 < rows; r0 += chunk) {
         const int64_t rc = std::min(chunk, rows - r0);
         const int64_t ldk = ((rc + 63) / 64) * 64;
@@ -689,13 +696,29 @@ smp_status smp_sketch_block_csr(smp_handle* h, int64_t row0, int64_t rows, const
                                                 h->csr.kmaj, ldk, (int)kpad);
         if (e1 != cudaSuccess) h->csr.bounds_pre = false;
         CK(h, e1, "sketch_csr");
+        if (hprof) CK(h, cudaEventRecord(hev[0], h->st), "event");
         CK(h, smp::csr_densify(h->csr, a_rowptr, a_col, a_val, a_n, two ? b_rowptr : nullptr,
                                two ? b_col : nullptr, two ? b_val : nullptr, b_n, r0, rc, ldh,
                                h->csr.xhead, h->st),
            "densify");
+        if (hprof) CK(h, cudaEventRecord(hev[1], h->st), "event");
         smp_status s2 = sketch_dense_bf16(h, row0 + r0, rc, h->csr.xhead, ldh, n_head, 1, 0, true,
                                           h->csr.kmaj, h->csr.head_map);
         if (s2 != SMP_OK) return s2;
+        if (hprof) {
+          CK(h, cudaEventRecord(hev[2], h->st), "event");
+          CK(h, cudaEventSynchronize(hev[2]), "sync");
+          float a = 0.f, b = 0.f;
+          cudaEventElapsedTime(&a, hev[0], hev[1]);
+          cudaEventElapsedTime(&b, hev[1], hev[2]);
+          hms[0] += a;
+          hms[1] += b;
+        }
+      }
+      if (hprof) {
+        fprintf(stderr, "K3 head over %lld rows (%d columns): densify %.3f ms, K1+K2 %.3f ms\n",
+                (long long)rows, n_head, hms[0], hms[1]);
+        for (int i = 0; i < 3; ++i) cudaEventDestroy(hev[i]);
       }
       h->csr.bounds_pre = false;
       h->launches += 2 + (h->csr.launches - l0);

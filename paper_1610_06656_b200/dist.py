@@ -2,7 +2,7 @@
 
 ΠA = Σ_g Π[:, rows_g] A[rows_g, :] and ||A_i||² = Σ_g ||A_i^(g)||² are sums
 over row blocks (the Spark treeAggregate of P:145), so each rank sketches its
-own rows and the packed partials are combined by ONE all-reduce (NCCL over
+own rows and the packed partials are combined by all-reduce (NCCL over
 NVLink on B200; gloo works for the CPU tests).  Everything after the combine
 (finalize, Ω, M̃, WAltMin) is replicated: the hashes make Ω identical on every
 rank without further communication.
@@ -26,19 +26,34 @@ def shard_rows(d: int, world: int, rank: int, align: int = GEN_BLOCK):
     return min(d, b0 * align), min(d, b1 * align)
 
 
+def _coalesced_allreduce(tensors, group=None):
+    """The collective itself.  Buffers of one dtype are coalesced into one
+    NCCL group call; the fp32 sketch and the fp64 norms differ in dtype (which
+    NCCL's coalescing rejects), so one all-reduce per dtype is issued
+    asynchronously back to back and waited on together."""
+    by_dtype = {}
+    for t in tensors:
+        by_dtype.setdefault(t.dtype, []).append(t)
+    works = []
+    for group_tensors in by_dtype.values():
+        if len(group_tensors) > 1 and dist.get_backend(group) == "nccl":
+            with dist._coalescing_manager(group=group, async_ops=False):
+                for t in group_tensors:
+                    dist.all_reduce(t, group=group)
+        else:
+            for t in group_tensors:
+                works.append(dist.all_reduce(t, group=group, async_op=True))
+    for w in works:
+        w.wait()
+    return tensors
+
+
 def allreduce_partials(tensors, group=None):
     """Sum the partial sketch (fp32) and norm (fp64) buffers across ranks in
-    place, as one coalesced collective."""
+    place (one collective per dtype, see _coalesced_allreduce)."""
     if not dist.is_available() or not dist.is_initialized() or dist.get_world_size(group) == 1:
         return tensors
-    if dist.get_backend(group) == "nccl":
-        with dist._coalescing_manager(group=group, async_ops=False):
-            for t in tensors:
-                dist.all_reduce(t, group=group)
-    else:  # gloo coalesces only same-dtype tensors
-        for t in tensors:
-            dist.all_reduce(t, group=group)
-    return tensors
+    return _coalesced_allreduce(tensors, group)
 
 
 def combine(sketch, group=None):

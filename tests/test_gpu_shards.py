@@ -79,3 +79,43 @@ def test_row_sharded_handles_sum_to_single_pass(G):
     for h in hs:
         h.close()
     one.close()
+
+
+def _nccl_worker(port, out):
+    import os
+    import torch.distributed as dist
+    from paper_1610_06656_b200.dist import _coalesced_allreduce
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    a = torch.arange(10, dtype=torch.float32, device="cuda")
+    b = torch.arange(4, dtype=torch.float64, device="cuda") * 0.5
+    _coalesced_allreduce([a, b])           # the calls bench.py's combine makes
+    c = torch.ones(3, dtype=torch.float32, device="cuda")
+    _coalesced_allreduce([a, c, b])        # two fp32 buffers: the coalesced NCCL group
+    torch.cuda.synchronize()
+    out.put((a.cpu().numpy().tolist(), b.cpu().numpy().tolist()))
+    dist.destroy_process_group()
+
+
+def test_nccl_coalesced_allreduce_runs():
+    """The NCCL branch of the combine (one all-reduce per dtype; same-dtype
+    buffers in one coalesced group) on a 1-rank NCCL group: the API path the
+    N > 1 bench takes executes on this GPU and leaves the buffers intact (sum
+    over 1 rank).  Round 2 found here that NCCL's coalescing manager rejects
+    an fp32 + fp64 group."""
+    import socket
+    import torch.multiprocessing as mp
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=_nccl_worker, args=(port, q))
+    p.start()
+    a, b = q.get(timeout=120)
+    p.join(timeout=60)
+    assert p.exitcode == 0
+    assert a == list(range(10)) and b == [0.0, 0.5, 1.0, 1.5]

@@ -36,6 +36,15 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
+def _fresh(src: str, obj: str) -> bool:
+    if not os.path.exists(obj):
+        return False
+    hdrs = glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(CSRC, "*.h"))
+    hdrs.append(os.path.join(ROOT, "include", "smp.h"))
+    t = os.path.getmtime(obj)
+    return all(os.path.getmtime(d) < t for d in [src, *hdrs])
+
+
 def build(force: bool = False, verbose: bool = False, defines=(), out: str = None, only=()) -> str:
     """Compile csrc/*.cu (in parallel) and link libsmp.so.  `defines` and
     `out` produce tuning variants (e.g. libsmp_x4p3.so) next to the default."""
@@ -57,6 +66,9 @@ def build(force: bool = False, verbose: bool = False, defines=(), out: str = Non
             if not os.path.exists(ref):
                 raise RuntimeError(f"variant build needs the default object {ref}")
             procs.append((src, ref, None))
+            continue
+        if not force and not dflags and _fresh(src, obj):
+            procs.append((src, obj, None))  # incremental: object newer than its inputs
             continue
         cmd = [nvcc, *NVCC_FLAGS, *dflags, "-c", src, "-o", obj, "-I", os.path.join(ROOT, "include")]
         procs.append((src, obj, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE,

@@ -26,6 +26,9 @@
 // are order-dependent across chunks (the reductions race), so CSR sketches
 // agree with the oracle to ~1e-7 relative but are not bit-reproducible run
 // to run (K3).
+#include <algorithm>
+#include <utility>
+#include <vector>
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 #include <cstdio>
@@ -150,14 +153,14 @@ pi_panel_dual_kernel(uint64_t seed, int k, int kp, int kpad, int64_t t0, int row
 }
 
 // ---------------------------------------------------------------- K3b
-// keys[o] = (c_glob << tbits) | (t - p0), vals[o] = v for the nonzeros of
-// rows [p0, p0 + rows) of one matrix; warp per row; o = (entry index
-// relative to rowptr[0]) - ebase.
+// kv[o] = (key << 32) | bits(v), key = (c_glob << tbits) | (t - p0), for the
+// nonzeros of rows [p0, p0 + rows) of one matrix (the packed (value, key)
+// pair K3d reads; a radix sort on bits [32, 32 + key bits) orders it); warp
+// per row; o = (entry index relative to rowptr[0]) - ebase.
 __global__ void csr_keys_kernel(const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
                                 const float* __restrict__ val, int64_t p0, int rows,
                                 int64_t ebase, uint32_t cofs, int tbits, int64_t ncols,
-                                uint32_t* __restrict__ keys, float* __restrict__ vals,
-                                int* __restrict__ status) {
+                                uint64_t* __restrict__ kv, int* __restrict__ status) {
   const int lane = threadIdx.x & 31;
   const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
   const int64_t base = rowptr[0];  // col/val are indexed from rowptr[0]
@@ -167,9 +170,7 @@ __global__ void csr_keys_kernel(const int64_t* __restrict__ rowptr, const int32_
       const int32_t c = col[e];
       if (c < 0 || c >= ncols) atomicOr(status, 2);  // out-of-range column
       const uint32_t cg = (uint32_t)(c < 0 ? 0 : (c >= ncols ? 0 : c)) + cofs;
-      const int64_t o = e - ebase;
-      keys[o] = (cg << tbits) | (uint32_t)r;
-      vals[o] = val[e];
+      kv[e - ebase] = ((uint64_t)((cg << tbits) | (uint32_t)r) << 32) | __float_as_uint(val[e]);
     }
   }
 }
@@ -212,11 +213,16 @@ __device__ __forceinline__ void flush_col(uint32_t c, const float (&acc)[KV][8],
 
 template <int KV>
 __global__ void __launch_bounds__(256)
-csr_accumulate_kernel(const uint32_t* __restrict__ keys, const float* __restrict__ vals, int64_t n,
+csr_accumulate_kernel(const uint2* __restrict__ kv, int64_t n,
                       const uint16_t* __restrict__ pi, int kp, int k, int tbits,
                       float* __restrict__ acc_sk, double* __restrict__ acc_nrm, int do_norms,
-                      const uint32_t* __restrict__ n_dev) {
-  if (n_dev) n = min(n, (int64_t)*n_dev);  // tail entries actually scattered
+                      const uint32_t* __restrict__ seg_beg, const uint32_t* __restrict__ seg_end) {
+  // counting sort: the panel's tail is kv[*seg_beg (0 if null), *seg_end) (n bounds it)
+  if (seg_end) {
+    const int64_t b = seg_beg ? *seg_beg : 0;
+    kv += b;
+    n = min(n, (int64_t)*seg_end - b);
+  }
   const int lane = threadIdx.x & 31;
   const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
   const uint32_t tmask = (1u << tbits) - 1u;
@@ -240,8 +246,9 @@ csr_accumulate_kernel(const uint32_t* __restrict__ keys, const float* __restrict
       for (int u = 0; u < CSR_U; ++u) {
         const int64_t e = eb + u;
         ok[u] = e < e1;
-        kk[u] = ok[u] ? keys[e] : 0u;
-        vv[u] = ok[u] ? vals[e] : 0.f;
+        const uint2 q2 = ok[u] ? kv[e] : make_uint2(0u, 0u);
+        kk[u] = q2.y;
+        vv[u] = __uint_as_float(q2.x);
       }
 #pragma unroll
       for (int u = 0; u < CSR_U; ++u) {
@@ -299,165 +306,194 @@ csr_accumulate_kernel(const uint32_t* __restrict__ keys, const float* __restrict
 
 // ---------------------------------------------------------------- head/tail split
 // A nonzero goes to the tensor-core head path iff its column is a head column
-// (lut >= 0) and its value has at most 4 significant bits (small integer
-// counts): Gaussian Π (8 bits) times such a value is a 12-bit product, which
-// tcgen05 accumulates exactly (R21).  Everything else is the tail.
+// (slot lut[c] != CSR_NO_SLOT) and its value has at most 4 significant bits
+// (small integer counts): Gaussian Π (8 bits) times such a value is a 12-bit
+// product, which tcgen05 accumulates exactly (R21).  Everything
+// else is the tail.
+constexpr uint16_t CSR_NO_SLOT = 0xFFFF;
 __device__ __forceinline__ bool is_4bit(float v) {
   const uint32_t u = __float_as_uint(v);
   return ((u & 0x7F800000u) != 0x7F800000u) && ((u & 0x000FFFFFu) == 0u);
 }
-__device__ __forceinline__ bool is_head(const int32_t* __restrict__ lut, uint32_t cg, float v) {
-  return lut != nullptr && lut[cg] >= 0 && is_4bit(v);
-}
-// same test with the head-column flags staged in SMEM (hfl != nullptr)
-__device__ __forceinline__ bool is_head_s(const int32_t* __restrict__ lut, const uint8_t* hfl, uint32_t cg,
-                                          float v) {
-  if (lut == nullptr) return false;
-  return (hfl ? hfl[cg] != 0 : lut[cg] >= 0) && is_4bit(v);
-}
 
 // ---------------------------------------------------------------- K3c counting sort
-// CTA b owns panel rows [b·rows/G, (b+1)·rows/G) of both matrices.
-__device__ __forceinline__ void cta_rows(int rows, int& r0, int& r1) {
-  r0 = (int)(((int64_t)blockIdx.x * rows) / gridDim.x);
-  r1 = (int)(((int64_t)(blockIdx.x + 1) * rows) / gridDim.x);
-}
-
-// histT[b * ntot + c] = tail nonzeros of column c in CTA b's rows (c of B
-// offset by a_n).  A CTA's rows [r0, r1) own the CONTIGUOUS entry range
-// [rp[r0], rp[r1]) of each matrix, so the entries are streamed linearly
-// (coalesced, CSR_MLP independent loads in flight per thread); the row of an
-// entry is not needed for the histogram.
+// One counting sort per GROUP of panels (up to ~2^27 entries) orders the
+// nonzeros of the group's rows by (panel, column), so that every panel's tail
+// is one contiguous, column-grouped range for K3d.  Each panel is cut into S
+// row slices, one CTA per (panel, slice), about one CTA per SM over the
+// group: the CTA counts its slice's tail entries per column in SMEM (hist
+// pass), one scan over the (panel, column, slice) cells gives every CTA its
+// own base per column, and the scatter pass claims positions from SMEM
+// cursors.  A slice's entries are a contiguous range of each matrix, streamed
+// coalesced with CSR_MLP loads in flight per thread (the row of an entry,
+// needed by the scatter, by binary search in the slice's row offsets staged in
+// SMEM); the head slot table sits in SMEM beside the counters.  In the
+// scatter a tail entry costs one 8-byte (value, key) store.  Head entries
+// (tensor-core path) are not counted; the scatter writes them straight into
+// the dense head chunk, whose slice rows the CTA zeroes first (the
+// densification of the head is fused into this pass).  The order inside one
+// cell follows the SMEM atomics; K3d's fp32 sums are order-dependent anyway
+// (DESIGN.md §7).
 constexpr int CSR_T_THREADS = 1024;
 constexpr int CSR_MLP = 4;
 
-__global__ void __launch_bounds__(CSR_T_THREADS)
-csr_hist_kernel(const int64_t* __restrict__ arp, const int32_t* __restrict__ acol,
-                const float* __restrict__ aval, int64_t a_n, const int64_t* __restrict__ brp,
-                const int32_t* __restrict__ bcol, const float* __restrict__ bval, int64_t b_n,
-                int64_t p0, int rows, int ntot, const int32_t* __restrict__ lut, int sflags,
-                uint32_t* __restrict__ histT) {
-  extern __shared__ uint32_t hist[];
-  uint8_t* hfl = (lut && sflags) ? reinterpret_cast<uint8_t*>(hist + ntot) : nullptr;
-  for (int c = threadIdx.x; c < ntot; c += blockDim.x) {
-    hist[c] = 0u;
-    if (hfl) hfl[c] = lut[c] >= 0 ? 1 : 0;
-  }
-  __syncthreads();
-  int r0, r1;
-  cta_rows(rows, r0, r1);
-  for (int mat = 0; mat < 2; ++mat) {
-    const int64_t* rp = mat == 0 ? arp : brp;
-    if (!rp) continue;
-    const int32_t* col = mat == 0 ? acol : bcol;
-    const float* val = mat == 0 ? aval : bval;
-    const int64_t ncols = mat == 0 ? a_n : b_n;
-    const uint32_t cofs = mat == 0 ? 0u : (uint32_t)a_n;
-    const int64_t base = rp[0];
-    const int64_t e0 = rp[p0 + r0] - base, e1 = rp[p0 + r1] - base;
-    for (int64_t eb = e0 + threadIdx.x; eb < e1; eb += (int64_t)CSR_MLP * blockDim.x) {
-      int32_t c[CSR_MLP];
-      float v[CSR_MLP];
-#pragma unroll
-      for (int u = 0; u < CSR_MLP; ++u) {
-        const int64_t e = eb + (int64_t)u * blockDim.x;
-        c[u] = e < e1 ? col[e] : -1;
-        v[u] = (lut && e < e1) ? val[e] : 0.f;
-      }
-#pragma unroll
-      for (int u = 0; u < CSR_MLP; ++u)
-        if (eb + (int64_t)u * blockDim.x < e1) {
-          const uint32_t cg = (uint32_t)(c[u] < 0 || c[u] >= ncols ? 0 : c[u]) + cofs;
-          if (!is_head_s(lut, hfl, cg, v[u])) atomicAdd(&hist[cg], 1u);
-        }
-    }
-  }
-  __syncthreads();
-  // CTA-major (coalesced): histB[b * ntot + c]
-  for (int c = threadIdx.x; c < ntot; c += blockDim.x) histT[(int64_t)blockIdx.x * ntot + c] = hist[c];
+// L2 eviction priorities: the CSR stream is read once (evict_first); the
+// sorted (value, key) pairs are written in pieces by many CTAs over the whole
+// pass and read back by K3d, so they are kept (evict_last) — a partially
+// written 32-byte sector that leaves L2 early costs a DRAM read-modify-write.
+__device__ __forceinline__ uint64_t l2_policy_evict_first() {
+  uint64_t pol;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ uint64_t l2_policy_evict_last() {
+  uint64_t pol;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ int32_t ld_hint_s32(const int32_t* p, uint64_t pol) {
+  int32_t v;
+  asm volatile("ld.global.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ float ld_hint_f32(const float* p, uint64_t pol) {
+  float v;
+  asm volatile("ld.global.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ void st_hint_v2(uint2* p, uint2 v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v2.u32 [%0], {%1, %2}, %3;" ::"l"(p), "r"(v.x), "r"(v.y), "l"(pol)
+               : "memory");
 }
 
-// per column c: pre[b][c] = Σ_{b' < b} histB[b'][c] (in place) and
-// colsum[c] = Σ_b histB[b][c]; one thread per column, coalesced across columns
-__global__ void csr_colscan_kernel(uint32_t* __restrict__ histB, int ntot, int G, uint32_t* __restrict__ colsum) {
-  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < ntot; c += gridDim.x * blockDim.x) {
-    uint32_t run = 0;
-    for (int b = 0; b < G; ++b) {
-      const uint32_t v = histB[(int64_t)b * ntot + c];
-      histB[(int64_t)b * ntot + c] = run;
-      run += v;
-    }
-    colsum[c] = run;
-  }
+__device__ __forceinline__ uint32_t csr_cg(int32_t c, int64_t ncols, uint32_t cofs) {
+  return (uint32_t)(c < 0 || c >= ncols ? 0 : c) + cofs;
 }
 
-// keys/vals at offsT[c * G + b] + (rank within the CTA's column c, SMEM atomic
-// order); entries streamed linearly as in csr_hist_kernel, the row of an entry
-// found by binary search in the CTA's row pointers staged in SMEM.
-__global__ void __launch_bounds__(CSR_T_THREADS)
-csr_scatter_kernel(const int64_t* __restrict__ arp, const int32_t* __restrict__ acol,
-                   const float* __restrict__ aval, int64_t a_n, const int64_t* __restrict__ brp,
-                   const int32_t* __restrict__ bcol, const float* __restrict__ bval, int64_t b_n,
-                   int64_t p0, int rows, int ntot, int tbits, const int32_t* __restrict__ lut, int sflags,
-                   const uint32_t* __restrict__ offsT, uint32_t* __restrict__ keys,
-                   float* __restrict__ vals, int* __restrict__ status) {
-  extern __shared__ uint32_t cur[];
-  int r0, r1;
-  cta_rows(rows, r0, r1);
+struct CsrSortArgs {
+  const int64_t* arp;
+  const int32_t* acol;
+  const float* aval;
+  int64_t a_n;
+  const int64_t* brp;
+  const int32_t* bcol;
+  const float* bval;
+  int64_t b_n;
+  int64_t pr;               // rowptr index of the group's first row
+  int rows;                 // group rows
+  int tbits;                // panel rows = 2^tbits
+  int ntot;
+  int S;                    // slices (CTAs) per panel
+  const uint16_t* lut;      // head slot per column (CSR_NO_SLOT: tail), or null
+  int lut_smem;             // stage lut in SMEM
+  uint32_t* cells;          // hist: counts, scatter: exclusive starts; index (p*ntot + c)*S + s
+  uint2* kv;                // scatter: (value bits, key)
+  int* status;
+  uint16_t* xh;             // dense head chunk (null: no head)
+  int64_t ldh, xrow;
+  int n_head;
+};
+
+constexpr int CSR_SCATTER_RB = 64;  // scatter: rows per batch (head rows zeroed just before their values)
+
+template <bool SCATTER>
+__global__ void __launch_bounds__(CSR_T_THREADS, 1) csr_sort_pass_kernel(CsrSortArgs a) {
+  // SMEM: [ntot] counters | [ntot] u16 head slots | 2 x [nr+1] i32 row offsets (A, B)
+  extern __shared__ uint32_t sm_cnt[];
+  const int p = blockIdx.y, sl = blockIdx.x;
+  const int pb = p << a.tbits;
+  const int R = min(1 << a.tbits, a.rows - pb);
+  const int r0 = pb + (int)(((int64_t)sl * R) / a.S), r1 = pb + (int)(((int64_t)(sl + 1) * R) / a.S);
   const int nr = r1 - r0;
-  // layout: cur[ntot] | srp[nr + 1] (int64, 8-byte aligned) | hfl[ntot]
-  int64_t* srp = reinterpret_cast<int64_t*>(cur + ((ntot + 1) & ~1));
-  uint8_t* hfl = (lut && sflags) ? reinterpret_cast<uint8_t*>(srp + nr + 1) : nullptr;
-  // cursor = column base (exclusive scan of the column totals) + this CTA's
-  // prefix within the column (csr_colscan_kernel): offsT = [colbase | pre]
-  for (int c = threadIdx.x; c < ntot; c += blockDim.x) {
-    cur[c] = offsT[c] + offsT[ntot + (int64_t)blockIdx.x * ntot + c];
-    if (hfl) hfl[c] = lut[c] >= 0 ? 1 : 0;
+  uint16_t* slut = reinterpret_cast<uint16_t*>(sm_cnt + a.ntot);
+  int32_t* srp = reinterpret_cast<int32_t*>(sm_cnt + a.ntot + (a.lut_smem ? (a.ntot + 1) / 2 : 0));
+  const uint16_t* lut = (a.lut && a.lut_smem) ? slut : a.lut;
+  for (int c = threadIdx.x; c < a.ntot; c += blockDim.x) {
+    sm_cnt[c] = SCATTER ? a.cells[((int64_t)p * a.ntot + c) * a.S + sl] : 0u;
+    if (a.lut && a.lut_smem) slut[c] = a.lut[c];
   }
+  const uint32_t tmask = (1u << a.tbits) - 1u;
+  const uint64_t pol_first = l2_policy_evict_first(), pol_last = l2_policy_evict_last();
+  int64_t e0[2] = {0, 0};
+#pragma unroll
   for (int mat = 0; mat < 2; ++mat) {
-    const int64_t* rp = mat == 0 ? arp : brp;
+    const int64_t* rp = mat == 0 ? a.arp : a.brp;
     if (!rp) continue;
-    const int32_t* col = mat == 0 ? acol : bcol;
-    const float* val = mat == 0 ? aval : bval;
-    const int64_t ncols = mat == 0 ? a_n : b_n;
-    const uint32_t cofs = mat == 0 ? 0u : (uint32_t)a_n;
-    const int64_t base = rp[0];
-    __syncthreads();  // cur / hfl ready; srp free for this matrix
-    for (int i = threadIdx.x; i <= nr; i += blockDim.x) srp[i] = rp[p0 + r0 + i] - base;
-    __syncthreads();
-    const int64_t e0 = srp[0], e1 = srp[nr];
-    for (int64_t eb = e0 + threadIdx.x; eb < e1; eb += (int64_t)CSR_MLP * blockDim.x) {
-      int32_t c[CSR_MLP];
-      float v[CSR_MLP];
-#pragma unroll
-      for (int u = 0; u < CSR_MLP; ++u) {
-        const int64_t e = eb + (int64_t)u * blockDim.x;
-        c[u] = e < e1 ? col[e] : 0;
-        v[u] = e < e1 ? val[e] : 0.f;
+    e0[mat] = rp[a.pr + r0] - rp[0];
+    if (SCATTER)  // slice row offsets of this matrix, relative to its first entry
+      for (int i = threadIdx.x; i <= nr; i += blockDim.x)
+        srp[mat * (nr + 1) + i] = (int32_t)(rp[a.pr + r0 + i] - rp[0] - e0[mat]);
+  }
+  __syncthreads();
+  uint16_t* xh = SCATTER ? a.xh : nullptr;
+  const int nq = (a.n_head + 7) / 8;
+  // hist: the whole slice in one batch; scatter: batches of CSR_SCATTER_RB rows
+  const int rb_step = SCATTER ? CSR_SCATTER_RB : nr;
+  for (int rb = 0; rb < nr; rb += rb_step) {
+    const int re = min(nr, rb + rb_step);
+    if (xh) {  // zero the head slots of the batch's rows (coalesced), just before their values
+      for (int i = threadIdx.x; i < (re - rb) * nq; i += blockDim.x) {
+        const int64_t r = r0 + rb + i / nq;
+        reinterpret_cast<uint4*>(xh + (r + a.xrow) * a.ldh)[i % nq] = make_uint4(0u, 0u, 0u, 0u);
       }
+      __syncthreads();
+    }
+#pragma unroll 1
+    for (int mat = 0; mat < 2; ++mat) {
+      const int64_t* rp = mat == 0 ? a.arp : a.brp;
+      if (!rp) continue;
+      const int32_t* col = (mat == 0 ? a.acol : a.bcol) + e0[mat];
+      const float* val = (mat == 0 ? a.aval : a.bval) + e0[mat];
+      const int64_t ncols = mat == 0 ? a.a_n : a.b_n;
+      const uint32_t cofs = mat == 0 ? 0u : (uint32_t)a.a_n;
+      const int32_t* mrp = srp + mat * (nr + 1);
+      const int32_t eb0 = SCATTER ? mrp[rb] : 0;
+      const int32_t eb1 = SCATTER ? mrp[re] : (int32_t)(rp[a.pr + r1] - rp[0] - e0[mat]);
+      for (int32_t eb = eb0 + (int32_t)threadIdx.x; eb < eb1; eb += CSR_MLP * (int32_t)blockDim.x) {
+        int32_t c[CSR_MLP];
+        float v[CSR_MLP];
 #pragma unroll
-      for (int u = 0; u < CSR_MLP; ++u) {
-        const int64_t e = eb + (int64_t)u * blockDim.x;
-        if (e >= e1) continue;
-        if (c[u] < 0 || c[u] >= ncols) atomicOr(status, 2);  // out-of-range column
-        const uint32_t cg = (uint32_t)(c[u] < 0 || c[u] >= ncols ? 0 : c[u]) + cofs;
-        if (is_head_s(lut, hfl, cg, v[u])) continue;  // densified for the tensor cores
-        int lo = 0, hi = nr;                          // row: last i with srp[i] <= e
-        while (hi - lo > 1) {
-          const int mid = (lo + hi) >> 1;
-          if (srp[mid] <= e) lo = mid; else hi = mid;
+        for (int u = 0; u < CSR_MLP; ++u) {
+          const int32_t e = eb + u * (int32_t)blockDim.x;
+          c[u] = e < eb1 ? ld_hint_s32(col + e, pol_first) : 0;
+          v[u] = e < eb1 ? ld_hint_f32(val + e, pol_first) : 0.f;
         }
-        const uint32_t pos = atomicAdd(&cur[cg], 1u);
-        keys[pos] = (cg << tbits) | (uint32_t)(r0 + lo);
-        vals[pos] = v[u];
+#pragma unroll
+        for (int u = 0; u < CSR_MLP; ++u) {
+          const int32_t e = eb + u * (int32_t)blockDim.x;
+          if (e >= eb1) continue;
+          if (SCATTER && (c[u] < 0 || c[u] >= ncols)) atomicOr(a.status, 2);  // out-of-range column
+          const uint32_t cg = csr_cg(c[u], ncols, cofs);
+          const uint16_t slot = lut ? lut[cg] : CSR_NO_SLOT;
+          const bool head = slot != CSR_NO_SLOT && is_4bit(v[u]);
+          if (!SCATTER) {
+            if (!head) atomicAdd(&sm_cnt[cg], 1u);
+            continue;
+          }
+          if (head && !xh) continue;
+          int lo = rb, hi = re;  // slice row of entry e: last i with mrp[i] <= e
+          while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (mrp[mid] <= e) lo = mid; else hi = mid;
+          }
+          const int r = r0 + lo;
+          if (head) {
+            xh[((int64_t)r + a.xrow) * a.ldh + slot] = (uint16_t)(__float_as_uint(v[u]) >> 16);
+          } else {
+            const uint32_t pos = atomicAdd(&sm_cnt[cg], 1u);
+            st_hint_v2(a.kv + pos, make_uint2(__float_as_uint(v[u]), (cg << a.tbits) | ((uint32_t)r & tmask)),
+                       pol_last);
+          }
+        }
       }
     }
+    if (xh) __syncthreads();  // the batch's head values land before the next batch's zeros
   }
-}
-
-__global__ void csr_total_kernel(const uint32_t* __restrict__ colsum, const uint32_t* __restrict__ colbase,
-                                 int64_t ntot, uint32_t* __restrict__ total) {
-  if (threadIdx.x == 0 && blockIdx.x == 0) *total = ntot > 0 ? colbase[ntot - 1] + colsum[ntot - 1] : 0u;
+  if (!SCATTER) {
+    __syncthreads();
+    for (int c = threadIdx.x; c < a.ntot; c += blockDim.x)
+      a.cells[((int64_t)p * a.ntot + c) * a.S + sl] = sm_cnt[c];
+  }
 }
 
 constexpr int CSR_HIST_CTAS = 148;
@@ -481,6 +517,12 @@ static cudaError_t grow(T*& p, int64_t& cap, int64_t need) {
   } while (0)
 
 // ---------------------------------------------------------------- tensor-core head
+// CTA b owns block rows [b·rows/G, (b+1)·rows/G)
+__device__ __forceinline__ void cta_rows(int rows, int& r0, int& r1) {
+  r0 = (int)(((int64_t)blockIdx.x * rows) / gridDim.x);
+  r1 = (int)(((int64_t)(blockIdx.x + 1) * rows) / gridDim.x);
+}
+
 // column counts over the block (global column index: A then B)
 __global__ void __launch_bounds__(CSR_T_THREADS)
 csr_colcount_kernel(const int64_t* __restrict__ arp, const int32_t* __restrict__ acol, int64_t a_n,
@@ -524,44 +566,13 @@ __global__ void csr_head_flag_kernel(const uint32_t* __restrict__ cnt, int ntot,
 
 // slot = exclusive scan of the flags (column order: deterministic)
 __global__ void csr_head_map_kernel(const uint32_t* __restrict__ flag, const uint32_t* __restrict__ scan,
-                                    int ntot, int32_t* __restrict__ lut, int32_t* __restrict__ map,
+                                    int ntot, uint16_t* __restrict__ lut, int32_t* __restrict__ map,
                                     uint32_t* __restrict__ total) {
   for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < ntot; c += gridDim.x * blockDim.x) {
-    const int32_t slot = flag[c] ? (int32_t)scan[c] : -1;
-    lut[c] = slot;
-    if (slot >= 0) map[slot] = c;
+    // slots < ntot <= CSR_HIST_MAX_COLS < 0xFFFF
+    lut[c] = flag[c] ? (uint16_t)scan[c] : CSR_NO_SLOT;
+    if (flag[c]) map[scan[c]] = c;
     if (c == ntot - 1) *total = scan[c] + flag[c];
-  }
-}
-
-// X_head[t - r0][slot] = bf16(v) for head nonzeros of rows [r0, r0 + rows)
-__global__ void __launch_bounds__(256)
-csr_densify_kernel(const int64_t* __restrict__ arp, const int32_t* __restrict__ acol,
-                   const float* __restrict__ aval, int64_t a_n, const int64_t* __restrict__ brp,
-                   const int32_t* __restrict__ bcol, const float* __restrict__ bval, int64_t b_n,
-                   int64_t r0, int rows, const int32_t* __restrict__ lut, int64_t ldh,
-                   uint16_t* __restrict__ xh) {
-  const int lane = threadIdx.x & 31;
-  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
-  for (int64_t task = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); task < 2 * (int64_t)rows;
-       task += nw) {
-    const int mat = (int)(task & 1);
-    const int64_t r = task >> 1;
-    const int64_t* rp = mat == 0 ? arp : brp;
-    if (!rp) continue;
-    const int32_t* col = mat == 0 ? acol : bcol;
-    const float* val = mat == 0 ? aval : bval;
-    const int64_t ncols = mat == 0 ? a_n : b_n;
-    const uint32_t cofs = mat == 0 ? 0u : (uint32_t)a_n;
-    const int64_t base = rp[0];
-    const int64_t e0 = rp[r0 + r] - base, e1 = rp[r0 + r + 1] - base;
-    for (int64_t e = e0 + lane; e < e1; e += 32) {
-      const int32_t c = col[e];
-      if (c < 0 || c >= ncols) continue;
-      const float v = val[e];
-      const uint32_t cg = (uint32_t)c + cofs;
-      if (is_head(lut, cg, v)) xh[r * ldh + lut[cg]] = (uint16_t)(__float_as_uint(v) >> 16);
-    }
   }
 }
 
@@ -601,17 +612,6 @@ cudaError_t csr_select_head(CsrWorkspace& w, const int64_t* a_rowptr, const int3
   return cudaGetLastError();
 }
 
-cudaError_t csr_densify(CsrWorkspace& w, const int64_t* a_rowptr, const int32_t* a_col, const float* a_val,
-                        int64_t a_n, const int64_t* b_rowptr, const int32_t* b_col, const float* b_val,
-                        int64_t b_n, int64_t r0, int64_t rows, int64_t ldh, uint16_t* xh, cudaStream_t st) {
-  CSR_TRY(cudaMemsetAsync(xh, 0, (size_t)(((rows + 63) / 64) * 64) * ldh * 2, st));
-  const int blocks = (int)std::min<int64_t>((2 * rows + 7) / 8, 148 * 32);
-  csr_densify_kernel<<<blocks, 256, 0, st>>>(a_rowptr, a_col, a_val, a_n, b_rowptr, b_col, b_val, b_n, r0,
-                                             (int)rows, w.head_lut, ldh, xh);
-  w.launches += 1;
-  return cudaGetLastError();
-}
-
 // ---------------------------------------------------------------- driver
 __global__ void csr_bounds_kernel(const int64_t* __restrict__ arp, const int64_t* __restrict__ brp,
                                   int64_t rbase, int rows, int rp, int npan, int64_t* __restrict__ out) {
@@ -643,8 +643,7 @@ __global__ void pi_transpose_kernel(const uint16_t* __restrict__ pi, int kp, int
 }
 
 void csr_workspace_free(CsrWorkspace& w) {
-  cudaFree(w.pi); cudaFree(w.keys_in); cudaFree(w.keys_out); cudaFree(w.vals_in);
-  cudaFree(w.vals_out); cudaFree(w.cub_tmp); cudaFree(w.bounds_d); cudaFree(w.hist); cudaFree(w.offs);
+  cudaFree(w.pi); cudaFree(w.kv_in); cudaFree(w.kv_out); cudaFree(w.cub_tmp); cudaFree(w.bounds_d); cudaFree(w.hist); cudaFree(w.offs);
   cudaFree(w.ne_dev); cudaFree(w.head_lut); cudaFree(w.head_map); cudaFree(w.head_cnt); cudaFree(w.head_flag);
   cudaFree(w.xhead); cudaFree(w.head_tmp); cudaFree(w.kmaj);
   if (w.head_h) cudaFreeHost(w.head_h);
@@ -689,8 +688,9 @@ cudaError_t launch_sketch_csr(CsrWorkspace& w, int kind, uint64_t seed, int k, i
                               int64_t rows, const int64_t* a_rowptr, const int32_t* a_col,
                               const float* a_val, int64_t a_n, const int64_t* b_rowptr,
                               const int32_t* b_col, const float* b_val, int64_t b_n, float* acc_sk,
-                              double* acc_nrm, int* status, cudaStream_t st, const int32_t* head_lut,
-                              int64_t rbase, uint16_t* kmaj, int64_t kmaj_ld, int kpad) {
+                              double* acc_nrm, int* status, cudaStream_t st, const uint16_t* head_lut,
+                              int64_t rbase, uint16_t* kmaj, int64_t kmaj_ld, int kpad, uint16_t* xh,
+                              int64_t ldh, int n_head) {
   if (rows <= 0) return cudaSuccess;
   const int64_t ntot = a_n + (b_rowptr ? b_n : 0);
   const int cbits = bits_for(ntot - 1 > 0 ? ntot - 1 : 1);
@@ -731,45 +731,23 @@ cudaError_t launch_sketch_csr(CsrWorkspace& w, int kind, uint64_t seed, int k, i
   const int end_bit = tbits + cbits;
   const bool counting = ntot <= CSR_HIST_MAX_COLS;
   if (!counting) head_lut = nullptr;  // (the caller only selects heads when counting)
-  if (!counting) {
-    CSR_TRY(grow(w.keys_in, w.ent_cap_ki, max_ent));
-    CSR_TRY(grow(w.vals_in, w.ent_cap_vi, max_ent));
-  }
-  CSR_TRY(grow(w.keys_out, w.ent_cap_ko, max_ent));
-  CSR_TRY(grow(w.vals_out, w.ent_cap_vo, max_ent));
-  size_t need = 0;
-  if (counting) {
-    // w.offs = [colbase (ntot) | pre (G x ntot)], w.hist = colsum (ntot) scratch
-    const int64_t nh = ntot * (int64_t)CSR_HIST_CTAS;
-    CSR_TRY(grow(w.hist, w.hist_cap, ntot));
-    CSR_TRY(grow(w.offs, w.offs_cap, ntot + nh));
-    CSR_TRY(grow(w.ne_dev, w.ne_cap, 1));
-    CSR_TRY(cub::DeviceScan::ExclusiveSum(nullptr, need, w.hist, w.offs, (int)ntot, st));
-    static PerDeviceOnce attr;
-    if (attr.need()) {
-      CSR_TRY(cudaFuncSetAttribute(csr_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   227 * 1024));
-      CSR_TRY(cudaFuncSetAttribute(csr_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   227 * 1024));
-    }
-  } else {
-    CSR_TRY(cub::DeviceRadixSort::SortPairs(nullptr, need, w.keys_in, w.keys_out, w.vals_in, w.vals_out,
-                                            (int)std::max<int64_t>(max_ent, 1), 0, end_bit, st));
-  }
-  CSR_TRY(grow(w.cub_tmp, w.cub_cap, (int64_t)need));
-  // diagnostics (SMP_CSR_PROFILE=1): device time per K3 stage, summed over panels
+  if (!counting) xh = nullptr;
+  // diagnostics (SMP_CSR_PROFILE=1): device time per K3 stage, summed over
+  // panels — one event per stage boundary, read after the last (no syncs)
   const char* prof_env = getenv("SMP_CSR_PROFILE");
   const bool prof = prof_env && atoi(prof_env);
-  cudaEvent_t pev[5] = {};
-  float pms[4] = {0.f, 0.f, 0.f, 0.f};
-  if (prof)
-    for (int i = 0; i < 5; ++i) CSR_TRY(cudaEventCreate(&pev[i]));
-  for (int p = 0; p < npan; ++p) {
+  std::vector<std::pair<cudaEvent_t, int>> pev;  // (event, slot of the stage it ends)
+  float pms[3] = {0.f, 0.f, 0.f};  // sort (+ fused head densify), Π panel, accumulate
+  auto lap = [&](int slot) -> cudaError_t {
+    if (!prof) return cudaSuccess;
+    cudaEvent_t e;
+    CSR_TRY(cudaEventCreate(&e));
+    CSR_TRY(cudaEventRecord(e, st));
+    pev.emplace_back(e, slot);
+    return cudaSuccess;
+  };
+  auto gen_panel = [&](int p, int prow) {
     const int64_t p0 = (int64_t)p * rp;
-    if (prof) CSR_TRY(cudaEventRecord(pev[0], st));
-    const int prow = (int)std::min<int64_t>(rp, rows - p0);
-    const int64_t na = ab[p + 1] - ab[p], nb = bb[p + 1] - bb[p];
-    const int64_t ne = na + nb;
     if (kind == PI_GAUSSIAN && ((row0 + p0) & 3) == 0 && (kp & 1) == 0) {
       // one generation, both layouts (the head panel when kmaj is given)
       const int kcols = std::max(kp, kmaj ? kpad : 0);
@@ -786,46 +764,13 @@ cudaError_t launch_sketch_csr(CsrWorkspace& w, int kind, uint64_t seed, int k, i
         w.launches += 1;
       }
     }
-    const int64_t pr = rbase + p0;   // rowptr index of the panel's first row
-    if (prof) CSR_TRY(cudaEventRecord(pev[1], st));
-    if (ne == 0) continue;
-    if (counting) {
-      // head-column flags in SMEM beside the counters when they fit (no
-      // global lut gather per nonzero)
-      const int64_t srp_bytes = (int64_t)((prow + CSR_HIST_CTAS - 1) / CSR_HIST_CTAS + 2) * 8;
-      const int sflags = (head_lut && ntot * 5 + 8 + srp_bytes <= 227 * 1024) ? 1 : 0;
-      const size_t sm = (size_t)ntot * 4 + (sflags ? (((size_t)ntot + 15) & ~(size_t)15) : 0);
-      csr_hist_kernel<<<CSR_HIST_CTAS, CSR_T_THREADS, sm, st>>>(a_rowptr, a_col, a_val, a_n, b_rowptr,
-                                                                b_col, b_val, b_n, pr, prow, (int)ntot,
-                                                                head_lut, sflags, w.offs + ntot);
-      csr_colscan_kernel<<<(int)((ntot + 255) / 256), 256, 0, st>>>(w.offs + ntot, (int)ntot, CSR_HIST_CTAS,
-                                                                    w.hist);
-      size_t tmp = (size_t)w.cub_cap;
-      CSR_TRY(cub::DeviceScan::ExclusiveSum(w.cub_tmp, tmp, w.hist, w.offs, (int)ntot, st));
-      const int max_rows_cta = (prow + CSR_HIST_CTAS - 1) / CSR_HIST_CTAS + 1;
-      const size_t sm_sc = (size_t)((ntot + 1) & ~1) * 4 + (size_t)(max_rows_cta + 1) * 8 +
-                           (sflags ? (size_t)ntot : 0);
-      csr_scatter_kernel<<<CSR_HIST_CTAS, CSR_T_THREADS, sm_sc, st>>>(a_rowptr, a_col, a_val, a_n, b_rowptr,
-                                                                   b_col, b_val, b_n, pr, prow, (int)ntot,
-                                                                   tbits, head_lut, sflags, w.offs, w.keys_out,
-                                                                   w.vals_out, status);
-      csr_total_kernel<<<1, 32, 0, st>>>(w.hist, w.offs, ntot, w.ne_dev);
-    } else {
-      const int kb_blocks = (int)std::min<int64_t>((prow + 7) / 8, 148 * 16);
-      // A: entries ab[p] .. ab[p+1] (relative to a_rowptr[0]) -> keys[0 .. na)
-      csr_keys_kernel<<<kb_blocks, 256, 0, st>>>(a_rowptr, a_col, a_val, pr, prow, ab[p], 0u, tbits,
-                                                 a_n, w.keys_in, w.vals_in, status);
-      if (b_rowptr && nb > 0)
-        csr_keys_kernel<<<kb_blocks, 256, 0, st>>>(b_rowptr, b_col, b_val, pr, prow, bb[p] - na,
-                                                   (uint32_t)a_n, tbits, b_n, w.keys_in, w.vals_in, status);
-      size_t tmp = (size_t)w.cub_cap;
-      CSR_TRY(cub::DeviceRadixSort::SortPairs(w.cub_tmp, tmp, w.keys_in, w.keys_out, w.vals_in, w.vals_out,
-                                              (int)ne, 0, end_bit, st));
-    }
-    if (prof) CSR_TRY(cudaEventRecord(pev[2], st));
+    w.launches += 1;
+  };
+  auto accumulate = [&](int64_t ne, const uint32_t* sb, const uint32_t* se) -> cudaError_t {
     const int64_t tasks = (ne + CSR_CHUNK - 1) / CSR_CHUNK;
-    const int ablocks = (int)std::min<int64_t>((tasks + 7) / 8, 148 * 64);
-    const int kv = (kp + 255) / 256;
+    const int ablocks = (int)std::max<int64_t>(1, std::min<int64_t>((tasks + 7) / 8, 148 * 64));
+    const int kvw = (kp + 255) / 256;
+    const uint2* kv = reinterpret_cast<const uint2*>(w.kv_out);
     if (w.ev_pool) {
       while (w.ev_pool->size() < *w.ev_used + 2) {
         cudaEvent_t ev;
@@ -834,35 +779,159 @@ cudaError_t launch_sketch_csr(CsrWorkspace& w, int kind, uint64_t seed, int k, i
       }
       CSR_TRY(cudaEventRecord((*w.ev_pool)[*w.ev_used], st));
     }
-    switch (kv) {
-      case 1: csr_accumulate_kernel<1><<<ablocks, 256, 0, st>>>(w.keys_out, w.vals_out, ne, w.pi, kp, k, tbits, acc_sk, acc_nrm, 1, counting ? w.ne_dev : nullptr); break;
-      case 2: csr_accumulate_kernel<2><<<ablocks, 256, 0, st>>>(w.keys_out, w.vals_out, ne, w.pi, kp, k, tbits, acc_sk, acc_nrm, 1, counting ? w.ne_dev : nullptr); break;
-      case 3: case 4: csr_accumulate_kernel<4><<<ablocks, 256, 0, st>>>(w.keys_out, w.vals_out, ne, w.pi, kp, k, tbits, acc_sk, acc_nrm, 1, counting ? w.ne_dev : nullptr); break;
-      case 5: case 6: case 7: case 8: csr_accumulate_kernel<8><<<ablocks, 256, 0, st>>>(w.keys_out, w.vals_out, ne, w.pi, kp, k, tbits, acc_sk, acc_nrm, 1, counting ? w.ne_dev : nullptr); break;
-      default: csr_accumulate_kernel<16><<<ablocks, 256, 0, st>>>(w.keys_out, w.vals_out, ne, w.pi, kp, k, tbits, acc_sk, acc_nrm, 1, counting ? w.ne_dev : nullptr); break;
+    switch (kvw) {
+      case 1: csr_accumulate_kernel<1><<<ablocks, 256, 0, st>>>(kv, ne, w.pi, kp, k, tbits, acc_sk, acc_nrm, 1, sb, se); break;
+      case 2: csr_accumulate_kernel<2><<<ablocks, 256, 0, st>>>(kv, ne, w.pi, kp, k, tbits, acc_sk, acc_nrm, 1, sb, se); break;
+      case 3: case 4: csr_accumulate_kernel<4><<<ablocks, 256, 0, st>>>(kv, ne, w.pi, kp, k, tbits, acc_sk, acc_nrm, 1, sb, se); break;
+      case 5: case 6: case 7: case 8: csr_accumulate_kernel<8><<<ablocks, 256, 0, st>>>(kv, ne, w.pi, kp, k, tbits, acc_sk, acc_nrm, 1, sb, se); break;
+      default: csr_accumulate_kernel<16><<<ablocks, 256, 0, st>>>(kv, ne, w.pi, kp, k, tbits, acc_sk, acc_nrm, 1, sb, se); break;
     }
     CSR_TRY(cudaGetLastError());
     if (w.ev_pool) {
       CSR_TRY(cudaEventRecord((*w.ev_pool)[*w.ev_used + 1], st));
       *w.ev_used += 2;
     }
-    // Π panel + (counting: hist, colscan, 2 CUB scan kernels, scatter, total;
-    // radix: 1-2 key kernels + CUB sort passes) + accumulate
-    w.launches += counting ? 1 + 6 + 1 : 1 + 1 + (b_rowptr && nb > 0 ? 1 : 0) + 4 + 1;
-    if (prof) {
-      CSR_TRY(cudaEventRecord(pev[3], st));
-      CSR_TRY(cudaEventSynchronize(pev[3]));
-      for (int i = 0; i < 3; ++i) {
-        float ms = 0.f;
-        CSR_TRY(cudaEventElapsedTime(&ms, pev[i], pev[i + 1]));
-        pms[i] += ms;
+    w.launches += 1;
+    return cudaSuccess;
+  };
+  CSR_TRY(grow(w.pi, w.pi_cap, (int64_t)rp * kp));
+  CSR_TRY(lap(-1));
+  if (counting) {
+    // groups of consecutive panels with at most max(2^24, largest panel)
+    // entries: the group's sorted tail (8 B per entry) then stays L2-resident
+    // between the scatter and K3d
+    const int64_t cap = std::max<int64_t>(max_ent, 1ll << 24);
+    int gmax = 1;
+    for (int g0 = 0; g0 < npan;) {
+      int g1 = g0 + 1;
+      while (g1 < npan && (ab[g1 + 1] - ab[g0]) + (bb[g1 + 1] - bb[g0]) <= cap) ++g1;
+      gmax = std::max(gmax, g1 - g0);
+      g0 = g1;
+    }
+    // slices per panel: about one CTA per SM over the group, at most max_nr rows each
+    int dev = 0, nsm = 148;
+    CSR_TRY(cudaGetDevice(&dev));
+    CSR_TRY(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    // SMEM: counters (4 B) + head slots (2 B) per column when they fit + slice row offsets
+    const bool lut_smem = head_lut && ntot * 6 <= 160 * 1024;
+    const int64_t fixed = ntot * 4 + (lut_smem ? ((ntot + 1) / 2) * 4 : 0);
+    const int max_nr = (int)std::min<int64_t>(rp, (227 * 1024 - fixed) / 8 - 2);
+    if (max_nr < 64) return cudaErrorInvalidValue;
+    auto slices = [&](int gp) { return std::max({1, nsm / gp, (rp + max_nr - 1) / max_nr}); };
+    int64_t cells_max = 1;
+    for (int g = 1; g <= gmax; ++g) cells_max = std::max<int64_t>(cells_max, (int64_t)g * ntot * slices(g) + 1);
+    const size_t smem = (size_t)fixed + (size_t)(std::min(rp, (rp + slices(gmax) - 1) / slices(gmax) + 1) + 1) * 8;
+    CSR_TRY(grow(w.kv_out, w.ent_cap_ko, cap));
+    CSR_TRY(grow(w.hist, w.hist_cap, cells_max));
+    CSR_TRY(grow(w.offs, w.offs_cap, cells_max));
+    size_t need = 0;
+    CSR_TRY(cub::DeviceScan::ExclusiveSum(nullptr, need, w.hist, w.offs, (int)cells_max, st));
+    CSR_TRY(grow(w.cub_tmp, w.cub_cap, (int64_t)need));
+    static PerDeviceOnce attr;
+    if (attr.need()) {
+      CSR_TRY(cudaFuncSetAttribute(csr_sort_pass_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   227 * 1024));
+      CSR_TRY(cudaFuncSetAttribute(csr_sort_pass_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   227 * 1024));
+    }
+    for (int g0 = 0; g0 < npan;) {
+      int g1 = g0 + 1;
+      while (g1 < npan && (ab[g1 + 1] - ab[g0]) + (bb[g1 + 1] - bb[g0]) <= cap) ++g1;
+      const int gp = g1 - g0;
+      const int64_t r0g = (int64_t)g0 * rp;
+      const int grows = (int)(std::min<int64_t>((int64_t)g1 * rp, rows) - r0g);
+      if ((ab[g1] - ab[g0]) + (bb[g1] - bb[g0]) > 0) {
+        CsrSortArgs sa{};
+        sa.arp = a_rowptr; sa.acol = a_col; sa.aval = a_val; sa.a_n = a_n;
+        sa.brp = b_rowptr; sa.bcol = b_col; sa.bval = b_val; sa.b_n = b_n;
+        sa.pr = rbase + r0g;
+        sa.rows = grows;
+        sa.tbits = tbits;
+        sa.ntot = (int)ntot;
+        sa.S = slices(gp);
+        sa.lut = head_lut;
+        sa.lut_smem = lut_smem ? 1 : 0;
+        sa.status = status;
+        sa.xh = xh;
+        sa.ldh = ldh;
+        sa.xrow = r0g;
+        sa.n_head = n_head;
+        const int64_t cells = (int64_t)gp * ntot * sa.S;
+        dim3 grid((unsigned)sa.S, (unsigned)gp);
+        sa.cells = w.hist;
+        csr_sort_pass_kernel<false><<<grid, CSR_T_THREADS, smem, st>>>(sa);
+        CSR_TRY(cudaMemsetAsync(w.hist + cells, 0, 4, st));  // total at offs[cells]
+        size_t tmp = (size_t)w.cub_cap;
+        CSR_TRY(cub::DeviceScan::ExclusiveSum(w.cub_tmp, tmp, w.hist, w.offs, (int)(cells + 1), st));
+        sa.cells = w.offs;
+        sa.kv = reinterpret_cast<uint2*>(w.kv_out);
+        csr_sort_pass_kernel<true><<<grid, CSR_T_THREADS, smem, st>>>(sa);
+        CSR_TRY(cudaGetLastError());
+        w.launches += 4;
+        CSR_TRY(lap(0));
+        for (int p = g0; p < g1; ++p) {
+          const int prow = (int)std::min<int64_t>(rp, rows - (int64_t)p * rp);
+          gen_panel(p, prow);
+          CSR_TRY(lap(1));
+          const int64_t ne = (ab[p + 1] - ab[p]) + (bb[p + 1] - bb[p]);
+          if (ne == 0) continue;
+          // panel p of the group: cells [(p - g0)·ntot·S, (p - g0 + 1)·ntot·S)
+          const int64_t q = (int64_t)(p - g0) * ntot * sa.S;
+          CSR_TRY(accumulate(ne, w.offs + q, w.offs + q + ntot * sa.S));
+          CSR_TRY(lap(2));
+        }
+      } else {
+        if (xh && grows > 0)
+          CSR_TRY(cudaMemset2DAsync(xh + r0g * ldh, (size_t)ldh * 2, 0, (size_t)n_head * 2, (size_t)grows, st));
+        CSR_TRY(lap(0));
+        for (int p = g0; p < g1; ++p) {  // Π panels still feed the head's κ-major panel
+          gen_panel(p, (int)std::min<int64_t>(rp, rows - (int64_t)p * rp));
+          CSR_TRY(lap(1));
+        }
       }
+      g0 = g1;
+    }
+  } else {
+    CSR_TRY(grow(w.kv_in, w.ent_cap_ki, max_ent));
+    CSR_TRY(grow(w.kv_out, w.ent_cap_ko, max_ent));
+    size_t need = 0;
+    CSR_TRY(cub::DeviceRadixSort::SortKeys(nullptr, need, w.kv_in, w.kv_out, (int)std::max<int64_t>(max_ent, 1),
+                                           32, 32 + end_bit, st));
+    CSR_TRY(grow(w.cub_tmp, w.cub_cap, (int64_t)need));
+    for (int p = 0; p < npan; ++p) {
+      const int64_t p0 = (int64_t)p * rp;
+      const int prow = (int)std::min<int64_t>(rp, rows - p0);
+      const int64_t na = ab[p + 1] - ab[p], nb = bb[p + 1] - bb[p];
+      const int64_t ne = na + nb;
+      gen_panel(p, prow);
+      CSR_TRY(lap(1));
+      if (ne == 0) continue;
+      const int64_t pr = rbase + p0;  // rowptr index of the panel's first row
+      const int kb_blocks = (int)std::min<int64_t>((prow + 7) / 8, 148 * 16);
+      // A: entries ab[p] .. ab[p+1] (relative to a_rowptr[0]) -> kv[0 .. na)
+      csr_keys_kernel<<<kb_blocks, 256, 0, st>>>(a_rowptr, a_col, a_val, pr, prow, ab[p], 0u, tbits,
+                                                 a_n, w.kv_in, status);
+      if (b_rowptr && nb > 0)
+        csr_keys_kernel<<<kb_blocks, 256, 0, st>>>(b_rowptr, b_col, b_val, pr, prow, bb[p] - na,
+                                                   (uint32_t)a_n, tbits, b_n, w.kv_in, status);
+      size_t tmp = (size_t)w.cub_cap;
+      CSR_TRY(cub::DeviceRadixSort::SortKeys(w.cub_tmp, tmp, w.kv_in, w.kv_out, (int)ne, 32, 32 + end_bit, st));
+      w.launches += 1 + (b_rowptr && nb > 0 ? 1 : 0) + 4;
+      CSR_TRY(lap(0));
+      CSR_TRY(accumulate(ne, nullptr, nullptr));
+      CSR_TRY(lap(2));
     }
   }
   if (prof) {
-    fprintf(stderr, "K3 stages over %d panels: pi panel %.3f ms, transpose %.3f ms, accumulate %.3f ms\n",
-            npan, pms[0], pms[1], pms[2]);
-    for (int i = 0; i < 5; ++i) cudaEventDestroy(pev[i]);
+    if (!pev.empty()) CSR_TRY(cudaEventSynchronize(pev.back().first));
+    for (size_t i = 1; i < pev.size(); ++i) {
+      float ms = 0.f;
+      CSR_TRY(cudaEventElapsedTime(&ms, pev[i - 1].first, pev[i].first));
+      if (pev[i].second >= 0) pms[pev[i].second] += ms;
+    }
+    for (auto& e : pev) cudaEventDestroy(e.first);
+    fprintf(stderr, "K3 stages over %d panels: sort%s %.3f ms, pi panel %.3f ms, accumulate %.3f ms\n", npan,
+            xh ? " + head densify" : "", pms[0], pms[1], pms[2]);
   }
   return cudaGetLastError();
 }

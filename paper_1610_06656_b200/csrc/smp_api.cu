@@ -19,14 +19,6 @@
 
 cudaError_t smp_convert_f64_f32(const double* x, int64_t n, float* y, cudaStream_t st);
 
-namespace smp {
-cudaError_t launch_sketch_csr(int kind, uint64_t seed, int k, int64_t row0, int64_t rows,
-                              const int64_t* a_rowptr, const int32_t* a_col, const float* a_val,
-                              int64_t a_n, float* a_acc, double* a_nrm, const int64_t* b_rowptr,
-                              const int32_t* b_col, const float* b_val, int64_t b_n, float* b_acc,
-                              double* b_nrm, cudaStream_t st);
-}
-
 struct smp_handle {
   smp_sketch_desc d;
   cudaStream_t st = nullptr;
@@ -651,12 +643,12 @@ smp_status smp_sketch_block_csr(smp_handle* h, int64_t row0, int64_t rows, const
   h->csr.ev_used = &h->ev_used_n;
   // tensor-core head (K3): columns with density >= δ whose
   // nonzeros are small integers go through K1 as a dense bf16 matrix
-  static const double head_density = [] {
+  const double head_density = [] {  // read per call (tests switch it)
     const char* e = getenv("SMP_CSR_HEAD_DENSITY");
     return e ? atof(e) : 0.02;
   }();
   const int64_t a_n = h->n1, b_n = two ? h->n2 : 0;
-  const int32_t* lut = nullptr;
+  const uint16_t* lut = nullptr;
   if (head_density > 0.0) {
     int n_head = 0;
     CK(h, smp::csr_select_head(h->csr, a_rowptr, a_col, a_n, two ? b_rowptr : nullptr,
@@ -665,7 +657,7 @@ smp_status smp_sketch_block_csr(smp_handle* h, int64_t row0, int64_t rows, const
     if (n_head > 0) {
       // per head chunk: the tail K3 over the chunk's rows (which generates
       // each Π panel once and also transposes it into the κ-major head panel),
-      // then densify + K1 (PANEL) on the head with that panel
+      // then K1 (PANEL) on the head chunk that the same pass densified
       lut = h->csr.head_lut;
       const int64_t ldh = ((n_head + 63) / 64) * 64;
       const int64_t kpad = ((h->k + 255) / 256) * 256;
@@ -678,7 +670,7 @@ smp_status smp_sketch_block_csr(smp_handle* h, int64_t row0, int64_t rows, const
       CK(h, ensure(h->csr.kmaj, h->csr.kmaj_cap, kpad * cpad), "alloc head panel");
       h->csr.ev_pool = h->timing ? &h->ev_pool : nullptr;
       CK(h, smp::csr_bounds(h->csr, a_rowptr, two ? b_rowptr : nullptr, a_n + b_n, rows, h->st), "bounds");
-      // SMP_CSR_PROFILE=1: device time of the head (densify, K1 + K2) per call
+      // SMP_CSR_PROFILE=1: device time of the head's K1 + K2 per call
       const char* hp = getenv("SMP_CSR_PROFILE");
       const bool hprof = hp && atoi(hp);
       cudaEvent_t hev[3] = {};
@@ -689,18 +681,14 @@ smp_status smp_sketch_block_csr(smp_handle* h, int64_t row0, int64_t rows, const
         const int64_t rc = std::min(chunk, rows - r0);
         const int64_t ldk = ((rc + 63) / 64) * 64;
         if (rc != ldk) CK(h, cudaMemsetAsync(h->csr.kmaj, 0, kpad * ldk * 2, h->st), "memset");
+        // the tail sort also densifies the head entries of these rows into xhead
         cudaError_t e1 = smp::launch_sketch_csr(h->csr, pi_code(h), h->d.seed, h->k, row0 + r0, rc, a_rowptr,
                                                 a_col, a_val, h->n1, two ? b_rowptr : nullptr,
                                                 two ? b_col : nullptr, two ? b_val : nullptr, b_n,
                                                 h->acc_sk, h->acc_nrm, h->status, h->st, lut, r0,
-                                                h->csr.kmaj, ldk, (int)kpad);
+                                                h->csr.kmaj, ldk, (int)kpad, h->csr.xhead, ldh, n_head);
         if (e1 != cudaSuccess) h->csr.bounds_pre = false;
         CK(h, e1, "sketch_csr");
-        if (hprof) CK(h, cudaEventRecord(hev[0], h->st), "event");
-        CK(h, smp::csr_densify(h->csr, a_rowptr, a_col, a_val, a_n, two ? b_rowptr : nullptr,
-                               two ? b_col : nullptr, two ? b_val : nullptr, b_n, r0, rc, ldh,
-                               h->csr.xhead, h->st),
-           "densify");
         if (hprof) CK(h, cudaEventRecord(hev[1], h->st), "event");
         smp_status s2 = sketch_dense_bf16(h, row0 + r0, rc, h->csr.xhead, ldh, n_head, 1, 0, true,
                                           h->csr.kmaj, h->csr.head_map);
@@ -708,16 +696,14 @@ smp_status smp_sketch_block_csr(smp_handle* h, int64_t row0, int64_t rows, const
         if (hprof) {
           CK(h, cudaEventRecord(hev[2], h->st), "event");
           CK(h, cudaEventSynchronize(hev[2]), "sync");
-          float a = 0.f, b = 0.f;
-          cudaEventElapsedTime(&a, hev[0], hev[1]);
+          float b = 0.f;
           cudaEventElapsedTime(&b, hev[1], hev[2]);
-          hms[0] += a;
           hms[1] += b;
         }
       }
       if (hprof) {
-        fprintf(stderr, "K3 head over %lld rows (%d columns): densify %.3f ms, K1+K2 %.3f ms\n",
-                (long long)rows, n_head, hms[0], hms[1]);
+        fprintf(stderr, "K3 head over %lld rows (%d columns): K1+K2 %.3f ms\n", (long long)rows, n_head,
+                hms[1]);
         for (int i = 0; i < 3; ++i) cudaEventDestroy(hev[i]);
       }
       h->csr.bounds_pre = false;

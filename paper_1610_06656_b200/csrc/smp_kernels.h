@@ -60,20 +60,18 @@ cudaError_t launch_pairwise_sum(const double* x, int64_t n, double* scratch, dou
 struct CsrWorkspace {
   uint16_t* pi = nullptr;         // Π panel, Rp x kp bf16
   int64_t pi_cap = 0;
-  uint32_t* keys_in = nullptr;
-  uint32_t* keys_out = nullptr;
-  float* vals_in = nullptr;
-  float* vals_out = nullptr;
-  int64_t ent_cap_ki = 0, ent_cap_ko = 0, ent_cap_vi = 0, ent_cap_vo = 0;
+  uint64_t* kv_in = nullptr;      // packed (key << 32 | value bits) per tail nonzero
+  uint64_t* kv_out = nullptr;     // ... sorted by key (K3d input)
+  int64_t ent_cap_ki = 0, ent_cap_ko = 0;
   uint8_t* cub_tmp = nullptr;
   int64_t cub_cap = 0;
-  uint32_t* hist = nullptr;       // counting sort: [ntot][CTAs] counts and offsets
+  uint32_t* hist = nullptr;       // counting sort: (panel, column, slice) counts, then starts
   uint32_t* offs = nullptr;
   int64_t hist_cap = 0, offs_cap = 0;
   uint32_t* ne_dev = nullptr;     // [0] tail entries of the panel, [1] head columns
   int64_t ne_cap = 0;
   // tensor-core head (columns with density >= SMP_CSR_HEAD_DENSITY)
-  int32_t* head_lut = nullptr;    // [ntot] slot or -1
+  uint16_t* head_lut = nullptr;   // [ntot] slot or 0xFFFF (tail column)
   int32_t* head_map = nullptr;    // [slots] global column
   uint32_t* head_cnt = nullptr;
   uint32_t* head_flag = nullptr;  // [2 ntot]: flags, scan
@@ -108,11 +106,15 @@ cudaError_t launch_sketch_csr(CsrWorkspace& w, int kind, uint64_t seed, int k, i
                               const float* a_val, int64_t a_n, const int64_t* b_rowptr,
                               const int32_t* b_col, const float* b_val, int64_t b_n, float* acc_sk,
                               double* acc_nrm, int* status, cudaStream_t st,
-                              const int32_t* head_lut = nullptr, int64_t rbase = 0,
-                              uint16_t* kmaj = nullptr, int64_t kmaj_ld = 0, int kpad = 0);
+                              const uint16_t* head_lut = nullptr, int64_t rbase = 0,
+                              uint16_t* kmaj = nullptr, int64_t kmaj_ld = 0, int kpad = 0,
+                              uint16_t* xh = nullptr, int64_t ldh = 0, int n_head = 0);
 // (rbase: the call covers rowptr rows [rbase, rbase + rows) of the block,
-// global row0 = the global row of rowptr row rbase; kmaj: also transpose each
-// generated Π panel into kmaj[κ][t - row0] (ld kmaj_ld, kpad κ rows) for K1)
+// global row0 = the global row of rowptr row rbase; kmaj: also write each
+// generated Π panel into kmaj[κ][t - row0] (ld kmaj_ld, kpad κ rows) for K1;
+// xh: the head entries (head_lut) of row t - row0 go to xh[(t - row0) * ldh +
+// slot] as bf16, slots [0, n_head) of every row zeroed first — the dense head
+// chunk K1 reads, built by the same pass that sorts the tail)
 void csr_workspace_free(CsrWorkspace& w);
 int csr_panel_rows(int64_t ntot);  // rows of one K3 Π panel (2^15 for up to 2^17 columns)
 // read back every panel's entry boundaries for rows [0, rows) of the block
@@ -125,10 +127,6 @@ cudaError_t csr_bounds(CsrWorkspace& w, const int64_t* a_rowptr, const int64_t* 
 cudaError_t csr_select_head(CsrWorkspace& w, const int64_t* a_rowptr, const int32_t* a_col, int64_t a_n,
                             const int64_t* b_rowptr, const int32_t* b_col, int64_t b_n, int64_t rows,
                             double density, int* n_head, cudaStream_t st);
-// dense bf16 head chunk [rows][ldh] for rows [r0, r0 + rows) of the block
-cudaError_t csr_densify(CsrWorkspace& w, const int64_t* a_rowptr, const int32_t* a_col, const float* a_val,
-                        int64_t a_n, const int64_t* b_rowptr, const int32_t* b_col, const float* b_val,
-                        int64_t b_n, int64_t r0, int64_t rows, int64_t ldh, uint16_t* xh, cudaStream_t st);
 
 // ---- K5/K6 sampling and estimation (omega.cu)
 cudaError_t launch_alpha_beta(const double* a2, int64_t n1, const double* b2, int64_t n2,

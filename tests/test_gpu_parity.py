@@ -447,6 +447,39 @@ def test_sketch_csr_parity(d, n1, n2, za, zb, k, pi, row0, permute):
     assert np.array_equal(I.cpu().numpy(), Io) and np.array_equal(J.cpu().numpy(), Jo)
 
 
+@pytest.mark.parametrize("density,frac_vals", [
+    ("0", False),       # no tensor-core head: every nonzero through the sorted tail
+    ("1e-9", False),    # every non-empty column is a head column
+    ("0.02", True),     # head columns holding non-4-bit values: those entries stay in the tail
+])
+def test_sketch_csr_head_split_parity(density, frac_vals, monkeypatch):
+    """The head/tail split of K3 never changes the result:
+    the same CSR sketched with no head, an all-head split, and head columns
+    that carry values tcgen05 cannot take exactly (R21) all match the oracle."""
+    monkeypatch.setenv("SMP_CSR_HEAD_DENSITY", density)
+    d, n1, n2, k = 40000, 90, 70, 200
+    A = _csr(d, n1, 12, 8, 0)
+    B = _csr(d, n2, 9, 8, 1)
+    if frac_vals:   # every 7th entry gets a value with > 4 significant bits
+        for rp, col, val in (A, B):
+            val[::7] = val[::7] * 1.3 + 0.01
+    half = 20001   # a block boundary inside a Π panel, not 4-row aligned (generic Π panel path)
+    sk, fin = gpu_sketch_csr(d, n1, n2, k, PI["gaussian"], 13, A, B, splits=[(0, half), (half, d)])
+    skA, a2 = oracle.sketch_csr(PI["gaussian"], 13, k, n1, A[0].numpy(), A[1].numpy(), A[2].numpy())
+    skB, b2 = oracle.sketch_csr(PI["gaussian"], 13, k, n2, B[0].numpy(), B[1].numpy(), B[2].numpy())
+    As, _, _ = oracle.finalize(k, skA, a2)
+    Bs, _, _ = oracle.finalize(k, skB, b2)
+    ea = col_rel_err(fin["A_sk"], As)
+    eb = col_rel_err(fin["B_sk"], Bs)
+    assert ea.max() <= 1e-5 and eb.max() <= 1e-5, (ea.max(), eb.max())
+    if frac_vals:
+        np.testing.assert_allclose(fin["a_norm2"].cpu().numpy(), a2, rtol=1e-12)
+        np.testing.assert_allclose(fin["b_norm2"].cpu().numpy(), b2, rtol=1e-12)
+    else:
+        assert np.array_equal(fin["a_norm2"].cpu().numpy(), a2)
+        assert np.array_equal(fin["b_norm2"].cpu().numpy(), b2)
+
+
 def test_sketch_csr_bad_column_rejected():
     smp = _smp()
     d, n = 100, 10

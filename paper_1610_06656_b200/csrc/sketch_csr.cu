@@ -322,7 +322,8 @@ __device__ __forceinline__ bool is_4bit(float v) {
 // is one contiguous, column-grouped range for K3d.  Each panel is cut into S
 // row slices, one CTA per (panel, slice), about one CTA per SM over the
 // group: the CTA counts its slice's tail entries per column in SMEM (hist
-// pass), one scan over the (panel, column, slice) cells gives every CTA its
+// pass; counts stored CTA-contiguous), a prefix over the slices of every
+// (panel, column) cell plus one scan over the cells' totals give every CTA its
 // own base per column, and the scatter pass claims positions from SMEM
 // cursors.  A slice's entries are a contiguous range of each matrix, streamed
 // coalesced with CSR_MLP loads in flight per thread (the row of an entry,
@@ -335,7 +336,10 @@ __device__ __forceinline__ bool is_4bit(float v) {
 // cell follows the SMEM atomics; K3d's fp32 sums are order-dependent anyway
 // (DESIGN.md §7).
 constexpr int CSR_T_THREADS = 1024;
-constexpr int CSR_MLP = 4;
+#ifndef SMP_CSR_MLP
+#define SMP_CSR_MLP 8
+#endif
+constexpr int CSR_MLP = SMP_CSR_MLP;  // CSR loads in flight per thread (sort passes)
 
 // L2 eviction priorities: the CSR stream is read once (evict_first); the
 // sorted (value, key) pairs are written in pieces by many CTAs over the whole
@@ -366,9 +370,6 @@ __device__ __forceinline__ void st_hint_v2(uint2* p, uint2 v, uint64_t pol) {
                : "memory");
 }
 
-__device__ __forceinline__ uint32_t csr_cg(int32_t c, int64_t ncols, uint32_t cofs) {
-  return (uint32_t)(c < 0 || c >= ncols ? 0 : c) + cofs;
-}
 
 struct CsrSortArgs {
   const int64_t* arp;
@@ -386,7 +387,8 @@ struct CsrSortArgs {
   int S;                    // slices (CTAs) per panel
   const uint16_t* lut;      // head slot per column (CSR_NO_SLOT: tail), or null
   int lut_smem;             // stage lut in SMEM
-  uint32_t* cells;          // hist: counts, scatter: exclusive starts; index (p*ntot + c)*S + s
+  uint32_t* cnt;            // [(p*S + s)*ntot + c]: hist counts; scatter: prefix over earlier slices
+  const uint32_t* base;     // scatter: [p*ntot + c] start of cell (p, c) in kv
   uint2* kv;                // scatter: (value bits, key)
   int* status;
   uint16_t* xh;             // dense head chunk (null: no head)
@@ -394,11 +396,13 @@ struct CsrSortArgs {
   int n_head;
 };
 
-constexpr int CSR_SCATTER_RB = 64;  // scatter: rows per batch (head rows zeroed just before their values)
+constexpr int CSR_SCATTER_RB = 64;        // scatter: rows per batch (head rows zeroed just before their values)
+constexpr int CSR_ROWID_CAP = 24 * 1024;  // scatter: SMEM row ids of a batch's entries (else binary search)
 
 template <bool SCATTER>
 __global__ void __launch_bounds__(CSR_T_THREADS, 1) csr_sort_pass_kernel(CsrSortArgs a) {
   // SMEM: [ntot] counters | [ntot] u16 head slots | 2 x [nr+1] i32 row offsets (A, B)
+  //       | scatter: [CSR_ROWID_CAP] u8 batch row of each entry of the batch (A then B)
   extern __shared__ uint32_t sm_cnt[];
   const int p = blockIdx.y, sl = blockIdx.x;
   const int pb = p << a.tbits;
@@ -408,33 +412,68 @@ __global__ void __launch_bounds__(CSR_T_THREADS, 1) csr_sort_pass_kernel(CsrSort
   uint16_t* slut = reinterpret_cast<uint16_t*>(sm_cnt + a.ntot);
   int32_t* srp = reinterpret_cast<int32_t*>(sm_cnt + a.ntot + (a.lut_smem ? (a.ntot + 1) / 2 : 0));
   const uint16_t* lut = (a.lut && a.lut_smem) ? slut : a.lut;
-  for (int c = threadIdx.x; c < a.ntot; c += blockDim.x) {
-    sm_cnt[c] = SCATTER ? a.cells[((int64_t)p * a.ntot + c) * a.S + sl] : 0u;
-    if (a.lut && a.lut_smem) slut[c] = a.lut[c];
+  uint32_t* my_cnt = a.cnt + ((int64_t)p * a.S + sl) * a.ntot;
+  const uint32_t* my_base = a.base + (int64_t)p * a.ntot;
+  {  // counters (scatter: cursor = cell start + earlier slices) and head slots; 4 loads in flight
+    const bool sl_lut = a.lut && a.lut_smem;
+    for (int c0 = threadIdx.x; c0 < a.ntot; c0 += 4 * blockDim.x) {
+      uint32_t x[4];
+      uint16_t y[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int c = c0 + u * blockDim.x;
+        x[u] = (SCATTER && c < a.ntot) ? my_base[c] + my_cnt[c] : 0u;
+        y[u] = (sl_lut && c < a.ntot) ? a.lut[c] : CSR_NO_SLOT;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int c = c0 + u * blockDim.x;
+        if (c < a.ntot) {
+          sm_cnt[c] = x[u];
+          if (sl_lut) slut[c] = y[u];
+        }
+      }
+    }
   }
   const uint32_t tmask = (1u << a.tbits) - 1u;
   const uint64_t pol_first = l2_policy_evict_first(), pol_last = l2_policy_evict_last();
-  int64_t e0[2] = {0, 0};
-#pragma unroll
-  for (int mat = 0; mat < 2; ++mat) {
-    const int64_t* rp = mat == 0 ? a.arp : a.brp;
-    if (!rp) continue;
-    e0[mat] = rp[a.pr + r0] - rp[0];
-    if (SCATTER)  // slice row offsets of this matrix, relative to its first entry
-      for (int i = threadIdx.x; i <= nr; i += blockDim.x)
-        srp[mat * (nr + 1) + i] = (int32_t)(rp[a.pr + r0 + i] - rp[0] - e0[mat]);
+  const int64_t e0a = a.arp[a.pr + r0] - a.arp[0];
+  const int64_t e0b = a.brp ? a.brp[a.pr + r0] - a.brp[0] : 0;
+  if (SCATTER) {  // slice row offsets of each matrix, relative to its first entry
+    for (int i = threadIdx.x; i <= nr; i += blockDim.x) {
+      srp[i] = (int32_t)(a.arp[a.pr + r0 + i] - a.arp[0] - e0a);
+      if (a.brp) srp[nr + 1 + i] = (int32_t)(a.brp[a.pr + r0 + i] - a.brp[0] - e0b);
+    }
   }
   __syncthreads();
+  uint8_t* rowid = reinterpret_cast<uint8_t*>(srp + 2 * (nr + 1));
+  const int ncols_a = (int)a.a_n, ncols_b = (int)a.b_n;  // counting mode: ntot < 2^16
   uint16_t* xh = SCATTER ? a.xh : nullptr;
   const int nq = (a.n_head + 7) / 8;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
   // hist: the whole slice in one batch; scatter: batches of CSR_SCATTER_RB rows
   const int rb_step = SCATTER ? CSR_SCATTER_RB : nr;
   for (int rb = 0; rb < nr; rb += rb_step) {
     const int re = min(nr, rb + rb_step);
-    if (xh) {  // zero the head slots of the batch's rows (coalesced), just before their values
-      for (int i = threadIdx.x; i < (re - rb) * nq; i += blockDim.x) {
-        const int64_t r = r0 + rb + i / nq;
-        reinterpret_cast<uint4*>(xh + (r + a.xrow) * a.ldh)[i % nq] = make_uint4(0u, 0u, 0u, 0u);
+    // scatter: the batch row of every entry of the batch (warp per row), and
+    // the head slots of the batch's rows zeroed (coalesced) just before their values
+    bool ids = false;
+    int32_t id_ofs_b = 0;
+    if (SCATTER) {
+      id_ofs_b = srp[re] - srp[rb];  // A entries of the batch
+      const int32_t nb_ent = a.brp ? srp[nr + 1 + re] - srp[nr + 1 + rb] : 0;
+      ids = id_ofs_b + nb_ent <= CSR_ROWID_CAP;
+      for (int rr = rb + warp; rr < re; rr += nwarp) {
+        if (xh) {
+          uint4* row = reinterpret_cast<uint4*>(xh + ((int64_t)(r0 + rr) + a.xrow) * a.ldh);
+          for (int q = lane; q < nq; q += 32) row[q] = make_uint4(0u, 0u, 0u, 0u);
+        }
+        if (ids) {
+          for (int e = srp[rr] + lane; e < srp[rr + 1]; e += 32) rowid[e - srp[rb]] = (uint8_t)(rr - rb);
+          if (a.brp)
+            for (int e = srp[nr + 1 + rr] + lane; e < srp[nr + 1 + rr + 1]; e += 32)
+              rowid[id_ofs_b + e - srp[nr + 1 + rb]] = (uint8_t)(rr - rb);
+        }
       }
       __syncthreads();
     }
@@ -442,13 +481,15 @@ __global__ void __launch_bounds__(CSR_T_THREADS, 1) csr_sort_pass_kernel(CsrSort
     for (int mat = 0; mat < 2; ++mat) {
       const int64_t* rp = mat == 0 ? a.arp : a.brp;
       if (!rp) continue;
-      const int32_t* col = (mat == 0 ? a.acol : a.bcol) + e0[mat];
-      const float* val = (mat == 0 ? a.aval : a.bval) + e0[mat];
-      const int64_t ncols = mat == 0 ? a.a_n : a.b_n;
+      const int64_t e0 = mat == 0 ? e0a : e0b;
+      const int32_t* col = (mat == 0 ? a.acol : a.bcol) + e0;
+      const float* val = (mat == 0 ? a.aval : a.bval) + e0;
+      const int ncols = mat == 0 ? ncols_a : ncols_b;
       const uint32_t cofs = mat == 0 ? 0u : (uint32_t)a.a_n;
       const int32_t* mrp = srp + mat * (nr + 1);
       const int32_t eb0 = SCATTER ? mrp[rb] : 0;
-      const int32_t eb1 = SCATTER ? mrp[re] : (int32_t)(rp[a.pr + r1] - rp[0] - e0[mat]);
+      const uint8_t* mid8 = rowid + (mat == 0 ? 0 : id_ofs_b) - eb0;  // row id of entry e: mid8[e]
+      const int32_t eb1 = SCATTER ? mrp[re] : (int32_t)(rp[a.pr + r1] - rp[0] - e0);
       for (int32_t eb = eb0 + (int32_t)threadIdx.x; eb < eb1; eb += CSR_MLP * (int32_t)blockDim.x) {
         int32_t c[CSR_MLP];
         float v[CSR_MLP];
@@ -463,7 +504,7 @@ __global__ void __launch_bounds__(CSR_T_THREADS, 1) csr_sort_pass_kernel(CsrSort
           const int32_t e = eb + u * (int32_t)blockDim.x;
           if (e >= eb1) continue;
           if (SCATTER && (c[u] < 0 || c[u] >= ncols)) atomicOr(a.status, 2);  // out-of-range column
-          const uint32_t cg = csr_cg(c[u], ncols, cofs);
+          const uint32_t cg = (uint32_t)(c[u] < 0 || c[u] >= ncols ? 0 : c[u]) + cofs;
           const uint16_t slot = lut ? lut[cg] : CSR_NO_SLOT;
           const bool head = slot != CSR_NO_SLOT && is_4bit(v[u]);
           if (!SCATTER) {
@@ -471,10 +512,15 @@ __global__ void __launch_bounds__(CSR_T_THREADS, 1) csr_sort_pass_kernel(CsrSort
             continue;
           }
           if (head && !xh) continue;
-          int lo = rb, hi = re;  // slice row of entry e: last i with mrp[i] <= e
-          while (hi - lo > 1) {
-            const int mid = (lo + hi) >> 1;
-            if (mrp[mid] <= e) lo = mid; else hi = mid;
+          int lo = rb;  // slice row of entry e
+          if (ids) {
+            lo += mid8[e];
+          } else {  // last i with mrp[i] <= e
+            int hi = re;
+            while (hi - lo > 1) {
+              const int mid = (lo + hi) >> 1;
+              if (mrp[mid] <= e) lo = mid; else hi = mid;
+            }
           }
           const int r = r0 + lo;
           if (head) {
@@ -491,13 +537,56 @@ __global__ void __launch_bounds__(CSR_T_THREADS, 1) csr_sort_pass_kernel(CsrSort
   }
   if (!SCATTER) {
     __syncthreads();
-    for (int c = threadIdx.x; c < a.ntot; c += blockDim.x)
-      a.cells[((int64_t)p * a.ntot + c) * a.S + sl] = sm_cnt[c];
+    for (int c = threadIdx.x; c < a.ntot; c += blockDim.x) my_cnt[c] = sm_cnt[c];
+  }
+}
+
+// per cell (p, c): cnt[(p*S + s)*ntot + c] <- Σ_{s' < s} (in place), tot[p*ntot + c] = Σ_s.
+// Block (32 columns x 32 slice groups) per (p, 32-column chunk): each thread
+// sums its group's slices, a 32-step SMEM scan over the groups, then the
+// in-place prefixes (all loads of a thread in flight at once).
+constexpr int SLICE_SCAN_G = 32;
+__global__ void __launch_bounds__(1024) csr_slice_scan_kernel(uint32_t* __restrict__ cnt, int gp, int S, int ntot,
+                                                             uint32_t* __restrict__ tot) {
+  __shared__ uint32_t part[SLICE_SCAN_G][33];
+  const int cchunks = (ntot + 31) / 32;
+  const int p = blockIdx.x / cchunks, c = (blockIdx.x % cchunks) * 32 + threadIdx.x;
+  const int g = threadIdx.y;
+  const int per = (S + SLICE_SCAN_G - 1) / SLICE_SCAN_G;  // slices per group (<= 8 for S <= 256)
+  const int s0 = g * per, s1 = min(S, s0 + per);
+  uint32_t* q = cnt + (int64_t)p * S * ntot + c;
+  uint32_t v[8];
+  uint32_t sum = 0;
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    v[u] = (c < ntot && s0 + u < s1) ? q[(int64_t)(s0 + u) * ntot] : 0u;
+    sum += v[u];
+  }
+  part[g][threadIdx.x] = sum;
+  __syncthreads();
+  if (g == 0) {
+    uint32_t run = 0;
+    for (int i = 0; i < SLICE_SCAN_G; ++i) {
+      const uint32_t t = part[i][threadIdx.x];
+      part[i][threadIdx.x] = run;
+      run += t;
+    }
+    if (c < ntot) tot[(int64_t)p * ntot + c] = run;
+  }
+  __syncthreads();
+  uint32_t run = part[g][threadIdx.x];
+  if (c < ntot) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (s0 + u < s1) {
+        q[(int64_t)(s0 + u) * ntot] = run;
+        run += v[u];
+      }
   }
 }
 
 constexpr int CSR_HIST_CTAS = 148;
-constexpr int CSR_HIST_MAX_COLS = 53248;  // 208 KB of SMEM counters
+constexpr int CSR_HIST_MAX_COLS = 40960;  // 160 KB of SMEM counters (+ row ids, row offsets)
 
 template <class T>
 static cudaError_t grow(T*& p, int64_t& cap, int64_t need) {
@@ -815,17 +904,20 @@ cudaError_t launch_sketch_csr(CsrWorkspace& w, int kind, uint64_t seed, int k, i
     // SMEM: counters (4 B) + head slots (2 B) per column when they fit + slice row offsets
     const bool lut_smem = head_lut && ntot * 6 <= 160 * 1024;
     const int64_t fixed = ntot * 4 + (lut_smem ? ((ntot + 1) / 2) * 4 : 0);
-    const int max_nr = (int)std::min<int64_t>(rp, (227 * 1024 - fixed) / 8 - 2);
+    const int max_nr = (int)std::min<int64_t>(rp, (227 * 1024 - CSR_ROWID_CAP - fixed) / 8 - 2);
     if (max_nr < 64) return cudaErrorInvalidValue;
-    auto slices = [&](int gp) { return std::max({1, nsm / gp, (rp + max_nr - 1) / max_nr}); };
+    auto slices = [&](int gp) { return std::max({1, nsm / gp, (rp + max_nr - 1) / max_nr}); };  // <= 256 (slice scan)
+    if (slices(1) > 8 * SLICE_SCAN_G) return cudaErrorInvalidValue;
     int64_t cells_max = 1;
-    for (int g = 1; g <= gmax; ++g) cells_max = std::max<int64_t>(cells_max, (int64_t)g * ntot * slices(g) + 1);
-    const size_t smem = (size_t)fixed + (size_t)(std::min(rp, (rp + slices(gmax) - 1) / slices(gmax) + 1) + 1) * 8;
+    for (int g = 1; g <= gmax; ++g) cells_max = std::max<int64_t>(cells_max, (int64_t)g * ntot * slices(g));
+    const size_t smem_rows = (size_t)(std::min(rp, (rp + slices(gmax) - 1) / slices(gmax) + 1) + 1) * 8;
+    const size_t smem = (size_t)fixed + smem_rows;
+    const size_t smem_sc = smem + CSR_ROWID_CAP;
     CSR_TRY(grow(w.kv_out, w.ent_cap_ko, cap));
-    CSR_TRY(grow(w.hist, w.hist_cap, cells_max));
-    CSR_TRY(grow(w.offs, w.offs_cap, cells_max));
+    CSR_TRY(grow(w.hist, w.hist_cap, cells_max));                 // per-slice counts / prefixes
+    CSR_TRY(grow(w.offs, w.offs_cap, 2 * ((int64_t)gmax * ntot + 1)));  // cell totals | cell starts
     size_t need = 0;
-    CSR_TRY(cub::DeviceScan::ExclusiveSum(nullptr, need, w.hist, w.offs, (int)cells_max, st));
+    CSR_TRY(cub::DeviceScan::ExclusiveSum(nullptr, need, w.offs, w.offs, (int)((int64_t)gmax * ntot + 1), st));
     CSR_TRY(grow(w.cub_tmp, w.cub_cap, (int64_t)need));
     static PerDeviceOnce attr;
     if (attr.need()) {
@@ -856,18 +948,22 @@ cudaError_t launch_sketch_csr(CsrWorkspace& w, int kind, uint64_t seed, int k, i
         sa.ldh = ldh;
         sa.xrow = r0g;
         sa.n_head = n_head;
-        const int64_t cells = (int64_t)gp * ntot * sa.S;
+        const int64_t pc = (int64_t)gp * ntot;  // (panel, column) cells
+        uint32_t* tot = w.offs;
+        uint32_t* start = w.offs + pc + 1;
         dim3 grid((unsigned)sa.S, (unsigned)gp);
-        sa.cells = w.hist;
+        sa.cnt = w.hist;
+        sa.base = start;
         csr_sort_pass_kernel<false><<<grid, CSR_T_THREADS, smem, st>>>(sa);
-        CSR_TRY(cudaMemsetAsync(w.hist + cells, 0, 4, st));  // total at offs[cells]
+        csr_slice_scan_kernel<<<(unsigned)(gp * ((ntot + 31) / 32)), dim3(32, SLICE_SCAN_G), 0, st>>>(
+            w.hist, gp, sa.S, (int)ntot, tot);
+        CSR_TRY(cudaMemsetAsync(tot + pc, 0, 4, st));  // start[pc] = total
         size_t tmp = (size_t)w.cub_cap;
-        CSR_TRY(cub::DeviceScan::ExclusiveSum(w.cub_tmp, tmp, w.hist, w.offs, (int)(cells + 1), st));
-        sa.cells = w.offs;
+        CSR_TRY(cub::DeviceScan::ExclusiveSum(w.cub_tmp, tmp, tot, start, (int)(pc + 1), st));
         sa.kv = reinterpret_cast<uint2*>(w.kv_out);
-        csr_sort_pass_kernel<true><<<grid, CSR_T_THREADS, smem, st>>>(sa);
+        csr_sort_pass_kernel<true><<<grid, CSR_T_THREADS, smem_sc, st>>>(sa);
         CSR_TRY(cudaGetLastError());
-        w.launches += 4;
+        w.launches += 5;
         CSR_TRY(lap(0));
         for (int p = g0; p < g1; ++p) {
           const int prow = (int)std::min<int64_t>(rp, rows - (int64_t)p * rp);
@@ -875,9 +971,9 @@ cudaError_t launch_sketch_csr(CsrWorkspace& w, int kind, uint64_t seed, int k, i
           CSR_TRY(lap(1));
           const int64_t ne = (ab[p + 1] - ab[p]) + (bb[p + 1] - bb[p]);
           if (ne == 0) continue;
-          // panel p of the group: cells [(p - g0)·ntot·S, (p - g0 + 1)·ntot·S)
-          const int64_t q = (int64_t)(p - g0) * ntot * sa.S;
-          CSR_TRY(accumulate(ne, w.offs + q, w.offs + q + ntot * sa.S));
+          // panel p of the group: kv[start[(p - g0)·ntot], start[(p - g0 + 1)·ntot])
+          const int64_t q = (int64_t)(p - g0) * ntot;
+          CSR_TRY(accumulate(ne, start + q, start + q + ntot));
           CSR_TRY(lap(2));
         }
       } else {

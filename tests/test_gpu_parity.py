@@ -480,6 +480,22 @@ def test_sketch_csr_head_split_parity(density, frac_vals, monkeypatch):
         assert np.array_equal(fin["b_norm2"].cpu().numpy(), b2)
 
 
+def test_sketch_csr_many_columns_radix_path():
+    """More columns than the SMEM counting sort holds (ntot > 40960): the
+    per-panel radix-sort path of K3, no tensor-core head."""
+    d, n1, n2, k = 3000, 30000, 20000, 96
+    A = _csr(d, n1, 6, 4, 0)
+    B = _csr(d, n2, 5, 4, 1)
+    sk, fin = gpu_sketch_csr(d, n1, n2, k, PI["gaussian"], 17, A, B, splits=[(0, 1000), (1000, d)])
+    skA, a2 = oracle.sketch_csr(PI["gaussian"], 17, k, n1, A[0].numpy(), A[1].numpy(), A[2].numpy())
+    skB, b2 = oracle.sketch_csr(PI["gaussian"], 17, k, n2, B[0].numpy(), B[1].numpy(), B[2].numpy())
+    As, _, _ = oracle.finalize(k, skA, a2)
+    Bs, _, _ = oracle.finalize(k, skB, b2)
+    assert col_rel_err(fin["A_sk"], As).max() <= 1e-5 and col_rel_err(fin["B_sk"], Bs).max() <= 1e-5
+    assert np.array_equal(fin["a_norm2"].cpu().numpy(), a2)
+    assert np.array_equal(fin["b_norm2"].cpu().numpy(), b2)
+
+
 def test_sketch_csr_bad_column_rejected():
     smp = _smp()
     d, n = 100, 10

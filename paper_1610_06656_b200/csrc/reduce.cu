@@ -30,10 +30,20 @@ __global__ void reduce_sketch_kernel(const float* __restrict__ part, int splits,
         }
       }
     }
-    // output column: c, or map[c] (scattered head columns of the CSR path)
+    // output column: c, or map[c] (scattered head columns of the CSR path;
+    // added atomically there: K3's tail may add into the same column on
+    // another stream — CSR sums are order-dependent anyway)
     const int64_t c = e / k;
     const int64_t eo = map ? (int64_t)map[c] * k + (e - c * k) : e;
-    if constexpr (VEC == 4) {
+    if (map) {
+      if constexpr (VEC == 4) {
+        asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(acc + eo), "f"(s[0]), "f"(s[1]),
+                     "f"(s[2]), "f"(s[3])
+                     : "memory");
+      } else {
+        atomicAdd(acc + eo, s[0]);
+      }
+    } else if constexpr (VEC == 4) {
       float4* dst = reinterpret_cast<float4*>(acc + eo);
       float4 a = *dst;
       a.x += s[0]; a.y += s[1]; a.z += s[2]; a.w += s[3];
@@ -74,7 +84,8 @@ __global__ void reduce_norms_kernel(const double* __restrict__ pnorm, int slots,
       for (int u = 0; u < 8; ++u) s += v[u];
     }
     for (; q < slots; ++q) s += pnorm[(int64_t)q * n + c];
-    nacc[map ? (int64_t)map[c] : c] += s;
+    if (map) atomicAdd(nacc + map[c], s);  // (see reduce_sketch_kernel)
+    else nacc[c] += s;
   }
 }
 

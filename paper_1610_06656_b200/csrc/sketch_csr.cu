@@ -94,59 +94,57 @@ __global__ void pi_panel_kernel(int kind, uint64_t seed, int k, int kp, int64_t 
   }
 }
 
-// K3a' (Gaussian Π with a tensor-core head): one generation of a 32-row ×
-// 64-κ tile into SMEM, written out in BOTH layouts — row-major for the tail
-// (pi[(t - t0) * kp + κ], κ < kp) and κ-major for K1's head panel
-// (kmaj[κ * ld + t_off + t - t0], κ < kpad) — with coalesced stores on both
-// sides (no second pass over the panel).  t0 % 4 == 0.
-constexpr int DUAL_ROWS = 32, DUAL_K = 64;
+// K3a' (Gaussian Π with a tensor-core head): one generation of a 64-row ×
+// 32-κ tile written in BOTH layouts — row-major for the tail (pi[(t - t0) *
+// kp + κ], κ < kp) and κ-major for K1's head panel (kmaj[κ * ld + t_off + t -
+// t0], κ < kpad).  Thread (κ, 8-row group): two Philox calls give its 8
+// consecutive rows, stored as one 16-byte κ-major vector; the row-major side
+// goes through an SMEM tile (one 16-byte store per thread).  t0 % 4 == 0.
+constexpr int DUAL_ROWS = 64, DUAL_K = 32;
 __global__ void __launch_bounds__(256)
 pi_panel_dual_kernel(uint64_t seed, int k, int kp, int kpad, int64_t t0, int rows, uint16_t* __restrict__ pi,
                      uint16_t* __restrict__ kmaj, int64_t ld, int64_t t_off) {
-  __shared__ uint16_t tile[DUAL_ROWS][DUAL_K + 2];
+  __shared__ __align__(16) uint16_t tile[DUAL_ROWS][DUAL_K + 8];
   const int tid = threadIdx.x;
   const int r0 = blockIdx.x * DUAL_ROWS, c0 = blockIdx.y * DUAL_K;
   const uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
-  {
-    const int kq = tid & (DUAL_K - 1);
-    const int kappa = c0 + kq;
+  const int kq = tid & (DUAL_K - 1), rg = tid >> 5;  // κ within the tile, 8-row group 0..7
+  const int kappa = c0 + kq;
+  const int rt = r0 + 8 * rg;                        // first of the thread's 8 rows
+  uint32_t z[4] = {0u, 0u, 0u, 0u};                  // bf16 pairs: rows (0,1), (2,3), (4,5), (6,7)
+  if (kappa < k) {
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-      const int g = (tid >> 6) + 4 * h;              // 4-row group 0..7 of the tile
-      const int rt = r0 + 4 * g;
-      uint16_t z[4] = {0, 0, 0, 0};
-      if (kappa < k && rt < rows) {
-        const uint64_t tq = (uint64_t)(t0 + rt) >> 2;
+      if (rt + 4 * h < rows) {
+        const uint64_t tq = (uint64_t)(t0 + rt + 4 * h) >> 2;
         const u32x4 w = philox4x32_10((uint32_t)tq, (uint32_t)kappa, (uint32_t)(tq >> 32), TAG_GAUSSIAN, k0, k1);
-        gauss_pair(w.x, w.y, z[0], z[1]);
-        gauss_pair(w.z, w.w, z[2], z[3]);
+        z[2 * h] = gauss_pair_bits(w.x, w.y);
+        z[2 * h + 1] = gauss_pair_bits(w.z, w.w);
       }
-#pragma unroll
-      for (int j = 0; j < 4; ++j) tile[4 * g + j][kq] = z[j];
     }
   }
-  __syncthreads();
-  // row-major: 32 rows x 64 κ, 4-byte stores (2 κ), 128 B per row
-  for (int e = tid; e < DUAL_ROWS * (DUAL_K / 2); e += blockDim.x) {
-    const int r = e / (DUAL_K / 2), cp = e % (DUAL_K / 2);
-    const int kappa = c0 + 2 * cp;
-    if (r0 + r < rows && kappa < kp)
-      *reinterpret_cast<uint32_t*>(pi + (int64_t)(r0 + r) * kp + kappa) =
-          *reinterpret_cast<const uint32_t*>(&tile[r][2 * cp]);
+  // κ-major: 8 consecutive rows of one κ
+  if (kmaj && kappa < kpad && rt < rows) {
+    uint16_t* dst = kmaj + (int64_t)kappa * ld + t_off + rt;
+    if (rt + 8 <= rows && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
+      *reinterpret_cast<uint4*>(dst) = make_uint4(z[0], z[1], z[2], z[3]);
+    } else {
+      for (int j = 0; j < 8 && rt + j < rows; ++j) dst[j] = (uint16_t)(z[j >> 1] >> (16 * (j & 1)));
+    }
   }
-  // κ-major: 64 κ x 32 rows, 4-byte stores (2 rows), 64 B per κ
-  if (kmaj) {
-    for (int e = tid; e < DUAL_K * (DUAL_ROWS / 2); e += blockDim.x) {
-      const int c = e / (DUAL_ROWS / 2), rp2 = e % (DUAL_ROWS / 2);
-      const int kappa = c0 + c, r = r0 + 2 * rp2;
-      if (kappa < kpad && r < rows) {
-        uint16_t* dst = kmaj + (int64_t)kappa * ld + t_off + r;
-        const uint32_t v = (uint32_t)tile[2 * rp2][c] | ((uint32_t)tile[2 * rp2 + 1][c] << 16);
-        if (r + 1 < rows && ((reinterpret_cast<uintptr_t>(dst) & 3) == 0)) *reinterpret_cast<uint32_t*>(dst) = v;
-        else {
-          dst[0] = (uint16_t)v;
-          if (r + 1 < rows) dst[1] = (uint16_t)(v >> 16);
-        }
+#pragma unroll
+  for (int j = 0; j < 8; ++j) tile[8 * rg + j][kq] = (uint16_t)(z[j >> 1] >> (16 * (j & 1)));
+  __syncthreads();
+  // row-major: 64 rows x 32 κ, one 16-byte store (8 κ) per thread
+  {
+    const int r = tid >> 2, cq = (tid & 3) * 8;
+    const int kb = c0 + cq;
+    if (r0 + r < rows && kb < kp) {
+      uint16_t* dst = pi + (int64_t)(r0 + r) * kp + kb;
+      if (kb + 8 <= kp && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
+        *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(&tile[r][cq]);
+      } else {
+        for (int j = 0; j < 8 && kb + j < kp; ++j) dst[j] = tile[r][cq + j];
       }
     }
   }
@@ -734,7 +732,11 @@ __global__ void pi_transpose_kernel(const uint16_t* __restrict__ pi, int kp, int
 void csr_workspace_free(CsrWorkspace& w) {
   cudaFree(w.pi); cudaFree(w.kv_in); cudaFree(w.kv_out); cudaFree(w.cub_tmp); cudaFree(w.bounds_d); cudaFree(w.hist); cudaFree(w.offs);
   cudaFree(w.ne_dev); cudaFree(w.head_lut); cudaFree(w.head_map); cudaFree(w.head_cnt); cudaFree(w.head_flag);
-  cudaFree(w.xhead); cudaFree(w.head_tmp); cudaFree(w.kmaj);
+  cudaFree(w.xhead); cudaFree(w.head_tmp); cudaFree(w.kmaj); cudaFree(w.xhead1); cudaFree(w.kmaj1);
+  for (int b = 0; b < 2; ++b) {
+    if (w.ev_tail[b]) cudaEventDestroy(w.ev_tail[b]);
+    if (w.ev_head[b]) cudaEventDestroy(w.ev_head[b]);
+  }
   if (w.head_h) cudaFreeHost(w.head_h);
   if (w.bounds_h) cudaFreeHost(w.bounds_h);
   w = CsrWorkspace{};

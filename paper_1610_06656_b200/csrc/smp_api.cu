@@ -664,47 +664,100 @@ smp_status smp_sketch_block_csr(smp_handle* h, int64_t row0, int64_t rows, const
       const int64_t rp = smp::csr_panel_rows(a_n + b_n);
       int64_t chunk = std::min<int64_t>(rows, (1ll << 30) / (ldh * 2));            // 1 GB dense chunk
       chunk = std::min<int64_t>(chunk, (512ll << 20) / (kpad * 2));                // 512 MB Π panel
+      if (const char* e = getenv("SMP_CSR_HEAD_CHUNK")) chunk = std::min<int64_t>(chunk, atoll(e));  // tests
       chunk = std::max<int64_t>(rp, (chunk / rp) * rp);
       const int64_t cpad = ((std::min(chunk, rows) + 63) / 64) * 64;
+      // SMP_CSR_HEAD_OVERLAP=1: the head K1 of a chunk on a side stream,
+      // overlapped with the next chunk's tail (tensor cores + TMA vs L2
+      // gathers + SIMT), double-buffered; default: serial on the main stream
+      const bool ovl = [] {
+        const char* e = getenv("SMP_CSR_HEAD_OVERLAP");
+        return e ? atoi(e) != 0 : false;  // measured: no gain (K1 and the sort passes contend for SMs)
+      }() && rows > chunk;
+      uint16_t* xhb[2] = {nullptr, nullptr};
+      uint16_t* kmb[2] = {nullptr, nullptr};
       CK(h, ensure(h->csr.xhead, h->csr.xhead_cap, cpad * ldh), "alloc head");
       CK(h, ensure(h->csr.kmaj, h->csr.kmaj_cap, kpad * cpad), "alloc head panel");
+      xhb[0] = xhb[1] = h->csr.xhead;
+      kmb[0] = kmb[1] = h->csr.kmaj;
+      cudaStream_t side = h->st;
+      if (ovl) {
+        CK(h, ensure(h->csr.xhead1, h->csr.xhead1_cap, cpad * ldh), "alloc head");
+        CK(h, ensure(h->csr.kmaj1, h->csr.kmaj1_cap, kpad * cpad), "alloc head panel");
+        xhb[1] = h->csr.xhead1;
+        kmb[1] = h->csr.kmaj1;
+        if (!h->aux_st) CK(h, cudaStreamCreateWithFlags(&h->aux_st, cudaStreamNonBlocking), "stream");
+        side = h->aux_st;
+        for (int b = 0; b < 2; ++b) {
+          if (!h->csr.ev_tail[b]) CK(h, cudaEventCreateWithFlags(&h->csr.ev_tail[b], cudaEventDisableTiming), "event");
+          if (!h->csr.ev_head[b]) CK(h, cudaEventCreateWithFlags(&h->csr.ev_head[b], cudaEventDisableTiming), "event");
+        }
+        // the side stream starts after everything already queued on the main one
+        CK(h, cudaEventRecord(h->csr.ev_tail[0], h->st), "event");
+        CK(h, cudaStreamWaitEvent(side, h->csr.ev_tail[0], 0), "wait");
+      }
       h->csr.ev_pool = h->timing ? &h->ev_pool : nullptr;
       CK(h, smp::csr_bounds(h->csr, a_rowptr, two ? b_rowptr : nullptr, a_n + b_n, rows, h->st), "bounds");
-      // SMP_CSR_PROFILE=1: device time of the head's K1 + K2 per call
+      // SMP_CSR_PROFILE=1: device time of the head's K1 + K2 (side stream)
       const char* hp = getenv("SMP_CSR_PROFILE");
       const bool hprof = hp && atoi(hp);
-      cudaEvent_t hev[3] = {};
-      float hms[2] = {0.f, 0.f};
-      if (hprof)
-        for (int i = 0; i < 3; ++i) CK(h, cudaEventCreate(&hev[i]), "event");
-      for (int64_t r0 = 0; r0 < rows; r0 += chunk) {
+      std::vector<cudaEvent_t> hev;
+      int c = 0;
+      for (int64_t r0 = 0; r0 < rows; r0 += chunk, ++c) {
+        const int b = ovl ? (c & 1) : 0;
         const int64_t rc = std::min(chunk, rows - r0);
         const int64_t ldk = ((rc + 63) / 64) * 64;
-        if (rc != ldk) CK(h, cudaMemsetAsync(h->csr.kmaj, 0, kpad * ldk * 2, h->st), "memset");
-        // the tail sort also densifies the head entries of these rows into xhead
+        // buffers b are free once the head K1 of chunk c - 2 has read them
+        if (ovl && c >= 2) CK(h, cudaStreamWaitEvent(h->st, h->csr.ev_head[b], 0), "wait");
+        if (rc != ldk) CK(h, cudaMemsetAsync(kmb[b], 0, kpad * ldk * 2, h->st), "memset");
+        // the tail sort also densifies the head entries of these rows into xhb[b]
         cudaError_t e1 = smp::launch_sketch_csr(h->csr, pi_code(h), h->d.seed, h->k, row0 + r0, rc, a_rowptr,
                                                 a_col, a_val, h->n1, two ? b_rowptr : nullptr,
                                                 two ? b_col : nullptr, two ? b_val : nullptr, b_n,
                                                 h->acc_sk, h->acc_nrm, h->status, h->st, lut, r0,
-                                                h->csr.kmaj, ldk, (int)kpad, h->csr.xhead, ldh, n_head);
+                                                kmb[b], ldk, (int)kpad, xhb[b], ldh, n_head);
         if (e1 != cudaSuccess) h->csr.bounds_pre = false;
         CK(h, e1, "sketch_csr");
-        if (hprof) CK(h, cudaEventRecord(hev[1], h->st), "event");
-        smp_status s2 = sketch_dense_bf16(h, row0 + r0, rc, h->csr.xhead, ldh, n_head, 1, 0, true,
-                                          h->csr.kmaj, h->csr.head_map);
+        if (ovl) {
+          CK(h, cudaEventRecord(h->csr.ev_tail[b], h->st), "event");
+          CK(h, cudaStreamWaitEvent(side, h->csr.ev_tail[b], 0), "wait");
+        }
+        if (hprof) {
+          hev.emplace_back();
+          CK(h, cudaEventCreate(&hev.back()), "event");
+          CK(h, cudaEventRecord(hev.back(), side), "event");
+        }
+        // K1 (PANEL) + K2 on the head chunk; K2 and the norm reduce add into
+        // the head columns atomically (a tail entry with a non-4-bit value may
+        // hit the same column concurrently)
+        cudaStream_t main_st = h->st;
+        h->st = side;
+        smp_status s2 = sketch_dense_bf16(h, row0 + r0, rc, xhb[b], ldh, n_head, 1, 0, true, kmb[b],
+                                          h->csr.head_map);
+        h->st = main_st;
         if (s2 != SMP_OK) return s2;
         if (hprof) {
-          CK(h, cudaEventRecord(hev[2], h->st), "event");
-          CK(h, cudaEventSynchronize(hev[2]), "sync");
-          float b = 0.f;
-          cudaEventElapsedTime(&b, hev[1], hev[2]);
-          hms[1] += b;
+          hev.emplace_back();
+          CK(h, cudaEventCreate(&hev.back()), "event");
+          CK(h, cudaEventRecord(hev.back(), side), "event");
         }
+        if (ovl) CK(h, cudaEventRecord(h->csr.ev_head[b], side), "event");
+      }
+      if (ovl) {  // the main stream continues after the last head K1
+        CK(h, cudaEventRecord(h->csr.ev_head[0], side), "event");
+        CK(h, cudaStreamWaitEvent(h->st, h->csr.ev_head[0], 0), "wait");
       }
       if (hprof) {
-        fprintf(stderr, "K3 head over %lld rows (%d columns): K1+K2 %.3f ms\n", (long long)rows, n_head,
-                hms[1]);
-        for (int i = 0; i < 3; ++i) cudaEventDestroy(hev[i]);
+        float tot = 0.f;
+        CK(h, cudaEventSynchronize(hev.back()), "sync");
+        for (size_t i = 0; i + 1 < hev.size(); i += 2) {
+          float ms = 0.f;
+          cudaEventElapsedTime(&ms, hev[i], hev[i + 1]);
+          tot += ms;
+        }
+        for (auto e : hev) cudaEventDestroy(e);
+        fprintf(stderr, "K3 head over %lld rows (%d columns): K1+K2 %.3f ms (%s)\n", (long long)rows, n_head, tot,
+                ovl ? "side stream, overlapped with the tail" : "serial");
       }
       h->csr.bounds_pre = false;
       h->launches += 2 + (h->csr.launches - l0);

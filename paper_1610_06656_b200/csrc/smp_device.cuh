@@ -75,7 +75,10 @@ __device__ __forceinline__ uint16_t bf16_rne_bits(float x) {
   return (uint16_t)((u + 0x7FFFu + lsb) >> 16);
 }
 
-__device__ __forceinline__ void gauss_pair(uint32_t wa, uint32_t wb, uint16_t& z0, uint16_t& z1) {
+// (z1 << 16) | z0 of G(wa, wb); z = bf16_rne(ρ·c), bf16_rne(ρ·s)
+// by one cvt.rn.bf16x2.f32 (round to nearest even, as bf16_rne_bits: the
+// products are finite)
+__device__ __forceinline__ uint32_t gauss_pair_bits(uint32_t wa, uint32_t wb) {
   const float L0 = 0x1.000000p+0f, L1 = -0x1.000000p-1f, L2 = 0x1.5555c6p-2f,
               L3 = -0x1.00003ep-2f, L4 = 0x1.996178p-3f, L5 = -0x1.54e596p-3f,
               L6 = 0x1.28ce66p-3f, L7 = -0x1.0e2b8ep-3f, L8 = 0x1.ac49bap-4f,
@@ -118,8 +121,16 @@ __device__ __forceinline__ void gauss_pair(uint32_t wa, uint32_t wb, uint16_t& z
   const float b = (qq & 1u) ? cs : sn;
   const float c = ((qq + 1u) & 2u) ? -a : a;
   const float s = (qq & 2u) ? -b : b;
-  z0 = bf16_rne_bits(__fmul_rn(rho, c));
-  z1 = bf16_rne_bits(__fmul_rn(rho, s));
+  const float p0 = __fmul_rn(rho, c), p1 = __fmul_rn(rho, s);
+  uint32_t z;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(z) : "f"(p1), "f"(p0));
+  return z;
+}
+
+__device__ __forceinline__ void gauss_pair(uint32_t wa, uint32_t wb, uint16_t& z0, uint16_t& z1) {
+  const uint32_t z = gauss_pair_bits(wa, wb);
+  z0 = (uint16_t)(z & 0xFFFFu);
+  z1 = (uint16_t)(z >> 16);
 }
 
 __device__ __forceinline__ uint64_t srht_row(uint64_t seed, int L, uint32_t kappa) {

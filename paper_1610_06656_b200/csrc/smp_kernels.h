@@ -81,6 +81,11 @@ struct CsrWorkspace {
   int64_t xhead_cap = 0;
   uint16_t* kmaj = nullptr;       // κ-major Π of the head chunk (transposed K3 panels)
   int64_t kmaj_cap = 0;
+  uint16_t* xhead1 = nullptr;     // second buffers: the head K1 of chunk c runs on a side
+  int64_t xhead1_cap = 0;         // stream while the tail of chunk c + 1 fills these
+  uint16_t* kmaj1 = nullptr;
+  int64_t kmaj1_cap = 0;
+  cudaEvent_t ev_tail[2] = {nullptr, nullptr}, ev_head[2] = {nullptr, nullptr};
   int64_t* head_h = nullptr;      // pinned
 
   int64_t* bounds_d = nullptr;

@@ -447,17 +447,22 @@ def test_sketch_csr_parity(d, n1, n2, za, zb, k, pi, row0, permute):
     assert np.array_equal(I.cpu().numpy(), Io) and np.array_equal(J.cpu().numpy(), Jo)
 
 
-@pytest.mark.parametrize("density,frac_vals", [
-    ("0", False),       # no tensor-core head: every nonzero through the sorted tail
-    ("1e-9", False),    # every non-empty column is a head column
-    ("0.02", True),     # head columns holding non-4-bit values: those entries stay in the tail
+@pytest.mark.parametrize("density,frac_vals,chunk", [
+    ("0", False, None),       # no tensor-core head: every nonzero through the sorted tail
+    ("1e-9", False, None),    # every non-empty column is a head column
+    ("0.02", True, None),     # head columns holding non-4-bit values: those entries stay in the tail
+    ("0.02", True, "32768"),  # 3 head chunks: head K1 on the side stream, double-buffered
 ])
-def test_sketch_csr_head_split_parity(density, frac_vals, monkeypatch):
+def test_sketch_csr_head_split_parity(density, frac_vals, chunk, monkeypatch):
     """The head/tail split of K3 never changes the result:
-    the same CSR sketched with no head, an all-head split, and head columns
-    that carry values tcgen05 cannot take exactly (R21) all match the oracle."""
+    the same CSR sketched with no head, an all-head split, head columns
+    that carry values tcgen05 cannot take exactly (R21), and the head K1 of
+    one chunk overlapped with the next chunk's tail all match the oracle."""
     monkeypatch.setenv("SMP_CSR_HEAD_DENSITY", density)
-    d, n1, n2, k = 40000, 90, 70, 200
+    if chunk:
+        monkeypatch.setenv("SMP_CSR_HEAD_CHUNK", chunk)
+        monkeypatch.setenv("SMP_CSR_HEAD_OVERLAP", "1")
+    d, n1, n2, k = (70000 if chunk else 40000), 90, 70, 200
     A = _csr(d, n1, 12, 8, 0)
     B = _csr(d, n2, 9, 8, 1)
     if frac_vals:   # every 7th entry gets a value with > 4 significant bits

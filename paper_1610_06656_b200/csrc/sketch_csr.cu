@@ -206,8 +206,23 @@ __device__ __forceinline__ void flush_col(uint32_t c, const float (&acc)[KV][8],
         if (kb + j < k) atomicAdd(dst + kb + j, acc[i][j]);
     }
   }
+  // v² partials live in lanes 0..3 (fast path: lane u takes entry u of a group)
+  nrm += __shfl_down_sync(0xFFFFFFFFu, nrm, 2);
+  nrm += __shfl_down_sync(0xFFFFFFFFu, nrm, 1);
   if (do_norms && lane == 0) atomicAdd(acc_nrm + c, nrm);
 }
+
+// Warps take fixed chunks of CSR_CHUNK sorted entries; lanes own 8·KV κ
+// (κ = 8·(lane + 32 i) .. +7), so the panel pitch kp is KV·256 (zero padded)
+// and every π load is unconditional.  Entries are taken U at a time: the U
+// (value, key) pairs are broadcast loads, their 2·KV π vectors are issued
+// together, and when all U belong to the running column and carry
+// bf16-exact values (integer counts) the group is 16·KV FHFMA.BF16 per entry
+// with no per-entry branch; otherwise entries are taken one by one (column
+// change -> flush, general fp32 values).  Lane u < U accumulates v² of entry
+// u of each group (fp64); the lanes are summed at the flush.
+template <int KV>
+struct AccU { static constexpr int U = KV <= 2 ? 4 : (KV <= 4 ? 2 : 1); };
 
 template <int KV>
 __global__ void __launch_bounds__(256)
@@ -215,6 +230,7 @@ csr_accumulate_kernel(const uint2* __restrict__ kv, int64_t n,
                       const uint16_t* __restrict__ pi, int kp, int k, int tbits,
                       float* __restrict__ acc_sk, double* __restrict__ acc_nrm, int do_norms,
                       const uint32_t* __restrict__ seg_beg, const uint32_t* __restrict__ seg_end) {
+  constexpr int U = AccU<KV>::U;
   // counting sort: the panel's tail is kv[*seg_beg (0 if null), *seg_end) (n bounds it)
   if (seg_end) {
     const int64_t b = seg_beg ? *seg_beg : 0;
@@ -224,6 +240,7 @@ csr_accumulate_kernel(const uint2* __restrict__ kv, int64_t n,
   const int lane = threadIdx.x & 31;
   const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
   const uint32_t tmask = (1u << tbits) - 1u;
+  const uint16_t* pil = pi + 8 * lane;
   for (int64_t task = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
        task * CSR_CHUNK < n; task += nw) {
     const int64_t e0 = task * CSR_CHUNK;
@@ -234,56 +251,70 @@ csr_accumulate_kernel(const uint2* __restrict__ kv, int64_t n,
 #pragma unroll
       for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
     double nrm = 0.0;
-    uint32_t cur = 0xFFFFFFFFu;
-    for (int64_t eb = e0; eb < e1; eb += CSR_U) {
-      uint32_t kk[CSR_U];
-      float vv[CSR_U];
-      bool ok[CSR_U];
-      uint4 q[CSR_U][KV];
+    uint32_t cur = __ldg(&kv[e0].y) >> tbits;
+    for (int64_t eb = e0; eb < e1; eb += U) {
+      const int cnt = (int)min((int64_t)U, e1 - eb);
+      uint32_t kk[U], vb[U];
+      uint4 q[U][KV];
 #pragma unroll
-      for (int u = 0; u < CSR_U; ++u) {
-        const int64_t e = eb + u;
-        ok[u] = e < e1;
-        const uint2 q2 = ok[u] ? kv[e] : make_uint2(0u, 0u);
-        kk[u] = q2.y;
-        vv[u] = __uint_as_float(q2.x);
+      for (int u = 0; u < U; ++u) {
+        // past the chunk end: repeat the last entry with value 0 (same column, adds nothing)
+        const uint2 x = __ldg(&kv[eb + min(u, cnt - 1)]);
+        kk[u] = x.y;
+        vb[u] = u < cnt ? x.x : 0u;
       }
 #pragma unroll
-      for (int u = 0; u < CSR_U; ++u) {
-        const uint16_t* row = pi + (int64_t)(kk[u] & tmask) * kp;
+      for (int u = 0; u < U; ++u) {
+        const uint16_t* row = pil + (int64_t)(kk[u] & tmask) * kp;
 #pragma unroll
-        for (int i = 0; i < KV; ++i) {
-          const int kb = 8 * (lane + 32 * i);
-          q[u][i] = kb < kp ? *reinterpret_cast<const uint4*>(row + kb) : make_uint4(0, 0, 0, 0);
-        }
+        for (int i = 0; i < KV; ++i) q[u][i] = __ldg(reinterpret_cast<const uint4*>(row + 256 * i));
       }
+      uint32_t low = 0;
 #pragma unroll
-      for (int u = 0; u < CSR_U; ++u) {
-        if (!ok[u]) continue;
-        const uint32_t c = kk[u] >> tbits;
-        if (c != cur) {
-          if (cur != 0xFFFFFFFFu) {
-            flush_col<KV>(cur, acc, nrm, k, acc_sk, acc_nrm, lane, do_norms != 0);
+      for (int u = 0; u < U; ++u) low |= vb[u];
+      if ((kk[0] >> tbits) == cur && (kk[U - 1] >> tbits) == cur && (low & 0xFFFFu) == 0u) {
+        // fast path: one column, bf16-exact values: v·π exact, FHFMA.BF16 without unpacking
 #pragma unroll
-            for (int i = 0; i < KV; ++i)
-#pragma unroll
-              for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
-            nrm = 0.0;
-          }
-          cur = c;
-        }
-        const float v = vv[u];
-        nrm = fma((double)v, (double)v, nrm);
-        const uint32_t vbits = __float_as_uint(v);
-        if ((vbits & 0xFFFFu) == 0u) {
-          // v is bf16-exact (e.g. integer counts < 256): v·π is exact and one
-          // FHFMA.BF16 per entry accumulates it in fp32 without unpacking π
-          const uint32_t vb = vbits >> 16;
+        for (int u = 0; u < U; ++u) {
 #pragma unroll
           for (int i = 0; i < KV; ++i) {
-            const uint32_t w[4] = {q[u][i].x, q[u][i].y, q[u][i].z, q[u][i].w};
+            fma_bf16s_x2_f32(vb[u] >> 16, q[u][i].x, acc[i][0], acc[i][1]);
+            fma_bf16s_x2_f32(vb[u] >> 16, q[u][i].y, acc[i][2], acc[i][3]);
+            fma_bf16s_x2_f32(vb[u] >> 16, q[u][i].z, acc[i][4], acc[i][5]);
+            fma_bf16s_x2_f32(vb[u] >> 16, q[u][i].w, acc[i][6], acc[i][7]);
+          }
+        }
+        if (lane < U) {
+          uint32_t mine = vb[0];
 #pragma unroll
-            for (int j = 0; j < 4; ++j) fma_bf16s_x2_f32(vb, w[j], acc[i][2 * j], acc[i][2 * j + 1]);
+          for (int u = 1; u < U; ++u) mine = lane == u ? vb[u] : mine;
+          const double v = (double)__uint_as_float(mine);
+          nrm = fma(v, v, nrm);
+        }
+        continue;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (u >= cnt) break;
+        const uint32_t c = kk[u] >> tbits;
+        if (c != cur) {
+          flush_col<KV>(cur, acc, nrm, k, acc_sk, acc_nrm, lane, do_norms != 0);
+#pragma unroll
+          for (int i = 0; i < KV; ++i)
+#pragma unroll
+            for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
+          nrm = 0.0;
+          cur = c;
+        }
+        const float v = __uint_as_float(vb[u]);
+        if (lane == 0) nrm = fma((double)v, (double)v, nrm);
+        if ((vb[u] & 0xFFFFu) == 0u) {
+#pragma unroll
+          for (int i = 0; i < KV; ++i) {
+            fma_bf16s_x2_f32(vb[u] >> 16, q[u][i].x, acc[i][0], acc[i][1]);
+            fma_bf16s_x2_f32(vb[u] >> 16, q[u][i].y, acc[i][2], acc[i][3]);
+            fma_bf16s_x2_f32(vb[u] >> 16, q[u][i].z, acc[i][4], acc[i][5]);
+            fma_bf16s_x2_f32(vb[u] >> 16, q[u][i].w, acc[i][6], acc[i][7]);
           }
         } else {
 #pragma unroll
@@ -298,7 +329,7 @@ csr_accumulate_kernel(const uint2* __restrict__ kv, int64_t n,
         }
       }
     }
-    if (cur != 0xFFFFFFFFu) flush_col<KV>(cur, acc, nrm, k, acc_sk, acc_nrm, lane, do_norms != 0);
+    flush_col<KV>(cur, acc, nrm, k, acc_sk, acc_nrm, lane, do_norms != 0);
   }
 }
 
@@ -789,7 +820,9 @@ cudaError_t launch_sketch_csr(CsrWorkspace& w, int kind, uint64_t seed, int k, i
   const int tbits = std::min(15, 32 - cbits);
   if (tbits < 6) return cudaErrorInvalidValue;  // more than 2^26 columns
   const int rp = 1 << tbits;                      // panel rows
-  const int kp = (k + 7) & ~7;
+  // Π panel pitch: the κ slices of K3d's lanes, 256·KV with KV in {1, 2, 4, 8, 16} (zero padded)
+  const int kvt = k <= 256 ? 1 : k <= 512 ? 2 : k <= 1024 ? 4 : k <= 2048 ? 8 : 16;
+  const int kp = 256 * kvt;
   const int npan = (int)((rows + rp - 1) / rp);
   const int64_t* ab;
   const int64_t* bb;
@@ -860,7 +893,7 @@ cudaError_t launch_sketch_csr(CsrWorkspace& w, int kind, uint64_t seed, int k, i
   auto accumulate = [&](int64_t ne, const uint32_t* sb, const uint32_t* se) -> cudaError_t {
     const int64_t tasks = (ne + CSR_CHUNK - 1) / CSR_CHUNK;
     const int ablocks = (int)std::max<int64_t>(1, std::min<int64_t>((tasks + 7) / 8, 148 * 64));
-    const int kvw = (kp + 255) / 256;
+    const int kvw = kvt;
     const uint2* kv = reinterpret_cast<const uint2*>(w.kv_out);
     if (w.ev_pool) {
       while (w.ev_pool->size() < *w.ev_used + 2) {

@@ -224,8 +224,11 @@ __device__ __forceinline__ void flush_col(uint32_t c, const float (&acc)[KV][8],
 template <int KV>
 struct AccU { static constexpr int U = KV <= 2 ? 4 : (KV <= 4 ? 2 : 1); };
 
+#ifndef SMP_CSR_ACC_MINB
+#define SMP_CSR_ACC_MINB 3  // (measured: 1 or 4 blocks per SM are 15-50% slower)
+#endif
 template <int KV>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, KV <= 2 ? SMP_CSR_ACC_MINB : 1)
 csr_accumulate_kernel(const uint2* __restrict__ kv, int64_t n,
                       const uint16_t* __restrict__ pi, int kp, int k, int tbits,
                       float* __restrict__ acc_sk, double* __restrict__ acc_nrm, int do_norms,

@@ -136,6 +136,25 @@ def make_inputs(cfgname, cfg, r0, r1, device):
     raise ValueError(f"{cfgname}: dense bench configs are cfg0, cfg1, cfg2, cfg4")
 
 
+def csr_tail_nnz(A, B, n1, n2, rows, density=None):
+    """Nonzeros K3d (the SIMT tail) processes: those NOT in a tensor-core head
+    column (a column with >= ceil(density·rows) nonzeros over the block, with a
+    value of at most 4 significant bits) — the library's head rule
+    (K3), recounted here for the K3d roofline."""
+    if density is None:
+        density = float(os.environ.get("SMP_CSR_HEAD_DENSITY", "0.02"))
+    if density <= 0:
+        return A[1].numel() + B[1].numel()
+    thr = max(1, math.ceil(density * rows))
+    tail = 0
+    for (_, col, val), n in ((A, n1), (B, n2)):
+        head_col = torch.bincount(col.long(), minlength=n) >= thr
+        bits = val.view(torch.int32)
+        four = ((bits & 0x7F800000) != 0x7F800000) & ((bits & 0x000FFFFF) == 0)
+        tail += int((~(head_col[col.long()] & four)).sum())
+    return tail
+
+
 def make_inputs_csr(cfg, r0, r1, device):
     """cfg3 rows [r0, r1) of A and B in CSR (R18); rowptr relative to the block."""
     A = synth.csr_block(r0, r1 - r0, cfg["n1"], cfg["nnz_a"], cfg["seed"], 0, device=device)
@@ -356,6 +375,7 @@ def main():
         inp = IN_CSR_F32
         my_bytes = csr_bytes(A) + csr_bytes(B)
         nnz = A[1].numel() + B[1].numel()
+        tail_nnz = csr_tail_nnz(A, B, cfg["n1"], cfg["n2"], r1 - r0)
         t = torch.tensor([float(my_bytes), float(nnz)], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(t)
@@ -450,15 +470,34 @@ def main():
         sm_max = 1965.0 if not clk else clk["sm_max_mhz"]
         alu_peak = 148 * 128 * 2 * sm_max * 1e6 / 1e12
         flops_step = 2.0 * k * nnz * 1.0
-        ach = flops_step / (t_sketch * 1e-3) / 1e12
+        ach_stage = flops_step / (t_sketch * 1e-3) / 1e12
         k3_ms_step = k1_ms / max(args.steps, 1)
+        # dominant kernel: K3d (csr_accumulate_kernel), one launch per Π panel,
+        # timed with CUDA events on its stream; algorithmic work = 2k FLOP per
+        # tail nonzero (FHFMA.BF16 on the SIMT pipe), its π rows (kp bf16 per
+        # nonzero) gathered from the L2-resident panel
+        k3_launch_ms = k1_ms / max(k1_n, 1)
+        launches_per_step = max(k1_n // max(args.steps, 1), 1)
+        tail_launch = tail_nnz / launches_per_step
+        flops_launch = 2.0 * k * tail_launch
+        ach = flops_launch / (k3_launch_ms * 1e-3) / 1e12
+        kp_pad = 256 * (1 if k <= 256 else 2 if k <= 512 else 4 if k <= 1024 else 8 if k <= 2048 else 16)
+        traffic = None
+        tfile = os.path.join(ROOT, "profiles", "k1_traffic.json")
+        if os.path.exists(tfile):
+            traffic = json.load(open(tfile)).get(cfgname)
         roof = {"bound": "alu", "achieved": ach, "peak": alu_peak, "unit": "TFLOP/s",
-                "frac": ach / alu_peak, "traffic": None,
-                "kernel": "K3 sparse sketch (head: sketch_tc_kernel, tail: csr_accumulate_kernel + transpose)",
+                "frac": ach / alu_peak, "traffic": traffic,
+                "kernel": "csr_accumulate_kernel (K3d, SIMT tail)",
                 "peak_source": "derived: 148 SMs x 128 FP32 lanes x 2 FLOP x %.0f MHz" % sm_max,
-                "timed": "sketch stage (CUDA events), all K3 kernels",
-                "tail_csr_accumulate_ms_per_step": k3_ms_step,
-                "algorithmic_per_step": {"flops": flops_step, "nnz": nnz}}
+                "k3d_ms_per_launch": k3_launch_ms,
+                "k3d_share_of_stage": k3_ms_step / t_sketch,
+                "algorithmic_per_launch": {"flops": flops_launch, "tail_nnz": tail_launch,
+                                           "l2_pi_gather_bytes": tail_launch * kp_pad * 2},
+                "l2_pi_gather_tb_s": tail_launch * kp_pad * 2 / (k3_launch_ms * 1e-3) / 1e12,
+                "stage_view": {"achieved": ach_stage, "peak": alu_peak, "frac": ach_stage / alu_peak,
+                               "unit": "TFLOP/s", "nnz": nnz, "tail_nnz": tail_nnz,
+                               "timed": "sketch stage (CUDA events): head K1 + Π panels + sort + K3d"}}
         roofline_time = max(total_bytes / (pk["hbm"] * 1e9), 2.0 * k * total_nnz / (pk["tc"] * 1e12))
     else:
         # roofline of K1 (per launch = one matrix over this rank's rows),

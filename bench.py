@@ -138,17 +138,24 @@ def make_inputs(cfgname, cfg, r0, r1, device):
 
 def csr_tail_nnz(A, B, n1, n2, rows, density=None):
     """Nonzeros K3d (the SIMT tail) processes: those NOT in a tensor-core head
-    column (a column with >= ceil(density·rows) nonzeros over the block, with a
-    value of at most 4 significant bits) — the library's head rule
-    (K3), recounted here for the K3d roofline."""
+    column (a column with >= ceil(density·counted rows) nonzeros in the
+    library's row sample, with a value of at most 4 significant bits) — the
+    library's head rule (K3), recounted here for the K3d roofline."""
     if density is None:
         density = float(os.environ.get("SMP_CSR_HEAD_DENSITY", "0.02"))
     if density <= 0:
         return A[1].numel() + B[1].numel()
-    thr = max(1, math.ceil(density * rows))
+    seg, segs = 4096, 64          # the library counts 64 evenly spaced 4096-row segments
+    sample = rows > seg * segs
+    thr = max(1, math.ceil(density * (seg * segs if sample else rows)))
     tail = 0
-    for (_, col, val), n in ((A, n1), (B, n2)):
-        head_col = torch.bincount(col.long(), minlength=n) >= thr
+    for (rp, col, val), n in ((A, n1), (B, n2)):
+        if sample:
+            stride = rows // segs
+            cs = torch.cat([col[int(rp[s * stride]):int(rp[s * stride + seg])] for s in range(segs)])
+        else:
+            cs = col
+        head_col = torch.bincount(cs.long(), minlength=n) >= thr
         bits = val.view(torch.int32)
         four = ((bits & 0x7F800000) != 0x7F800000) & ((bits & 0x000FFFFF) == 0)
         tail += int((~(head_col[col.long()] & four)).sum())

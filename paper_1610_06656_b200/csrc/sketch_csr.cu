@@ -644,16 +644,20 @@ __device__ __forceinline__ void cta_rows(int rows, int& r0, int& r1) {
   r1 = (int)(((int64_t)(blockIdx.x + 1) * rows) / gridDim.x);
 }
 
-// column counts over the block (global column index: A then B)
+// column counts over a row sample of the block (global column index: A then
+// B): the sample is `segs` segments of `seg` rows spaced evenly over the block
+// (virtual row v -> block row (v / seg)·stride + v % seg); all rows when the
+// block is small.  The head choice only routes columns between two exact
+// paths, so a sample serves (K3).
 __global__ void __launch_bounds__(CSR_T_THREADS)
 csr_colcount_kernel(const int64_t* __restrict__ arp, const int32_t* __restrict__ acol, int64_t a_n,
                     const int64_t* __restrict__ brp, const int32_t* __restrict__ bcol, int64_t b_n,
-                    int rows, int ntot, uint32_t* __restrict__ cnt) {
+                    int vrows, int seg, int64_t stride, int ntot, uint32_t* __restrict__ cnt) {
   extern __shared__ uint32_t hist[];
   for (int c = threadIdx.x; c < ntot; c += blockDim.x) hist[c] = 0u;
   __syncthreads();
   int r0, r1;
-  cta_rows(rows, r0, r1);
+  cta_rows(vrows, r0, r1);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (int mat = 0; mat < 2; ++mat) {
     const int64_t* rp = mat == 0 ? arp : brp;
@@ -662,7 +666,8 @@ csr_colcount_kernel(const int64_t* __restrict__ arp, const int32_t* __restrict__
     const int64_t ncols = mat == 0 ? a_n : b_n;
     const uint32_t cofs = mat == 0 ? 0u : (uint32_t)a_n;
     const int64_t base = rp[0];
-    for (int r = r0 + warp; r < r1; r += nw) {
+    for (int v = r0 + warp; v < r1; v += nw) {
+      const int64_t r = (int64_t)(v / seg) * stride + v % seg;
       const int64_t e0 = rp[r] - base, e1 = rp[r + 1] - base;
       for (int64_t eb = e0 + lane; eb < e1; eb += 128) {
         int32_t c[4];
@@ -712,9 +717,15 @@ cudaError_t csr_select_head(CsrWorkspace& w, const int64_t* a_rowptr, const int3
   if (attr.need())
     CSR_TRY(cudaFuncSetAttribute(csr_colcount_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  CSR_HIST_MAX_COLS * 4));
+  // row sample: 64 segments of 4096 rows (all rows up to 2^18)
+  const int seg = 4096, segs = 64;
+  const bool sample = rows > (int64_t)seg * segs;
+  const int vrows = sample ? seg * segs : (int)rows;
+  const int64_t stride = sample ? rows / segs : seg;
   csr_colcount_kernel<<<148, CSR_T_THREADS, ntot * 4, st>>>(a_rowptr, a_col, a_n, b_rowptr, b_col, b_n,
-                                                           (int)rows, (int)ntot, w.head_cnt);
-  const uint32_t thr = (uint32_t)std::max(1.0, std::ceil(density * (double)rows));
+                                                           vrows, sample ? seg : (int)rows, sample ? stride : 0,
+                                                           (int)ntot, w.head_cnt);
+  const uint32_t thr = (uint32_t)std::max(1.0, std::ceil(density * (double)vrows));
   const int blocks = (int)((ntot + 255) / 256);
   csr_head_flag_kernel<<<blocks, 256, 0, st>>>(w.head_cnt, (int)ntot, thr, w.head_flag);
   size_t need = 0;

@@ -126,8 +126,9 @@ int csr_panel_rows(int64_t ntot);  // rows of one K3 Π panel (2^15 for up to 2^
 // once (one sync) so that per-chunk launch_sketch_csr calls need none
 cudaError_t csr_bounds(CsrWorkspace& w, const int64_t* a_rowptr, const int64_t* b_rowptr, int64_t ntot,
                        int64_t rows, cudaStream_t st);
-// head columns: count nonzeros per column over the block, select columns with
-// count >= density * rows (slots in column order) -> w.head_lut / w.head_map;
+// head columns: count nonzeros per column over the block (over 64 evenly
+// spaced segments of 4096 rows when the block is longer), select columns with
+// count >= density * counted rows (slots in column order) -> w.head_lut / w.head_map;
 // *n_head = number of slots (synchronises)
 cudaError_t csr_select_head(CsrWorkspace& w, const int64_t* a_rowptr, const int32_t* a_col, int64_t a_n,
                             const int64_t* b_rowptr, const int32_t* b_col, int64_t b_n, int64_t rows,

@@ -431,10 +431,11 @@ struct CsrSortArgs {
 constexpr int CSR_SCATTER_RB = 64;        // scatter: rows per batch (head rows zeroed just before their values)
 constexpr int CSR_ROWID_CAP = 24 * 1024;  // scatter: SMEM row ids of a batch's entries (else binary search)
 
-template <bool SCATTER>
+// HEAD: 0 no head columns, 1 head slot table staged in SMEM, 2 read from global
+template <bool SCATTER, int HEAD>
 __global__ void __launch_bounds__(CSR_T_THREADS, 1) csr_sort_pass_kernel(CsrSortArgs a) {
-  // SMEM: [ntot] counters | [ntot] u16 head slots | 2 x [nr+1] i32 row offsets (A, B)
-  //       | scatter: [CSR_ROWID_CAP] u8 batch row of each entry of the batch (A then B)
+  // SMEM: [ntot] counters | [ntot] u16 head slots (HEAD 1) | 2 x [nr+1] i32 row
+  //       offsets (A, B) | scatter: [CSR_ROWID_CAP] u8 batch row of each entry of the batch (A then B)
   extern __shared__ uint32_t sm_cnt[];
   const int p = blockIdx.y, sl = blockIdx.x;
   const int pb = p << a.tbits;
@@ -442,12 +443,11 @@ __global__ void __launch_bounds__(CSR_T_THREADS, 1) csr_sort_pass_kernel(CsrSort
   const int r0 = pb + (int)(((int64_t)sl * R) / a.S), r1 = pb + (int)(((int64_t)(sl + 1) * R) / a.S);
   const int nr = r1 - r0;
   uint16_t* slut = reinterpret_cast<uint16_t*>(sm_cnt + a.ntot);
-  int32_t* srp = reinterpret_cast<int32_t*>(sm_cnt + a.ntot + (a.lut_smem ? (a.ntot + 1) / 2 : 0));
-  const uint16_t* lut = (a.lut && a.lut_smem) ? slut : a.lut;
+  int32_t* srp = reinterpret_cast<int32_t*>(sm_cnt + a.ntot + (HEAD == 1 ? (a.ntot + 1) / 2 : 0));
+  uint8_t* rowid = reinterpret_cast<uint8_t*>(srp + 2 * (nr + 1));
   uint32_t* my_cnt = a.cnt + ((int64_t)p * a.S + sl) * a.ntot;
   const uint32_t* my_base = a.base + (int64_t)p * a.ntot;
   {  // counters (scatter: cursor = cell start + earlier slices) and head slots; 4 loads in flight
-    const bool sl_lut = a.lut && a.lut_smem;
     for (int c0 = threadIdx.x; c0 < a.ntot; c0 += 4 * blockDim.x) {
       uint32_t x[4];
       uint16_t y[4];
@@ -455,56 +455,62 @@ __global__ void __launch_bounds__(CSR_T_THREADS, 1) csr_sort_pass_kernel(CsrSort
       for (int u = 0; u < 4; ++u) {
         const int c = c0 + u * blockDim.x;
         x[u] = (SCATTER && c < a.ntot) ? my_base[c] + my_cnt[c] : 0u;
-        y[u] = (sl_lut && c < a.ntot) ? a.lut[c] : CSR_NO_SLOT;
+        y[u] = (HEAD == 1 && c < a.ntot) ? a.lut[c] : CSR_NO_SLOT;
       }
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const int c = c0 + u * blockDim.x;
         if (c < a.ntot) {
           sm_cnt[c] = x[u];
-          if (sl_lut) slut[c] = y[u];
+          if (HEAD == 1) slut[c] = y[u];
         }
       }
     }
   }
-  const uint32_t tmask = (1u << a.tbits) - 1u;
+  const uint32_t tbits = (uint32_t)a.tbits, tmask = (1u << a.tbits) - 1u;
   const uint64_t pol_first = l2_policy_evict_first(), pol_last = l2_policy_evict_last();
   const int64_t e0a = a.arp[a.pr + r0] - a.arp[0];
   const int64_t e0b = a.brp ? a.brp[a.pr + r0] - a.brp[0] : 0;
   if (SCATTER) {  // slice row offsets of each matrix, relative to its first entry
     for (int i = threadIdx.x; i <= nr; i += blockDim.x) {
       srp[i] = (int32_t)(a.arp[a.pr + r0 + i] - a.arp[0] - e0a);
-      if (a.brp) srp[nr + 1 + i] = (int32_t)(a.brp[a.pr + r0 + i] - a.brp[0] - e0b);
+      srp[nr + 1 + i] = a.brp ? (int32_t)(a.brp[a.pr + r0 + i] - a.brp[0] - e0b) : 0;
     }
   }
   __syncthreads();
-  uint8_t* rowid = reinterpret_cast<uint8_t*>(srp + 2 * (nr + 1));
-  const int ncols_a = (int)a.a_n, ncols_b = (int)a.b_n;  // counting mode: ntot < 2^16
-  uint16_t* xh = SCATTER ? a.xh : nullptr;
+  uint16_t* xh = (SCATTER && HEAD != 0) ? a.xh : nullptr;
   const int nq = (a.n_head + 7) / 8;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
-  // hist: the whole slice in one batch; scatter: batches of CSR_SCATTER_RB rows
-  const int rb_step = SCATTER ? CSR_SCATTER_RB : nr;
-  for (int rb = 0; rb < nr; rb += rb_step) {
-    const int re = min(nr, rb + rb_step);
-    // scatter: the batch row of every entry of the batch (warp per row), and
-    // the head slots of the batch's rows zeroed (coalesced) just before their values
-    bool ids = false;
-    int32_t id_ofs_b = 0;
+  const int ncols_a = (int)a.a_n, ncols_b = (int)a.b_n;  // counting mode: ntot < 2^16
+  uint2* kvp = a.kv;
+  // hist: the whole slice in one batch; scatter: batches of at most
+  // CSR_SCATTER_RB rows and CSR_ROWID_CAP entries (a longer row is a batch of its own)
+  for (int rb = 0; rb < nr;) {
+    int re = nr;
+    if (SCATTER) {  // largest re <= rb + RB with the batch's entries <= CAP (uniform search)
+      int lo = rb + 1, hi = min(nr, rb + CSR_SCATTER_RB);
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if ((srp[mid] - srp[rb]) + (srp[nr + 1 + mid] - srp[nr + 1 + rb]) <= CSR_ROWID_CAP) lo = mid;
+        else hi = mid - 1;
+      }
+      re = lo;
+    }
+    const int32_t nba = SCATTER ? srp[re] - srp[rb] : 0;
+    const bool single = SCATTER && re == rb + 1;  // one row: no row ids needed
+    uint16_t* xb = xh ? xh + ((int64_t)(r0 + rb) + a.xrow) * a.ldh : nullptr;  // the batch's first head row
     if (SCATTER) {
-      id_ofs_b = srp[re] - srp[rb];  // A entries of the batch
-      const int32_t nb_ent = a.brp ? srp[nr + 1 + re] - srp[nr + 1 + rb] : 0;
-      ids = id_ofs_b + nb_ent <= CSR_ROWID_CAP;
+      // row ids of the batch's entries (warp per row), and the head slots of
+      // the batch's rows zeroed (coalesced) just before their values
       for (int rr = rb + warp; rr < re; rr += nwarp) {
-        if (xh) {
-          uint4* row = reinterpret_cast<uint4*>(xh + ((int64_t)(r0 + rr) + a.xrow) * a.ldh);
+        if (xb) {
+          uint4* row = reinterpret_cast<uint4*>(xb + (int64_t)(rr - rb) * a.ldh);
           for (int q = lane; q < nq; q += 32) row[q] = make_uint4(0u, 0u, 0u, 0u);
         }
-        if (ids) {
+        if (!single) {
           for (int e = srp[rr] + lane; e < srp[rr + 1]; e += 32) rowid[e - srp[rb]] = (uint8_t)(rr - rb);
-          if (a.brp)
-            for (int e = srp[nr + 1 + rr] + lane; e < srp[nr + 1 + rr + 1]; e += 32)
-              rowid[id_ofs_b + e - srp[nr + 1 + rb]] = (uint8_t)(rr - rb);
+          for (int e = srp[nr + 1 + rr] + lane; e < srp[nr + 1 + rr + 1]; e += 32)
+            rowid[nba + e - srp[nr + 1 + rb]] = (uint8_t)(rr - rb);
         }
       }
       __syncthreads();
@@ -520,8 +526,8 @@ __global__ void __launch_bounds__(CSR_T_THREADS, 1) csr_sort_pass_kernel(CsrSort
       const uint32_t cofs = mat == 0 ? 0u : (uint32_t)a.a_n;
       const int32_t* mrp = srp + mat * (nr + 1);
       const int32_t eb0 = SCATTER ? mrp[rb] : 0;
-      const uint8_t* mid8 = rowid + (mat == 0 ? 0 : id_ofs_b) - eb0;  // row id of entry e: mid8[e]
       const int32_t eb1 = SCATTER ? mrp[re] : (int32_t)(rp[a.pr + r1] - rp[0] - e0);
+      const uint8_t* mid8 = rowid + (mat == 0 ? 0 : nba) - eb0;  // batch row of entry e: mid8[e]
       for (int32_t eb = eb0 + (int32_t)threadIdx.x; eb < eb1; eb += CSR_MLP * (int32_t)blockDim.x) {
         int32_t c[CSR_MLP];
         float v[CSR_MLP];
@@ -535,37 +541,32 @@ __global__ void __launch_bounds__(CSR_T_THREADS, 1) csr_sort_pass_kernel(CsrSort
         for (int u = 0; u < CSR_MLP; ++u) {
           const int32_t e = eb + u * (int32_t)blockDim.x;
           if (e >= eb1) continue;
-          if (SCATTER && (c[u] < 0 || c[u] >= ncols)) atomicOr(a.status, 2);  // out-of-range column
-          const uint32_t cg = (uint32_t)(c[u] < 0 || c[u] >= ncols ? 0 : c[u]) + cofs;
-          const uint16_t slot = lut ? lut[cg] : CSR_NO_SLOT;
-          const bool head = slot != CSR_NO_SLOT && is_4bit(v[u]);
+          const bool bad = c[u] < 0 || c[u] >= ncols;
+          if (SCATTER && bad) atomicOr(a.status, 2);  // out-of-range column
+          const uint32_t cg = (uint32_t)(bad ? 0 : c[u]) + cofs;
+          bool head = false;
+          uint32_t slot = 0;
+          if (HEAD != 0) {
+            slot = HEAD == 1 ? slut[cg] : __ldg(a.lut + cg);
+            head = slot != CSR_NO_SLOT && is_4bit(v[u]);
+          }
           if (!SCATTER) {
             if (!head) atomicAdd(&sm_cnt[cg], 1u);
             continue;
           }
-          if (head && !xh) continue;
-          int lo = rb;  // slice row of entry e
-          if (ids) {
-            lo += mid8[e];
-          } else {  // last i with mrp[i] <= e
-            int hi = re;
-            while (hi - lo > 1) {
-              const int mid = (lo + hi) >> 1;
-              if (mrp[mid] <= e) lo = mid; else hi = mid;
-            }
-          }
-          const int r = r0 + lo;
+          const uint32_t lo = single ? 0u : (uint32_t)mid8[e];  // row within the batch
           if (head) {
-            xh[((int64_t)r + a.xrow) * a.ldh + slot] = (uint16_t)(__float_as_uint(v[u]) >> 16);
+            if (xb) xb[lo * (uint32_t)a.ldh + slot] = (uint16_t)(__float_as_uint(v[u]) >> 16);
           } else {
             const uint32_t pos = atomicAdd(&sm_cnt[cg], 1u);
-            st_hint_v2(a.kv + pos, make_uint2(__float_as_uint(v[u]), (cg << a.tbits) | ((uint32_t)r & tmask)),
+            st_hint_v2(kvp + pos, make_uint2(__float_as_uint(v[u]), (cg << tbits) | ((uint32_t)(r0 + rb) + lo) & tmask),
                        pol_last);
           }
         }
       }
     }
-    if (xh) __syncthreads();  // the batch's head values land before the next batch's zeros
+    if (SCATTER) __syncthreads();  // row ids and head rows reused by the next batch
+    rb = re;
   }
   if (!SCATTER) {
     __syncthreads();
@@ -970,11 +971,15 @@ cudaError_t launch_sketch_csr(CsrWorkspace& w, int kind, uint64_t seed, int k, i
     CSR_TRY(grow(w.cub_tmp, w.cub_cap, (int64_t)need));
     static PerDeviceOnce attr;
     if (attr.need()) {
-      CSR_TRY(cudaFuncSetAttribute(csr_sort_pass_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   227 * 1024));
-      CSR_TRY(cudaFuncSetAttribute(csr_sort_pass_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   227 * 1024));
+      const int mx = 227 * 1024;
+      CSR_TRY(cudaFuncSetAttribute(csr_sort_pass_kernel<false, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+      CSR_TRY(cudaFuncSetAttribute(csr_sort_pass_kernel<false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+      CSR_TRY(cudaFuncSetAttribute(csr_sort_pass_kernel<false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+      CSR_TRY(cudaFuncSetAttribute(csr_sort_pass_kernel<true, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+      CSR_TRY(cudaFuncSetAttribute(csr_sort_pass_kernel<true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+      CSR_TRY(cudaFuncSetAttribute(csr_sort_pass_kernel<true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
     }
+    const int head_mode = !head_lut ? 0 : (lut_smem ? 1 : 2);
     for (int g0 = 0; g0 < npan;) {
       int g1 = g0 + 1;
       while (g1 < npan && (ab[g1 + 1] - ab[g0]) + (bb[g1 + 1] - bb[g0]) <= cap) ++g1;
@@ -1003,14 +1008,22 @@ cudaError_t launch_sketch_csr(CsrWorkspace& w, int kind, uint64_t seed, int k, i
         dim3 grid((unsigned)sa.S, (unsigned)gp);
         sa.cnt = w.hist;
         sa.base = start;
-        csr_sort_pass_kernel<false><<<grid, CSR_T_THREADS, smem, st>>>(sa);
+        switch (head_mode) {
+          case 0: csr_sort_pass_kernel<false, 0><<<grid, CSR_T_THREADS, smem, st>>>(sa); break;
+          case 1: csr_sort_pass_kernel<false, 1><<<grid, CSR_T_THREADS, smem, st>>>(sa); break;
+          default: csr_sort_pass_kernel<false, 2><<<grid, CSR_T_THREADS, smem, st>>>(sa); break;
+        }
         csr_slice_scan_kernel<<<(unsigned)(gp * ((ntot + 31) / 32)), dim3(32, SLICE_SCAN_G), 0, st>>>(
             w.hist, gp, sa.S, (int)ntot, tot);
         CSR_TRY(cudaMemsetAsync(tot + pc, 0, 4, st));  // start[pc] = total
         size_t tmp = (size_t)w.cub_cap;
         CSR_TRY(cub::DeviceScan::ExclusiveSum(w.cub_tmp, tmp, tot, start, (int)(pc + 1), st));
         sa.kv = reinterpret_cast<uint2*>(w.kv_out);
-        csr_sort_pass_kernel<true><<<grid, CSR_T_THREADS, smem_sc, st>>>(sa);
+        switch (head_mode) {
+          case 0: csr_sort_pass_kernel<true, 0><<<grid, CSR_T_THREADS, smem_sc, st>>>(sa); break;
+          case 1: csr_sort_pass_kernel<true, 1><<<grid, CSR_T_THREADS, smem_sc, st>>>(sa); break;
+          default: csr_sort_pass_kernel<true, 2><<<grid, CSR_T_THREADS, smem_sc, st>>>(sa); break;
+        }
         CSR_TRY(cudaGetLastError());
         w.launches += 5;
         CSR_TRY(lap(0));

@@ -422,6 +422,8 @@ def main():
         sk.finalize()
         evs[1].record(stream)
         I, J, val, qh = sk.sample_estimate(m, cfg["seed"], sampler=args.sampler)
+        if len(evs) > 3:
+            evs[3].record(stream)
         U, V = sk.waltmin(I, J, val, qh, r, T, init_iters=args.init_iters, seed=cfg["seed"],
                           partition=args.partition)
         if host is not None:
@@ -443,7 +445,7 @@ def main():
     for _ in range(args.warmup):
         step([torch.cuda.Event(enable_timing=True) for _ in range(3)])
     # timed region (inputs 4.3+ GB >> 126 MB L2: no flush needed)
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
     sk.set_timing(True)
     sk.kernel_timing()
     launches0 = sk.kernel_launches
@@ -458,6 +460,8 @@ def main():
     clk = clocks.stop()
     t_sketch = sum(e[0].elapsed_time(e[1]) for e in evs) / args.steps
     t_step = sum(e[0].elapsed_time(e[2]) for e in evs) / args.steps
+    t_omega = sum(e[1].elapsed_time(e[3]) for e in evs) / args.steps   # Ω draw + M̃ (lines 3-4)
+    t_wm = sum(e[3].elapsed_time(e[2]) for e in evs) / args.steps      # WAltMin (line 5)
     if world > 1:
         t = torch.tensor([t_sketch, t_step, k1_ms / max(k1_n, 1)], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -615,6 +619,8 @@ def main():
             **({"nnz": int(total_nnz)} if csr else {}),
             "smp_pca_sec": t_step * 1e-3,
             "sketch_ms": t_sketch,
+            "omega_mtilde_ms": t_omega,
+            "waltmin_ms": t_wm,
             "roofline_pct_of_stage": 100.0 * roofline_time / (t_sketch * 1e-3),
             "roofline": roof,
             "cpu_baseline": cpu,

@@ -281,14 +281,17 @@ cudaError_t run_waltmin(const WaltminArgs& a, cudaStream_t st) {
   // heavy rows / columns (REUSE_ALL only): stable compaction (fixed order ->
   // fixed CTA assignment -> deterministic Gram partials)
   const int64_t nmax = std::max<int64_t>(std::max<int64_t>(n1, n2), 1);
-  // Split a row over a CTA only when it is long in absolute terms AND several
-  // times a warp's average share: the CTA runs its heavy rows before its light
-  // ones, so splitting rows near the average only serialises work (cfg1:
-  // rows <= 564 samples, 119 per warp -> none split).  SMP_WM_HEAVY overrides
-  // the threshold (0 = warp-per-row only; tuning).
+  // Split a row over a CTA when it has more than WM_HEAVY = 1024 samples: a
+  // warp walks its rows one after another, latency-bound (~64 samples per
+  // L2 round trip), so one long row sets the phase time however light the
+  // warp's other rows are (cfg3: fully sampled rows of 8,000-10,000 samples
+  // against 3,254 per warp on average; measured per WAltMin call: threshold
+  // 1024 -> 8.2 ms, 2048 -> 9.3, 4096 -> 11.3, 4x the per-warp average
+  // (13,018) -> 13.7; cfg1 (rows <= 564) splits none; cfg2 4.8 ms either way,
+  // 512 no better).  SMP_WM_HEAVY overrides the threshold (0 = warp-per-row
+  // only; tuning).
   const char* hv = getenv("SMP_WM_HEAVY");
-  const int64_t avg_warp = cnt / ((int64_t)gctas * WM_WARPS) + 1;
-  const int64_t heavy_thr = fresh ? 0 : (hv ? atoll(hv) : std::max<int64_t>(WM_HEAVY, 4 * avg_warp));
+  const int64_t heavy_thr = fresh ? 0 : (hv ? atoll(hv) : (int64_t)WM_HEAVY);
   uint8_t *hfr = nullptr, *hfc = nullptr;
   int32_t *hidx = nullptr, *hlr = nullptr, *hlc = nullptr, *nh = nullptr;
   if (heavy_thr > 0) {

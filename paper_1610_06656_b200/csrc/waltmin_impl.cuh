@@ -478,15 +478,28 @@ __device__ __forceinline__ void spmm_accum(int64_t q0, int64_t q1, const int32_t
                                            const double* Xs, bool l1, double (&acc)[R]) {
   constexpr int U = WMUnroll<R>::U;
   const int lane = threadIdx.x & 31;
+  // software-pipelined: the next group's (coef, index) loads are issued before
+  // this group's factor-row gathers, so a group costs one L2 round trip, not two
+  double cn[U];
+  int32_t on[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const int64_t q = q0 + lane + 32 * u;
+    const bool ok = q < q1;
+    cn[u] = ok ? coef[q] : 0.0;
+    on[u] = ok ? other[q] : 0;
+  }
   for (int64_t base = q0 + lane; base < q1; base += 32 * U) {
     double c[U];
     int32_t oi[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const int64_t q = base + 32 * u;
+      c[u] = cn[u];
+      oi[u] = on[u];
+      const int64_t q = base + 32 * (U + u);
       const bool ok = q < q1;
-      c[u] = ok ? coef[q] : 0.0;
-      oi[u] = ok ? other[q] : 0;
+      cn[u] = ok ? coef[q] : 0.0;
+      on[u] = ok ? other[q] : 0;
     }
     double x[U][R];
 #pragma unroll
@@ -619,16 +632,30 @@ __device__ __forceinline__ void als_accum(int64_t q0, int64_t q1, const int32_t*
   constexpr int NG = R * (R + 1) / 2;
   constexpr int U = WMUnroll<R>::U;
   const int lane = threadIdx.x & 31;
+  // software-pipelined as spmm_accum: next group's (w, w·M̃, index) loads first
+  double wn[U], vn[U];
+  int32_t on[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const int64_t q = q0 + lane + 32 * u;
+    const bool ok = q < q1;
+    wn[u] = ok ? w[q] : 0.0;
+    vn[u] = ok ? wv[q] : 0.0;
+    on[u] = ok ? other[q] : 0;
+  }
   for (int64_t base = q0 + lane; base < q1; base += 32 * U) {
     double ws[U], vs[U];
     int32_t oi[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const int64_t q = base + 32 * u;
+      ws[u] = wn[u];
+      vs[u] = vn[u];
+      oi[u] = on[u];
+      const int64_t q = base + 32 * (U + u);
       const bool ok = q < q1;
-      ws[u] = ok ? w[q] : 0.0;
-      vs[u] = ok ? wv[q] : 0.0;
-      oi[u] = ok ? other[q] : 0;
+      wn[u] = ok ? w[q] : 0.0;
+      vn[u] = ok ? wv[q] : 0.0;
+      on[u] = ok ? other[q] : 0;
     }
     double x[U][R];
 #pragma unroll

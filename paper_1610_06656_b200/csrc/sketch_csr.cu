@@ -369,7 +369,10 @@ __device__ __forceinline__ bool is_4bit(float v) {
 // (DESIGN.md §7).
 constexpr int CSR_T_THREADS = 1024;
 #ifndef SMP_CSR_MLP
-#define SMP_CSR_MLP 8
+#define SMP_CSR_MLP 4
+#endif
+#ifndef SMP_CSR_PIPE
+#define SMP_CSR_PIPE 1  // (4 pipelined: 0.91 ms per 12 panels; 8 unpipelined 0.98, 8 pipelined 1.05)
 #endif
 constexpr int CSR_MLP = SMP_CSR_MLP;  // CSR loads in flight per thread (sort passes)
 
@@ -528,14 +531,34 @@ __global__ void __launch_bounds__(CSR_T_THREADS, 1) csr_sort_pass_kernel(CsrSort
       const int32_t eb0 = SCATTER ? mrp[rb] : 0;
       const int32_t eb1 = SCATTER ? mrp[re] : (int32_t)(rp[a.pr + r1] - rp[0] - e0);
       const uint8_t* mid8 = rowid + (mat == 0 ? 0 : nba) - eb0;  // batch row of entry e: mid8[e]
+#if SMP_CSR_PIPE
+      // software-pipelined: the next group's loads are issued before this
+      // group's entries are processed
+      int32_t cn[CSR_MLP];
+      float vn[CSR_MLP];
+#pragma unroll
+      for (int u = 0; u < CSR_MLP; ++u) {
+        const int32_t e = eb0 + (int32_t)threadIdx.x + u * (int32_t)blockDim.x;
+        cn[u] = e < eb1 ? ld_hint_s32(col + e, pol_first) : 0;
+        vn[u] = e < eb1 ? ld_hint_f32(val + e, pol_first) : 0.f;
+      }
+#endif
       for (int32_t eb = eb0 + (int32_t)threadIdx.x; eb < eb1; eb += CSR_MLP * (int32_t)blockDim.x) {
         int32_t c[CSR_MLP];
         float v[CSR_MLP];
 #pragma unroll
         for (int u = 0; u < CSR_MLP; ++u) {
+#if SMP_CSR_PIPE
+          c[u] = cn[u];
+          v[u] = vn[u];
+          const int32_t e = eb + (CSR_MLP + u) * (int32_t)blockDim.x;
+          cn[u] = e < eb1 ? ld_hint_s32(col + e, pol_first) : 0;
+          vn[u] = e < eb1 ? ld_hint_f32(val + e, pol_first) : 0.f;
+#else
           const int32_t e = eb + u * (int32_t)blockDim.x;
           c[u] = e < eb1 ? ld_hint_s32(col + e, pol_first) : 0;
           v[u] = e < eb1 ? ld_hint_f32(val + e, pol_first) : 0.f;
+#endif
         }
 #pragma unroll
         for (int u = 0; u < CSR_MLP; ++u) {

@@ -222,7 +222,10 @@ __device__ __forceinline__ void flush_col(uint32_t c, const float (&acc)[KV][8],
 // change -> flush, general fp32 values).  Lane u < U accumulates v² of entry
 // u of each group (fp64); the lanes are summed at the flush.
 template <int KV>
-struct AccU { static constexpr int U = KV <= 2 ? 4 : (KV <= 4 ? 2 : 1); };
+#ifndef SMP_CSR_ACC_U
+#define SMP_CSR_ACC_U 4
+#endif
+struct AccU { static constexpr int U = KV <= 2 ? SMP_CSR_ACC_U : (KV <= 4 ? 2 : 1); };
 
 #ifndef SMP_CSR_ACC_MINB
 #define SMP_CSR_ACC_MINB 3  // (measured: 1 or 4 blocks per SM are 15-50% slower)

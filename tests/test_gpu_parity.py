@@ -501,6 +501,43 @@ def test_sketch_csr_many_columns_radix_path():
     assert np.array_equal(fin["b_norm2"].cpu().numpy(), b2)
 
 
+def test_sketch_csr_dense_and_empty_rows():
+    """Ragged CSR: a row holding every column of A (30,000 nonzeros: a scatter
+    batch of its own, beyond the per-batch row-id capacity), runs of empty
+    rows, and rows of one nonzero, with the tensor-core head on."""
+    d, n1, n2, k = 3000, 30000, 9000, 64
+    rng = np.random.default_rng(5)
+    cols_a, cols_b, rpa, rpb = [], [], [0], [0]
+    for t in range(d):
+        if t == 1234:
+            ca = np.arange(n1)
+        elif 500 <= t < 700:
+            ca = np.array([], dtype=np.int64)
+        elif t % 97 == 0:
+            ca = rng.choice(n1, 1)
+        else:
+            ca = np.sort(rng.choice(n1, 6, replace=False))
+        cb = np.array([], dtype=np.int64) if 600 <= t < 900 else np.sort(rng.choice(n2, 4, replace=False))
+        cols_a.append(ca)
+        cols_b.append(cb)
+        rpa.append(rpa[-1] + len(ca))
+        rpb.append(rpb[-1] + len(cb))
+    ca = np.concatenate(cols_a).astype(np.int32)
+    cb = np.concatenate(cols_b).astype(np.int32)
+    va = rng.integers(1, 6, len(ca)).astype(np.float32)
+    vb = rng.integers(1, 6, len(cb)).astype(np.float32)
+    A = (torch.tensor(rpa, dtype=torch.int64), torch.from_numpy(ca), torch.from_numpy(va))
+    B = (torch.tensor(rpb, dtype=torch.int64), torch.from_numpy(cb), torch.from_numpy(vb))
+    sk, fin = gpu_sketch_csr(d, n1, n2, k, PI["gaussian"], 19, A, B, splits=[(0, 1500), (1500, d)])
+    skA, a2 = oracle.sketch_csr(PI["gaussian"], 19, k, n1, A[0].numpy(), A[1].numpy(), A[2].numpy())
+    skB, b2 = oracle.sketch_csr(PI["gaussian"], 19, k, n2, B[0].numpy(), B[1].numpy(), B[2].numpy())
+    As, _, _ = oracle.finalize(k, skA, a2)
+    Bs, _, _ = oracle.finalize(k, skB, b2)
+    assert col_rel_err(fin["A_sk"], As).max() <= 1e-5 and col_rel_err(fin["B_sk"], Bs).max() <= 1e-5
+    assert np.array_equal(fin["a_norm2"].cpu().numpy(), a2)
+    assert np.array_equal(fin["b_norm2"].cpu().numpy(), b2)
+
+
 def test_sketch_csr_bad_column_rejected():
     smp = _smp()
     d, n = 100, 10

@@ -31,6 +31,7 @@
 // to both CTAs.
 #include <cuda.h>
 #include <cudaTypedefs.h>
+#include <cstdlib>
 #include "smp_device.cuh"
 #include "smp_kernels.h"
 
@@ -44,20 +45,26 @@ constexpr int TC_BK = 64;                         // X rows per K-block
 #define SMP_X_STAGES 8
 #endif
 constexpr int X_STAGES = SMP_X_STAGES;            // SMEM ring (HBM latency hiding)
-#ifndef SMP_PI_STAGES
-#define SMP_PI_STAGES 4
-#endif
-constexpr int PI_STAGES = SMP_PI_STAGES;          // TMEM ring for Π (A operand)
+// Π generator warp sets (4 warps each) are a template parameter GS of K1:
+// 2 when every CTA pair owns the only κ tile of its X tile (k <= 256: the norm
+// warps are on duty for every K-block and the SM's issue slots are shared), 3
+// when several κ tiles share an X tile (the generators are then the MMA's
+// feeder: cfg2 no-MMA generator throughput 23.7 -> 19.5 ms per launch, full
+// kernel 31.0 -> 29.6 ms under the power cap; profiles/round2/k1_gen_sets.log).
+constexpr int MAX_GEN_SETS = 4;
+constexpr int PI_STAGES = 2 * MAX_GEN_SETS;       // barrier slots; a GS build uses 2*GS TMEM stages
 constexpr int X_STAGE = TC_BK * HALF_N * 2;       // 16 KB
 constexpr int ACC_COLS = TC_BN;                   // fp32 accumulator columns
 constexpr int PI_COLS = TC_BK / 2;                // 64 bf16 per lane = 32 columns
 constexpr int TMEM_COLS = 512;
 static_assert(ACC_COLS + PI_STAGES * PI_COLS <= TMEM_COLS, "TMEM budget");
+// each set takes every GS-th pair of K-blocks; a set may run at most one
+// ring phase ahead of the MMA only if the ring holds one pair per set
+// (so the TMEM ring is 2*GS stages)
 // Warp roles: 0 TMA, 1 MMA (leader) + TMEM alloc, 2 relay, 3 spare,
-// 4..7 and 16..19 Π generators (two sets, one warp per TMEM lane quadrant
-// each; the sets take alternate pairs of K-blocks), 8..15 norm warps + TMEM
-// epilogue.
-constexpr int NUM_GEN_WARPS = 8;
+// 4..7, 16..19 (and 20..23, 24..27 for GEN_SETS = 3, 4) Π generators (one warp
+// per TMEM lane quadrant per set; the sets take the pairs of K-blocks round
+// robin), 8..15 norm warps + TMEM epilogue.
 constexpr int NUM_NORM_WARPS = 8;                 // warps 8..15
 constexpr int NORM_RG = (32 * NUM_NORM_WARPS) / 16;   // row groups (16 chunks per row)
 constexpr int NORM_ROWS = TC_BK / NORM_RG;        // rows per norm thread per stage
@@ -75,7 +82,7 @@ constexpr int P_STAGE = X_STAGE + PI_TILE;        // 32 KB
 constexpr int P_BARS = 3 * P_STAGES + 2 * PI_STAGES + 1;
 constexpr int P_SMEM = P_STAGES * P_STAGE + NORM_RED + P_BARS * 8 + 16 + 1024;
 static_assert(P_SMEM <= 227 * 1024, "K1 (panel) exceeds the 227 KB SMEM budget");
-constexpr int TC_THREADS = 32 * 20;
+constexpr int tc_threads(int gs) { return 32 * (12 + 4 * gs); }   // sets 2.. at warps 20, 24, ...
 
 struct RadCache {
   uint64_t g;
@@ -160,10 +167,12 @@ __device__ __forceinline__ void gen_pi_half(int kind, uint64_t seed, uint32_t ka
   }
 }
 
-template <bool PANEL>
-__global__ void __launch_bounds__(TC_THREADS, 1)
+template <bool PANEL, int GS>
+__global__ void __launch_bounds__(tc_threads(GS), 1)
 sketch_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap tmap_pi,
                  SketchTCParams p) {
+  static_assert(GS >= 2 && GS <= MAX_GEN_SETS, "generator sets");
+  constexpr int PIS = 2 * GS;                        // Π TMEM ring stages (one pair per set)
   constexpr int NST = PANEL ? P_STAGES : X_STAGES;   // ring stages
   constexpr int STG = PANEL ? P_STAGE : X_STAGE;     // bytes per stage
   extern __shared__ uint8_t smem_raw[];
@@ -199,7 +208,7 @@ sketch_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant
       mbar_init(&ready[s], 2);
     }
     for (int s = 0; s < PI_STAGES; ++s) {
-      mbar_init(&pfull[s], NUM_GEN_WARPS / 2);   // one set of 4 warps writes a stage
+      mbar_init(&pfull[s], 4);   // one set of 4 warps writes a stage
       mbar_init(&pempty[s], 1);
     }
     mbar_init(tmem_full, 1);
@@ -234,7 +243,7 @@ sketch_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant
       const uint32_t idesc = make_idesc_bf16(256, 256, 0, 1);
       const uint32_t x_addr = smem_u32(x_s);
       for (int it = 0; it < nkb; ++it) {
-        const int s = it % NST, ps = it % PI_STAGES;
+        const int s = it % NST, ps = it % PIS;
         mbar_wait(&ready[s], (uint32_t)(it / NST) & 1u);
         tc_fence_after();
         if (!(p.debug & 4)) {
@@ -261,9 +270,9 @@ sketch_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant
     if (lane == 0) {
       const uint32_t leader_ready = mapa_shared(smem_u32(ready), 0);
       for (int it = 0; it < nkb; ++it) {
-        const int s = it % NST, ps = it % PI_STAGES;
+        const int s = it % NST, ps = it % PIS;
         mbar_wait(&xfull[s], (uint32_t)(it / NST) & 1u);
-        if (!PANEL) mbar_wait(&pfull[ps], (uint32_t)(it / PI_STAGES) & 1u);
+        if (!PANEL) mbar_wait(&pfull[ps], (uint32_t)(it / PIS) & 1u);
         mbar_arrive_cluster(leader_ready + 8u * (uint32_t)s);
       }
     }
@@ -276,7 +285,7 @@ sketch_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant
     // its latency overlaps the store (idle in PANEL mode: Π arrives by TMA)
     if (PANEL) goto role_done;
     const int quad = warp & 3;
-    const int set = warp >= 16 ? 1 : 0;
+    const int set = warp < 8 ? 0 : ((warp - 16) >> 2) + 1;
     const int kl = 32 * quad + lane;
     const int kappa = kappa0 + kl;
     const bool valid = kappa < p.k;
@@ -290,11 +299,11 @@ sketch_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant
     }
     const bool word_kind = p.kind == PI_RADEMACHER || p.kind >= PI_SRHT_BASE;
     const uint32_t taddr = tbase + ((uint32_t)(32 * quad) << 16) + ACC_COLS;
-    for (int jp = set; 2 * jp < nkb; jp += 2) {
+    for (int jp = set; 2 * jp < nkb; jp += GS) {
       for (int h = 0; h < 2; ++h) {
         const int it = 2 * jp + h;
         if (it >= nkb) break;
-        const int ps = it % PI_STAGES;
+        const int ps = it % PIS;
         const uint64_t t0 = (uint64_t)p.row0 + (uint64_t)(kb_begin + it) * TC_BK;
         uint32_t o[16], o2[16];
         if (p.debug & 2) {
@@ -304,13 +313,13 @@ sketch_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant
           gen_pi_half(p.kind, p.seed, (uint32_t)kappa, valid, t0, rc, o, srht_s, srht_walsh);
           gen_pi_half(p.kind, p.seed, (uint32_t)kappa, valid, t0 + 32, rc, o2, srht_s, srht_walsh);
         }
-        mbar_wait(&pempty[ps], ((uint32_t)(it / PI_STAGES) & 1u) ^ 1u);
+        mbar_wait(&pempty[ps], ((uint32_t)(it / PIS) & 1u) ^ 1u);
         tc_fence_after();
         tmem_st_32x32b_x16(taddr + ps * PI_COLS, o);
         tmem_st_32x32b_x16(taddr + ps * PI_COLS + 16, o2);
         if (h == 1 || it + 1 == nkb) {
           // prefetch the Philox words of this set's next pair
-          const int itn = 2 * (jp + 2);
+          const int itn = 2 * (jp + GS);
           if (word_kind && valid && itn < nkb && !(p.debug & 2)) {
             const uint64_t tn = (uint64_t)p.row0 + (uint64_t)(kb_begin + itn) * TC_BK;
             if ((tn & 31) == 0) {
@@ -535,18 +544,27 @@ cudaError_t launch_sketch_tc(const void* X, int64_t ldx, SketchTCParams p, cudaS
   } else {
     tmap_pi = tmap;
   }
-  static PerDeviceOnce attr_set[2];
+  // generator sets: 3 when several κ tiles share each X tile (see GS above);
+  // SMP_K1_GEN_SETS = 2..4 overrides (tuning only)
+  int gs = (!panel && p.k_tiles >= 2) ? 3 : 2;
+  if (const char* e = getenv("SMP_K1_GEN_SETS")) {
+    const int v = atoi(e);
+    if (v >= 2 && v <= MAX_GEN_SETS) gs = v;
+  }
+  if (panel) gs = 2;  // Π arrives by TMA: the generator warps idle
+  static PerDeviceOnce attr_set[4];
   const int smem = panel ? P_SMEM : TC_SMEM;
-  if (attr_set[panel].need()) {
-    cudaError_t e = panel ? cudaFuncSetAttribute(sketch_tc_kernel<true>,
-                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, P_SMEM)
-                          : cudaFuncSetAttribute(sketch_tc_kernel<false>,
-                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM);
+  const void* fn = panel ? (const void*)sketch_tc_kernel<true, 2>
+                   : gs == 2 ? (const void*)sketch_tc_kernel<false, 2>
+                   : gs == 3 ? (const void*)sketch_tc_kernel<false, 3>
+                             : (const void*)sketch_tc_kernel<false, 4>;
+  if (attr_set[panel ? 0 : gs - 1].need()) {
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
   }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(2u * (unsigned)(p.n_tiles * p.k_tiles * p.splits));
-  cfg.blockDim = dim3(TC_THREADS);
+  cfg.blockDim = dim3((unsigned)tc_threads(gs));
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
@@ -556,8 +574,8 @@ cudaError_t launch_sketch_tc(const void* X, int64_t ldx, SketchTCParams p, cudaS
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return panel ? cudaLaunchKernelEx(&cfg, sketch_tc_kernel<true>, tmap, tmap_pi, p)
-               : cudaLaunchKernelEx(&cfg, sketch_tc_kernel<false>, tmap, tmap_pi, p);
+  void* args[] = {(void*)&tmap, (void*)&tmap_pi, (void*)&p};
+  return cudaLaunchKernelExC(&cfg, fn, args);
 }
 
 }  // namespace smp

@@ -101,6 +101,22 @@ def test_sketch_bf16_parity(d, n1, n2, k, pi):
     check_sketch(fin, orc)
 
 
+@pytest.mark.parametrize("gen_sets", ["", "2", "3", "4"])
+def test_sketch_generator_sets(monkeypatch, gen_sets):
+    """K1 with 2, 3 or 4 Π generator warp sets (TMEM ring of 2·GS stages; the
+    default picks 3 when several κ tiles share an X tile): same sketch as the
+    oracle — every set's K-block pairs, the ring phases and the Philox
+    prefetch of the next pair are exercised (k = 700: 3 κ tiles, ragged)."""
+    if gen_sets:
+        monkeypatch.setenv("SMP_K1_GEN_SETS", gen_sets)
+    d, n1, n2, k = 24000, 300, 200, 700
+    A = synth.gaussian_small(d, n1, seed=11, scale_cols=True).to(torch.bfloat16)
+    B = synth.gaussian_small(d, n2, seed=12).to(torch.bfloat16)
+    _, fin = gpu_sketch(A, B, k, PI["rademacher"], seed=13)
+    orc = oracle_sketch(A, B, k, PI["rademacher"], seed=13)
+    check_sketch(fin, orc)
+
+
 @pytest.mark.parametrize("d,n,k,pi", [(2000, 100, 64, "rademacher"), (1500, 70, 256, "gaussian")])
 def test_sketch_f32_parity(d, n, k, pi):
     """fp32 inputs go through the exact 3-term bf16 split."""

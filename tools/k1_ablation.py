@@ -3,7 +3,9 @@ switched off (SMP_K1_DEBUG bits: 1 = no norms, 2 = constant Π instead of the
 Philox generator, 4 = no MMA), each mode run for ~reps launches back to back.
 Diagnostics only (the sketches of modes != 0 are wrong by construction).
 
-    python tools/k1_ablation.py [cfg1|cfg2] [reps]
+    python tools/k1_ablation.py [cfg1|cfg2] [reps] [modes, e.g. 0,5,1]
+
+SMP_LIB=paper_1610_06656_b200/libsmp_<variant>.so selects a tuning build.
 """
 import os
 import sys
@@ -27,7 +29,9 @@ def main():
     A, B = bench.make_inputs(name, cfg, 0, cfg["d"], dev)
     sk = SMPSketch(cfg["d"], cfg["n1"], cfg["n2"], cfg["k"], pi=bench.pi_code(cfg), seed=cfg["seed"],
                    input=IN_DENSE_BF16, device=dev)
-    for mode in [0, 1, 2, 3, 4, 5, 6, 7, 0]:
+    modes = [int(x) for x in sys.argv[3].split(",")] if len(sys.argv) > 3 else [0, 1, 2, 3, 4, 5, 6, 7, 0]
+    lib = os.path.basename(os.environ.get("SMP_LIB", "libsmp.so"))
+    for mode in modes:
         os.environ["SMP_K1_DEBUG"] = str(mode)
         sk.reset()
         sk.block(0, A, B)
@@ -44,7 +48,7 @@ def main():
         c = clk.stop()
         sk.set_timing(False)
         parts = [p for b, p in ((1, "no-norms"), (2, "const-Pi"), (4, "no-MMA")) if mode & b]
-        print(f"{name} mode {mode} ({'+'.join(parts) or 'full'}): {ms / max(n, 1):.4f} ms/launch "
+        print(f"{lib} {name} mode {mode} ({'+'.join(parts) or 'full'}): {ms / max(n, 1):.4f} ms/launch "
               f"over {n} launches, sm {c and c['sm_mhz']} MHz {c and c['reasons']}", flush=True)
     os.environ.pop("SMP_K1_DEBUG")
     sk.close()

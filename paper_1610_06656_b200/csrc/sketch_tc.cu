@@ -229,7 +229,7 @@ sketch_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant
     if (lane == 0) {
       for (int it = 0; it < nkb; ++it) {
         const int s = it % NST;
-        mbar_wait(&xempty[s], ((uint32_t)(it / NST) & 1u) ^ 1u);
+        mbar_wait_backoff(&xempty[s], ((uint32_t)(it / NST) & 1u) ^ 1u, p.backoff_ns);
         mbar_arrive_expect_tx(&xfull[s], STG);
         const int row = (kb_begin + it) * TC_BK;
         tma_load_2d(x_s + s * STG, &tmap, &xfull[s], n0, row);
@@ -313,7 +313,7 @@ sketch_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant
           gen_pi_half(p.kind, p.seed, (uint32_t)kappa, valid, t0, rc, o, srht_s, srht_walsh);
           gen_pi_half(p.kind, p.seed, (uint32_t)kappa, valid, t0 + 32, rc, o2, srht_s, srht_walsh);
         }
-        mbar_wait(&pempty[ps], ((uint32_t)(it / PIS) & 1u) ^ 1u);
+        mbar_wait_backoff(&pempty[ps], ((uint32_t)(it / PIS) & 1u) ^ 1u, p.backoff_ns);
         tc_fence_after();
         tmem_st_32x32b_x16(taddr + ps * PI_COLS, o);
         tmem_st_32x32b_x16(taddr + ps * PI_COLS + 16, o2);
@@ -349,7 +349,7 @@ sketch_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant
     int duty_ctr = kb_begin % p.k_tiles;
     for (int it = 0; it < nkb; ++it) {
       const int s = it % NST;
-      mbar_wait(&xfull[s], (uint32_t)(it / NST) & 1u);
+      mbar_wait_backoff(&xfull[s], (uint32_t)(it / NST) & 1u, p.backoff_ns);
       const bool duty = norms_on && duty_ctr == kt;
       if (++duty_ctr == p.k_tiles) duty_ctr = 0;
       if (duty) {
@@ -398,7 +398,7 @@ sketch_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant
     const int quad = warp & 3;
     const int chalf = (warp - 8) >> 2;
     if (nkb > 0) {
-      mbar_wait(tmem_full, 0);
+      mbar_wait_backoff(tmem_full, 0, p.backoff_ns ? 4 * p.backoff_ns : 0);
       tc_fence_after();
     }
     const int kappa = kappa0 + 32 * quad + lane;

@@ -152,6 +152,11 @@ int pi_code(const smp_handle* h) {
 constexpr int K1_MAX_KB = 1024;        // 65,536 rows per accumulation chain (±1 Π)
 constexpr int K1_MAX_KB_GAUSS = 256;   // 16,384 rows (Gaussian Π)
 
+// K1's off-critical-path barrier waiters (TMA producer, Π generators, norm
+// warps, epilogue) sleep this long between tests instead of spinning
+// (SMP_K1_BACKOFF_NS overrides; 0 = spin).
+constexpr uint32_t K1_BACKOFF_NS = 0;
+
 int choose_splits(int tiles, int kb_total, int max_kb) {
   const int sms = 148;
   const int smin = std::max(1, (kb_total + max_kb - 1) / max_kb);
@@ -187,6 +192,7 @@ smp_status sketch_dense_bf16(smp_handle* h, int64_t row0, int64_t rows, const vo
   p.kind = pi_code(h);
   p.do_norms = do_norms ? 1 : 0;
   { const char* dbg = getenv("SMP_K1_DEBUG"); p.debug = dbg ? atoi(dbg) : 0; }
+  { const char* bo = getenv("SMP_K1_BACKOFF_NS"); p.backoff_ns = bo ? (uint32_t)atoi(bo) : K1_BACKOFF_NS; }
   p.seed = h->d.seed;
   CK(h, ensure(h->part, h->part_cap, (int64_t)p.splits * ncols * k), "alloc partials");
   CK(h, ensure(h->pnorm, h->pnorm_cap, (int64_t)p.splits * p.k_tiles * ncols), "alloc pnorm");

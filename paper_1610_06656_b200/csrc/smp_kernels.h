@@ -18,6 +18,7 @@ struct SketchTCParams {
   int32_t kind;      // PI_*
   int32_t do_norms;
   int32_t debug;     // tuning experiments only (SMP_K1_DEBUG): 1 skip norms, 2 skip Π gen, 4 skip MMA
+  uint32_t backoff_ns;  // K1: __nanosleep between barrier tests of the off-critical-path waiters (0 = spin)
   uint64_t seed;
   float* part;       // [splits][n][k]
   double* pnorm;     // [splits * k_tiles][n]

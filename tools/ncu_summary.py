@@ -56,22 +56,29 @@ def launches(path, out):
     hi = [i for i, r in enumerate(rows) if "Kernel Name" in r][0]
     hdr, data = rows[hi], rows[hi + 1:]
     ik, iv, iu = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
-    agg = collections.defaultdict(lambda: [0, 0.0])
+    im = hdr.index("Metric Name") if "Metric Name" in hdr else None
+    agg = collections.defaultdict(lambda: [0, 0.0, 0.0])  # launches, us, DRAM MB
+    scale_t = {"ns": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3, "msecond": 1e3, "nsecond": 1e-3}
+    scale_b = {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3}
     for r in data:
         if len(r) <= iv:
             continue
+        name = r[ik].split("(")[0][:70]
+        metric = r[im] if im is not None else "gpu__time_duration.sum"
         v = float(r[iv].replace(",", ""))
-        v = v / 1000 if r[iu] == "ns" else v * 1000 if r[iu] == "ms" else v
-        agg[r[ik].split("(")[0][:70]][0] += 1
-        agg[r[ik].split("(")[0][:70]][1] += v
-    ours = {k: v for k, v in agg.items() if "smp" in k or "cub::" in k}
+        if metric == "gpu__time_duration.sum":
+            agg[name][0] += 1
+            agg[name][1] += v * scale_t.get(r[iu], 1.0)
+        elif metric.startswith("dram__bytes"):
+            agg[name][2] += v * scale_b.get(r[iu], 1e-6)
+    ours = {k: v for k, v in agg.items() if "smp" in k or "cub::" in k or "CUB" in k}
     tot = sum(v[1] for v in ours.values())
     lines = [f"# ncu launch list (gpu__time_duration.sum, --clock-control none): `{path}`", "",
              "Cold-cache, serialised per-launch times: compare SHARES, not absolutes.", "",
              f"Library kernels only (data generation excluded): {sum(v[0] for v in ours.values())} launches, {tot:.1f} us", "",
-             "| kernel | launches | total us | share |", "|---|---|---|---|"]
-    for k, (n, t) in sorted(ours.items(), key=lambda x: -x[1][1]):
-        lines.append(f"| {k} | {n} | {t:.1f} | {100 * t / tot:.1f}% |")
+             "| kernel | launches | total us | share | DRAM MB |", "|---|---|---|---|---|"]
+    for k, (n, t, mb) in sorted(ours.items(), key=lambda x: -x[1][1]):
+        lines.append(f"| {k} | {n} | {t:.1f} | {100 * t / tot:.1f}% | {mb:.1f} |")
     open(out, "w").write("\n".join(lines) + "\n")
 
 

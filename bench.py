@@ -521,6 +521,18 @@ def main():
     value = total_bytes / (t_sketch * 1e-3) / 1e9
 
     pk = peaks()
+
+    def l2_view(tb_s):
+        """K3d against the measured L2 -> SM gather rate of its own access
+        pattern (tools/l2_probe.py: 1 KB rows at hashed indices of a 32 MB
+        L2-resident panel, no arithmetic; profiles/round2/l2_probe.json)."""
+        f = os.path.join(ROOT, "profiles", "round2", "l2_probe.json")
+        if not os.path.exists(f):
+            return None
+        peak = json.load(open(f))["best_32mb_tb_s"]
+        return {"achieved": tb_s, "peak": peak, "unit": "TB/s", "frac": tb_s / peak,
+                "peak_source": "measured L2 gather probe, 32 MB panel (profiles/round2/l2_probe.json)"}
+
     if csr:
         # the sparse sketch as a whole (K3: tensor-core head through K1 + the
         # SIMT tail K3a-d), timed as the sketch stage: 2k FLOP per nonzero
@@ -555,6 +567,7 @@ def main():
                 "algorithmic_per_launch": {"flops": flops_launch, "tail_nnz": tail_launch,
                                            "l2_pi_gather_bytes": tail_launch * kp_pad * 2},
                 "l2_pi_gather_tb_s": tail_launch * kp_pad * 2 / (k3_launch_ms * 1e-3) / 1e12,
+                "l2_view": l2_view(tail_launch * kp_pad * 2 / (k3_launch_ms * 1e-3) / 1e12),
                 "stage_view": {"achieved": ach_stage, "peak": alu_peak, "frac": ach_stage / alu_peak,
                                "unit": "TFLOP/s", "nnz": nnz, "tail_nnz": tail_nnz,
                                "timed": "sketch stage (CUDA events): head K1 + Π panels + sort + K3d"}}

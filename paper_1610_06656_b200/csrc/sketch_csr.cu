@@ -820,9 +820,18 @@ static int bits_for(int64_t x) {  // smallest b with 2^b > x
   return b;
 }
 
+// panel rows = 2^tbits: the 32-bit sort key packs (column << tbits | row);
+// at most 2^15 rows (a 32 MB bf16 Π panel at k = 512 stays L2-resident);
+// SMP_CSR_PANEL_BITS lowers the cap (tuning only)
+static int csr_tbits_cap() {
+  const char* e = getenv("SMP_CSR_PANEL_BITS");
+  const int v = e ? atoi(e) : 15;
+  return std::max(8, std::min(15, v));
+}
+
 int csr_panel_rows(int64_t ntot) {
   const int cbits = bits_for(ntot - 1 > 0 ? ntot - 1 : 1);
-  return 1 << std::max(0, std::min(15, 32 - cbits));
+  return 1 << std::max(0, std::min(csr_tbits_cap(), 32 - cbits));
 }
 
 cudaError_t csr_bounds(CsrWorkspace& w, const int64_t* a_rowptr, const int64_t* b_rowptr, int64_t ntot,
@@ -858,7 +867,7 @@ cudaError_t launch_sketch_csr(CsrWorkspace& w, int kind, uint64_t seed, int k, i
   const int64_t ntot = a_n + (b_rowptr ? b_n : 0);
   const int cbits = bits_for(ntot - 1 > 0 ? ntot - 1 : 1);
   if (cbits > 31) return cudaErrorInvalidValue;
-  const int tbits = std::min(15, 32 - cbits);
+  const int tbits = std::min(csr_tbits_cap(), 32 - cbits);
   if (tbits < 6) return cudaErrorInvalidValue;  // more than 2^26 columns
   const int rp = 1 << tbits;                      // panel rows
   // Π panel pitch: the κ slices of K3d's lanes, 256·KV with KV in {1, 2, 4, 8, 16} (zero padded)

@@ -825,8 +825,8 @@ static int bits_for(int64_t x) {  // smallest b with 2^b > x
 // SMP_CSR_PANEL_BITS lowers the cap (tuning only)
 static int csr_tbits_cap() {
   const char* e = getenv("SMP_CSR_PANEL_BITS");
-  const int v = e ? atoi(e) : 15;
-  return std::max(8, std::min(15, v));
+  const int v = e ? atoi(e) : 15;  // (values up to 17 accepted for experiments)
+  return std::max(8, std::min(17, v));
 }
 
 int csr_panel_rows(int64_t ntot) {

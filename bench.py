@@ -401,7 +401,7 @@ def main():
     from paper_1610_06656_b200 import dist as smp_dist
 
     def combine():
-        if world > 1:   # all-reduce of the packed partials, one per dtype
+        if world > 1:   # ONE all-reduce of the fp64 exchange buffer
             smp_dist.combine(sk)
 
     csr_pipe = {}

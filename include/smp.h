@@ -130,6 +130,18 @@ SMP_API smp_status smp_sketch_block_csr(smp_handle* h, int64_t row0, int64_t row
 SMP_API smp_status smp_sketch_partials(smp_handle* h, float** sk, int64_t* sk_count, double** nrm,
                                int64_t* nrm_count);
 
+/* The same partials as ONE fp64 exchange buffer for a single all-reduce-sum
+ * (the north star's "one NCCL allreduce"): *buf (device, owned
+ * by the handle, valid until the next pack or smp_destroy) receives
+ * [n_tot·k sketch sums widened exactly to fp64 | n_tot norms²], *count its
+ * length in doubles.  Enqueued on the handle's stream (no host sync): the
+ * caller's collective must be ordered after it on that stream.  After the
+ * all-reduce, smp_sketch_unpack_partials writes the reduced buffer back into
+ * the accumulators (sketch rounded to fp32 once), ready for
+ * smp_finalize_norms.  Errors: SMP_EINVAL (null handle / arguments), SMP_ECUDA. */
+SMP_API smp_status smp_sketch_pack_partials(smp_handle* h, double** buf, int64_t* count);
+SMP_API smp_status smp_sketch_unpack_partials(smp_handle* h);
+
 /* Finalize: Ã = (sum)·fp32(1/sqrt(k)), ||Ã_i|| (fp64 → fp32
  * out), ||A||_F² and ||B||_F² by the fixed pairwise tree (R5).
  * Any output pointer may be NULL.  A_sk: n1×k, B_sk: n2×k (= A_sk's content

@@ -24,7 +24,7 @@ EXPORTS = [
     "smp_sketch_partials", "smp_finalize_norms", "smp_sample_estimate", "smp_waltmin",
     "smp_sketch_reset", "smp_kernel_launches", "smp_destroy", "smp_last_error", "smp_status_str",
     "smp_set_timing", "smp_kernel_timing", "smp_sample_estimate_ex", "smp_norms_block",
-    "smp_exact_entries_block",
+    "smp_exact_entries_block", "smp_sketch_pack_partials", "smp_sketch_unpack_partials",
 ]
 
 
@@ -75,6 +75,8 @@ def load(path: str = None):
     lib.smp_sketch_block_csr.argtypes = [H, i64, i64, P, P, P, i64, P, P, P, i64]
     lib.smp_sketch_partials.argtypes = [H, ctypes.POINTER(P), ctypes.POINTER(i64),
                                         ctypes.POINTER(P), ctypes.POINTER(i64)]
+    lib.smp_sketch_pack_partials.argtypes = [H, ctypes.POINTER(P), ctypes.POINTER(i64)]
+    lib.smp_sketch_unpack_partials.argtypes = [H]
     lib.smp_finalize_norms.argtypes = [H, P, P, P, P, P, P, P]
     lib.smp_sample_estimate.argtypes = [H, f64, u64, i32, i64, P, P, P, P, ctypes.POINTER(i64)]
     lib.smp_sample_estimate_ex.argtypes = [H, f64, u64, i32, i32, i64, P, P, P, P, ctypes.POINTER(i64)]

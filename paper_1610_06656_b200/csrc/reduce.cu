@@ -1,6 +1,7 @@
 // K2 (partial combine), fp32 split planes, K4 (finalize, P:82,
 // P:313) and the R5 pairwise Frobenius tree.  All reductions use a fixed
 // order so that results are bit-reproducible run to run.
+#include <algorithm>
 #include "smp_device.cuh"
 #include "smp_kernels.h"
 
@@ -285,6 +286,43 @@ cudaError_t launch_pairwise_sum(const double* x, int64_t n, double* scratch, dou
   while (p < n) p <<= 1;
   if (n <= 0) p = 0;
   pairwise_sum_kernel<<<1, 1024, 0, st>>>(x, n, p, scratch, out);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- combine exchange
+// The cross-shard combine (P:145 treeAggregate) is ONE
+// all-reduce-sum of a single fp64 buffer [sketch sums (n_tot·k) | norms² (n_tot)]:
+// the fp32 sketch partials widened exactly, the fp64 norms copied.  The sum of
+// G <= 8 widened fp32 partials in fp64 is exact unless their exponents span
+// more than 29 binades, so the reduction order NCCL picks does not change
+// the result; the unpack rounds the sketch sum to fp32 once.
+__global__ void pack_partials_kernel(const float* __restrict__ sk, int64_t nsk, const double* __restrict__ nrm,
+                                     int64_t nn, double* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nsk + nn;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = i < nsk ? (double)sk[i] : nrm[i - nsk];
+}
+
+__global__ void unpack_partials_kernel(const double* __restrict__ in, int64_t nsk, int64_t nn,
+                                       float* __restrict__ sk, double* __restrict__ nrm) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nsk + nn;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    if (i < nsk) sk[i] = __double2float_rn(in[i]);
+    else nrm[i - nsk] = in[i];
+  }
+}
+
+static int exch_blocks(int64_t n) { return (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 8)); }
+
+cudaError_t launch_pack_partials(const float* sk, int64_t nsk, const double* nrm, int64_t nn, double* out,
+                                 cudaStream_t st) {
+  pack_partials_kernel<<<exch_blocks(nsk + nn), 256, 0, st>>>(sk, nsk, nrm, nn, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_unpack_partials(const double* in, int64_t nsk, int64_t nn, float* sk, double* nrm,
+                                   cudaStream_t st) {
+  unpack_partials_kernel<<<exch_blocks(nsk + nn), 256, 0, st>>>(in, nsk, nn, sk, nrm);
   return cudaGetLastError();
 }
 

@@ -31,6 +31,8 @@ struct smp_handle {
   int64_t part_cap = 0;
   double* pnorm = nullptr;
   int64_t pnorm_cap = 0;
+  double* xchg = nullptr;      // combine exchange buffer [ntot*k | ntot] (fp64)
+  int64_t xchg_cap = 0;
   uint16_t* planes = nullptr;
   int64_t planes_cap = 0;
   // pipelined plane split (sketch_dense_split): double buffers, aux stream
@@ -498,7 +500,7 @@ smp_status smp_sketch_reset(smp_handle* h) {
 void smp_destroy(smp_handle* h) {
   if (!h) return;
   if (h->st) cudaStreamSynchronize(h->st);
-  cudaFree(h->acc_sk); cudaFree(h->acc_nrm); cudaFree(h->part); cudaFree(h->pnorm);
+  cudaFree(h->acc_sk); cudaFree(h->acc_nrm); cudaFree(h->part); cudaFree(h->pnorm); cudaFree(h->xchg);
   smp::mn_workspace_free(h->mn);
   cudaFree(h->lela_at); cudaFree(h->lela_bt); cudaFree(h->lela_pn);
   cudaFree(h->planes); cudaFree(h->pi_panel); cudaFree(h->fin_sk); cudaFree(h->fin_sknorm); cudaFree(h->fin_D);
@@ -865,6 +867,29 @@ smp_status smp_sketch_partials(smp_handle* h, float** sk, int64_t* sk_count, dou
   if (sk_count) *sk_count = h->ntot * (int64_t)h->k;
   if (nrm) *nrm = h->acc_nrm;
   if (nrm_count) *nrm_count = h->ntot;
+  return SMP_OK;
+}
+
+smp_status smp_sketch_pack_partials(smp_handle* h, double** buf, int64_t* count) {
+  NvtxRange nvtx_("smp_sketch_pack_partials");
+  if (!h || !buf || !count) return SMP_EINVAL;
+  const int64_t nsk = h->ntot * (int64_t)h->k, nn = h->ntot;
+  CK(h, ensure(h->xchg, h->xchg_cap, nsk + nn), "alloc exchange");
+  CK(h, smp::launch_pack_partials(h->acc_sk, nsk, h->acc_nrm, nn, h->xchg, h->st), "pack partials");
+  h->launches += 1;
+  *buf = h->xchg;
+  *count = nsk + nn;
+  return SMP_OK;
+}
+
+smp_status smp_sketch_unpack_partials(smp_handle* h) {
+  NvtxRange nvtx_("smp_sketch_unpack_partials");
+  if (!h) return SMP_EINVAL;
+  const int64_t nsk = h->ntot * (int64_t)h->k, nn = h->ntot;
+  if (!h->xchg || h->xchg_cap < nsk + nn) return fail(h, SMP_EINVAL, "call smp_sketch_pack_partials first");
+  CK(h, smp::launch_unpack_partials(h->xchg, nsk, nn, h->acc_sk, h->acc_nrm, h->st), "unpack partials");
+  h->launches += 1;
+  h->finalized = false;
   return SMP_OK;
 }
 

@@ -35,6 +35,12 @@ int sketch_tc_smem_bytes();
 // p.n = input columns, p.n_tiles = ceil(n / 128); part = [splits][3 n][k].
 cudaError_t launch_sketch_tc_f32(const float* X, int64_t ldx, SketchTCParams p, int mode, cudaStream_t st);
 
+// ---- combine exchange (reduce.cu): [sk (fp32 -> fp64) | nrm] in one fp64 buffer, and back
+cudaError_t launch_pack_partials(const float* sk, int64_t nsk, const double* nrm, int64_t nn, double* out,
+                                 cudaStream_t st);
+cudaError_t launch_unpack_partials(const double* in, int64_t nsk, int64_t nn, float* sk, double* nrm,
+                                   cudaStream_t st);
+
 // ---- K2 partial reduce, fp32 split, K4 finalize (reduce.cu)
 // acc[c][κ] += Σ_s Σ_pl part[s][pl*n + c][κ]   (planes pl = 0..planes-1)
 // map (optional): output column of input column c is map[c] (acc is then the

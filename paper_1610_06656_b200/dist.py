@@ -2,7 +2,7 @@
 
 ΠA = Σ_g Π[:, rows_g] A[rows_g, :] and ||A_i||² = Σ_g ||A_i^(g)||² are sums
 over row blocks (the Spark treeAggregate of P:145), so each rank sketches its
-own rows and the packed partials are combined by all-reduce (NCCL over
+own rows and the packed partials are combined by ONE all-reduce (NCCL over
 NVLink on B200; gloo works for the CPU tests).  Everything after the combine
 (finalize, Ω, M̃, WAltMin) is replicated: the hashes make Ω identical on every
 rank without further communication.
@@ -57,7 +57,21 @@ def allreduce_partials(tensors, group=None):
 
 
 def combine(sketch, group=None):
-    """All-reduce an SMPSketch's packed partials in place (before finalize)."""
-    sk, nrm = sketch.partials()
-    allreduce_partials([sk, nrm], group=group)
-    return sk, nrm
+    """Combine an SMPSketch's row-shard partials with ONE all-reduce (before
+    finalize): the library packs [fp32 sketch sums widened to fp64 | fp64
+    norms²] into one exchange buffer on its stream (smp_sketch_pack_partials),
+    NCCL sums it in place, and the library writes it back
+    (smp_sketch_unpack_partials; the sketch rounded to fp32 once).  The fp64
+    sum of <= 8 widened fp32 partials is exact in practice, so the result does
+    not depend on NCCL's reduction order."""
+    if not dist.is_available() or not dist.is_initialized() or dist.get_world_size(group) == 1:
+        return sketch.partials()
+    buf = sketch.pack_partials()
+    if buf.is_cuda:
+        # the collective on the handle's stream: after the pack, before the unpack
+        with torch.cuda.stream(sketch.stream):
+            dist.all_reduce(buf, group=group)
+    else:
+        dist.all_reduce(buf, group=group)
+    sketch.unpack_partials()
+    return sketch.partials()

@@ -159,6 +159,19 @@ class SMPSketch:
         b = torch.as_tensor(_DevArray(nr.value, nrn.value, "<f8", self), device=self.device)
         return a, b
 
+    def pack_partials(self):
+        """The partials as ONE fp64 device buffer [sketch sums | norms²]
+        (smp_sketch_pack_partials) for a single all-reduce across row shards
+        (DESIGN.md §6); enqueued on the handle's stream."""
+        buf, n = ctypes.c_void_p(), ctypes.c_int64()
+        self._check(self.lib.smp_sketch_pack_partials(self.h, ctypes.byref(buf), ctypes.byref(n)),
+                    "smp_sketch_pack_partials")
+        return torch.as_tensor(_DevArray(buf.value, n.value, "<f8", self), device=self.device)
+
+    def unpack_partials(self):
+        """Write the (all-reduced) exchange buffer back into the accumulators."""
+        self._check(self.lib.smp_sketch_unpack_partials(self.h), "smp_sketch_unpack_partials")
+
     def finalize(self):
         dev = self.device
         A_sk = torch.empty(self.n1, self.k, dtype=torch.float32, device=dev)

@@ -76,6 +76,15 @@ class _StubSketch:
     def partials(self):
         return self.sk, self.nrm
 
+    def pack_partials(self):            # smp_sketch_pack_partials: [sk widened | nrm] in fp64
+        self.buf = torch.cat([self.sk.double(), self.nrm])
+        return self.buf
+
+    def unpack_partials(self):          # smp_sketch_unpack_partials: sk rounded to fp32 once
+        n = self.sk.numel()
+        self.sk.copy_(self.buf[:n].float())
+        self.nrm.copy_(self.buf[n:])
+
 
 def _combine_worker(rank, world, port, X, k, out):
     from paper_1610_06656_b200.dist import combine

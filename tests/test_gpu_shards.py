@@ -26,8 +26,9 @@ def _smp():
     return smp
 
 
-@pytest.mark.parametrize("G", [2, 4, 8])
-def test_row_sharded_handles_sum_to_single_pass(G):
+@pytest.mark.parametrize("G,via", [(2, "partials"), (4, "partials"), (8, "partials"), (2, "exchange"),
+                                   (8, "exchange")])
+def test_row_sharded_handles_sum_to_single_pass(G, via):
     smp = _smp()
     d, n, k = 8 * synth.GEN_BLOCK, 256, 256
     dev = torch.device("cuda", 0)
@@ -50,11 +51,20 @@ def test_row_sharded_handles_sum_to_single_pass(G):
         with pytest.raises(smp.SmpError):          # rows outside the handle's range are rejected
             h.block(out, A[out:out + 64], B[out:out + 64])
         hs.append(h)
-    sk0, nr0 = hs[0].partials()
-    for h in hs[1:]:
-        sk, nr = h.partials()
-        sk0 += sk
-        nr0 += nr
+    if via == "partials":
+        sk0, nr0 = hs[0].partials()
+        for h in hs[1:]:
+            sk, nr = h.partials()
+            sk0 += sk
+            nr0 += nr
+    else:
+        # the single fp64 exchange buffer that dist.combine all-reduces
+        bufs = [h.pack_partials() for h in hs]
+        torch.cuda.synchronize()
+        acc = bufs[0]
+        for b in bufs[1:]:
+            acc += b
+        hs[0].unpack_partials()
     fG = hs[0].finalize()
     e = col_rel_err(fG["A_sk"], f1["A_sk"].cpu().double().numpy())
     assert e.max() <= 1e-5, e.max()
@@ -79,6 +89,59 @@ def test_row_sharded_handles_sum_to_single_pass(G):
     for h in hs:
         h.close()
     one.close()
+
+
+def _nccl_combine_worker(port, out):
+    import os
+    import torch.distributed as dist
+    from paper_1610_06656_b200 import dist as smp_dist
+    smp = _smp()
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dev = torch.device("cuda", 0)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=dev)
+    d, n, k = 2 * synth.GEN_BLOCK, 300, 256
+    A = synth.gaussian_small(d, n, seed=21, scale_cols=True).to(torch.bfloat16).to(dev)
+    B = synth.gaussian_small(d, n, seed=22).to(torch.bfloat16).to(dev)
+    res = []
+    for comb in (False, True):
+        h = smp.SMPSketch(d, n, n, k, pi=smp.PI_RADEMACHER, seed=5, device=dev)
+        h.block(0, A, B)
+        if comb:
+            # the N > 1 bench's combine on a 1-rank NCCL group: pack -> all-reduce -> unpack
+            orig = dist.get_world_size
+            dist.get_world_size = lambda group=None: 2   # take the collective branch
+            try:
+                smp_dist.combine(h)
+            finally:
+                dist.get_world_size = orig
+        f = h.finalize()
+        res.append([f[x].cpu() for x in ("A_sk", "B_sk", "a_norm2", "b_norm2")])
+        h.close()
+    out.put(all(torch.equal(x, y) for x, y in zip(*res)))
+    dist.destroy_process_group()
+
+
+def test_nccl_single_allreduce_combine_is_exact():
+    """dist.combine = smp_sketch_pack_partials -> ONE NCCL all-reduce of the
+    fp64 exchange buffer -> smp_sketch_unpack_partials, run on a 1-rank NCCL
+    group: the round trip (fp32 widened to fp64, summed over one rank,
+    rounded back) must leave the finalized sketch and norms bit-identical."""
+    import socket
+    import torch.multiprocessing as mp
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=_nccl_combine_worker, args=(port, q))
+    p.start()
+    ok = q.get(timeout=300)
+    p.join(timeout=60)
+    assert p.exitcode == 0
+    assert ok
 
 
 def _nccl_worker(port, out):

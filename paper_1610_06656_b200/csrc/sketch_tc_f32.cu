@@ -29,11 +29,17 @@ namespace smp {
 namespace f32k {
 constexpr int BK = 64;                      // rows per K-block
 constexpr int HALF_N = 64;                  // input columns per SM
-constexpr int NSTG = 4;                     // X + Π ring
+#ifndef SMP_F32_NSTG
+#define SMP_F32_NSTG 4
+#endif
+#ifndef SMP_F32_NPL
+#define SMP_F32_NPL 2
+#endif
+constexpr int NSTG = SMP_F32_NSTG;          // X + Π ring
 constexpr int X_BYTES = BK * HALF_N * 4;    // 16 KB fp32
 constexpr int PI_BYTES = 128 * BK * 2;      // 16 KB
 constexpr int STG = X_BYTES + PI_BYTES;     // 32 KB
-constexpr int NPL = 2;                      // plane ring
+constexpr int NPL = SMP_F32_NPL;            // plane ring
 constexpr int PLANE = BK * HALF_N * 2;      // 8 KB bf16
 constexpr int PSLOT = 3 * PLANE;            // 24 KB
 constexpr int NCONV = 16;                   // converter warps (8..23)

@@ -33,21 +33,40 @@ constexpr int HALF_N = 64;                  // input columns per SM
 #define SMP_F32_NSTG 4
 #endif
 #ifndef SMP_F32_NPL
-#define SMP_F32_NPL 2
+#define SMP_F32_NPL 3
 #endif
 constexpr int NSTG = SMP_F32_NSTG;          // X + Π ring
 constexpr int X_BYTES = BK * HALF_N * 4;    // 16 KB fp32
 constexpr int PI_BYTES = 128 * BK * 2;      // 16 KB
-constexpr int STG = X_BYTES + PI_BYTES;     // 32 KB
+// SPLIT: the fp32 X tile and the Π tile live in rings of their own.  An X
+// stage is free as soon as the converters have read it (the MMA never reads
+// fp32), so its TMA runs NX K-blocks ahead of the converters instead of being
+// tied to the MMA's completion; a Π stage is freed by the MMA's commit.
+#ifndef SMP_F32_SPLIT
+#define SMP_F32_SPLIT 0
+#endif
+#ifndef SMP_F32_NPI
+#define SMP_F32_NPI 3
+#endif
+#ifndef SMP_F32_X_PROMO
+#define SMP_F32_X_PROMO CU_TENSOR_MAP_L2_PROMOTION_L2_256B
+#endif
+constexpr bool SPLIT = SMP_F32_SPLIT != 0;
+constexpr int NPI = SPLIT ? SMP_F32_NPI : NSTG;          // Π ring stages
+constexpr int STG = SPLIT ? X_BYTES : X_BYTES + PI_BYTES;   // bytes per X(+Π) stage
+constexpr int PI_RING = SPLIT ? NPI * PI_BYTES : 0;
 constexpr int NPL = SMP_F32_NPL;            // plane ring
 constexpr int PLANE = BK * HALF_N * 2;      // 8 KB bf16
 constexpr int PSLOT = 3 * PLANE;            // 24 KB
-constexpr int NCONV = 16;                   // converter warps (8..23)
+#ifndef SMP_F32_NCONV
+#define SMP_F32_NCONV 16
+#endif
+constexpr int NCONV = SMP_F32_NCONV;        // converter warps (8..)
 constexpr int RG = 2 * NCONV;               // row groups (32 lanes x NCONV / 16 chunks)
 constexpr int ROWS_PT = BK / RG;            // rows per converter thread per K-block
 constexpr int RED = RG * HALF_N * 8;        // 8 KB fp64 norm reduction
-constexpr int BARS = 2 * NSTG + 3 * NPL + 1;
-constexpr int SMEM = NSTG * STG + NPL * PSLOT + RED + BARS * 8 + 16 + 1024;
+constexpr int BARS = 2 * NSTG + 3 * NPL + 1 + 2 * NPI;
+constexpr int SMEM = NSTG * STG + PI_RING + NPL * PSLOT + RED + BARS * 8 + 16 + 1024;
 static_assert(SMEM <= 227 * 1024, "K1F exceeds the SMEM budget");
 constexpr int THREADS = 32 * (8 + NCONV);
 constexpr int TMEM_COLS = 512;
@@ -72,14 +91,17 @@ sketch_tc_f32_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_co
   const uint32_t raw_addr = smem_u32(smem_raw);
   uint8_t* smem = smem_raw + (((raw_addr + 1023u) & ~1023u) - raw_addr);
   uint8_t* st_s = smem;                                   // [NSTG][X 16 KB | Π 16 KB]
-  uint8_t* pl_s = smem + NSTG * STG;                      // [NPL][3][8 KB]
+  uint8_t* pi_s = smem + NSTG * STG;                      // SPLIT: [NPI][Π 16 KB]
+  uint8_t* pl_s = pi_s + PI_RING;                         // [NPL][3][8 KB]
   double* red = reinterpret_cast<double*>(pl_s + NPL * PSLOT);   // [RG][64]
   uint64_t* xfull = reinterpret_cast<uint64_t*>(pl_s + NPL * PSLOT + RED);
   uint64_t* xempty = xfull + NSTG;
   uint64_t* pfull = xempty + NSTG;    // converters -> relay (this CTA's planes of slot ps)
   uint64_t* pempty = pfull + NPL;     // MMA commit -> converters
   uint64_t* ready = pempty + NPL;     // leader only: both CTAs' slot ps ready
-  uint64_t* tmem_full = ready + NPL;
+  uint64_t* pifull = ready + NPL;     // SPLIT: Π tile landed
+  uint64_t* piempty = pifull + NPI;   // SPLIT: MMA commit -> Π producer
+  uint64_t* tmem_full = piempty + NPI;
   uint32_t* tmem_base_s = reinterpret_cast<uint32_t*>(tmem_full + 1);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -90,14 +112,21 @@ sketch_tc_f32_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_co
   const int split = bid;
   const int kb_begin = (int)(((int64_t)split * p.kb_total) / p.splits);
   const int kb_end = (int)(((int64_t)(split + 1) * p.kb_total) / p.splits);
-  const int nkb = kb_end - kb_begin;
+  const int nkb_all = kb_end - kb_begin;
+  // ablation (SMP_K1F_DEBUG & 512): the TMA producer alone, consuming its own stages
+  const bool tma_solo = (p.debug & 512) != 0;
+  const int nkb = tma_solo ? 0 : nkb_all;
   const int n0 = nt * 2 * HALF_N + (int)rank * HALF_N;   // this SM's input columns
   const int kappa0 = kt * 256 + (int)rank * 128;
 
   if (tid == 0) {
     for (int s = 0; s < NSTG; ++s) {
       mbar_init(&xfull[s], 1);
-      mbar_init(&xempty[s], 1 + NCONV);
+      mbar_init(&xempty[s], SPLIT ? NCONV : 1 + NCONV);
+    }
+    for (int s = 0; s < NPI; ++s) {
+      mbar_init(&pifull[s], 1);
+      mbar_init(&piempty[s], 1);
     }
     for (int s = 0; s < NPL; ++s) {
       mbar_init(&pfull[s], NCONV);
@@ -120,14 +149,32 @@ sketch_tc_f32_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_co
   if (warp == 0) {
     // ---------------- TMA producer: fp32 X half tile + Π tile per stage
     if (lane == 0) {
-      for (int it = 0; it < nkb; ++it) {
+      for (int it = 0; it < nkb_all; ++it) {
         const int s = it % NSTG;
-        mbar_wait(&xempty[s], ((uint32_t)(it / NSTG) & 1u) ^ 1u);
-        mbar_arrive_expect_tx(&xfull[s], STG);
+        if (!tma_solo) mbar_wait(&xempty[s], ((uint32_t)(it / NSTG) & 1u) ^ 1u);
+        else if (it >= NSTG) mbar_wait(&xfull[s], ((uint32_t)(it / NSTG) & 1u) ^ 1u);
+        // ablation (SMP_K1F_DEBUG): 128 = no Π TMA, 256 = no X TMA
+        const bool ld_pi = !SPLIT && !(p.debug & 128), ld_x = !(p.debug & 256);
+        mbar_arrive_expect_tx(&xfull[s], (ld_x ? X_BYTES : 0) + (ld_pi ? PI_BYTES : 0));
         const int row = (kb_begin + it) * BK;
-        tma_load_2d(st_s + s * STG, &tmap_x, &xfull[s], n0, row);
-        tma_load_2d(st_s + s * STG + 8192, &tmap_x, &xfull[s], n0 + 32, row);
-        tma_load_2d(st_s + s * STG + X_BYTES, &tmap_pi, &xfull[s], row, kappa0);
+        if (ld_x) {
+          tma_load_2d(st_s + s * STG, &tmap_x, &xfull[s], n0, row);
+          tma_load_2d(st_s + s * STG + 8192, &tmap_x, &xfull[s], n0 + 32, row);
+        }
+        if (ld_pi) tma_load_2d(st_s + s * STG + X_BYTES, &tmap_pi, &xfull[s], row, kappa0);
+      }
+      if (tma_solo)
+        for (int it = nkb_all > NSTG ? nkb_all - NSTG : 0; it < nkb_all; ++it)
+          mbar_wait(&xfull[it % NSTG], (uint32_t)(it / NSTG) & 1u);
+    }
+  } else if (SPLIT && warp == 3) {
+    // ---------------- TMA producer of the Π ring (SPLIT)
+    if (lane == 0) {
+      for (int it = 0; it < nkb; ++it) {
+        const int s = it % NPI;
+        mbar_wait(&piempty[s], ((uint32_t)(it / NPI) & 1u) ^ 1u);
+        mbar_arrive_expect_tx(&pifull[s], PI_BYTES);
+        tma_load_2d(pi_s + s * PI_BYTES, &tmap_pi, &pifull[s], (kb_begin + it) * BK, kappa0);
       }
     }
   } else if (warp == 1) {
@@ -138,20 +185,25 @@ sketch_tc_f32_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_co
       // Π tile (A) is read twice per K-step instead of three times
       const uint32_t idesc256 = make_idesc_bf16(256, 256, 0, 1);
       const uint32_t idesc128 = make_idesc_bf16(256, 128, 0, 1);
-      const uint32_t st_addr = smem_u32(st_s), pl_addr = smem_u32(pl_s);
+      const uint32_t pl_addr = smem_u32(pl_s);
+      const uint32_t a_addr = SPLIT ? smem_u32(pi_s) : smem_u32(st_s) + X_BYTES;
+      constexpr int A_STRIDE = SPLIT ? PI_BYTES : STG;
       for (int it = 0; it < nkb; ++it) {
-        const int s = it % NSTG, ps = it % NPL;
+        const int s = it % NSTG, ps = it % NPL, pis = it % NPI;
         mbar_wait(&ready[ps], (uint32_t)(it / NPL) & 1u);
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < BK / 16; ++kk) {
-          const uint64_t adesc = make_sdesc_sw128(st_addr + s * STG + X_BYTES + kk * 32, 16, 1024);
+          const uint64_t adesc = make_sdesc_sw128(a_addr + pis * A_STRIDE + kk * 32, 16, 1024);
           const uint64_t b01 = make_sdesc_sw128(pl_addr + ps * PSLOT + kk * 2048, 8192, 1024);
           const uint64_t b2 = make_sdesc_sw128(pl_addr + ps * PSLOT + 2 * PLANE + kk * 2048, 8192, 1024);
+          if (p.debug & 4) continue;   // ablation (SMP_K1F_DEBUG): no MMA
           tc_mma2_ss(tbase, adesc, b01, idesc256, (it | kk) != 0 ? 1u : 0u);
+          if (p.debug & 32) continue;  // ablation: no third-plane MMA
           tc_mma2_ss(tbase + 256, adesc, b2, idesc128, (it | kk) != 0 ? 1u : 0u);
         }
-        tc_commit2(&xempty[s], 0x3);
+        if (SPLIT) tc_commit2(&piempty[pis], 0x3);
+        else tc_commit2(&xempty[s], 0x3);
         tc_commit2(&pempty[ps], 0x3);
       }
       tc_commit2(tmem_full, 0x3);
@@ -163,6 +215,7 @@ sketch_tc_f32_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_co
       for (int it = 0; it < nkb; ++it) {
         const int ps = it % NPL;
         mbar_wait(&pfull[ps], (uint32_t)(it / NPL) & 1u);
+        if (SPLIT) mbar_wait(&pifull[it % NPI], (uint32_t)(it / NPI) & 1u);
         mbar_arrive_cluster_release(leader_ready + 8u * (uint32_t)ps);
       }
     }
@@ -175,7 +228,7 @@ sketch_tc_f32_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_co
     const int box = q >> 3, chunk = q & 7;
     const int c0 = 32 * box + 4 * chunk;   // first of this thread's 4 columns
     double nacc[4] = {0.0, 0.0, 0.0, 0.0};
-    const bool norms_on = p.do_norms != 0;
+    const bool norms_on = p.do_norms != 0 && !(p.debug & 1);
     int duty_ctr = kb_begin % p.k_tiles;
     // first plane: 4 significant bits (Gaussian Π) or 8 (±1 Π), RNE on the
     // fp32 pattern (zero and subnormal patterns round to themselves' prefix,
@@ -185,8 +238,13 @@ sketch_tc_f32_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_co
     const uint32_t rmask = (1u << rb) - 1u, rhalf = (1u << (rb - 1)) - 1u;
     for (int it = 0; it < nkb; ++it) {
       const int s = it % NSTG, ps = it % NPL;
+#ifdef SMP_F32_ELECT_POLL
+      mbar_wait_warp(&xfull[s], (uint32_t)(it / NSTG) & 1u);
+      mbar_wait_warp(&pempty[ps], ((uint32_t)(it / NPL) & 1u) ^ 1u);
+#else
       mbar_wait(&xfull[s], (uint32_t)(it / NSTG) & 1u);
       mbar_wait(&pempty[ps], ((uint32_t)(it / NPL) & 1u) ^ 1u);
+#endif
       const bool duty = norms_on && duty_ctr == kt;
       if (++duty_ctr == p.k_tiles) duty_ctr = 0;
       const uint8_t* xb = st_s + s * STG + box * 8192;
@@ -194,6 +252,7 @@ sketch_tc_f32_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_co
       const int pc = c0 >> 3, po = (c0 & 7) * 2;
 #pragma unroll
       for (int i = 0; i < ROWS_PT; ++i) {
+        if (p.debug & 64) break;     // ablation: no conversion
         const int r = rg + RG * i;
         const float4 v = *reinterpret_cast<const float4*>(xb + r * 128 + ((chunk ^ (r & 7)) << 4));
         const float x[4] = {v.x, v.y, v.z, v.w};
@@ -316,7 +375,7 @@ cudaError_t launch_sketch_tc_f32(const float* X, int64_t ldx, SketchTCParams p, 
     cuuint32_t box[2] = {32, 64};
     cuuint32_t estr[2] = {1, 1};
     if (enc(&tmap_x, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(X), dims, strides, box, estr,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, SMP_F32_X_PROMO,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return cudaErrorInvalidValue;
   }

@@ -369,7 +369,7 @@ smp_status sketch_dense_f32_fused(smp_handle* h, int64_t row0, int64_t rows, con
     p.pnorm = h->pnorm;
     p.pi_panel = h->pi_panel;
     p.pi_ld = ld;
-    p.debug = 0;
+    { const char* dbg = getenv("SMP_K1F_DEBUG"); p.debug = dbg ? atoi(dbg) : 0; }  // ablation only
     if (h->timing) {
       while (h->ev_pool.size() < h->ev_used_n + 2) {
         cudaEvent_t e;

@@ -252,6 +252,32 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 #endif
 }
 
+// Warp-wide wait with ONE polling lane: lane 0 tests the barrier (predicated
+// inside the asm, so the warp never diverges), the result is broadcast with a
+// shuffle, and once the phase has completed every lane observes it itself
+// with a single test (the acquire each reader of TMA-written data needs).
+// 32 lanes polling one mbarrier are 32 requests to the SM's barrier unit per
+// test; the TMA's complete_tx updates and tcgen05.commit arrivals queue behind
+// them.  All 32 lanes of the warp must call it.
+__device__ __forceinline__ void mbar_wait_warp(uint64_t* bar, uint32_t parity) {
+  const uint32_t addr = smem_u32(bar);
+  const uint32_t lane = threadIdx.x & 31u;
+  uint32_t ok;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred P1, P2;\n\t"
+        "setp.eq.u32 P2, %3, 0;\n\t"
+        "mov.u32 %0, 0;\n\t"
+        "@P2 mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2, %4;\n\t"
+        "@P2 selp.u32 %0, 1, 0, P1;\n\t}"
+        : "=r"(ok)
+        : "r"(addr), "r"(parity), "r"(lane), "r"(0x989680u)
+        : "memory");
+    ok = __shfl_sync(0xffffffffu, ok, 0);
+  } while (!ok);
+  mbar_wait(bar, parity);
+}
+
 // Wait with a back-off for warps whose wait is off the critical path (they
 // sit ahead of a deep ring): one non-suspending test, then __nanosleep(ns)
 // between tests, so that a parked warp stops taking issue slots from the

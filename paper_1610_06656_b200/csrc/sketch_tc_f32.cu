@@ -72,6 +72,18 @@ constexpr int THREADS = 32 * (8 + NCONV);
 constexpr int TMEM_COLS = 512;
 }  // namespace f32k
 
+// SMP_F32_TRACE (tuning builds only): per-K-block clock64 stamps of one CTA
+// pair's pipeline events, read back with smp_debug_k1f_trace
+#ifdef SMP_F32_TRACE
+__device__ unsigned long long g_k1f_trace[2][8][512];
+#define K1F_TR(ev, it)                                                             \
+  do {                                                                             \
+    if ((blockIdx.x >> 1) == SMP_F32_TRACE && (it) < 512) g_k1f_trace[rank][ev][it] = clock64(); \
+  } while (0)
+#else
+#define K1F_TR(ev, it)
+#endif
+
 // round to b significant bits (RNE on the fp32 pattern); see reduce.cu
 __device__ __forceinline__ float f32k_round_sig(float x, int b) {
   const uint32_t u = __float_as_uint(x);
@@ -81,6 +93,35 @@ __device__ __forceinline__ float f32k_round_sig(float x, int b) {
   const uint32_t lsb = (u >> drop) & 1u;
   const uint32_t mag = ((u & 0x7FFFFFFFu) + half - 1u + lsb) & ~((1u << drop) - 1u);
   return __uint_as_float((u & 0x80000000u) | mag);
+}
+
+// (hi << 16) | lo of bf16_rne(a) (lo) and bf16_rne(b) (hi): one F2FP instead of
+// the 4-instruction integer RNE per value (same bits for finite inputs)
+__device__ __forceinline__ uint32_t f32k_bf16x2(float a, float b) {
+  uint32_t z;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(z) : "f"(b), "f"(a));
+  return z;
+}
+
+// (hi, lo) += x² in double-float arithmetic on the fp32 pipe: p + e = x² exactly
+// (FMA residual), TwoSum(hi, p) exactly, the small terms gathered in lo.  The
+// pair carries ~46 significant bits (relative error < 2^-44 over a CTA's
+// K-range); it replaces a F2F.F64.F32 + DFMA per element, which the trace showed
+// as +1,100 cycles on every K-block with norm duty.  Valid while x² and its
+// residual stay normal fp32 numbers: |x| in [2^-40, 2^41) or x = 0 (subnormal
+// x: x² < 2^-252, dropped); other magnitudes take the fp64 path (f32k_sq_fast).
+__device__ __forceinline__ bool f32k_sq_fast(float x) {
+  const uint32_t t = __float_as_uint(x) & 0x7F800000u;       // biased exponent field
+  return t == 0u || (t - 0x2B800000u) <= 0x28000000u;        // exponent in [87, 167]
+}
+__device__ __forceinline__ void f32k_sq_acc(float x, float& hi, float& lo) {
+  const float p = __fmul_rn(x, x);
+  const float e = __fmaf_rn(x, x, -p);
+  const float s = __fadd_rn(hi, p);
+  const float bb = __fsub_rn(s, hi);
+  const float err = __fadd_rn(__fsub_rn(hi, __fsub_rn(s, bb)), __fsub_rn(p, bb));
+  hi = s;
+  lo = __fadd_rn(lo, __fadd_rn(err, e));
 }
 
 __global__ void __launch_bounds__(f32k::THREADS, 1)
@@ -153,6 +194,7 @@ sketch_tc_f32_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_co
         const int s = it % NSTG;
         if (!tma_solo) mbar_wait(&xempty[s], ((uint32_t)(it / NSTG) & 1u) ^ 1u);
         else if (it >= NSTG) mbar_wait(&xfull[s], ((uint32_t)(it / NSTG) & 1u) ^ 1u);
+        K1F_TR(0, it);
         // ablation (SMP_K1F_DEBUG): 128 = no Π TMA, 256 = no X TMA
         const bool ld_pi = !SPLIT && !(p.debug & 128), ld_x = !(p.debug & 256);
         mbar_arrive_expect_tx(&xfull[s], (ld_x ? X_BYTES : 0) + (ld_pi ? PI_BYTES : 0));
@@ -192,6 +234,7 @@ sketch_tc_f32_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_co
         const int s = it % NSTG, ps = it % NPL, pis = it % NPI;
         mbar_wait(&ready[ps], (uint32_t)(it / NPL) & 1u);
         tc_fence_after();
+        K1F_TR(5, it);
 #pragma unroll
         for (int kk = 0; kk < BK / 16; ++kk) {
           const uint64_t adesc = make_sdesc_sw128(a_addr + pis * A_STRIDE + kk * 32, 16, 1024);
@@ -205,6 +248,7 @@ sketch_tc_f32_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_co
         if (SPLIT) tc_commit2(&piempty[pis], 0x3);
         else tc_commit2(&xempty[s], 0x3);
         tc_commit2(&pempty[ps], 0x3);
+        K1F_TR(6, it);
       }
       tc_commit2(tmem_full, 0x3);
     }
@@ -216,6 +260,7 @@ sketch_tc_f32_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_co
         const int ps = it % NPL;
         mbar_wait(&pfull[ps], (uint32_t)(it / NPL) & 1u);
         if (SPLIT) mbar_wait(&pifull[it % NPI], (uint32_t)(it / NPI) & 1u);
+        K1F_TR(4, it);
         mbar_arrive_cluster_release(leader_ready + 8u * (uint32_t)ps);
       }
     }
@@ -227,7 +272,8 @@ sketch_tc_f32_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_co
     const int q = g & 15, rg = g >> 4;
     const int box = q >> 3, chunk = q & 7;
     const int c0 = 32 * box + 4 * chunk;   // first of this thread's 4 columns
-    double nacc[4] = {0.0, 0.0, 0.0, 0.0};
+    float nhi[4] = {0.f, 0.f, 0.f, 0.f}, nlo[4] = {0.f, 0.f, 0.f, 0.f};
+    double nacc[4] = {0.0, 0.0, 0.0, 0.0};   // elements outside the fp32-safe range (rare)
     const bool norms_on = p.do_norms != 0 && !(p.debug & 1);
     int duty_ctr = kb_begin % p.k_tiles;
     // first plane: 4 significant bits (Gaussian Π) or 8 (±1 Π), RNE on the
@@ -243,7 +289,9 @@ sketch_tc_f32_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_co
       mbar_wait_warp(&pempty[ps], ((uint32_t)(it / NPL) & 1u) ^ 1u);
 #else
       mbar_wait(&xfull[s], (uint32_t)(it / NSTG) & 1u);
+      if (tid == 256) K1F_TR(1, it);
       mbar_wait(&pempty[ps], ((uint32_t)(it / NPL) & 1u) ^ 1u);
+      if (tid == 256) K1F_TR(2, it);
 #endif
       const bool duty = norms_on && duty_ctr == kt;
       if (++duty_ctr == p.k_tiles) duty_ctr = 0;
@@ -258,34 +306,41 @@ sketch_tc_f32_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_co
         const float x[4] = {v.x, v.y, v.z, v.w};
         if (duty) {
 #pragma unroll
-          for (int j = 0; j < 4; ++j) nacc[j] = fma((double)x[j], (double)x[j], nacc[j]);
+          for (int j = 0; j < 4; ++j) {
+            if (f32k_sq_fast(x[j])) f32k_sq_acc(x[j], nhi[j], nlo[j]);
+            else nacc[j] = fma((double)x[j], (double)x[j], nacc[j]);
+          }
         }
-        uint32_t b1[4], b2[4], b3[4];
+        // plane 1 by the integer RNE (4 or 8 significant bits), planes 2 and 3
+        // by packed bf16 RNE converts (plane 3 of a ±1 Π is the exact 8-bit
+        // remainder, which the convert leaves unchanged)
+        uint32_t b1[4];
+        float r1[4], r2[4];
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           const uint32_t u = __float_as_uint(x[j]);
           const uint32_t h = (u + rhalf + ((u >> rb) & 1u)) & ~rmask;
-          const float r1 = __fsub_rn(x[j], __uint_as_float(h));
-          const uint32_t u1 = __float_as_uint(r1);
-          const uint32_t h1 = (u1 + 0x7FFFu + ((u1 >> 16) & 1u)) & 0xFFFF0000u;
-          const float r2 = __fsub_rn(r1, __uint_as_float(h1));
-          const uint32_t u2 = __float_as_uint(r2);
+          r1[j] = __fsub_rn(x[j], __uint_as_float(h));
           b1[j] = h;
-          b2[j] = h1;
-          b3[j] = mode == 4 ? ((u2 + 0x7FFFu + ((u2 >> 16) & 1u)) & 0xFFFF0000u) : u2;
         }
+        const uint32_t p2a = f32k_bf16x2(r1[0], r1[1]), p2b = f32k_bf16x2(r1[2], r1[3]);
+        r2[0] = __fsub_rn(r1[0], __uint_as_float(p2a << 16));
+        r2[1] = __fsub_rn(r1[1], __uint_as_float(p2a & 0xFFFF0000u));
+        r2[2] = __fsub_rn(r1[2], __uint_as_float(p2b << 16));
+        r2[3] = __fsub_rn(r1[3], __uint_as_float(p2b & 0xFFFF0000u));
+        const uint32_t p3a = f32k_bf16x2(r2[0], r2[1]), p3b = f32k_bf16x2(r2[2], r2[3]);
         // element (r, c) of a 64x64 bf16 SW128 tile: r*128 + ((c>>3) ^ (r&7))*16 + (c&7)*2;
         // this thread's 4 columns share one 16-byte chunk
         const uint32_t off = (uint32_t)(r * 128 + ((pc ^ (r & 7)) << 4) + po);
         *reinterpret_cast<uint2*>(pb + off) =
             make_uint2(__byte_perm(b1[0], b1[1], 0x7632), __byte_perm(b1[2], b1[3], 0x7632));
-        *reinterpret_cast<uint2*>(pb + PLANE + off) =
-            make_uint2(__byte_perm(b2[0], b2[1], 0x7632), __byte_perm(b2[2], b2[3], 0x7632));
-        *reinterpret_cast<uint2*>(pb + 2 * PLANE + off) =
-            make_uint2(__byte_perm(b3[0], b3[1], 0x7632), __byte_perm(b3[2], b3[3], 0x7632));
+        *reinterpret_cast<uint2*>(pb + PLANE + off) = make_uint2(p2a, p2b);
+        *reinterpret_cast<uint2*>(pb + 2 * PLANE + off) = make_uint2(p3a, p3b);
       }
       fence_proxy_async_smem();   // generic-proxy plane writes -> visible to the tensor core
       __syncwarp();
+      if (tid == 256) K1F_TR(3, it);
+      if (tid == 32 * (8 + NCONV - 1)) K1F_TR(7, it);
       if (lane == 0) {
         mbar_arrive(&xempty[s]);
         mbar_arrive(&pfull[ps]);
@@ -293,7 +348,7 @@ sketch_tc_f32_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_co
     }
     // norm partials: fixed-order reduction over the 16 row groups
 #pragma unroll
-    for (int j = 0; j < 4; ++j) red[rg * HALF_N + c0 + j] = nacc[j];
+    for (int j = 0; j < 4; ++j) red[rg * HALF_N + c0 + j] = ((double)nhi[j] + (double)nlo[j]) + nacc[j];
     named_bar_sync(1, 32 * NCONV);
     const int slot = split * p.k_tiles + kt;
     if (g < HALF_N) {
@@ -362,6 +417,12 @@ static PFN_cuTensorMapEncodeTiled_v12000 f32k_encode_fn() {
   }
   return fn;
 }
+
+#ifdef SMP_F32_TRACE
+extern "C" __attribute__((visibility("default"))) int smp_debug_k1f_trace(unsigned long long* out) {
+  return (int)cudaMemcpyFromSymbol(out, g_k1f_trace, sizeof(g_k1f_trace));
+}
+#endif
 
 int sketch_tc_f32_cols_per_tile() { return 2 * f32k::HALF_N; }
 

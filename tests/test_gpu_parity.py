@@ -126,6 +126,29 @@ def test_sketch_f32_parity(d, n, k, pi):
     check_sketch(fin, orc)
 
 
+def test_sketch_f32_norms_extreme_magnitudes():
+    """K1F accumulates Σx² as fp32 double-float pairs while x² and its FMA
+    residual are normal fp32 numbers (|x| in [2^-40, 2^41)) and in fp64
+    otherwise: columns scaled from 1e-30 to 1e18 (x² under- and overflows
+    fp32 at both ends) must still give the oracle's fp64 norms, and the
+    sketch its 1e-5 (the plane split is scale-free)."""
+    d, n = 4096, 128
+    A = synth.gaussian_small(d, n, seed=31).float()
+    B = synth.gaussian_small(d, n, seed=32).float()
+    exps = torch.tensor([-30, -22, -13, -12, -6, 0, 5, 12, 13, 18], dtype=torch.float64)
+    sa = (10.0 ** exps[torch.arange(n) % len(exps)]).float()
+    A = A * sa[None, :]
+    B = B * sa.flip(0)[None, :]
+    B[::3, 7] = 0.0   # exact zeros mixed into a tiny-magnitude column
+    _, fin = gpu_sketch(A, B, 64, PI["rademacher"], seed=3)
+    orc = oracle_sketch(A, B, 64, PI["rademacher"], seed=3)
+    ea = col_rel_err(fin["A_sk"], orc["As"])
+    eb = col_rel_err(fin["B_sk"], orc["Bs"])
+    assert ea.max() <= 1e-5 and eb.max() <= 1e-5, (ea.max(), eb.max())
+    np.testing.assert_allclose(fin["a_norm2"].cpu().numpy(), orc["a2"], rtol=1e-12, atol=0)
+    np.testing.assert_allclose(fin["b_norm2"].cpu().numpy(), orc["b2"], rtol=1e-12, atol=0)
+
+
 def test_sketch_unaligned_row0_and_blocks():
     """Global row offsets not multiple of 32/64 exercise the generic Π path;
     blocks in arbitrary order sum to the whole."""

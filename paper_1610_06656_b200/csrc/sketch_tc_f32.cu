@@ -52,6 +52,13 @@ constexpr int PI_BYTES = 128 * BK * 2;      // 16 KB
 #define SMP_F32_X_PROMO CU_TENSOR_MAP_L2_PROMOTION_L2_256B
 #endif
 constexpr bool SPLIT = SMP_F32_SPLIT != 0;
+// DIRECT: each converter warp arrives on the LEADER CTA's ready barrier itself
+// (release at cluster scope) instead of going through a local barrier and the
+// relay thread: one hop less in the per-stage chain that bounds K1F.
+#ifndef SMP_F32_DIRECT
+#define SMP_F32_DIRECT 0
+#endif
+constexpr bool DIRECT = SMP_F32_DIRECT != 0 && !SPLIT;
 constexpr int NPI = SPLIT ? SMP_F32_NPI : NSTG;          // Π ring stages
 constexpr int STG = SPLIT ? X_BYTES : X_BYTES + PI_BYTES;   // bytes per X(+Π) stage
 constexpr int PI_RING = SPLIT ? NPI * PI_BYTES : 0;
@@ -172,7 +179,7 @@ sketch_tc_f32_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_co
     for (int s = 0; s < NPL; ++s) {
       mbar_init(&pfull[s], NCONV);
       mbar_init(&pempty[s], 1);
-      mbar_init(&ready[s], 2);
+      mbar_init(&ready[s], DIRECT ? 2 * NCONV : 2);
     }
     mbar_init(tmem_full, 1);
     fence_mbar_init();
@@ -254,7 +261,7 @@ sketch_tc_f32_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_co
     }
   } else if (warp == 2) {
     // ---------------- relay: this CTA's planes of slot ps (and its Π) are ready
-    if (lane == 0) {
+    if (lane == 0 && !DIRECT) {
       const uint32_t leader_ready = mapa_shared(smem_u32(ready), 0);
       for (int it = 0; it < nkb; ++it) {
         const int ps = it % NPL;
@@ -280,6 +287,7 @@ sketch_tc_f32_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_co
     // fp32 pattern (zero and subnormal patterns round to themselves' prefix,
     // so the remainders stay exact); then bf16 RNE; then the exact (±1) or
     // rounded (Gaussian, remainder dropped) third plane
+    const uint32_t conv_ready = mapa_shared(smem_u32(ready), 0);   // DIRECT: the leader's barrier
     const uint32_t rb = mode == 4 ? 20u : 16u;           // dropped bits of plane 1
     const uint32_t rmask = (1u << rb) - 1u, rhalf = (1u << (rb - 1)) - 1u;
     for (int it = 0; it < nkb; ++it) {
@@ -343,7 +351,8 @@ sketch_tc_f32_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_co
       if (tid == 32 * (8 + NCONV - 1)) K1F_TR(7, it);
       if (lane == 0) {
         mbar_arrive(&xempty[s]);
-        mbar_arrive(&pfull[ps]);
+        if (DIRECT) mbar_arrive_cluster_release(conv_ready + 8u * (uint32_t)ps);
+        else mbar_arrive(&pfull[ps]);
       }
     }
     // norm partials: fixed-order reduction over the 16 row groups

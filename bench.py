@@ -556,7 +556,7 @@ def main():
         kp_pad = 256 * (1 if k <= 256 else 2 if k <= 512 else 4 if k <= 1024 else 8 if k <= 2048 else 16)
         traffic = None
         tfile = os.path.join(ROOT, "profiles", "k1_traffic.json")
-        if os.path.exists(tfile):
+        if os.path.exists(tfile) and world == 1:   # ncu capture of the N=1 launch shape
             traffic = json.load(open(tfile)).get(cfgname)
         roof = {"bound": "alu", "achieved": ach, "peak": alu_peak, "unit": "TFLOP/s",
                 "frac": ach / alu_peak, "traffic": traffic,
@@ -589,7 +589,7 @@ def main():
         t_tc = flops_launch / (pk["tc"] * 1e12)
         traffic = None
         tfile = os.path.join(ROOT, "profiles", "k1_traffic.json")
-        if os.path.exists(tfile):
+        if os.path.exists(tfile) and world == 1:   # ncu capture of the N=1 launch shape
             traffic = json.load(open(tfile)).get(cfgname)
         kname = "sketch_tc_f32_kernel (K1F)" if inp == IN_DENSE_F32 else "sketch_tc_kernel (K1)"
         if t_tc >= t_hbm:

@@ -167,6 +167,18 @@ __device__ __forceinline__ void gen_pi_half(int kind, uint64_t seed, uint32_t ka
   }
 }
 
+// SMP_K1_TRACE=<pair index> (tuning builds only): clock64 stamps of one CTA
+// pair's pipeline events per K-block, read back with smp_debug_k1_trace
+#ifdef SMP_K1_TRACE
+__device__ unsigned long long g_k1_trace[2][8][512];
+#define K1_TR(ev, it)                                                              \
+  do {                                                                             \
+    if ((blockIdx.x >> 1) == SMP_K1_TRACE && (it) < 512) g_k1_trace[rank][ev][it] = clock64(); \
+  } while (0)
+#else
+#define K1_TR(ev, it)
+#endif
+
 template <bool PANEL, int GS>
 __global__ void __launch_bounds__(tc_threads(GS), 1)
 sketch_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap tmap_pi,
@@ -230,6 +242,7 @@ sketch_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant
       for (int it = 0; it < nkb; ++it) {
         const int s = it % NST;
         mbar_wait_backoff(&xempty[s], ((uint32_t)(it / NST) & 1u) ^ 1u, p.backoff_ns);
+        K1_TR(0, it);
         mbar_arrive_expect_tx(&xfull[s], STG);
         const int row = (kb_begin + it) * TC_BK;
         tma_load_2d(x_s + s * STG, &tmap, &xfull[s], n0, row);
@@ -246,6 +259,7 @@ sketch_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant
         const int s = it % NST, ps = it % PIS;
         mbar_wait(&ready[s], (uint32_t)(it / NST) & 1u);
         tc_fence_after();
+        K1_TR(5, it);
         if (!(p.debug & 4)) {
 #pragma unroll
           for (int kk = 0; kk < TC_BK / 16; ++kk) {
@@ -262,6 +276,7 @@ sketch_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant
         }
         tc_commit2(&xempty[s], 0x3);
         if (!PANEL) tc_commit2(&pempty[ps], 0x3);
+        K1_TR(6, it);
       }
       tc_commit2(tmem_full, 0x3);
     }
@@ -272,7 +287,9 @@ sketch_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant
       for (int it = 0; it < nkb; ++it) {
         const int s = it % NST, ps = it % PIS;
         mbar_wait(&xfull[s], (uint32_t)(it / NST) & 1u);
+        K1_TR(1, it);
         if (!PANEL) mbar_wait(&pfull[ps], (uint32_t)(it / PIS) & 1u);
+        K1_TR(4, it);
         mbar_arrive_cluster(leader_ready + 8u * (uint32_t)s);
       }
     }
@@ -306,6 +323,7 @@ sketch_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant
         const int ps = it % PIS;
         const uint64_t t0 = (uint64_t)p.row0 + (uint64_t)(kb_begin + it) * TC_BK;
         uint32_t o[16], o2[16];
+        if (quad == 0 && lane == 0) K1_TR(2, it);
         if (p.debug & 2) {
 #pragma unroll
           for (int i = 0; i < 16; ++i) o[i] = o2[i] = 0x3F803F80u;
@@ -313,8 +331,10 @@ sketch_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant
           gen_pi_half(p.kind, p.seed, (uint32_t)kappa, valid, t0, rc, o, srht_s, srht_walsh);
           gen_pi_half(p.kind, p.seed, (uint32_t)kappa, valid, t0 + 32, rc, o2, srht_s, srht_walsh);
         }
+        if (quad == 0 && lane == 0) K1_TR(3, it);
         mbar_wait_backoff(&pempty[ps], ((uint32_t)(it / PIS) & 1u) ^ 1u, p.backoff_ns);
         tc_fence_after();
+        if (quad == 0 && lane == 0) K1_TR(7, it);
         tmem_st_32x32b_x16(taddr + ps * PI_COLS, o);
         tmem_st_32x32b_x16(taddr + ps * PI_COLS + 16, o2);
         if (h == 1 || it + 1 == nkb) {
@@ -512,6 +532,12 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
   }
   return fn;
 }
+
+#ifdef SMP_K1_TRACE
+extern "C" __attribute__((visibility("default"))) int smp_debug_k1_trace(unsigned long long* out) {
+  return (int)cudaMemcpyFromSymbol(out, g_k1_trace, sizeof(g_k1_trace));
+}
+#endif
 
 int sketch_tc_smem_bytes() { return TC_SMEM; }
 int sketch_tc_ctas_per_tile() { return 2; }

@@ -107,11 +107,29 @@ __device__ __forceinline__ uint32_t rad_word(RadCache& c, uint64_t W, uint32_t k
 // (rows 2p, 2p+1) is built with one shift and one LOP3.
 __device__ __forceinline__ uint32_t rad_pos(uint32_t e) { return (e >> 1) | ((e & 1u) << 4); }
 
+// (a & b) | c in ONE LOP3 with b and c in registers: written as two C
+// operators with two immediates the compiler emits two LOP3s per bf16 pair
+// (a LOP3 has one immediate slot), i.e. 3 instructions per pair with the
+// shift instead of 2 — a quarter of the generator warps' instructions, which
+// pace cfg1 (profiles/round2/k1_trace_cfg1.log).
+__device__ __forceinline__ uint32_t lop3_and_or(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t d;
+  asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+// a constant the compiler cannot fold back into an immediate
+__device__ __forceinline__ uint32_t opaque_u32(uint32_t v) {
+  uint32_t d;
+  asm volatile("mov.u32 %0, %1;" : "=r"(d) : "r"(v));
+  return d;
+}
+
 // Half a κ row of the Π tile, rows t0..t0+31: 32 bf16 packed in 16 words
 // (word p = rows 2p (low half) and 2p+1 (high half)), the TMEM A layout.
 __device__ __forceinline__ void gen_pi_half(int kind, uint64_t seed, uint32_t kappa, bool valid,
                                             uint64_t t0, RadCache& rc, uint32_t (&o)[16],
-                                            uint64_t srht_s, uint32_t srht_walsh) {
+                                            uint64_t srht_s, uint32_t srht_walsh,
+                                            uint32_t sign_mask, uint32_t one_pair) {
   const uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
   if (!valid) {
 #pragma unroll
@@ -125,12 +143,12 @@ __device__ __forceinline__ void gen_pi_half(int kind, uint64_t seed, uint32_t ka
     const uint32_t hb = (uint32_t)__popcll((unsigned long long)(srht_s & t0)) & 1u;
     const uint32_t w = dw ^ srht_walsh ^ (0u - hb);
 #pragma unroll
-    for (int p = 0; p < 16; ++p) o[p] = 0x3F803F80u | ((w * (1u << (15 - p))) & 0x80008000u);
+    for (int p = 0; p < 16; ++p) o[p] = lop3_and_or(w * (1u << (15 - p)), sign_mask, one_pair);
   } else if (kind == PI_RADEMACHER && (t0 & 31) == 0) {
     const uint32_t w = rad_word(rc, t0 >> 5, kappa, k0, k1);
 #pragma unroll
-    for (int p = 0; p < 16; ++p)  // shift as a multiply: IMAD on the FMA pipe, LOP3 on ALU
-      o[p] = 0x3F803F80u | ((w * (1u << (15 - p))) & 0x80008000u);
+    for (int p = 0; p < 16; ++p)  // shift as a multiply: IMAD on the FMA pipe, one LOP3 on ALU
+      o[p] = lop3_and_or(w * (1u << (15 - p)), sign_mask, one_pair);
   } else if (kind == PI_GAUSSIAN && (t0 & 3) == 0) {
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
@@ -315,6 +333,7 @@ sketch_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant
       srht_walsh = walsh32_interleaved((uint32_t)(srht_s & 31u));
     }
     const bool word_kind = p.kind == PI_RADEMACHER || p.kind >= PI_SRHT_BASE;
+    const uint32_t sign_mask = opaque_u32(0x80008000u), one_pair = opaque_u32(0x3F803F80u);
     const uint32_t taddr = tbase + ((uint32_t)(32 * quad) << 16) + ACC_COLS;
     for (int jp = set; 2 * jp < nkb; jp += GS) {
       for (int h = 0; h < 2; ++h) {
@@ -328,8 +347,9 @@ sketch_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant
 #pragma unroll
           for (int i = 0; i < 16; ++i) o[i] = o2[i] = 0x3F803F80u;
         } else {
-          gen_pi_half(p.kind, p.seed, (uint32_t)kappa, valid, t0, rc, o, srht_s, srht_walsh);
-          gen_pi_half(p.kind, p.seed, (uint32_t)kappa, valid, t0 + 32, rc, o2, srht_s, srht_walsh);
+          gen_pi_half(p.kind, p.seed, (uint32_t)kappa, valid, t0, rc, o, srht_s, srht_walsh, sign_mask, one_pair);
+          gen_pi_half(p.kind, p.seed, (uint32_t)kappa, valid, t0 + 32, rc, o2, srht_s, srht_walsh, sign_mask,
+                      one_pair);
         }
         if (quad == 0 && lane == 0) K1_TR(3, it);
         mbar_wait_backoff(&pempty[ps], ((uint32_t)(it / PIS) & 1u) ^ 1u, p.backoff_ns);
@@ -360,6 +380,9 @@ sketch_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant
     const int g = tid - 256;
     const int q = g & 15, rg = g >> 4;
     const int box = q >> 3, chunk = q & 7;
+    // (fp32 double-float column sums, as K1F uses, were measured here too:
+    // cfg1 0.545 vs 0.550 ms, cfg2 30.3 vs 29.5 ms per launch — the 56 extra
+    // FADDs per K-block cost the power-capped cfg2 more than the fp64 adds)
     double acc[8];
 #pragma unroll
     for (int e = 0; e < 8; ++e) acc[e] = 0.0;

@@ -339,7 +339,44 @@ smp_status sketch_dense_f32_fused(smp_handle* h, int64_t row0, int64_t rows, con
   const int64_t kpad = (int64_t)k_tiles * 256;
   int64_t chunk = std::min<int64_t>(rows, (512ll << 20) / (kpad * 2));
   chunk = std::max<int64_t>(64, (chunk / 64) * 64);
-  for (int64_t r0 = 0; r0 < rows; r0 += chunk) {
+  // Several row chunks: the Π panel of chunk c + 1 is generated on a second
+  // stream while K1F runs chunk c (two panel buffers).  The panel kernel is
+  // pure ALU work with no SMEM, so its blocks fit beside K1F's one CTA per SM
+  // and fill the issue slots K1F leaves (cfg4: 0.58 ms of panel per 3.1 ms of
+  // K1F, 12.6% of the step when serial).  SMP_F32_PANEL_OVERLAP=0: serial.
+  const int64_t nchunks = (rows + chunk - 1) / chunk;
+  const bool pipe = nchunks >= 2 && [] {
+    const char* e = getenv("SMP_F32_PANEL_OVERLAP");
+    return e ? atoi(e) != 0 : true;
+  }();
+  const int64_t ld_max = ((std::min(chunk, rows) + 63) / 64) * 64;
+  uint16_t* pan[2] = {nullptr, nullptr};
+  auto gen_panel = [&](int64_t c, cudaStream_t st) -> cudaError_t {
+    const int64_t r0c = c * chunk, rcc = std::min(chunk, rows - r0c);
+    const int64_t ldc = ((rcc + 63) / 64) * 64;
+    return launch_pi_panel_kmajor(pi_code(h), h->d.seed, k, (int)kpad, row0 + r0c, ldc, ldc, pan[c & 1], st);
+  };
+  if (pipe) {
+    CK(h, ensure(h->pi_panel, h->pi_panel_cap, kpad * ld_max), "alloc pi panel");
+    CK(h, ensure(h->panel2[0], h->panel2_cap[0], kpad * ld_max), "alloc pi panel");
+    pan[0] = h->pi_panel;
+    pan[1] = h->panel2[0];
+    if (!h->aux_st) CK(h, cudaStreamCreateWithFlags(&h->aux_st, cudaStreamNonBlocking), "stream");
+    for (int b = 0; b < 2; ++b) {
+      if (!h->ev_prep[b]) CK(h, cudaEventCreateWithFlags(&h->ev_prep[b], cudaEventDisableTiming), "event");
+      if (!h->ev_free[b]) CK(h, cudaEventCreateWithFlags(&h->ev_free[b], cudaEventDisableTiming), "event");
+    }
+    if (!h->ev_sync) CK(h, cudaEventCreateWithFlags(&h->ev_sync, cudaEventDisableTiming), "event");
+    // the second stream starts after everything already queued on the main one
+    CK(h, cudaEventRecord(h->ev_sync, h->st), "event");
+    CK(h, cudaStreamWaitEvent(h->aux_st, h->ev_sync, 0), "wait");
+    CK(h, gen_panel(0, h->aux_st), "pi panel");
+    CK(h, cudaEventRecord(h->ev_prep[0], h->aux_st), "event");
+    h->launches += 1;
+    h->panel_row0 = -1;   // the cached single-chunk panel is overwritten
+  }
+  int64_t ci = 0;
+  for (int64_t r0 = 0; r0 < rows; r0 += chunk, ++ci) {
     const int64_t rc = std::min(chunk, rows - r0);
     SketchTCParams p{};
     p.rows = rc;
@@ -356,18 +393,29 @@ smp_status sketch_dense_f32_fused(smp_handle* h, int64_t row0, int64_t rows, con
     const int64_t ld = (int64_t)p.kb_total * 64;
     CK(h, ensure(h->part, h->part_cap, (int64_t)p.splits * 3 * n * k), "alloc partials");
     CK(h, ensure(h->pnorm, h->pnorm_cap, (int64_t)p.splits * p.k_tiles * n), "alloc pnorm");
-    CK(h, ensure(h->pi_panel, h->pi_panel_cap, kpad * ld), "alloc pi panel");
-    const bool cached = h->panel_row0 == p.row0 && h->panel_ld == ld && h->panel_kpad == kpad;
-    if (!cached) {
-      CK(h, launch_pi_panel_kmajor(p.kind, p.seed, k, (int)kpad, p.row0, ld, ld, h->pi_panel, h->st), "pi panel");
-      h->launches += 1;
-      h->panel_row0 = p.row0;
-      h->panel_ld = ld;
-      h->panel_kpad = kpad;
+    if (pipe) {
+      if (ci + 1 < nchunks) {
+        // buffer (ci + 1) & 1 was last read by K1F of chunk ci - 1
+        if (ci >= 1) CK(h, cudaStreamWaitEvent(h->aux_st, h->ev_free[(ci + 1) & 1], 0), "wait");
+        CK(h, gen_panel(ci + 1, h->aux_st), "pi panel");
+        CK(h, cudaEventRecord(h->ev_prep[(ci + 1) & 1], h->aux_st), "event");
+        h->launches += 1;
+      }
+      CK(h, cudaStreamWaitEvent(h->st, h->ev_prep[ci & 1], 0), "wait");
+    } else {
+      CK(h, ensure(h->pi_panel, h->pi_panel_cap, kpad * ld), "alloc pi panel");
+      const bool cached = h->panel_row0 == p.row0 && h->panel_ld == ld && h->panel_kpad == kpad;
+      if (!cached) {
+        CK(h, launch_pi_panel_kmajor(p.kind, p.seed, k, (int)kpad, p.row0, ld, ld, h->pi_panel, h->st), "pi panel");
+        h->launches += 1;
+        h->panel_row0 = p.row0;
+        h->panel_ld = ld;
+        h->panel_kpad = kpad;
+      }
     }
     p.part = h->part;
     p.pnorm = h->pnorm;
-    p.pi_panel = h->pi_panel;
+    p.pi_panel = pipe ? pan[ci & 1] : h->pi_panel;
     p.pi_ld = ld;
     { const char* dbg = getenv("SMP_K1F_DEBUG"); p.debug = dbg ? atoi(dbg) : 0; }  // ablation only
     if (h->timing) {
@@ -383,6 +431,7 @@ smp_status sketch_dense_f32_fused(smp_handle* h, int64_t row0, int64_t rows, con
       CK(h, cudaEventRecord(h->ev_pool[h->ev_used_n + 1], h->st), "event");
       h->ev_used_n += 2;
     }
+    if (pipe) CK(h, cudaEventRecord(h->ev_free[ci & 1], h->st), "event");
     CK(h, launch_reduce_sketch(h->part, p.splits, 3, n, k, h->acc_sk + col_off * k, h->st), "reduce_sketch");
     CK(h, launch_reduce_norms(h->pnorm, p.splits * p.k_tiles, n, h->acc_nrm + col_off, h->st), "reduce_norms");
     h->launches += 3;

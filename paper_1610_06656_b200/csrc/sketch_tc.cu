@@ -535,9 +535,11 @@ __global__ void pi_panel_kmajor_kernel(int kind, uint64_t seed, int k, int kpad,
 }
 
 cudaError_t launch_pi_panel_kmajor(int kind, uint64_t seed, int k, int kpad, int64_t t0, int64_t rows,
-                                   int64_t ld, uint16_t* panel, cudaStream_t st) {
+                                   int64_t ld, uint16_t* panel, cudaStream_t st, int blocks_per_sm) {
+  // blocks_per_sm = 1: a background launch that leaves every SM room for a
+  // K1F CTA beside it (256 threads x 40 registers next to K1F's 768 x 72)
   const int64_t tot = ((rows + 3) / 4) * kpad;  // upper bound on threads needed
-  const int blocks = (int)std::min<int64_t>((tot + 255) / 256, 148 * 16);
+  const int blocks = (int)std::min<int64_t>((tot + 255) / 256, 148 * (blocks_per_sm > 0 ? blocks_per_sm : 16));
   pi_panel_kmajor_kernel<<<blocks, 256, 0, st>>>(kind, seed, k, kpad, t0, rows, ld, panel);
   return cudaGetLastError();
 }

@@ -340,10 +340,13 @@ smp_status sketch_dense_f32_fused(smp_handle* h, int64_t row0, int64_t rows, con
   int64_t chunk = std::min<int64_t>(rows, (512ll << 20) / (kpad * 2));
   chunk = std::max<int64_t>(64, (chunk / 64) * 64);
   // Several row chunks: the Π panel of chunk c + 1 is generated on a second
-  // stream while K1F runs chunk c (two panel buffers).  The panel kernel is
-  // pure ALU work with no SMEM, so its blocks fit beside K1F's one CTA per SM
-  // and fill the issue slots K1F leaves (cfg4: 0.58 ms of panel per 3.1 ms of
-  // K1F, 12.6% of the step when serial).  SMP_F32_PANEL_OVERLAP=0: serial.
+  // stream (two panel buffers), released as soon as K1F of chunk c - 1 is done,
+  // so it runs under the K2 / norm reduce of chunk c - 1 and the ramp of K1F(c)
+  // instead of after them.  Measured on cfg4 (0.58 ms of panel per 3.1 ms of
+  // K1F): stage 15.6 vs 15.9-16.2 ms serial.  A true side-by-side run does not
+  // pay: only ONE 256-thread panel block fits beside a K1F CTA (registers), and
+  // at 1-2 blocks per SM the latency-bound panel kernel takes longer than K1F
+  // (SMP_F32_PANEL_BLOCKS=1: 19.3 ms, 2: 18.4 ms).  SMP_F32_PANEL_OVERLAP=0: serial.
   const int64_t nchunks = (rows + chunk - 1) / chunk;
   const bool pipe = nchunks >= 2 && [] {
     const char* e = getenv("SMP_F32_PANEL_OVERLAP");
@@ -351,10 +354,15 @@ smp_status sketch_dense_f32_fused(smp_handle* h, int64_t row0, int64_t rows, con
   }();
   const int64_t ld_max = ((std::min(chunk, rows) + 63) / 64) * 64;
   uint16_t* pan[2] = {nullptr, nullptr};
+  const int bg_blocks = [] {   // blocks per SM of the background panel launches (tuning)
+    const char* e = getenv("SMP_F32_PANEL_BLOCKS");
+    return e ? atoi(e) : 16;
+  }();
   auto gen_panel = [&](int64_t c, cudaStream_t st) -> cudaError_t {
     const int64_t r0c = c * chunk, rcc = std::min(chunk, rows - r0c);
     const int64_t ldc = ((rcc + 63) / 64) * 64;
-    return launch_pi_panel_kmajor(pi_code(h), h->d.seed, k, (int)kpad, row0 + r0c, ldc, ldc, pan[c & 1], st);
+    return launch_pi_panel_kmajor(pi_code(h), h->d.seed, k, (int)kpad, row0 + r0c, ldc, ldc, pan[c & 1], st,
+                                  c == 0 ? 16 : bg_blocks);
   };
   if (pipe) {
     CK(h, ensure(h->pi_panel, h->pi_panel_cap, kpad * ld_max), "alloc pi panel");

@@ -27,7 +27,7 @@ struct SketchTCParams {
 };
 // Π(κ, t) for t in [t0, t0 + rows) into panel[κ * ld + t - t0] (bf16 bits; rows padded by the caller)
 cudaError_t launch_pi_panel_kmajor(int kind, uint64_t seed, int k, int kpad, int64_t t0, int64_t rows,
-                                   int64_t ld, uint16_t* panel, cudaStream_t st);
+                                   int64_t ld, uint16_t* panel, cudaStream_t st, int blocks_per_sm = 16);
 cudaError_t launch_sketch_tc(const void* X, int64_t ldx, SketchTCParams p, cudaStream_t st);
 int sketch_tc_smem_bytes();
 // K1F (sketch_tc_f32.cu): fp32 X with the bf16 plane split fused in; Π from

@@ -482,7 +482,10 @@ __global__ void pi_panel_kmajor_kernel(int kind, uint64_t seed, int k, int kpad,
   // Rademacher: thread per (κ, 32-row word), one Philox call per 128 rows
   // (the word of DESIGN.md §3.3), 64 bytes written; otherwise thread per
   // (κ, 4-row group), one Philox call for the Gaussian stream, 8 bytes.
-  const int grp = (kind == PI_RADEMACHER && (t0 & 31) == 0) ? 32 : 4;
+  // Gaussian, 8-aligned rows and pitch: thread per (κ, 8-row group), two
+  // independent Philox calls in flight and one 16-byte store
+  const int grp = (kind == PI_RADEMACHER && (t0 & 31) == 0) ? 32
+                  : (kind == PI_GAUSSIAN && (t0 & 7) == 0 && (ld & 7) == 0) ? 8 : 4;
   const int64_t ng = (rows + grp - 1) / grp;
   const uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
   // (e < 2^32 for any panel K1 uses: kpad <= 4096 and rows / grp < 2^20)
@@ -508,6 +511,20 @@ __global__ void pi_panel_kmajor_kernel(int kind, uint64_t seed, int k, int kpad,
       uint4* d4 = reinterpret_cast<uint4*>(dst);
 #pragma unroll
       for (int q = 0; q < 4; ++q) d4[q] = make_uint4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
+      continue;
+    }
+    if (grp == 8) {
+      uint4 v = make_uint4(0u, 0u, 0u, 0u);
+      if (kappa < k) {
+        const uint64_t tq = (uint64_t)t >> 2, tq1 = tq + 1;
+        const u32x4 w0 = philox4x32_10((uint32_t)tq, (uint32_t)kappa, (uint32_t)(tq >> 32), TAG_GAUSSIAN, k0, k1);
+        const u32x4 w1 = philox4x32_10((uint32_t)tq1, (uint32_t)kappa, (uint32_t)(tq1 >> 32), TAG_GAUSSIAN, k0, k1);
+        v.x = gauss_pair_bits(w0.x, w0.y);
+        v.y = gauss_pair_bits(w0.z, w0.w);
+        v.z = gauss_pair_bits(w1.x, w1.y);
+        v.w = gauss_pair_bits(w1.z, w1.w);
+      }
+      *reinterpret_cast<uint4*>(dst) = v;
       continue;
     }
     uint16_t z[4];
@@ -538,7 +555,7 @@ cudaError_t launch_pi_panel_kmajor(int kind, uint64_t seed, int k, int kpad, int
                                    int64_t ld, uint16_t* panel, cudaStream_t st, int blocks_per_sm) {
   // blocks_per_sm = 1: a background launch that leaves every SM room for a
   // K1F CTA beside it (256 threads x 40 registers next to K1F's 768 x 72)
-  const int64_t tot = ((rows + 3) / 4) * kpad;  // upper bound on threads needed
+  const int64_t tot = ((rows + 3) / 4) * kpad;  // upper bound on threads needed (grid-stride loop)
   const int blocks = (int)std::min<int64_t>((tot + 255) / 256, 148 * (blocks_per_sm > 0 ? blocks_per_sm : 16));
   pi_panel_kmajor_kernel<<<blocks, 256, 0, st>>>(kind, seed, k, kpad, t0, rows, ld, panel);
   return cudaGetLastError();
